@@ -1,0 +1,176 @@
+/*
+ * mds.h — C-ABI of the B200-native condensed-KKT hot path of the mixed
+ * dense-sparse (MDS) interior-point method (arxiv/paper_2605_13736,
+ * PAPER.md §2, "Porting the Nonlinear Optimization Library HiOp to
+ * Accelerator-Based Hardware Architectures").
+ *
+ * One Newton iteration's KKT work (Fig.1):
+ *   mds_condense     Eq.(5) -> Eq.(6): eliminate the diagonal sparse block
+ *                    (K3 "M := M + A D B^T") -> dense M, rhs_c
+ *   mds_factor       Bunch-Kaufman LDL^T of M with inertia (K4)
+ *   mds_solve        forward/backward solves + sparse-step recovery (K4 + K2)
+ *   ipm_step_vectors fraction-to-boundary + norms (K1)
+ *
+ * ---------------------------------------------------------------------------
+ * Conventions (apply to every entry point)
+ *  - All pointers named *_dev or documented "device" are CUDA device pointers
+ *    owned by the CALLER; the library allocates nothing inside the hot calls
+ *    (only mds_plan_create allocates, for the pattern-derived index maps).
+ *  - Dense symmetric matrices are column-major with leading dimension ld >= N;
+ *    only the LOWER triangle is read or written (LAPACK uplo='L').  Element
+ *    (i,j), i >= j, is at A[i + j*ld].
+ *  - J_s is CSR n_s x m with ROWS = sparse variables (reading R1 in DESIGN.md):
+ *    row k lists the constraints sparse variable k enters; column c < m_E is an
+ *    equality row g of Eq.(5), c >= m_E an inequality row h.  CSR must be
+ *    canonical (sorted, unique column indices per row).
+ *  - Unknown order of M / rhs_c / dxy is (x_d, y_g, y_h), as Eq.(6)
+ *    (PAPER.md:169-176).  N = n_d + m_E + m_I.
+ *  - `stream` is a cudaStream_t passed as void*.  Every call is asynchronous
+ *    and stream-ordered, except mds_factor with inertia_host != NULL, which
+ *    synchronises the stream to return the inertia (the IPM must branch on it,
+ *    PAPER.md:161).
+ *  - Return value: MDS_OK, or an argument error detected on the host
+ *    (MDS_ERR_ARG / MDS_ERR_PATTERN / MDS_ERR_WORKSPACE) or a CUDA launch error
+ *    (MDS_ERR_CUDA).  Data-dependent errors are written to *status_dev (a
+ *    device int32 the caller zeroes; the first error wins).
+ *  - FP64 throughout.
+ * ---------------------------------------------------------------------------
+ */
+#ifndef MDS_B200_H
+#define MDS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MDS_OK = 0,
+    MDS_ERR_ARG = -1,          /* null pointer, negative size, ld < N          */
+    MDS_ERR_PATTERN = -2,      /* CSR unsorted / duplicate / out of range      */
+    MDS_ERR_NONPOSITIVE = -3,  /* q_k = h_ss+sigma_s+delta_w <= 0 or d_h <= 0  */
+    MDS_ERR_NONFINITE = -4,    /* NaN/Inf in M before factoring                */
+    MDS_ERR_SINGULAR = -5,     /* zero 1x1 pivot (|d| <= tol) met by the solve */
+    MDS_ERR_NOT_INTERIOR = -6, /* x not strictly inside a finite bound, z <= 0 */
+    MDS_ERR_CUDA = -7,         /* CUDA launch / runtime error                  */
+    MDS_ERR_WORKSPACE = -8     /* workspace too small                          */
+} mds_status;
+
+/* Inertia triple (positive, zero, negative eigenvalue counts). */
+typedef struct {
+    int64_t pos, zero, neg;
+} mds_inertia;
+
+/* Opaque, immutable per-sparsity-pattern plan (the pattern is fixed across IPM
+ * iterations).  Holds device copies of the CSR pattern of J_s and its
+ * constraint-major transpose map.  Shareable across streams. */
+typedef struct mds_plan mds_plan;
+
+/* Library version string, e.g. "mds_b200 0.1 sm_100a". */
+const char *mds_version(void);
+
+/* Build a plan from the HOST CSR pattern of J_s (rowptr[n_s+1], colidx[nnz]).
+ * Validates the pattern (MDS_ERR_PATTERN) and uploads index maps to the
+ * current device.  *out receives the plan. */
+int mds_plan_create(int64_t n_s, int64_t n_d, int64_t m_E, int64_t m_I,
+                    const int32_t *rowptr_host, const int32_t *colidx_host, mds_plan **out);
+int mds_plan_destroy(mds_plan *plan);
+/* Dimensions of a plan: out[0..4] = n_s, n_d, m_E, m_I, nnz. */
+int mds_plan_dims(const mds_plan *plan, int64_t *out5);
+
+/* ---------------------------------------------------------------------------
+ * mds_condense — Eq.(5) -> Eq.(6) with the regularisation
+ * of PAPER.md:161 folded in:
+ *   q_k   = h_ss[k] + sigma_s[k] + delta_w ;  w_k = 1/q_k         (Q_{x_s}^{-1})
+ *   M_xx  = H_dd + diag(sigma_d) + delta_w I                        (block (1,1))
+ *   M_yx  = J_d                                                     (blocks (2,1),(3,1))
+ *   M_yy  = -J_s^T diag(w) J_s - diag(0_{m_E}, 1/d_h) - delta_c I   (blocks (2,2)..(3,3))
+ *   rhs_c = [ r_xd ; r_y - J_s^T (w .* r_xs) ]
+ * Inputs (device): js_val[nnz] (values in the plan's CSR order); h_ss, sigma_s
+ * [n_s]; H_dd [n_d x n_d, ldh, lower read]; sigma_d [n_d]; J_d [m x n_d, ldj];
+ * d_h [m_I]; r [n_s + N] = (r_xs, r_xd, r_yg, r_yh) or NULL (then rhs_c is not
+ * written).  Outputs (device): M [N x N, ldm, lower written], rhs_c [N] (or
+ * NULL), w_out [n_s] (kept for mds_solve's recovery).
+ * Data errors: MDS_ERR_NONPOSITIVE if some q_k <= 0 or d_h <= 0. */
+int mds_condense(const mds_plan *plan, const double *js_val, const double *h_ss, const double *sigma_s,
+                 const double *H_dd, int64_t ldh, const double *sigma_d, const double *J_d, int64_t ldj,
+                 const double *d_h, double delta_w, double delta_c, const double *r,
+                 double *M, int64_t ldm, double *rhs_c, double *w_out, int32_t *status_dev, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * mds_factor — Bunch-Kaufman LDL^T of the symmetric indefinite M (PAPER.md:191:
+ * "MAGMA uses the Bunch-Kaufman diagonal pivoting method to form a LDL^T
+ * factorization ... the inertia ... can be effectively computed from the D
+ * matrix"), alpha = (1+sqrt(17))/8, blocked, FP64.
+ * In place: on return M holds D and unit-L below the diagonal, in
+ * EXPLICIT-permutation form  P M P^T = L D L^T.  A 2x2 block of D at (k,k+1)
+ * keeps its diagonal entries on the diagonal and its off-diagonal d21 in the
+ * UPPER slot (k, k+1) of M (the one upper-triangle element written), with
+ * L(k+1,k) = 0.
+ * piv [2N] (device int32, caller-owned): piv[0..N) = per-step pivot record in
+ * LAPACK 1-based encoding (piv[k]=p+1 for a 1x1 pivot that interchanged k and
+ * p; piv[k]=piv[k+1]=-(p+1) for a 2x2 pivot at (k,k+1)); piv[N..2N) = the
+ * final permutation (row i of P M P^T is row piv[N+i] of M).  The pair (M,piv)
+ * is consumed only by mds_solve.
+ * zero_tol: pivots with |d| <= zero_tol count as zero; zero_tol < 0 selects
+ * N * eps * ||M||_inf (computed on device; reading R4 in DESIGN.md).
+ * inertia_dev: device mds_inertia (written).  inertia_host: if non-NULL the
+ * call synchronises `stream` and copies the inertia there (3 integers cross
+ * the bus, nothing else).
+ * work: device workspace of at least mds_factor_workspace_size(N) bytes.
+ * Data errors: MDS_ERR_NONFINITE if M holds NaN/Inf (then nothing is
+ * factored). */
+size_t mds_factor_workspace_size(int64_t N);
+int mds_factor(int64_t N, double *M, int64_t ldm, int32_t *piv, double zero_tol,
+               mds_inertia *inertia_dev, mds_inertia *inertia_host, int32_t *status_dev,
+               void *work, size_t work_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * mds_solve — x = P^T L^{-T} D^{-1} L^{-1} P rhs_c with mds_factor's output,
+ * then the sparse-step recovery from the first block row of Eq.(5):
+ *   dx_s = w .* (r_xs - J_s dy)        (K2 mixed sparse mat-vec)
+ * Inputs (device): LD, piv from mds_factor; rhs_c [N]; js_val [nnz]; w [n_s]
+ * (from mds_condense); r_xs [n_s].  Outputs (device): dxy [N] = (dx_d, dy_g,
+ * dy_h); dx_s [n_s] (skipped if plan is NULL or dx_s is NULL).  dxy may alias
+ * rhs_c.  work: >= mds_solve_workspace_size(N) bytes.
+ * Data errors: MDS_ERR_SINGULAR if a 1x1 pivot has |d| <= zero_tol (same
+ * meaning as in mds_factor; < 0 selects the value mds_factor computed, which it
+ * leaves in its workspace — pass the same `fwork` pointer, or NULL to use 0). */
+size_t mds_solve_workspace_size(int64_t N);
+int mds_solve(const mds_plan *plan, int64_t N, const double *LD, int64_t ldm, const int32_t *piv,
+              const double *rhs_c, const double *js_val, const double *w, const double *r_xs,
+              double *dxy, double *dx_s, double zero_tol, const void *fwork,
+              int32_t *status_dev, void *work, size_t work_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * ipm_step_vectors — barrier vector kernels (K1), one fused pass:
+ * fraction-to-boundary ("the point that is feasible with respect
+ * to the bounds constraints and is the farthest away ... requires a 'reduce'"),
+ * complementarity and residual norms, optional barrier diagonal sigma.
+ * Bounds with |b| >= 1e20 are infinite (reading R10).  tau in (0,1).
+ *   out[0] alpha_p  = min(1, min tau*(x-lo)/(-dx) [dx<0], tau*(up-x)/dx [dx>0])
+ *   out[1] alpha_d  = min(1, min tau*zl/(-dzl) [dzl<0], tau*zu/(-dzu) [dzu<0])
+ *   out[2] compl_inf= max |(x-lo)*zl - mu|, |(up-x)*zu - mu|   (finite bounds)
+ *   out[3] compl_sum= sum (x-lo)*zl + (up-x)*zu                (finite bounds)
+ *   out[4] n_compl  = number of finite bounds (as double)
+ *   out[5] first_bad= lowest index not strictly interior (or z<=0), else -1
+ *   out[6+i] = ||res_i||_inf, i < n_res (n_res <= 8)
+ * Inputs (device) x, dx, lo, up, zl, zu, dzl, dzu [n]; res: HOST array of
+ * n_res device pointers, res_len: HOST array of their lengths.  Outputs
+ * (device): out [6 + n_res] doubles; sigma_out [n] (= zl/(x-lo) + zu/(up-x),
+ * infinite-bound terms 0) or NULL.  work: >= ipm_step_vectors_workspace_size(n)
+ * bytes, ZEROED once before first use (the kernel leaves it zeroed).
+ * Data errors: MDS_ERR_NOT_INTERIOR. */
+size_t ipm_step_vectors_workspace_size(int64_t n);
+int ipm_step_vectors(int64_t n, const double *x, const double *dx, const double *lo, const double *up,
+                     const double *zl, const double *zu, const double *dzl, const double *dzu,
+                     double tau, double mu, int32_t n_res, const double *const *res, const int64_t *res_len,
+                     double *out, double *sigma_out, int32_t *status_dev,
+                     void *work, size_t work_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MDS_B200_H */

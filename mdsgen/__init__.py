@@ -291,5 +291,6 @@ def config_problem(cfg: str, seed: Optional[int] = None, pattern="uniform", inst
 
 
 def step_vectors_for(prob: MDSProblem, seed: int, mu=0.1):
-    """K1 inputs sized like the problem: n_b = n_s + n_d + m_I bounded components."""
-    return step_vectors(prob.n_s + prob.n_d + prob.m_I, seed, mu=mu)
+    """K1 inputs for the primal block (x_s, x_d): n_b = n_s + n_d components
+    (the primal direction itself comes from the solve)."""
+    return step_vectors(prob.n_s + prob.n_d, seed, mu=mu)

@@ -1,0 +1,183 @@
+"""paper_2605_13736_b200 — B200-native condensed-KKT hot path of the MDS IPM.
+
+Thin Python binding (argument marshalling only) over the C-ABI library
+``libmds_b200.so`` declared in ``include/mds.h``:  ``mds_condense``,
+``mds_factor``, ``mds_solve``, ``ipm_step_vectors`` (§2, Eq.(5)-(6),
+K1-K4 of PAPER.md:182-191).  Every step of the path runs in the library's
+sm_100a kernels; PyTorch provides device memory, streams and process groups.
+
+There is NO CPU fallback: importing this package on a box without the built
+library raises, and every call requires CUDA tensors.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from .errors import (MDSError, DimensionError, MalformedMatrixError, CompressionError, NumericError,
+                     SingularError, NotInteriorError, CudaError, WorkspaceError, raise_for)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmds_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"paper_2605_13736_b200: native library {LIB_PATH} is missing — run "
+                      "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+_P, _I64, _D, _I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int32
+_lib.mds_version.restype = ctypes.c_char_p
+_lib.mds_plan_create.argtypes = [_I64, _I64, _I64, _I64, _P, _P, ctypes.POINTER(ctypes.c_void_p)]
+_lib.mds_plan_destroy.argtypes = [_P]
+_lib.mds_plan_dims.argtypes = [_P, _P]
+_lib.mds_condense.argtypes = [_P, _P, _P, _P, _P, _I64, _P, _P, _I64, _P, _D, _D, _P, _P, _I64, _P, _P, _P, _P]
+_lib.mds_factor_workspace_size.restype = ctypes.c_size_t
+_lib.mds_factor_workspace_size.argtypes = [_I64]
+_lib.mds_factor.argtypes = [_I64, _P, _I64, _P, _D, _P, _P, _P, _P, ctypes.c_size_t, _P]
+_lib.mds_solve_workspace_size.restype = ctypes.c_size_t
+_lib.mds_solve_workspace_size.argtypes = [_I64]
+_lib.mds_solve.argtypes = [_P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _D, _P, _P, _P, ctypes.c_size_t, _P]
+_lib.ipm_step_vectors_workspace_size.restype = ctypes.c_size_t
+_lib.ipm_step_vectors_workspace_size.argtypes = [_I64]
+_lib.ipm_step_vectors.argtypes = [_I64, _P, _P, _P, _P, _P, _P, _P, _P, _D, _D, _I32, _P, _P, _P, _P, _P, _P,
+                                  ctypes.c_size_t, _P]
+for _f in ("mds_plan_create", "mds_plan_destroy", "mds_plan_dims", "mds_condense", "mds_factor", "mds_solve",
+           "ipm_step_vectors"):
+    getattr(_lib, _f).restype = ctypes.c_int
+
+EXPORTS = ["mds_version", "mds_plan_create", "mds_plan_destroy", "mds_plan_dims", "mds_condense",
+           "mds_factor_workspace_size", "mds_factor", "mds_solve_workspace_size", "mds_solve",
+           "ipm_step_vectors_workspace_size", "ipm_step_vectors"]
+
+
+def version() -> str:
+    return _lib.mds_version().decode()
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("expected a torch tensor")
+    if not t.is_cuda:
+        raise DimensionError("tensor must live on a CUDA device (no CPU fallback)")
+    if not t.is_contiguous():
+        raise DimensionError("tensor must be contiguous")
+    return t.data_ptr()
+
+
+def _f64(t, n=None):
+    if t is not None and t.dtype != torch.float64:
+        raise DimensionError("FP64 tensor required")
+    if t is not None and n is not None and t.numel() < n:
+        raise DimensionError(f"tensor has {t.numel()} elements, need {n}")
+    return _ptr(t)
+
+
+def _stream(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check(code, what):
+    if code != 0:
+        raise_for(code, what)
+
+
+class Plan:
+    """mds_plan: the J_s sparsity pattern (host CSR, rows = sparse variables),
+    validated and uploaded once; fixed across IPM iterations."""
+
+    def __init__(self, n_s, n_d, m_E, m_I, rowptr, colidx):
+        import numpy as np
+        rp = np.ascontiguousarray(np.asarray(rowptr), dtype=np.int32)
+        ci = np.ascontiguousarray(np.asarray(colidx), dtype=np.int32)
+        if rp.shape[0] != n_s + 1:
+            raise DimensionError("rowptr must have n_s+1 entries")
+        h = ctypes.c_void_p()
+        code = _lib.mds_plan_create(n_s, n_d, m_E, m_I, rp.ctypes.data if n_s >= 0 else None,
+                                    ci.ctypes.data if ci.size else None, ctypes.byref(h))
+        _check(code, "mds_plan_create")
+        self._h = h
+        self.n_s, self.n_d, self.m_E, self.m_I = int(n_s), int(n_d), int(m_E), int(m_I)
+        self.nnz = int(rp[-1]) if n_s > 0 else 0
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def N(self):
+        return self.n_d + self.m_E + self.m_I
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.mds_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def condense(plan: Plan, js_val, h_ss, sigma_s, H_dd, ldh, sigma_d, J_d, ldj, d_h, delta_w, delta_c, r,
+             M, ldm, rhs_c, w_out, status, stream=None):
+    """mds_condense (Eq.(5)->Eq.(6)); see include/mds.h."""
+    code = _lib.mds_condense(plan.handle, _f64(js_val), _f64(h_ss), _f64(sigma_s), _f64(H_dd), int(ldh),
+                             _f64(sigma_d), _f64(J_d), int(ldj), _f64(d_h), float(delta_w), float(delta_c),
+                             _f64(r), _f64(M), int(ldm), _f64(rhs_c), _f64(w_out), _ptr(status), _stream(stream))
+    _check(code, "mds_condense")
+
+
+def factor_workspace_size(N):
+    return int(_lib.mds_factor_workspace_size(int(N)))
+
+
+def solve_workspace_size(N):
+    return int(_lib.mds_solve_workspace_size(int(N)))
+
+
+def step_vectors_workspace_size(n):
+    return int(_lib.ipm_step_vectors_workspace_size(int(n)))
+
+
+class Inertia(ctypes.Structure):
+    _fields_ = [("pos", ctypes.c_int64), ("zero", ctypes.c_int64), ("neg", ctypes.c_int64)]
+
+
+def factor(N, M, ldm, piv, zero_tol, inertia_dev, status, work, sync=True, stream=None):
+    """mds_factor (Bunch-Kaufman LDL^T + inertia).  Returns the inertia tuple
+    when sync=True (one 24-byte D2H copy), else None."""
+    host = Inertia() if sync else None
+    code = _lib.mds_factor(int(N), _f64(M), int(ldm), _ptr(piv), float(zero_tol), _ptr(inertia_dev),
+                           ctypes.byref(host) if sync else None, _ptr(status), _ptr(work),
+                           work.numel() * work.element_size(), _stream(stream))
+    _check(code, "mds_factor")
+    return (host.pos, host.zero, host.neg) if sync else None
+
+
+def solve(plan, N, LD, ldm, piv, rhs_c, js_val, w, r_xs, dxy, dx_s, zero_tol, fwork, status, work, stream=None):
+    """mds_solve (explicit-permutation LDL^T solve + dx_s recovery)."""
+    code = _lib.mds_solve(plan.handle if plan is not None else None, int(N), _f64(LD), int(ldm), _ptr(piv),
+                          _f64(rhs_c), _f64(js_val), _f64(w), _f64(r_xs), _f64(dxy), _f64(dx_s), float(zero_tol),
+                          _ptr(fwork), _ptr(status), _ptr(work), work.numel() * work.element_size(),
+                          _stream(stream))
+    _check(code, "mds_solve")
+
+
+def step_vectors(n, x, dx, lo, up, zl, zu, dzl, dzu, tau, mu, out, sigma_out, status, work, res=(), stream=None):
+    """ipm_step_vectors (fraction-to-boundary + norms, one fused pass)."""
+    nres = len(res)
+    arr_p = (ctypes.c_void_p * max(nres, 1))(*[_f64(t) for t in res]) if nres else None
+    arr_l = (ctypes.c_int64 * max(nres, 1))(*[t.numel() for t in res]) if nres else None
+    code = _lib.ipm_step_vectors(int(n), _f64(x), _f64(dx), _f64(lo), _f64(up), _f64(zl), _f64(zu), _f64(dzl),
+                                 _f64(dzu), float(tau), float(mu), nres, arr_p, arr_l, _f64(out), _f64(sigma_out),
+                                 _ptr(status), _ptr(work), work.numel() * work.element_size(), _stream(stream))
+    _check(code, "ipm_step_vectors")
+
+
+from .step import KKTStep, DeviceProblem  # noqa: E402,F401

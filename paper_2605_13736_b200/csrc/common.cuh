@@ -1,0 +1,60 @@
+// common.cuh — shared device helpers of the product path (NOT shared with oracle/).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "../../include/mds.h"
+
+#define MDS_INF_BOUND 1e20
+
+// first data error wins (status starts at 0, codes are negative)
+__device__ __forceinline__ void mds_set_status(int32_t* status, int32_t code) {
+  if (status) atomicCAS(reinterpret_cast<int*>(status), 0, code);
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// (value, index) arg-max with the LOWEST index on ties (IDAMAX semantics, reading R5)
+struct ArgMax { double v; int i; };
+__device__ __forceinline__ ArgMax am_better(ArgMax a, ArgMax b) {
+  if (b.v > a.v) return b;
+  if (b.v == a.v && b.i < a.i) return b;
+  return a;
+}
+__device__ __forceinline__ ArgMax warp_argmax(ArgMax a) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ArgMax b;
+    b.v = __shfl_xor_sync(0xffffffffu, a.v, o);
+    b.i = __shfl_xor_sync(0xffffffffu, a.i, o);
+    a = am_better(a, b);
+  }
+  return a;
+}
+
+#define MDS_CUDA_TRY(expr)                                  \
+  do {                                                      \
+    cudaError_t _e = (expr);                                \
+    if (_e != cudaSuccess) return MDS_ERR_CUDA;             \
+  } while (0)
+
+#define MDS_LAUNCH_CHECK()                                  \
+  do {                                                      \
+    cudaError_t _e = cudaGetLastError();                    \
+    if (_e != cudaSuccess) return MDS_ERR_CUDA;             \
+  } while (0)
+
+static inline int64_t mds_cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -1,0 +1,272 @@
+// condense.cu — mds_plan_* and mds_condense: Eq.(5) -> Eq.(6) of PAPER.md
+// (K3 "M := M + A D B^T", fused over CSR
+// instead of the paper's three triplet launches).
+//
+// Kernels (HBM-bound; algorithmic bytes in DESIGN.md §Roofline):
+//   k_condense_w      w_k = 1/(h_ss+sigma_s+delta_w), status on q<=0          (grid-stride)
+//   k_condense_dense  columns j < n_d: M[j:n_d,j] = H_dd+diag, M[n_d:,j] = J_d,
+//                     rhs_c[0:n_d] = r_xd                                     (CTA per column)
+//   k_condense_yy     columns n_d+c: one WARP owns output column c of M_yy,
+//                     accumulates -sum_k w_k J[k,c] J[k,c1] (c1 >= c) in a
+//                     private shared-memory column (no FP64 smem atomics: lanes
+//                     that collide on c1 are serialised via __match_any_sync),
+//                     then writes the column once, coalesced; also rhs_c[n_d+c].
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "common.cuh"
+
+struct mds_plan {
+  int64_t n_s, n_d, m_E, m_I, nnz;
+  int32_t* rowptr;   // [n_s+1] device
+  int32_t* colidx;   // [nnz]   device
+  int32_t* tptr;     // [m+1]   constraint-major transpose: entries of column c
+  int2* tkp;         // [nnz]   (k, p): sparse variable k, CSR position p of (k,c)
+  int32_t max_col_len;
+};
+
+extern "C" const char* mds_version(void) { return "mds_b200 0.1 sm_100a"; }
+
+extern "C" int mds_plan_create(int64_t n_s, int64_t n_d, int64_t m_E, int64_t m_I,
+                               const int32_t* rowptr, const int32_t* colidx, mds_plan** out) {
+  if (!out || n_s < 0 || n_d < 0 || m_E < 0 || m_I < 0) return MDS_ERR_ARG;
+  if (n_s > 0 && (!rowptr)) return MDS_ERR_ARG;
+  const int64_t m = m_E + m_I;
+  if (m + n_d > (int64_t)1 << 30) return MDS_ERR_ARG;
+  int64_t nnz = n_s > 0 ? rowptr[n_s] : 0;
+  if (n_s > 0 && rowptr[0] != 0) return MDS_ERR_PATTERN;
+  if (nnz > 0 && !colidx) return MDS_ERR_ARG;
+  // validate canonical CSR (reading R13): sorted, unique, in range
+  for (int64_t k = 0; k < n_s; k++) {
+    if (rowptr[k + 1] < rowptr[k]) return MDS_ERR_PATTERN;
+    for (int64_t p = rowptr[k]; p < rowptr[k + 1]; p++) {
+      if (colidx[p] < 0 || colidx[p] >= m) return MDS_ERR_PATTERN;
+      if (p > rowptr[k] && colidx[p] <= colidx[p - 1]) return MDS_ERR_PATTERN;
+    }
+  }
+  // constraint-major transpose (counting sort; entries of a column in k order)
+  std::vector<int32_t> tptr(m + 1, 0);
+  for (int64_t p = 0; p < nnz; p++) tptr[colidx[p] + 1]++;
+  for (int64_t c = 0; c < m; c++) tptr[c + 1] += tptr[c];
+  std::vector<int2> tkp(std::max<int64_t>(nnz, 1));
+  {
+    std::vector<int32_t> fill(tptr.begin(), tptr.end() - 1);
+    for (int64_t k = 0; k < n_s; k++)
+      for (int64_t p = rowptr[k]; p < rowptr[k + 1]; p++) tkp[fill[colidx[p]]++] = make_int2((int)k, (int)p);
+  }
+  int32_t maxlen = 0;
+  for (int64_t c = 0; c < m; c++) maxlen = std::max(maxlen, tptr[c + 1] - tptr[c]);
+
+  mds_plan* P = new (std::nothrow) mds_plan();
+  if (!P) return MDS_ERR_ARG;
+  P->n_s = n_s; P->n_d = n_d; P->m_E = m_E; P->m_I = m_I; P->nnz = nnz; P->max_col_len = maxlen;
+  P->rowptr = nullptr; P->colidx = nullptr; P->tptr = nullptr; P->tkp = nullptr;
+  bool ok = cudaMalloc(&P->rowptr, sizeof(int32_t) * (n_s + 1)) == cudaSuccess &&
+            cudaMalloc(&P->colidx, sizeof(int32_t) * std::max<int64_t>(nnz, 1)) == cudaSuccess &&
+            cudaMalloc(&P->tptr, sizeof(int32_t) * (m + 1)) == cudaSuccess &&
+            cudaMalloc(&P->tkp, sizeof(int2) * std::max<int64_t>(nnz, 1)) == cudaSuccess;
+  if (ok) {
+    std::vector<int32_t> rp(n_s + 1, 0);
+    if (n_s > 0) std::memcpy(rp.data(), rowptr, sizeof(int32_t) * (n_s + 1));
+    ok = cudaMemcpy(P->rowptr, rp.data(), sizeof(int32_t) * (n_s + 1), cudaMemcpyHostToDevice) == cudaSuccess &&
+         (nnz == 0 || cudaMemcpy(P->colidx, colidx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice) == cudaSuccess) &&
+         cudaMemcpy(P->tptr, tptr.data(), sizeof(int32_t) * (m + 1), cudaMemcpyHostToDevice) == cudaSuccess &&
+         (nnz == 0 || cudaMemcpy(P->tkp, tkp.data(), sizeof(int2) * nnz, cudaMemcpyHostToDevice) == cudaSuccess);
+  }
+  if (!ok) {
+    cudaFree(P->rowptr); cudaFree(P->colidx); cudaFree(P->tptr); cudaFree(P->tkp);
+    delete P;
+    return MDS_ERR_CUDA;
+  }
+  *out = P;
+  return MDS_OK;
+}
+
+extern "C" int mds_plan_destroy(mds_plan* P) {
+  if (!P) return MDS_ERR_ARG;
+  cudaFree(P->rowptr); cudaFree(P->colidx); cudaFree(P->tptr); cudaFree(P->tkp);
+  delete P;
+  return MDS_OK;
+}
+
+extern "C" int mds_plan_dims(const mds_plan* P, int64_t* out) {
+  if (!P || !out) return MDS_ERR_ARG;
+  out[0] = P->n_s; out[1] = P->n_d; out[2] = P->m_E; out[3] = P->m_I; out[4] = P->nnz;
+  return MDS_OK;
+}
+
+// accessor for solve.cu (same library)
+const int32_t* mds_plan_rowptr(const mds_plan* P) { return P->rowptr; }
+const int32_t* mds_plan_colidx(const mds_plan* P) { return P->colidx; }
+
+// ---------------------------------------------------------------------------
+// w_k = 1/q_k, q_k = h_ss + sigma_s + delta_w  (Q_{x_s}^{-1}, A2 PAPER.md:121)
+__global__ void k_condense_w(int64_t n_s, const double* __restrict__ h_ss, const double* __restrict__ sigma_s,
+                             double delta_w, double* __restrict__ w, int32_t* status) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n_s; k += (int64_t)gridDim.x * blockDim.x) {
+    double q = h_ss[k] + sigma_s[k] + delta_w;
+    if (!(q > 0.0)) mds_set_status(status, MDS_ERR_NONPOSITIVE);
+    w[k] = 1.0 / q;
+  }
+}
+
+// dense blocks of Eq.(6): column j < n_d of M (lower): rows j..n_d-1 from H_dd
+// (+sigma_d+delta_w on the diagonal), rows n_d..N-1 from J_d column j.
+__global__ void k_condense_dense(int64_t n_d, int64_t m, const double* __restrict__ H, int64_t ldh,
+                                 const double* __restrict__ sigma_d, double delta_w,
+                                 const double* __restrict__ Jd, int64_t ldj,
+                                 double* __restrict__ M, int64_t ldm,
+                                 const double* __restrict__ r_xd, double* __restrict__ rhs_c) {
+  for (int64_t j = blockIdx.x; j < n_d; j += gridDim.x) {
+    double* Mj = M + j * ldm;
+    const double* Hj = H + j * ldh;
+    const double* Jj = Jd + j * ldj;
+    for (int64_t i = j + threadIdx.x; i < n_d; i += blockDim.x) {
+      double v = Hj[i];
+      if (i == j) v = v + sigma_d[j] + delta_w;
+      Mj[i] = v;
+    }
+    for (int64_t c = threadIdx.x; c < m; c += blockDim.x) Mj[n_d + c] = Jj[c];
+    if (threadIdx.x == 0 && rhs_c) rhs_c[j] = r_xd[j];
+  }
+}
+
+// M_yy column c (rows c..m-1 of the (y,y) block), one warp per column.
+// acc[i] holds M_yy[c+i, c] for i in [0, m-c).  Column order is folded
+// (c, m-1-c) so CTAs get balanced work.
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+k_condense_yy(int64_t n_d, int64_t m_E, int64_t m, int64_t acc_len,
+              const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
+              const double* __restrict__ val, const int32_t* __restrict__ tptr, const int2* __restrict__ tkp,
+              const double* __restrict__ w, const double* __restrict__ d_h, double delta_c,
+              const double* __restrict__ r, int64_t n_s, double* __restrict__ M, int64_t ldm,
+              double* __restrict__ rhs_c, int32_t* status) {
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* acc = smem + (size_t)warp * acc_len;
+  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
+  if (gw >= m) return;
+  const int64_t c = (gw & 1) ? (m - 1 - (gw >> 1)) : (gw >> 1);
+  const int64_t len = m - c;
+  const unsigned lanemask_lt = (1u << lane) - 1u;
+  const double* r_xs = r;                       // may be NULL
+  double rsum = 0.0;
+  // process the column in chunks of acc_len rows (one chunk when m <= acc_len)
+  for (int64_t base = 0; base < len; base += acc_len) {
+    const int64_t clen = (len - base < acc_len) ? (len - base) : acc_len;
+    for (int64_t i = lane; i < clen; i += 32) acc[i] = 0.0;
+    __syncwarp();
+    const int32_t e0 = tptr[c], e1 = tptr[c + 1];
+    for (int32_t e = e0; e < e1; e += 32) {
+      const int32_t my = e + lane;
+      const bool act = my < e1;
+      int k = 0, p = 0, pend = 0;
+      double t = 0.0;
+      if (act) {
+        int2 kp = tkp[my];
+        k = kp.x; p = kp.y;
+        pend = rowptr[k + 1];
+        const double wk = w[k];
+        const double v = val[p];
+        t = v * wk;
+        if (base == 0 && r_xs) rsum += t * r_xs[k];
+      }
+      // walk the row suffix p..pend-1 (entries with c1 >= c, sorted ascending)
+      int q = p;
+      while (__any_sync(0xffffffffu, act && q < pend)) {
+        const bool live = act && q < pend;
+        int64_t c1 = -1;
+        double upd = 0.0;
+        if (live) {
+          c1 = (int64_t)colidx[q] - c - base;
+          upd = t * val[q];
+          if (c1 < 0 || c1 >= clen) c1 = -1;   // outside this chunk
+        }
+        const bool go = c1 >= 0;
+        const unsigned gomask = __ballot_sync(0xffffffffu, go);
+        if (go) {
+          const unsigned peers = __match_any_sync(gomask, (int)c1);
+          if (peers == (1u << lane)) {
+            acc[c1] -= upd;
+          } else {
+            const int rank = __popc(peers & lanemask_lt);
+            const int gs = __popc(peers);
+            for (int s = 0; s < gs; s++) {
+              if (rank == s) acc[c1] -= upd;
+              __syncwarp(peers);
+            }
+          }
+        }
+        __syncwarp();
+        if (live) q++;
+      }
+    }
+    __syncwarp();
+    // diagonal terms -diag(0_{m_E}, 1/d_h) - delta_c I, then one coalesced column write
+    double* Mc = M + (n_d + c) * ldm + n_d + c + base;
+    for (int64_t i = lane; i < clen; i += 32) {
+      double v = acc[i];
+      if (base + i == 0) {
+        v = v - delta_c;
+        if (c >= m_E) {
+          double dh = d_h[c - m_E];
+          if (!(dh > 0.0)) mds_set_status(status, MDS_ERR_NONPOSITIVE);
+          v = v - 1.0 / dh;
+        }
+      }
+      Mc[i] = v;
+    }
+    __syncwarp();
+  }
+  if (rhs_c && r_xs) {
+    rsum = warp_sum(rsum);
+    if (lane == 0) rhs_c[n_d + c] = r[n_s + n_d + c] - rsum;
+  }
+}
+
+extern "C" int mds_condense(const mds_plan* P, const double* js_val, const double* h_ss, const double* sigma_s,
+                            const double* H_dd, int64_t ldh, const double* sigma_d, const double* J_d, int64_t ldj,
+                            const double* d_h, double delta_w, double delta_c, const double* r,
+                            double* M, int64_t ldm, double* rhs_c, double* w_out, int32_t* status, void* stream) {
+  if (!P) return MDS_ERR_ARG;
+  const int64_t n_s = P->n_s, n_d = P->n_d, m = P->m_E + P->m_I, N = n_d + m;
+  if (N == 0) return MDS_OK;
+  if (!M || ldm < N) return MDS_ERR_ARG;
+  if (n_s > 0 && (!h_ss || !sigma_s || !w_out || (P->nnz > 0 && !js_val))) return MDS_ERR_ARG;
+  if (n_d > 0 && (!H_dd || ldh < n_d || !sigma_d)) return MDS_ERR_ARG;
+  if (n_d > 0 && m > 0 && (!J_d || ldj < m)) return MDS_ERR_ARG;
+  if (P->m_I > 0 && !d_h) return MDS_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (rhs_c && !r) rhs_c = nullptr;
+  if (n_s > 0) {
+    int64_t blocks = std::min<int64_t>(mds_cdiv(n_s, 256), 148 * 16);
+    k_condense_w<<<(unsigned)blocks, 256, 0, st>>>(n_s, h_ss, sigma_s, delta_w, w_out, status);
+    MDS_LAUNCH_CHECK();
+  }
+  if (n_d > 0) {
+    int64_t blocks = std::min<int64_t>(n_d, 148 * 8);
+    k_condense_dense<<<(unsigned)blocks, 256, 0, st>>>(n_d, m, H_dd, ldh, sigma_d, delta_w, J_d, ldj, M, ldm,
+                                                     r ? r + n_s : nullptr, rhs_c);
+    MDS_LAUNCH_CHECK();
+  }
+  if (m > 0) {
+    constexpr int WARPS = 4;
+    int64_t acc_len = std::min<int64_t>(((m + 31) / 32) * 32, 4096);
+    size_t smem = sizeof(double) * acc_len * WARPS;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(k_condense_yy<WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8 * WARPS);
+      attr_set = true;
+    }
+    int64_t blocks = mds_cdiv(m, WARPS);
+    k_condense_yy<WARPS><<<(unsigned)blocks, WARPS * 32, smem, st>>>(
+        n_d, P->m_E, m, acc_len, P->rowptr, P->colidx, js_val, P->tptr, P->tkp, w_out, d_h, delta_c,
+        r, n_s, M, ldm, rhs_c, status);
+    MDS_LAUNCH_CHECK();
+  }
+  return MDS_OK;
+}

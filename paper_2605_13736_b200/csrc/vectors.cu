@@ -1,0 +1,191 @@
+// vectors.cu — ipm_step_vectors: the barrier vector kernels (K1)
+// in ONE fused HBM pass: fraction-to-boundary min-reductions,
+// complementarity max/sum, residual inf-norms, optional barrier diagonal sigma.
+// Grid-stride over n with 128-bit loads; per-CTA partials reduced by the last
+// CTA to finish (deterministic fixed-order final reduction).  Bytes/element:
+// 8 inputs x 8 B (+8 B sigma write) — HBM-bound.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace {
+constexpr int VT = 256;             // threads per CTA
+constexpr int MAXRES = 8;
+constexpr int NPART = 6 + MAXRES;   // partial slots per CTA
+
+struct ResPtrs {
+  const double* p[MAXRES];
+  int64_t len[MAXRES];
+  int n;
+};
+
+struct Part {
+  double ap, ad, cinf, csum, nc;
+  long long bad;
+  double res[MAXRES];
+};
+
+__device__ __forceinline__ void elem(int64_t i, double x, double dx, double lo, double up, double zl, double zu,
+                                     double dzl, double dzu, double tau, double mu, Part& P, double* sigma) {
+  const bool hl = fabs(lo) < MDS_INF_BOUND, hu = fabs(up) < MDS_INF_BOUND;
+  double s = 0.0;
+  if (hl) {
+    const double gap = __dsub_rn(x, lo);
+    if (!(gap > 0.0) || !(zl > 0.0)) P.bad = min(P.bad, (long long)i);
+    if (dx < 0.0) P.ap = fmin(P.ap, __ddiv_rn(__dmul_rn(tau, gap), -dx));
+    if (dzl < 0.0) P.ad = fmin(P.ad, __ddiv_rn(__dmul_rn(tau, zl), -dzl));
+    const double c = __dmul_rn(gap, zl);
+    P.cinf = fmax(P.cinf, fabs(__dsub_rn(c, mu)));
+    P.csum += c;
+    P.nc += 1.0;
+    s = __dadd_rn(s, __ddiv_rn(zl, gap));
+  }
+  if (hu) {
+    const double gap = __dsub_rn(up, x);
+    if (!(gap > 0.0) || !(zu > 0.0)) P.bad = min(P.bad, (long long)i);
+    if (dx > 0.0) P.ap = fmin(P.ap, __ddiv_rn(__dmul_rn(tau, gap), dx));
+    if (dzu < 0.0) P.ad = fmin(P.ad, __ddiv_rn(__dmul_rn(tau, zu), -dzu));
+    const double c = __dmul_rn(gap, zu);
+    P.cinf = fmax(P.cinf, fabs(__dsub_rn(c, mu)));
+    P.csum += c;
+    P.nc += 1.0;
+    s = __dadd_rn(s, __ddiv_rn(zu, gap));
+  }
+  if (sigma) sigma[i] = s;
+}
+
+__global__ void __launch_bounds__(VT)
+k_step_vectors(int64_t n, const double* __restrict__ x, const double* __restrict__ dx,
+               const double* __restrict__ lo, const double* __restrict__ up,
+               const double* __restrict__ zl, const double* __restrict__ zu,
+               const double* __restrict__ dzl, const double* __restrict__ dzu,
+               double tau, double mu, ResPtrs R, double* __restrict__ out, double* __restrict__ sigma,
+               int32_t* status, double* __restrict__ partials, unsigned int* counter) {
+  Part P;
+  P.ap = 1.0; P.ad = 1.0; P.cinf = 0.0; P.csum = 0.0; P.nc = 0.0; P.bad = LLONG_MAX;
+#pragma unroll
+  for (int j = 0; j < MAXRES; j++) P.res[j] = 0.0;
+  const int64_t tid = blockIdx.x * (int64_t)VT + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * VT;
+  // pairs of elements with 128-bit loads when all arrays are 16-byte aligned
+  const bool al = ((((uintptr_t)x | (uintptr_t)dx | (uintptr_t)lo | (uintptr_t)up | (uintptr_t)zl | (uintptr_t)zu |
+                     (uintptr_t)dzl | (uintptr_t)dzu | (uintptr_t)sigma) & 15) == 0);
+  if (al) {
+    const int64_t n2 = n / 2;
+    for (int64_t t = tid; t < n2; t += nthr) {
+      double2 X = reinterpret_cast<const double2*>(x)[t], DX = reinterpret_cast<const double2*>(dx)[t];
+      double2 LO = reinterpret_cast<const double2*>(lo)[t], UP = reinterpret_cast<const double2*>(up)[t];
+      double2 ZL = reinterpret_cast<const double2*>(zl)[t], ZU = reinterpret_cast<const double2*>(zu)[t];
+      double2 DZL = reinterpret_cast<const double2*>(dzl)[t], DZU = reinterpret_cast<const double2*>(dzu)[t];
+      elem(2 * t, X.x, DX.x, LO.x, UP.x, ZL.x, ZU.x, DZL.x, DZU.x, tau, mu, P, sigma);
+      elem(2 * t + 1, X.y, DX.y, LO.y, UP.y, ZL.y, ZU.y, DZL.y, DZU.y, tau, mu, P, sigma);
+    }
+    if (tid == 0 && (n & 1)) {
+      int64_t i = n - 1;
+      elem(i, x[i], dx[i], lo[i], up[i], zl[i], zu[i], dzl[i], dzu[i], tau, mu, P, sigma);
+    }
+  } else {
+    for (int64_t i = tid; i < n; i += nthr)
+      elem(i, x[i], dx[i], lo[i], up[i], zl[i], zu[i], dzl[i], dzu[i], tau, mu, P, sigma);
+  }
+  for (int j = 0; j < R.n; j++) {
+    const double* v = R.p[j];
+    double mx = 0.0;
+    for (int64_t i = tid; i < R.len[j]; i += nthr) mx = fmax(mx, fabs(v[i]));
+    P.res[j] = mx;
+  }
+  // CTA reduction (fixed order)
+  __shared__ double sh[VT / 32][NPART];
+  __shared__ long long shb[VT / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double a0 = warp_min(P.ap), a1 = warp_min(P.ad), a2 = warp_max(P.cinf), a3 = warp_sum(P.csum), a4 = warp_sum(P.nc);
+  long long b = P.bad;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) b = min(b, (long long)__shfl_xor_sync(0xffffffffu, b, o));
+  double rr[MAXRES];
+#pragma unroll
+  for (int j = 0; j < MAXRES; j++) rr[j] = warp_max(P.res[j]);
+  if (lane == 0) {
+    sh[warp][0] = a0; sh[warp][1] = a1; sh[warp][2] = a2; sh[warp][3] = a3; sh[warp][4] = a4;
+    shb[warp] = b;
+#pragma unroll
+    for (int j = 0; j < MAXRES; j++) sh[warp][6 + j] = rr[j];
+  }
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    double q0 = sh[0][0], q1 = sh[0][1], q2 = sh[0][2], q3 = sh[0][3], q4 = sh[0][4];
+    long long qb = shb[0];
+    double qr[MAXRES];
+    for (int j = 0; j < MAXRES; j++) qr[j] = sh[0][6 + j];
+    for (int w = 1; w < VT / 32; w++) {
+      q0 = fmin(q0, sh[w][0]); q1 = fmin(q1, sh[w][1]); q2 = fmax(q2, sh[w][2]);
+      q3 += sh[w][3]; q4 += sh[w][4]; qb = min(qb, shb[w]);
+      for (int j = 0; j < MAXRES; j++) qr[j] = fmax(qr[j], sh[w][6 + j]);
+    }
+    double* my = partials + (size_t)blockIdx.x * NPART;
+    my[0] = q0; my[1] = q1; my[2] = q2; my[3] = q3; my[4] = q4;
+    my[5] = __longlong_as_double(qb);
+    for (int j = 0; j < MAXRES; j++) my[6 + j] = qr[j];
+    __threadfence();
+    unsigned prev = atomicAdd(counter, 1u);
+    last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  // last CTA: fixed-order reduction over CTA partials (deterministic)
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const volatile double* pp = partials;
+    double q0 = 1.0, q1 = 1.0, q2 = 0.0, q3 = 0.0, q4 = 0.0;
+    long long qb = LLONG_MAX;
+    double qr[MAXRES];
+    for (int j = 0; j < MAXRES; j++) qr[j] = 0.0;
+    for (unsigned c = 0; c < gridDim.x; c++) {
+      const volatile double* my = pp + (size_t)c * NPART;
+      q0 = fmin(q0, my[0]); q1 = fmin(q1, my[1]); q2 = fmax(q2, my[2]); q3 += my[3]; q4 += my[4];
+      qb = min(qb, __double_as_longlong(my[5]));
+      for (int j = 0; j < MAXRES; j++) qr[j] = fmax(qr[j], my[6 + j]);
+    }
+    out[0] = q0; out[1] = q1; out[2] = q2; out[3] = q3; out[4] = q4;
+    out[5] = (qb == LLONG_MAX) ? -1.0 : (double)qb;
+    for (int j = 0; j < R.n; j++) out[6 + j] = qr[j];
+    if (qb != LLONG_MAX) mds_set_status(status, MDS_ERR_NOT_INTERIOR);
+    *counter = 0u;   // leave the workspace reusable (graph replays)
+  }
+}
+
+int vec_grid(int64_t n) {
+  int64_t b = mds_cdiv(std::max<int64_t>(n, 1), 2 * VT * 4);
+  return (int)std::min<int64_t>(std::max<int64_t>(b, 1), 148 * 8);
+}
+}  // namespace
+
+extern "C" size_t ipm_step_vectors_workspace_size(int64_t n) {
+  return 256 + sizeof(double) * NPART * (size_t)vec_grid(n);
+}
+
+extern "C" int ipm_step_vectors(int64_t n, const double* x, const double* dx, const double* lo, const double* up,
+                                const double* zl, const double* zu, const double* dzl, const double* dzu,
+                                double tau, double mu, int32_t n_res, const double* const* res,
+                                const int64_t* res_len, double* out, double* sigma_out, int32_t* status,
+                                void* work, size_t work_bytes, void* stream) {
+  if (n < 0 || !out || n_res < 0 || n_res > MAXRES) return MDS_ERR_ARG;
+  if (n > 0 && (!x || !dx || !lo || !up || !zl || !zu || !dzl || !dzu)) return MDS_ERR_ARG;
+  if (n_res > 0 && (!res || !res_len)) return MDS_ERR_ARG;
+  if (!work || work_bytes < ipm_step_vectors_workspace_size(n)) return MDS_ERR_WORKSPACE;
+  ResPtrs R;
+  R.n = n_res;
+  for (int j = 0; j < MAXRES; j++) { R.p[j] = nullptr; R.len[j] = 0; }
+  for (int j = 0; j < n_res; j++) {
+    if (res_len[j] < 0 || (res_len[j] > 0 && !res[j])) return MDS_ERR_ARG;
+    R.p[j] = res[j]; R.len[j] = res_len[j];
+  }
+  unsigned int* counter = reinterpret_cast<unsigned int*>(work);
+  double* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(work) + 256);
+  int grid = vec_grid(n);
+  k_step_vectors<<<grid, VT, 0, (cudaStream_t)stream>>>(n, x, dx, lo, up, zl, zu, dzl, dzu, tau, mu, R, out,
+                                                         sigma_out, status, partials, counter);
+  MDS_LAUNCH_CHECK();
+  return MDS_OK;
+}

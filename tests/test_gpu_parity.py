@@ -1,0 +1,261 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle on the same
+seeded inputs.  Bars (BASELINE.json north_star):
+  inertia bit-exact; ||x_gpu - x_or||_inf/||x_or||_inf <= 1e-8; relative
+  residual ||M x - b||_inf/||b||_inf <= 1e-10 on well-conditioned inputs;
+  condensation M within 1e-13 (relative to ||M||_max), w bit-exact;
+  step vectors: alpha/compl_inf/sigma bit-exact, sums 1e-12."""
+import numpy as np
+import pytest
+
+import mdsgen
+import oracle
+from tests.helpers import rel_inf, sym_from_lower
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2605_13736_b200 as mds  # noqa: E402
+
+X_TOL = 1e-8
+RES_TOL = 1e-10
+
+
+def run_step(prob, sv=None, zero_tol=-1.0):
+    dp = mds.DeviceProblem(prob)
+    st = mds.KKTStep(dp, sv=sv, zero_tol=zero_tol)
+    st.run(sync_inertia=True)
+    torch.cuda.synchronize()
+    return st, st.results()
+
+
+def upload_dense(A):
+    """Run only the factor+solve on an arbitrary symmetric matrix (lower used)."""
+    N = A.shape[0]
+    ldm = N + (N % 2)
+    M = torch.zeros(ldm * N, dtype=torch.float64, device="cuda")
+    host = np.zeros((N, ldm))
+    host[:, :N] = np.asarray(A).T      # row j of host = column j of A
+    M.copy_(torch.from_numpy(host.reshape(-1)))
+    return M, ldm
+
+
+def factor_solve_dense(A, b, zero_tol=-1.0):
+    N = A.shape[0]
+    M, ldm = upload_dense(A)
+    piv = torch.empty(2 * N, dtype=torch.int32, device="cuda")
+    ine_d = torch.zeros(3, dtype=torch.int64, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    fwork = torch.empty(mds.factor_workspace_size(N), dtype=torch.uint8, device="cuda")
+    swork = torch.empty(mds.solve_workspace_size(N), dtype=torch.uint8, device="cuda")
+    ine = mds.factor(N, M, ldm, piv, zero_tol, ine_d, status, fwork, sync=True)
+    rhs = torch.as_tensor(b, dtype=torch.float64, device="cuda").contiguous()
+    x = torch.empty(N, dtype=torch.float64, device="cuda")
+    mds.solve(None, N, M, ldm, piv, rhs, None, None, None, x, None, zero_tol, fwork, status, swork)
+    torch.cuda.synchronize()
+    return ine, x.cpu().numpy(), int(status.item()), piv.cpu().numpy()
+
+
+def check_x(A, b, x, x_or):
+    As = sym_from_lower(A)
+    res = np.abs(As @ x - b).max() / np.abs(b).max()
+    assert res <= RES_TOL, res
+    assert rel_inf(x, x_or) <= X_TOL, rel_inf(x, x_or)
+
+
+# ---------------------------------------------------------------- condensation
+@pytest.mark.parametrize("shape,pattern,dw,dc", [
+    ((400, 20, 10, 10), "uniform", 0.0, 0.0),          # C1
+    ((3000, 70, 33, 40), "local", 0.01, 1e-8),          # several warps/chunks, ragged
+    ((20000, 150, 100, 157), "uniform", 0.0, 0.3),
+    ((5000, 0, 60, 70), "local", 0.0, 0.0),             # n_d = 0
+    ((4000, 50, 90, 0), "uniform", 0.0, 0.0),           # m_I = 0
+    ((0, 40, 10, 10), "uniform", 0.0, 0.0),             # n_s = 0
+])
+def test_condense_parity(shape, pattern, dw, dc):
+    prob = mdsgen.g1_quasidefinite(*shape, seed=sum(shape), pattern=pattern, delta_w=dw, delta_c=dc)
+    M_or, rhs_or, w_or = oracle.condense(prob)
+    dp = mds.DeviceProblem(prob)
+    st = mds.KKTStep(dp)
+    mds.condense(dp.plan, dp.val, dp.h_ss, dp.sigma_s, dp.H_dd, dp.ldh, dp.sigma_d, dp.J_d, dp.ldj, dp.d_h,
+                 dp.delta_w, dp.delta_c, dp.r, st.M, st.ldm, st.rhs, st.w, st.status)
+    torch.cuda.synchronize()
+    M = st.M_host()
+    scale = max(np.abs(np.tril(M_or)).max(), 1.0)
+    assert np.abs(np.tril(M) - np.tril(M_or)).max() <= 1e-13 * scale
+    np.testing.assert_array_equal(st.w[:prob.n_s].cpu().numpy(), w_or)
+    assert rel_inf(st.rhs[:prob.N].cpu().numpy(), rhs_or) <= 1e-13
+    assert int(st.status.item()) == 0
+
+
+def test_condense_nonpositive_status():
+    prob = mdsgen.g1_quasidefinite(500, 10, 5, 5, seed=2)
+    prob.h_ss = prob.h_ss.copy()
+    prob.h_ss[7] = -10.0
+    dp = mds.DeviceProblem(prob)
+    st = mds.KKTStep(dp)
+    mds.condense(dp.plan, dp.val, dp.h_ss, dp.sigma_s, dp.H_dd, dp.ldh, dp.sigma_d, dp.J_d, dp.ldj, dp.d_h,
+                 dp.delta_w, dp.delta_c, dp.r, st.M, st.ldm, st.rhs, st.w, st.status)
+    torch.cuda.synchronize()
+    assert int(st.status.item()) == mds.CompressionError.code
+
+
+def test_plan_rejects_bad_pattern():
+    prob = mdsgen.g1_quasidefinite(50, 4, 3, 3, seed=1)
+    ci = prob.colidx.copy()
+    k = int(np.argmax(np.diff(prob.rowptr) >= 2))
+    p = prob.rowptr[k]
+    ci[p], ci[p + 1] = ci[p + 1], ci[p]
+    with pytest.raises(mds.MalformedMatrixError):
+        mds.Plan(prob.n_s, prob.n_d, prob.m_E, prob.m_I, prob.rowptr, ci)
+
+
+# ---------------------------------------------------------------- factor + solve
+@pytest.mark.parametrize("shape", [(400, 20, 10, 10), (2000, 64, 40, 26), (6000, 200, 77, 56),
+                                   (30000, 300, 200, 223)])
+def test_full_step_parity_quasidefinite(shape):
+    prob = mdsgen.g1_quasidefinite(*shape, seed=11 + shape[1])
+    sv = mdsgen.step_vectors_for(prob, seed=5)
+    st, out = run_step(prob, sv=sv)
+    ref = oracle.newton_step(prob)
+    assert out["status"] == 0
+    assert out["inertia"] == ref["inertia"] == prob.expected_inertia
+    check_x(ref["M"], ref["rhs_c"], out["dxy"], ref["dxy"])
+    assert rel_inf(out["dx_s"], ref["dx_s"]) <= X_TOL
+    # step vectors on the oracle's own direction vs the GPU's: compare to oracle on the GPU direction
+    dx = np.concatenate([out["dx_s"], out["dxy"][:prob.n_d]])
+    s, v, sig = oracle.step_vectors(sv.x, dx, sv.lo, sv.up, sv.zl, sv.zu, sv.dzl, sv.dzu, sv.tau, sv.mu)
+    assert out["vec"]["alpha_p"] == v["alpha_p"]
+    assert out["vec"]["alpha_d"] == v["alpha_d"]
+    assert out["vec"]["compl_inf"] == v["compl_inf"]
+    assert abs(out["vec"]["compl_sum"] - v["compl_sum"]) <= 1e-12 * abs(v["compl_sum"])
+    assert out["vec"]["n_compl"] == v["n_compl"] and out["vec"]["first_bad"] == v["first_bad"] == -1
+    assert out["vec"]["res_inf"] == oracle.norm_inf(prob.r)
+    np.testing.assert_array_equal(out["sigma"], sig)
+
+
+def test_indefinite_inertia_parity():
+    prob = mdsgen.g2_indefinite(3000, 150, 60, 70, seed=5, p_neg=17)
+    st, out = run_step(prob)
+    ref = oracle.newton_step(prob)
+    assert out["inertia"] == ref["inertia"] == prob.expected_inertia
+    check_x(ref["M"], ref["rhs_c"], out["dxy"], ref["dxy"])
+
+
+@pytest.mark.parametrize("N,n2", [(70, 10), (200, 40), (333, 60), (700, 150)])
+def test_prescribed_spectrum_pivoting(N, n2):
+    # 2x2 pivots and interchanges across panel boundaries (slow path)
+    A, ine = mdsgen.g3_prescribed(N, seed=N + 1, n2x2=n2)
+    b = np.random.default_rng(N).standard_normal(N)
+    LD, ipiv, _ = oracle.bk_factor(A)
+    tol = oracle.default_tol(A)
+    x_or = oracle.bk_solve(LD, ipiv, b, tol)
+    g_ine, x, status, piv = factor_solve_dense(A, b)
+    assert status == 0
+    assert g_ine == oracle.inertia(LD, ipiv, tol) == ine
+    check_x(A, b, x, x_or)
+
+
+@pytest.mark.parametrize("N", [5, 63, 64, 65, 130, 257])
+def test_random_symmetric_shrunk_diag(N):
+    A = mdsgen.g4_random_symmetric(N, 3 * N, shrink_diag=True)
+    b = np.random.default_rng(N).standard_normal(N)
+    LD, ipiv, _ = oracle.bk_factor(A)
+    tol = oracle.default_tol(A)
+    x_or = oracle.bk_solve(LD, ipiv, b, tol)
+    g_ine, x, status, piv = factor_solve_dense(A, b)
+    assert g_ine == oracle.inertia(LD, ipiv, tol)
+    As = sym_from_lower(A)
+    # random symmetric matrices can be ill-conditioned: backward-error gate (R9)
+    res = np.abs(As @ x - b).max() / (np.abs(As).sum(1).max() * np.abs(x).max() + np.abs(b).max())
+    assert res <= 100 * N * np.finfo(float).eps
+    cond = np.linalg.cond(As)
+    assert rel_inf(x, x_or) <= max(X_TOL, 100 * N * np.finfo(float).eps * cond)
+
+
+def test_singular_zero_pivot():
+    prob = mdsgen.g5_singular(3000, 40, 30, 30, seed=4)
+    st, out = run_step(prob)
+    assert out["inertia"] == prob.expected_inertia
+    assert out["status"] == mds.SingularError.code
+
+
+def test_identity_and_small_examples():
+    for A, ine in [(np.eye(3), (3, 0, 0)), (np.diag([-1.0, -2.0]), (0, 0, 2)),
+                   (np.array([[0.0, 1.0], [1.0, 0.0]]), (1, 0, 1))]:
+        b = np.arange(1, A.shape[0] + 1, dtype=float)
+        g_ine, x, status, _ = factor_solve_dense(A, b)
+        assert g_ine == ine
+        np.testing.assert_allclose(sym_from_lower(A) @ x, b, rtol=0, atol=1e-15)
+
+
+def test_nonfinite_input():
+    A = mdsgen.g4_random_symmetric(100, 1)
+    A[50, 3] = np.inf
+    N = 100
+    M, ldm = upload_dense(A)
+    piv = torch.empty(2 * N, dtype=torch.int32, device="cuda")
+    ine_d = torch.zeros(3, dtype=torch.int64, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    fwork = torch.empty(mds.factor_workspace_size(N), dtype=torch.uint8, device="cuda")
+    mds.factor(N, M, ldm, piv, -1.0, ine_d, status, fwork, sync=True)
+    assert int(status.item()) == mds.NumericError.code
+
+
+# ---------------------------------------------------------------- step vectors
+@pytest.mark.parametrize("n", [1, 2, 31, 1000, 100001])
+def test_step_vectors_parity(n):
+    sv = mdsgen.step_vectors(n, seed=n)
+    d = lambda a: torch.as_tensor(a, dtype=torch.float64, device="cuda").contiguous()
+    out = torch.zeros(16, dtype=torch.float64, device="cuda")
+    sig = torch.empty(n, dtype=torch.float64, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    work = torch.zeros(mds.step_vectors_workspace_size(n), dtype=torch.uint8, device="cuda")
+    res = d(np.random.default_rng(1).standard_normal(n + 3))
+    for _ in range(2):   # workspace must be reusable
+        mds.step_vectors(n, d(sv.x), d(sv.dx), d(sv.lo), d(sv.up), d(sv.zl), d(sv.zu), d(sv.dzl), d(sv.dzu),
+                         sv.tau, sv.mu, out, sig, status, work, res=(res,))
+    torch.cuda.synchronize()
+    s, v, sg = oracle.step_vectors(sv.x, sv.dx, sv.lo, sv.up, sv.zl, sv.zu, sv.dzl, sv.dzu, sv.tau, sv.mu)
+    o = out.cpu().numpy()
+    assert o[0] == v["alpha_p"] and o[1] == v["alpha_d"] and o[2] == v["compl_inf"]
+    assert abs(o[3] - v["compl_sum"]) <= 1e-12 * max(abs(v["compl_sum"]), 1e-300)
+    assert int(o[4]) == v["n_compl"] and int(o[5]) == v["first_bad"] == -1
+    assert o[6] == np.abs(res.cpu().numpy()).max()
+    np.testing.assert_array_equal(sig.cpu().numpy(), sg)
+    assert int(status.item()) == 0
+
+
+def test_step_vectors_not_interior():
+    sv = mdsgen.step_vectors(5000, seed=3)
+    x = sv.x.copy()
+    fin = np.where(np.abs(sv.lo) < 1e20)[0]
+    x[fin[10]] = sv.lo[fin[10]] - 1.0
+    d = lambda a: torch.as_tensor(a, dtype=torch.float64, device="cuda").contiguous()
+    out = torch.zeros(16, dtype=torch.float64, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    work = torch.zeros(mds.step_vectors_workspace_size(5000), dtype=torch.uint8, device="cuda")
+    mds.step_vectors(5000, d(x), d(sv.dx), d(sv.lo), d(sv.up), d(sv.zl), d(sv.zu), d(sv.dzl), d(sv.dzu),
+                     sv.tau, sv.mu, out, None, status, work)
+    torch.cuda.synchronize()
+    s, v, _ = oracle.step_vectors(x, sv.dx, sv.lo, sv.up, sv.zl, sv.zu, sv.dzl, sv.dzu, sv.tau, sv.mu)
+    assert int(out[5].item()) == v["first_bad"] == fin[10]
+    assert int(status.item()) == mds.NotInteriorError.code
+
+
+# ---------------------------------------------------------------- graph capture
+def test_graph_replay_matches_eager():
+    prob = mdsgen.g1_quasidefinite(5000, 100, 50, 50, seed=8)
+    sv = mdsgen.step_vectors_for(prob, seed=2)
+    dp = mds.DeviceProblem(prob)
+    st = mds.KKTStep(dp, sv=sv)
+    st.run()
+    eager = st.results()
+    g = st.capture()
+    g.replay()
+    rep = st.results()
+    assert rep["inertia"] == eager["inertia"]
+    np.testing.assert_array_equal(rep["dxy"], eager["dxy"])
+    np.testing.assert_array_equal(rep["dx_s"], eager["dx_s"])

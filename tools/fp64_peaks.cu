@@ -87,7 +87,7 @@ double run(K kern, int blocks, int threads, int iters, double flops_per_thread_i
 
 int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  int it = 20000;
+  int it = 2000;
   // m8n8k4: 2*8*8*4 = 512 flop per warp instr -> 16 per thread per mma
   run(dmma_loop<4>, sms * 4, 256, it, 4 * 16.0, "dmma_m8n8k4_c4_occ4x256");
   run(dmma_loop<8>, sms * 4, 256, it, 8 * 16.0, "dmma_m8n8k4_c8_occ4x256");

@@ -23,16 +23,20 @@ def dgemm(n=8192, seconds=4.0):
     return burst, sust
 
 if __name__ == "__main__":
+    os.makedirs("gpurun_out", exist_ok=True)
     out = {}
-    clk = subprocess.Popen("nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active --format=csv,noheader -lms 200", shell=True, stdout=subprocess.PIPE, text=True)
+    clk_log = open("gpurun_out/fp64_clocks.csv", "w")
+    clk = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
+                            "--format=csv,noheader", "-lms", "200"], stdout=clk_log, text=True)
     b, s = dgemm()
     out["cublas_dgemm_8192_burst_tflops"] = b
     out["cublas_dgemm_8192_sustained_tflops"] = s
     r = subprocess.run([os.path.join(os.path.dirname(__file__), "fp64_peaks")], capture_output=True, text=True)
     out["micro"] = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
-    clk.terminate()
-    lines = clk.stdout.read().splitlines()
-    out["clock_samples"] = lines[-40:]
+    clk.kill()
+    clk.wait()
+    clk_log.close()
+    out["clock_samples"] = open("gpurun_out/fp64_clocks.csv").read().splitlines()[-40:]
     print(json.dumps(out, indent=1))
     os.makedirs("gpurun_out", exist_ok=True)
     json.dump(out, open("gpurun_out/fp64_peaks.json", "w"), indent=1)
