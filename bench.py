@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""bench.py — one Newton step of the condensed-KKT hot path (§2:
+condense Eq.(5)->(6), Bunch-Kaufman LDL^T with inertia, solves + dx_s
+recovery, barrier vector kernels) on synthetic OPF-shaped MDS inputs.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+N=1 workload: BASELINE.json configs[2] "C3" (ACOPF-shaped, n_d+m = 8192,
+n_s = 1M) — the config the north star's FP64 target (N >= 8192) is quoted on.
+Multi-GPU (torchrun): C3 is one KKT system per Newton step and does not shard
+(BK needs a global pivot search per column), so ranks run independent
+replicas; value = steps of all ranks / max-rank time.
+
+--impl reference: the CPU oracle (oracle/, plain C, single thread) on a
+bounded sample of the same workload, extrapolated to the full step (see
+cpu_baseline.sample in the JSON line).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "condensed-KKT factor+solve/s, FP64 TFLOP/s vs peak; Newton iters/s"
+UNIT = "newton_iters/s"
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-sample", type=int, default=1536, help="oracle factor sample size (leading block)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            self.p.kill()
+            self.p.wait()
+        self.f.flush()
+
+    def summary(self):
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 7:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def fp64_peak():
+    try:
+        d = json.load(open(FP64_PEAK_FILE))
+        dm = max(m["tflops"] for m in d["micro"] if m["kernel"].startswith("dmma"))
+        return dm, d.get("cublas_dgemm_8192_burst_tflops")
+    except Exception:
+        return 37.2, None
+
+
+def measured_hbm():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def algorithmic(prob, panels):
+    """Algorithmic work of one step at this instance."""
+    n_s, n_d, m, nnz, N = prob.n_s, prob.n_d, prob.m, prob.nnz, prob.N
+    condense_bytes = (12 * nnz + 4 * (n_s + 1) + 16 * n_s + 8 * n_d * (n_d + 1) // 2 + 8 * m * n_d + 8 * n_d
+                      + 8 * prob.m_I + 8 * (n_s + N) + 8 * N + 8 * N * (N + 1) // 2 + 8 * n_s)
+    # trailing-update flops from the actual panel boundaries: sum n2 (n2+1) kb
+    upd = 0
+    ends = list(panels[1:]) + [N]
+    for s, e in zip(panels, ends):
+        n2 = int(N) - int(e)
+        upd += n2 * (n2 + 1) * (int(e) - int(s))
+    factor_flops = N ** 3 / 3.0
+    solve_flops = 2.0 * N * N
+    solve_bytes = 8 * N * N + 8 * 6 * N + 12 * nnz + 40 * n_s
+    return dict(condense_bytes=condense_bytes, update_flops=float(upd), factor_flops=factor_flops,
+                solve_flops=solve_flops, solve_bytes=solve_bytes)
+
+
+# ----------------------------------------------------------------------------- CPU oracle sample
+def oracle_sample(prob, sv, ns_factor, reps=1):
+    """Time the oracle on a bounded sample of one step; returns (projected s/step, detail)."""
+    import oracle
+    t0 = time.perf_counter()
+    M, rhs, w = oracle.condense(prob)
+    t_cond = time.perf_counter() - t0
+    N = M.shape[0]
+    ns = min(ns_factor, N)
+    A = np.asfortranarray(M[:ns, :ns])
+    t0 = time.perf_counter()
+    LD, ipiv, _ = oracle.bk_factor(A)
+    t_fac = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    tol = oracle.default_tol(A)
+    x = oracle.bk_solve(LD, ipiv, rhs[:ns], tol)
+    t_sol = time.perf_counter() - t0
+    dy = np.zeros(prob.m)
+    t0 = time.perf_counter()
+    dxs = oracle.recover(prob, w, prob.r[:prob.n_s], dy)
+    dx = np.concatenate([dxs, np.zeros(prob.n_d)])
+    oracle.step_vectors(sv.x, dx, sv.lo, sv.up, sv.zl, sv.zu, sv.dzl, sv.dzu, sv.tau, sv.mu)
+    oracle.norm_inf(prob.r)
+    t_vec = time.perf_counter() - t0
+    scale3 = (N / ns) ** 3
+    scale2 = (N / ns) ** 2
+    proj = t_cond + t_fac * scale3 + t_sol * scale2 + t_vec
+    sample = (f"oracle (plain C, 1 thread) on the full {N}x{N} condensation + recovery + step vectors, and BK "
+              f"factor+solve of the leading {ns}x{ns} block of M, extrapolated x(N/{ns})^3 (factor) and x(N/{ns})^2 "
+              f"(solve); measured {t_cond + t_fac + t_sol + t_vec:.2f} s of CPU work")
+    return proj, dict(t_condense=t_cond, t_factor_sample=t_fac, t_solve_sample=t_sol, t_vec=t_vec, ns=ns,
+                      sample=sample)
+
+
+def run_reference(args, rank, world):
+    import mdsgen
+    if rank != 0:
+        return
+    prob = mdsgen.config_problem(args.config)
+    sv = mdsgen.step_vectors_for(prob, seed=7)
+    for _ in range(args.warmup):
+        oracle_sample(prob, sv, min(args.ref_sample, 512))
+    projs = []
+    wall0 = time.perf_counter()
+    det = None
+    for _ in range(args.steps):
+        p, det = oracle_sample(prob, sv, args.ref_sample)
+        projs.append(p)
+    wall = time.perf_counter() - wall0
+    t_step = float(np.mean(projs))
+    val = 1.0 / t_step
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} " + CONFIG_DESC[args.config], "N": prob.N, "n_s": prob.n_s,
+                       "nnz": prob.nnz},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": det["sample"]},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": wall}
+    print(json.dumps(line), flush=True)
+
+
+CONFIG_DESC = {
+    "C1": "toy MDS n_s=400, n_d=20, m=20 (N=40), one Newton step",
+    "C2": "synthetic MDS N=n_d+m=1024, n_s=100k, CSR J_s ~5 nnz/row, one Newton step",
+    "C3": "ACOPF-shaped MDS N=n_d+m=8192 (n_d=4096, m_E=m_I=2048), n_s=1M, ~5 nnz/row, one Newton step",
+    "C4": "SCOPF scenario N=2048, n_s=131072 (single scenario)",
+}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_ours(args, rank, world):
+    import torch
+    import torch.distributed as dist
+
+    import mdsgen
+    import paper_2605_13736_b200 as mds
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    prob = mdsgen.config_problem(args.config)
+    sv = mdsgen.step_vectors_for(prob, seed=7)
+    dp = mds.DeviceProblem(prob)
+    st = mds.KKTStep(dp, sv=sv)
+    launches0 = mds.launch_count()
+    st.run()
+    torch.cuda.synchronize()
+    launches_per_step = mds.launch_count() - launches0
+    out0 = st.results()
+    if out0["status"] != 0 or out0["inertia"] != prob.expected_inertia:
+        raise SystemExit(f"bench: step failed status={out0['status']} inertia={out0['inertia']}")
+    panels = mds.factor_panels(st.fwork, prob.N)
+    alg = algorithmic(prob, panels)
+
+    use_graph = not args.no_graph
+    graph = st.capture() if use_graph else None
+    stream = torch.cuda.current_stream()
+
+    def step():
+        if graph is not None:
+            graph.replay()
+        else:
+            st.run()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = e0.elapsed_time(e1)
+    clocks = clk.summary()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = world * args.steps / (ms_max / 1e3)
+
+    # profiled eager pass: per-kernel-class device time (CUDA events on the launch stream)
+    mds.profile_begin()
+    st.run()
+    prof = mds.profile_end()
+    st.check_status()
+    tot = sum(v[0] for v in prof.values())
+    fac_ms = sum(prof[c][0] for c in ("anorm", "panel_diag", "panel_trsm", "panel_accept", "panel_slow", "update",
+                                      "finalize"))
+    sol_ms = sum(prof[c][0] for c in ("solve_gather", "solve_fwd", "solve_d", "solve_bwd", "solve_scatter",
+                                      "recover"))
+    cond_ms = sum(prof[c][0] for c in ("condense_w", "condense_dense", "condense_yy"))
+    dom = max(prof, key=lambda c: prof[c][0])
+    peak_dmma, peak_cublas = fp64_peak()
+    hbm, hbm_src = measured_hbm()
+    upd_ms, upd_n = prof["update"]
+    if dom == "update":
+        ach = alg["update_flops"] / (upd_ms * 1e-3) / 1e12
+        roof = {"kernel": "k_update (DMMA trailing update)", "bound": "tensor", "achieved": ach, "peak": peak_dmma,
+                "unit": "TFLOP/s", "frac": ach / peak_dmma, "traffic": None,
+                "peak_source": "measured FP64 DMMA ceiling, profiles/fp64_peaks_r01.json (cuBLAS DGEMM "
+                               f"{peak_cublas:.2f} TF/s); MEASURED_PEAKS.json has no FP64 entry",
+                "launches": upd_n, "avg_launch_us": upd_ms * 1e3 / max(upd_n, 1)}
+    else:
+        roof = {"kernel": dom, "bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None,
+                "traffic": None, "launches": prof[dom][1], "ms": prof[dom][0]}
+    kern = {c: {"ms": round(v[0], 4), "launches": v[1], "share": round(v[0] / tot, 4) if tot else 0}
+            for c, v in prof.items() if v[1]}
+
+    # end-to-end through the public API with HOST buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        ins = [dp.val, dp.h_ss, dp.sigma_s, dp.H_dd, dp.sigma_d, dp.J_d, dp.d_h, dp.r]
+        host = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t.cpu()) for t in ins]
+        outs = [st.dxy, st.dirn[:prob.n_s], st.inertia, st.vout]
+        hout = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in outs]
+        h2d = sum(t.numel() * t.element_size() for t in host)
+        d2h = sum(t.numel() * t.element_size() for t in hout)
+
+        def e2e_step():
+            for d_, h_ in zip(ins, host):
+                d_.copy_(h_, non_blocking=True)
+            step()
+            for h_, d_ in zip(hout, outs):
+                h_.copy_(d_, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * args.steps / (float(te.item()) / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        proj, det = oracle_sample(prob, sv, args.ref_sample)
+        cpu = {"value": 1.0 / proj, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": det["sample"]}
+
+    if rank == 0:
+        fs_ms = fac_ms + sol_ms
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"{args.config} " + CONFIG_DESC[args.config], "N": prob.N, "n_s": prob.n_s,
+                           "nnz": prob.nnz, "parallelism": f"replicas{world}" if world > 1 else "single",
+                           "l2": "inputs larger than L2 (M alone is %.0f MB)" % (8 * prob.N * prob.N / 1e6),
+                           "cuda_graph": use_graph},
+                "gpu_launches": launches_per_step * args.steps,
+                "roofline": roof,
+                "factor_solve_per_s": 1e3 / fs_ms,
+                "factor_solve_fp64_tflops": (alg["factor_flops"] + alg["solve_flops"]) / (fs_ms * 1e-3) / 1e12,
+                "factor_fp64_frac_of_peak": alg["factor_flops"] / (fac_ms * 1e-3) / 1e12 / peak_dmma,
+                "condense_gbs": alg["condense_bytes"] / (cond_ms * 1e-3) / 1e9,
+                "condense_frac_of_hbm": alg["condense_bytes"] / (cond_ms * 1e-3) / 1e9 / hbm,
+                "hbm_peak_gbs": hbm, "hbm_peak_source": hbm_src,
+                "phase_ms": {"condense": cond_ms, "factor": fac_ms, "solve": sol_ms,
+                             "vectors": prof["vectors"][0]},
+                "kernels": kern, "panels": int(len(panels)),
+                "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
+                "inertia": list(out0["inertia"])}
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        pass
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    run_ours(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -170,6 +170,28 @@ int ipm_step_vectors(int64_t n, const double *x, const double *dx, const double 
                      double *out, double *sigma_out, int32_t *status_dev,
                      void *work, size_t work_bytes, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Instrumentation (not on the hot path; used by bench.py for the roofline).
+ * mds_launch_count: number of kernels this library has launched since load.
+ * mds_profile_begin / mds_profile_end: while enabled, every kernel launch of
+ * the four calls above is bracketed by CUDA events recorded on its own stream;
+ * mds_profile_end synchronises those events and returns, per kernel class
+ * (MDS_PROF_* below, ncls >= MDS_PROF_COUNT), the summed duration in ms and
+ * the launch count.  Never enable while capturing a CUDA graph.
+ * mds_factor_panels: after mds_factor, copies the first column of every panel
+ * into starts_host[cap] (synchronous) and returns the number of panels, so
+ * the caller can compute the trailing update's algorithmic flops exactly. */
+enum {
+    MDS_PROF_CONDENSE_W = 0, MDS_PROF_CONDENSE_DENSE, MDS_PROF_CONDENSE_YY, MDS_PROF_ANORM,
+    MDS_PROF_PANEL_DIAG, MDS_PROF_PANEL_TRSM, MDS_PROF_PANEL_ACCEPT, MDS_PROF_PANEL_SLOW, MDS_PROF_UPDATE,
+    MDS_PROF_FINALIZE, MDS_PROF_SOLVE_GATHER, MDS_PROF_SOLVE_FWD, MDS_PROF_SOLVE_D, MDS_PROF_SOLVE_BWD,
+    MDS_PROF_SOLVE_SCATTER, MDS_PROF_RECOVER, MDS_PROF_VECTORS, MDS_PROF_COUNT
+};
+unsigned long long mds_launch_count(void);
+int mds_profile_begin(void);
+int mds_profile_end(double *ms_by_class, int64_t *launches_by_class, int ncls);
+int64_t mds_factor_panels(const void *fwork, int64_t N, int32_t *starts_host, int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

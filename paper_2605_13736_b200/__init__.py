@@ -43,13 +43,24 @@ _lib.ipm_step_vectors_workspace_size.restype = ctypes.c_size_t
 _lib.ipm_step_vectors_workspace_size.argtypes = [_I64]
 _lib.ipm_step_vectors.argtypes = [_I64, _P, _P, _P, _P, _P, _P, _P, _P, _D, _D, _I32, _P, _P, _P, _P, _P, _P,
                                   ctypes.c_size_t, _P]
+_lib.mds_launch_count.restype = ctypes.c_ulonglong
+_lib.mds_profile_begin.restype = ctypes.c_int
+_lib.mds_profile_end.restype = ctypes.c_int
+_lib.mds_profile_end.argtypes = [_P, _P, ctypes.c_int]
+_lib.mds_factor_panels.restype = ctypes.c_int64
+_lib.mds_factor_panels.argtypes = [_P, _I64, _P, _I64]
 for _f in ("mds_plan_create", "mds_plan_destroy", "mds_plan_dims", "mds_condense", "mds_factor", "mds_solve",
            "ipm_step_vectors"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 EXPORTS = ["mds_version", "mds_plan_create", "mds_plan_destroy", "mds_plan_dims", "mds_condense",
            "mds_factor_workspace_size", "mds_factor", "mds_solve_workspace_size", "mds_solve",
-           "ipm_step_vectors_workspace_size", "ipm_step_vectors"]
+           "ipm_step_vectors_workspace_size", "ipm_step_vectors", "mds_launch_count", "mds_profile_begin",
+           "mds_profile_end", "mds_factor_panels"]
+
+PROF_CLASSES = ["condense_w", "condense_dense", "condense_yy", "anorm", "panel_diag", "panel_trsm", "panel_accept",
+                "panel_slow", "update", "finalize", "solve_gather", "solve_fwd", "solve_d", "solve_bwd",
+                "solve_scatter", "recover", "vectors"]
 
 
 def version() -> str:
@@ -178,6 +189,35 @@ def step_vectors(n, x, dx, lo, up, zl, zu, dzl, dzu, tau, mu, out, sigma_out, st
                                  _f64(dzu), float(tau), float(mu), nres, arr_p, arr_l, _f64(out), _f64(sigma_out),
                                  _ptr(status), _ptr(work), work.numel() * work.element_size(), _stream(stream))
     _check(code, "ipm_step_vectors")
+
+
+def launch_count() -> int:
+    """Kernels launched by the library since load (the bench's gpu_launches evidence)."""
+    return int(_lib.mds_launch_count())
+
+
+def profile_begin():
+    _check(_lib.mds_profile_begin(), "mds_profile_begin")
+
+
+def profile_end():
+    """-> {class: (ms_total, launches)} for the kernels launched since profile_begin()."""
+    import numpy as np
+    n = len(PROF_CLASSES)
+    ms = np.zeros(n)
+    cnt = np.zeros(n, dtype=np.int64)
+    _check(_lib.mds_profile_end(ms.ctypes.data, cnt.ctypes.data, n), "mds_profile_end")
+    return {c: (float(ms[i]), int(cnt[i])) for i, c in enumerate(PROF_CLASSES)}
+
+
+def factor_panels(fwork, N):
+    """Panel start columns of the last mds_factor that used `fwork` (synchronous)."""
+    import numpy as np
+    buf = np.zeros(N + 1, dtype=np.int32)
+    n = int(_lib.mds_factor_panels(_ptr(fwork), int(N), buf.ctypes.data, N + 1))
+    if n < 0:
+        raise_for(n, "mds_factor_panels")
+    return buf[:n].copy()
 
 
 from .step import KKTStep, DeviceProblem  # noqa: E402,F401

@@ -39,6 +39,7 @@ extern "C" int mds_plan_create(int64_t n_s, int64_t n_d, int64_t m_E, int64_t m_
   int64_t nnz = n_s > 0 ? rowptr[n_s] : 0;
   if (n_s > 0 && rowptr[0] != 0) return MDS_ERR_PATTERN;
   if (nnz > 0 && !colidx) return MDS_ERR_ARG;
+  if (nnz >= ((int64_t)1 << 27)) return MDS_ERR_ARG;   // packed transpose map limit
   // validate canonical CSR (reading R13): sorted, unique, in range
   for (int64_t k = 0; k < n_s; k++) {
     if (rowptr[k + 1] < rowptr[k]) return MDS_ERR_PATTERN;
@@ -55,7 +56,11 @@ extern "C" int mds_plan_create(int64_t n_s, int64_t n_d, int64_t m_E, int64_t m_
   {
     std::vector<int32_t> fill(tptr.begin(), tptr.end() - 1);
     for (int64_t k = 0; k < n_s; k++)
-      for (int64_t p = rowptr[k]; p < rowptr[k + 1]; p++) tkp[fill[colidx[p]]++] = make_int2((int)k, (int)p);
+      for (int64_t p = rowptr[k]; p < rowptr[k + 1]; p++) {
+        // y = p | min(suffix length, 31) << 27  (31 = "look up rowptr")
+        const unsigned sl = (unsigned)std::min<int64_t>(rowptr[k + 1] - p, 31);
+        tkp[fill[colidx[p]]++] = make_int2((int)k, (int)((unsigned)p | (sl << 27)));
+      }
   }
   int32_t maxlen = 0;
   for (int64_t c = 0; c < m; c++) maxlen = std::max(maxlen, tptr[c + 1] - tptr[c]);
@@ -134,11 +139,21 @@ __global__ void k_condense_dense(int64_t n_d, int64_t m, const double* __restric
   }
 }
 
-// M_yy column c (rows c..m-1 of the (y,y) block), one warp per column.
-// acc[i] holds M_yy[c+i, c] for i in [0, m-c).  Column order is folded
-// (c, m-1-c) so CTAs get balanced work.
+// M_yy column c (rows c..m-1 of the (y,y) block).  One WARP owns output
+// column c (and its fold partner m-1-c, so every warp does equal work) and
+// accumulates -sum_k w_k J[k,c] J[k,c1] (c1 >= c) in a private shared-memory
+// column; the column is then written once, coalesced.  Per iteration each lane
+// takes U list entries (k, p, suffix length) of the constraint-major transpose
+// and issues all their gathers at once (latency-bound on L2 otherwise).  The
+// diagonal term (s = 0, every lane hits it) is a warp sum; off-diagonal lanes
+// that collide on the same c1 are serialised via __match_any_sync (no FP64
+// shared-memory atomics, which are CAS loops on sm_100a).  Deterministic.
+constexpr int YY_U = 2;      // list entries per lane per iteration
+constexpr int YY_SMAX = 8;   // suffix entries gathered up front (longer suffixes take a slow loop)
+constexpr unsigned TKP_PMASK = (1u << 27) - 1u;
+
 template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
+__global__ void __launch_bounds__(WARPS * 32, 1)
 k_condense_yy(int64_t n_d, int64_t m_E, int64_t m, int64_t acc_len,
               const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
               const double* __restrict__ val, const int32_t* __restrict__ tptr, const int2* __restrict__ tkp,
@@ -148,83 +163,128 @@ k_condense_yy(int64_t n_d, int64_t m_E, int64_t m, int64_t acc_len,
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* acc = smem + (size_t)warp * acc_len;
-  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
-  if (gw >= m) return;
-  const int64_t c = (gw & 1) ? (m - 1 - (gw >> 1)) : (gw >> 1);
-  const int64_t len = m - c;
+  const int64_t task = (int64_t)blockIdx.x * WARPS + warp;
+  const int64_t ntask = (m + 1) / 2;
+  if (task >= ntask) return;
   const unsigned lanemask_lt = (1u << lane) - 1u;
-  const double* r_xs = r;                       // may be NULL
-  double rsum = 0.0;
-  // process the column in chunks of acc_len rows (one chunk when m <= acc_len)
-  for (int64_t base = 0; base < len; base += acc_len) {
-    const int64_t clen = (len - base < acc_len) ? (len - base) : acc_len;
-    for (int64_t i = lane; i < clen; i += 32) acc[i] = 0.0;
-    __syncwarp();
+  for (int half = 0; half < 2; half++) {
+    const int64_t c = half ? (m - 1 - task) : task;
+    if (half && c == task) break;
+    const int64_t len = m - c;
+    double rsum = 0.0;
     const int32_t e0 = tptr[c], e1 = tptr[c + 1];
-    for (int32_t e = e0; e < e1; e += 32) {
-      const int32_t my = e + lane;
-      const bool act = my < e1;
-      int k = 0, p = 0, pend = 0;
-      double t = 0.0;
-      if (act) {
-        int2 kp = tkp[my];
-        k = kp.x; p = kp.y;
-        pend = rowptr[k + 1];
-        const double wk = w[k];
-        const double v = val[p];
-        t = v * wk;
-        if (base == 0 && r_xs) rsum += t * r_xs[k];
-      }
-      // walk the row suffix p..pend-1 (entries with c1 >= c, sorted ascending)
-      int q = p;
-      while (__any_sync(0xffffffffu, act && q < pend)) {
-        const bool live = act && q < pend;
-        int64_t c1 = -1;
-        double upd = 0.0;
-        if (live) {
-          c1 = (int64_t)colidx[q] - c - base;
-          upd = t * val[q];
-          if (c1 < 0 || c1 >= clen) c1 = -1;   // outside this chunk
-        }
-        const bool go = c1 >= 0;
-        const unsigned gomask = __ballot_sync(0xffffffffu, go);
-        if (go) {
-          const unsigned peers = __match_any_sync(gomask, (int)c1);
-          if (peers == (1u << lane)) {
-            acc[c1] -= upd;
-          } else {
-            const int rank = __popc(peers & lanemask_lt);
-            const int gs = __popc(peers);
-            for (int s = 0; s < gs; s++) {
-              if (rank == s) acc[c1] -= upd;
-              __syncwarp(peers);
-            }
+    for (int64_t base = 0; base < len; base += acc_len) {
+      const int64_t clen = (len - base < acc_len) ? (len - base) : acc_len;
+      for (int64_t i = lane; i < clen; i += 32) acc[i] = 0.0;
+      __syncwarp();
+      double diag = 0.0;
+      for (int32_t e = e0; e < e1; e += 32 * YY_U) {
+        int kk[YY_U], pp[YY_U], ln[YY_U];
+        double tt[YY_U];
+        int cs[YY_U][YY_SMAX];
+        double vs[YY_U][YY_SMAX];
+#pragma unroll
+        for (int u = 0; u < YY_U; u++) {
+          const int32_t my = e + u * 32 + lane;
+          ln[u] = 0; kk[u] = 0; pp[u] = 0;
+          if (my < e1) {
+            const int2 kp = tkp[my];
+            kk[u] = kp.x;
+            pp[u] = (int)((unsigned)kp.y & TKP_PMASK);
+            ln[u] = (int)((unsigned)kp.y >> 27);
+            if (ln[u] == 31) ln[u] = rowptr[kk[u] + 1] - pp[u];
           }
         }
-        __syncwarp();
-        if (live) q++;
-      }
-    }
-    __syncwarp();
-    // diagonal terms -diag(0_{m_E}, 1/d_h) - delta_c I, then one coalesced column write
-    double* Mc = M + (n_d + c) * ldm + n_d + c + base;
-    for (int64_t i = lane; i < clen; i += 32) {
-      double v = acc[i];
-      if (base + i == 0) {
-        v = v - delta_c;
-        if (c >= m_E) {
-          double dh = d_h[c - m_E];
-          if (!(dh > 0.0)) mds_set_status(status, MDS_ERR_NONPOSITIVE);
-          v = v - 1.0 / dh;
+#pragma unroll
+        for (int u = 0; u < YY_U; u++) {
+#pragma unroll
+          for (int s = 0; s < YY_SMAX; s++) {
+            cs[u][s] = -1;
+            vs[u][s] = 0.0;
+            if (s < ln[u]) { cs[u][s] = colidx[pp[u] + s]; vs[u][s] = val[pp[u] + s]; }
+          }
+          const double wk = (ln[u] > 0) ? w[kk[u]] : 0.0;
+          tt[u] = vs[u][0] * wk;
+          if (base == 0 && r && ln[u] > 0) rsum += tt[u] * r[kk[u]];
+        }
+        // s = 0: the diagonal (c1 == c) -- every lane hits it: warp sum, no scatter
+#pragma unroll
+        for (int u = 0; u < YY_U; u++) diag += tt[u] * vs[u][0];
+        // s >= 1: off-diagonal scatter into the private column
+#pragma unroll
+        for (int u = 0; u < YY_U; u++) {
+#pragma unroll
+          for (int s = 1; s < YY_SMAX; s++) {
+            int64_t c1 = -1;
+            if (s < ln[u]) {
+              c1 = (int64_t)cs[u][s] - c - base;
+              if (c1 < 0 || c1 >= clen) c1 = -1;
+            }
+            const bool go = c1 >= 0;
+            const unsigned gomask = __ballot_sync(0xffffffffu, go);
+            if (gomask == 0u) continue;
+            const double upd = tt[u] * vs[u][s];
+            if (go) {
+              const unsigned peers = __match_any_sync(gomask, (int)c1);
+              if (peers == (1u << lane)) {
+                acc[c1] -= upd;
+              } else {
+                const int rank = __popc(peers & lanemask_lt);
+                const int gs = __popc(peers);
+                for (int q = 0; q < gs; q++) {
+                  if (rank == q) acc[c1] -= upd;
+                  __syncwarp(peers);
+                }
+              }
+            }
+            __syncwarp();
+          }
+          // rare: suffix longer than YY_SMAX
+          for (int s = YY_SMAX; __any_sync(0xffffffffu, s < ln[u]); s++) {
+            int64_t c1 = -1;
+            double upd = 0.0;
+            if (s < ln[u]) {
+              c1 = (int64_t)colidx[pp[u] + s] - c - base;
+              upd = tt[u] * val[pp[u] + s];
+              if (c1 < 0 || c1 >= clen) c1 = -1;
+            }
+            const bool go = c1 >= 0;
+            const unsigned gomask = __ballot_sync(0xffffffffu, go);
+            if (go) {
+              const unsigned peers = __match_any_sync(gomask, (int)c1);
+              const int rank = __popc(peers & lanemask_lt);
+              const int gs = __popc(peers);
+              for (int q = 0; q < gs; q++) {
+                if (rank == q) acc[c1] -= upd;
+                __syncwarp(peers);
+              }
+            }
+            __syncwarp();
+          }
         }
       }
-      Mc[i] = v;
+      diag = warp_sum(diag);
+      __syncwarp();
+      // diagonal terms -diag(0_{m_E}, 1/d_h) - delta_c I, then one coalesced column write
+      double* Mc = M + (n_d + c) * ldm + n_d + c + base;
+      for (int64_t i = lane; i < clen; i += 32) {
+        double v = acc[i];
+        if (base + i == 0) {
+          v = -diag - delta_c;
+          if (c >= m_E) {
+            const double dh = d_h[c - m_E];
+            if (!(dh > 0.0)) mds_set_status(status, MDS_ERR_NONPOSITIVE);
+            v = v - 1.0 / dh;
+          }
+        }
+        Mc[i] = v;
+      }
+      __syncwarp();
     }
-    __syncwarp();
-  }
-  if (rhs_c && r_xs) {
-    rsum = warp_sum(rsum);
-    if (lane == 0) rhs_c[n_d + c] = r[n_s + n_d + c] - rsum;
+    if (rhs_c && r) {
+      rsum = warp_sum(rsum);
+      if (lane == 0) rhs_c[n_d + c] = r[n_s + n_d + c] - rsum;
+    }
   }
 }
 
@@ -244,29 +304,41 @@ extern "C" int mds_condense(const mds_plan* P, const double* js_val, const doubl
   if (rhs_c && !r) rhs_c = nullptr;
   if (n_s > 0) {
     int64_t blocks = std::min<int64_t>(mds_cdiv(n_s, 256), 148 * 16);
-    k_condense_w<<<(unsigned)blocks, 256, 0, st>>>(n_s, h_ss, sigma_s, delta_w, w_out, status);
-    MDS_LAUNCH_CHECK();
+    MDS_LAUNCH(PC_CONDENSE_W, st,
+               (k_condense_w<<<(unsigned)blocks, 256, 0, st>>>(n_s, h_ss, sigma_s, delta_w, w_out, status)));
   }
   if (n_d > 0) {
     int64_t blocks = std::min<int64_t>(n_d, 148 * 8);
-    k_condense_dense<<<(unsigned)blocks, 256, 0, st>>>(n_d, m, H_dd, ldh, sigma_d, delta_w, J_d, ldj, M, ldm,
-                                                     r ? r + n_s : nullptr, rhs_c);
-    MDS_LAUNCH_CHECK();
+    MDS_LAUNCH(PC_CONDENSE_DENSE, st,
+               (k_condense_dense<<<(unsigned)blocks, 256, 0, st>>>(n_d, m, H_dd, ldh, sigma_d, delta_w, J_d, ldj, M,
+                                                                 ldm, r ? r + n_s : nullptr, rhs_c)));
   }
   if (m > 0) {
-    constexpr int WARPS = 4;
-    int64_t acc_len = std::min<int64_t>(((m + 31) / 32) * 32, 4096);
-    size_t smem = sizeof(double) * acc_len * WARPS;
+    // warp-private accumulator columns: <= 4096 doubles each; warps per CTA sized to ~192 KB
+    const int64_t acc_len = std::min<int64_t>(((m + 31) / 32) * 32, 4096);
     static bool attr_set = false;
     if (!attr_set) {
-      cudaFuncSetAttribute(k_condense_yy<WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8 * WARPS);
+      cudaFuncSetAttribute(k_condense_yy<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * 4096 * 8);
+      cudaFuncSetAttribute(k_condense_yy<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 2048 * 8);
+      (void)cudaGetLastError();
       attr_set = true;
     }
-    int64_t blocks = mds_cdiv(m, WARPS);
-    k_condense_yy<WARPS><<<(unsigned)blocks, WARPS * 32, smem, st>>>(
-        n_d, P->m_E, m, acc_len, P->rowptr, P->colidx, js_val, P->tptr, P->tkp, w_out, d_h, delta_c,
-        r, n_s, M, ldm, rhs_c, status);
-    MDS_LAUNCH_CHECK();
+    const int64_t ntask = (m + 1) / 2;
+    if (acc_len > 2048) {
+      constexpr int W = 6;
+      size_t smem = sizeof(double) * acc_len * W;
+      MDS_LAUNCH(PC_CONDENSE_YY, st,
+                 (k_condense_yy<W><<<(unsigned)mds_cdiv(ntask, W), W * 32, smem, st>>>(
+                     n_d, P->m_E, m, acc_len, P->rowptr, P->colidx, js_val, P->tptr, P->tkp, w_out, d_h, delta_c,
+                     r, n_s, M, ldm, rhs_c, status)));
+    } else {
+      constexpr int W = 8;
+      size_t smem = sizeof(double) * acc_len * W;
+      MDS_LAUNCH(PC_CONDENSE_YY, st,
+                 (k_condense_yy<W><<<(unsigned)mds_cdiv(ntask, W), W * 32, smem, st>>>(
+                     n_d, P->m_E, m, acc_len, P->rowptr, P->colidx, js_val, P->tptr, P->tkp, w_out, d_h, delta_c,
+                     r, n_s, M, ldm, rhs_c, status)));
+    }
   }
   return MDS_OK;
 }

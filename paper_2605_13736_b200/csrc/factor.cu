@@ -25,9 +25,12 @@
 // final "undo"); k_factor_finalize converts to the explicit-permutation form
 // P M P^T = L D L^T consumed by mds_solve.
 #include <cooperative_groups.h>
+#include <cuda.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 
@@ -61,7 +64,10 @@ struct FWork {
   int* rhoinv;        // [N]
   double* rowsum;     // [N]
   double* Lblk;       // [NB*NB]
-  double* W;          // [ldw * WCOLS]
+  double* W;          // [ldw * WCOLS]  W panel of the current panel (host picks W0/W1 by panel parity)
+  double* W1;         // second W buffer (look-ahead: panel p+1 is formed while p's update still reads W)
+  int2* pinfo;        // [N+2] per-panel (k0, kb), written by k_panel_slow, read by the updates
+  int pidx;           // panel index of this launch (host loop counter)
   int64_t ldw;
 };
 
@@ -80,8 +86,11 @@ FWork carve(void* work, int64_t N, size_t* total) {
   f.rhoinv = reinterpret_cast<int*>(take(sizeof(int) * N));
   f.rowsum = reinterpret_cast<double*>(take(sizeof(double) * N));
   f.Lblk = reinterpret_cast<double*>(take(sizeof(double) * NB * NB));
-  f.ldw = align_up(std::max<int64_t>(N, 1), 4);
+  f.ldw = align_up(std::max<int64_t>(N, 1), 8);
   f.W = reinterpret_cast<double*>(take(sizeof(double) * f.ldw * WCOLS));
+  f.W1 = reinterpret_cast<double*>(take(sizeof(double) * f.ldw * WCOLS));
+  f.pinfo = reinterpret_cast<int2*>(take(sizeof(int2) * (N + 2)));
+  f.pidx = 0;
   if (total) *total = off;
   return f;
 }
@@ -157,14 +166,23 @@ __global__ void __launch_bounds__(1024) k_anorm_final(int64_t N, const double* r
 }
 
 // ---------------------------------------------------------------------------
-// F1: unpivoted LDL^T of the NB x NB diagonal block in shared memory.
-// Leaves W11 (updated, unscaled columns) in W, L11 in Lblk, d and the in-block
-// part of colmax in ctl.  A is NOT modified (rejected columns need originals).
+// F1: unpivoted LDL^T of the NB x NB diagonal block, register-blocked: a
+// 16x16 thread grid, each thread owning a 4x4 sub-block (rows tr+16a, cols
+// tc+16b) in registers; column j and row j of L^{-1} are broadcast through
+// shared memory once per elimination step (one __syncthreads per column).
+// The same elimination is applied to an identity block, accumulating
+// Linv = L11^{-1} (Gauss-Jordan style), so F2 can form W21 = A21 L11^{-T} as a
+// GEMM on the FP64 tensor cores (explicit inverted diagonal blocks, as MAGMA's
+// GPU trsm does).  Leaves W11 (updated, unscaled columns) in W, X = L11^{-T}
+// (row-major [t][j]) in Lblk, d and the in-block part of colmax in ctl.
+// A is NOT modified (rejected columns need their original values).
 __global__ void __launch_bounds__(256) k_panel_diag(int64_t N, const double* __restrict__ A, int64_t lda,
                                                     FWork f) {
   FCtl* ctl = f.ctl;
   if (ctl->abort) return;
-  __shared__ double Ad[NB * (NB + 1)];    // column-major, stride NB+1
+  __shared__ double colj[2][NB];
+  __shared__ double rowj[2][NB];
+  __shared__ double Wsh[NB * (NB + 1)];   // W11, column-major, stride NB+1
   __shared__ int s_k0;
   if (threadIdx.x == 0) s_k0 = ctl->k0 + ctl->kb;
   __syncthreads();
@@ -175,42 +193,75 @@ __global__ void __launch_bounds__(256) k_panel_diag(int64_t N, const double* __r
   }
   const int nbp = (int)((N - k0) < NB ? (N - k0) : NB);
   constexpr int S = NB + 1;
-  for (int idx = threadIdx.x; idx < nbp * nbp; idx += blockDim.x) {
-    const int i = idx % nbp, j = idx / nbp;
-    if (i >= j) Ad[j * S + i] = A[(k0 + i) + (k0 + j) * lda];
+  const int tr = threadIdx.x & 15, tc = threadIdx.x >> 4;
+  double a[4][4], li[4][4];
+#pragma unroll
+  for (int ai = 0; ai < 4; ai++)
+#pragma unroll
+    for (int bi = 0; bi < 4; bi++) {
+      const int r = tr + 16 * ai, c = tc + 16 * bi;
+      a[ai][bi] = (r >= c && r < nbp && c < nbp) ? A[(k0 + r) + (k0 + c) * lda] : 0.0;
+      li[ai][bi] = (r == c) ? 1.0 : 0.0;
+    }
+  // j = 16*js + jj with js a compile-time constant (keeps a/li in registers)
+#pragma unroll
+  for (int js = 0; js < 4; js++) {
+    for (int jj = 0; jj < 16; jj++) {
+      const int j = 16 * js + jj;
+      if (j >= nbp) break;
+      const int buf = j & 1;
+      if (tc == jj) {
+#pragma unroll
+        for (int ai = 0; ai < 4; ai++) {
+          const int r = tr + 16 * ai;
+          const double v = (r >= j && r < nbp) ? a[ai][js] : 0.0;
+          colj[buf][r] = v;
+          if (r >= j) Wsh[j * S + r] = v;
+        }
+      }
+      if (tr == jj) {
+#pragma unroll
+        for (int bi = 0; bi < 4; bi++) rowj[buf][tc + 16 * bi] = li[js][bi];
+      }
+      __syncthreads();
+      const double d = colj[buf][j];
+      const double r1 = (d != 0.0) ? 1.0 / d : 0.0;
+#pragma unroll
+      for (int ai = 0; ai < 4; ai++) {
+        const int r = tr + 16 * ai;
+        if (r > j) {
+          const double l = colj[buf][r] * r1;
+#pragma unroll
+          for (int bi = 0; bi < 4; bi++) {
+            const int c = tc + 16 * bi;
+            if (c > j && r >= c) a[ai][bi] -= l * colj[buf][c];
+            if (c <= j) li[ai][bi] -= l * rowj[buf][c];
+          }
+        }
+      }
+    }
   }
   __syncthreads();
-  for (int j = 0; j < nbp; j++) {
-    const double d = Ad[j * S + j];
-    const double r1 = (d != 0.0) ? 1.0 / d : 0.0;
-    // A22 -= (a r1) a^T over the trailing block (lower), a = column j (unscaled)
-    const int m = nbp - j - 1;
-    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
-      const int r = j + 1 + idx % m, c = j + 1 + idx / m;
-      if (r >= c) Ad[c * S + r] -= (Ad[j * S + r] * r1) * Ad[j * S + c];
+  // X[t][j] = Linv[j][t]  (row-major, NB x NB, zero outside nbp)
+#pragma unroll
+  for (int ai = 0; ai < 4; ai++)
+#pragma unroll
+    for (int bi = 0; bi < 4; bi++) {
+      const int r = tr + 16 * ai, c = tc + 16 * bi;   // Linv[r][c]
+      f.Lblk[c * NB + r] = (r < nbp && c < nbp) ? li[ai][bi] : 0.0;
     }
-    __syncthreads();
-  }
-  // W11 = updated columns (Ad lower), L11 = W11 * r1, in-block colmax, d
   for (int idx = threadIdx.x; idx < nbp * nbp; idx += blockDim.x) {
     const int r = idx % nbp, j = idx / nbp;
-    if (r >= j) {
-      const double wv = Ad[j * S + r];
-      f.W[(k0 + r) + j * f.ldw] = wv;
-      const double d = Ad[j * S + j];
-      const double r1 = (d != 0.0) ? 1.0 / d : 0.0;
-      f.Lblk[r + j * NB] = (r == j) ? 1.0 : wv * r1;
-    } else {
-      f.Lblk[r + j * NB] = 0.0;
-    }
+    if (r >= j) f.W[(k0 + r) + j * f.ldw] = Wsh[j * S + r];
   }
-  if (threadIdx.x < NB) {
-    const int j = threadIdx.x;
-    if (j < nbp) {
+  // in-block colmax of column j: warp w handles columns w, w+8, ...
+  {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int j = warp; j < nbp; j += 8) {
       double cm = 0.0;
-      for (int r = j + 1; r < nbp; r++) cm = fmax(cm, fabs(Ad[j * S + r]));
-      ctl->colmax[j] = dbits(cm);
-      ctl->d[j] = Ad[j * S + j];
+      for (int r = j + 1 + lane; r < nbp; r += 32) cm = fmax(cm, fabs(Wsh[j * S + r]));
+      cm = warp_max(cm);
+      if (lane == 0) { ctl->colmax[j] = dbits(cm); ctl->d[j] = Wsh[j * S + j]; }
     }
   }
   if (threadIdx.x == 0) {
@@ -222,51 +273,92 @@ __global__ void __launch_bounds__(256) k_panel_diag(int64_t N, const double* __r
   }
 }
 
-// F2: W21 = A21 L11^{-T} (forward substitution per row, registers) and the
-// colmax of every panel column over rows below the diagonal block.
-__global__ void __launch_bounds__(256) k_panel_trsm(int64_t N, const double* __restrict__ A, int64_t lda, FWork f) {
+// FP64 tensor-core fragment op: mma.sync m8n8k4 f64 (SASS DMMA.8x8x4).
+// a0 = A[g][q], b0 = B[q][g], {c0,c1} = C[g][2q], C[g][2q+1]  (g = lane>>2, q = lane&3)
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+constexpr int UT = 64;          // DMMA tile edge
+constexpr int US = UT + 4;      // smem row stride (conflict-free fragment loads)
+
+// F2: W21 = A21 * X (X = L11^{-T}) on the FP64 tensor cores, 64-row tiles,
+// K = 64; writes W21 and atomically max-reduces |W21| per column (colmax).
+__global__ void __launch_bounds__(128) k_panel_trsm(int64_t N, const double* __restrict__ A, int64_t lda, FWork f) {
   FCtl* ctl = f.ctl;
   if (ctl->abort) return;
   const int nbp = ctl->nbp;
   const int64_t k0 = ctl->k0;
   if (nbp == 0) return;
-  const int64_t rbase = k0 + nbp + (int64_t)blockIdx.x * 256;
-  if (rbase >= N) return;
-  __shared__ double Ls[NB * NB];    // Ls[t*NB + j] = L11[j, t]
-  __shared__ double wmax[8][NB];
-  for (int idx = threadIdx.x; idx < NB * NB; idx += 256) {
-    const int j = idx % NB, t = idx / NB;
-    Ls[idx] = (j < nbp && t < nbp) ? f.Lblk[j + t * NB] : 0.0;
+  const int64_t R0 = k0 + nbp + (int64_t)blockIdx.x * UT;
+  if (R0 >= N) return;
+  extern __shared__ double dsm[];
+  double* As = dsm;                 // [t][row]
+  double* Xs = dsm + NB * US;       // [t][j]
+  __shared__ double cmax[4][32];
+  for (int idx = threadIdx.x; idx < UT * NB; idx += 128) {
+    const int i = idx % UT, t = idx / UT;
+    As[t * US + i] = (t < nbp && R0 + i < N) ? A[(R0 + i) + (k0 + t) * lda] : 0.0;
+    Xs[t * US + i] = f.Lblk[t * NB + i];   // X[t][j=i]
   }
   __syncthreads();
-  const int64_t r = rbase + threadIdx.x;
-  const bool live = r < N;
-  double x[NB];
-#pragma unroll
-  for (int t = 0; t < NB; t++) x[t] = (live && t < nbp) ? A[r + (k0 + t) * lda] : 0.0;
-#pragma unroll
-  for (int j = 1; j < NB; j++) {
-    double s = x[j];
-#pragma unroll
-    for (int t = 0; t < j; t++) s -= x[t] * Ls[t * NB + j];
-    x[j] = s;
-  }
-  if (live) {
-#pragma unroll
-    for (int t = 0; t < NB; t++)
-      if (t < nbp) f.W[r + t * f.ldw] = x[t];
-  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int g = lane >> 2, q = lane & 3;
+  double acc[4][4][2];
 #pragma unroll
-  for (int t = 0; t < NB; t++) {
-    double v = warp_max(fabs(x[t]));
-    if (lane == 0) wmax[warp][t] = v;
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll 4
+  for (int t0 = 0; t0 < NB; t0 += 4) {
+    double av[4], bv[4];
+#pragma unroll
+    for (int a = 0; a < 4; a++) av[a] = As[(t0 + q) * US + wm + 8 * a + g];
+#pragma unroll
+    for (int b = 0; b < 4; b++) bv[b] = Xs[(t0 + q) * US + wn + 8 * b + g];
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+      for (int b = 0; b < 4; b++) dmma(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
   }
+  // store W21 and per-column max |W|
+  double cm[4][2];
+#pragma unroll
+  for (int b = 0; b < 4; b++) cm[b][0] = cm[b][1] = 0.0;
+#pragma unroll
+  for (int a = 0; a < 4; a++) {
+    const int64_t row = R0 + wm + 8 * a + g;
+    if (row < N) {
+#pragma unroll
+      for (int b = 0; b < 4; b++)
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const int col = wn + 8 * b + 2 * q + e;
+          if (col < nbp) {
+            f.W[row + col * f.ldw] = acc[a][b][e];
+            cm[b][e] = fmax(cm[b][e], fabs(acc[a][b][e]));
+          }
+        }
+    }
+  }
+  // reduce over the 8 row-groups g (lanes with equal q share columns)
+#pragma unroll
+  for (int b = 0; b < 4; b++)
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+      double v = cm[b][e];
+      v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 4));
+      v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 8));
+      v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 16));
+      if (g == 0) cmax[warp][8 * b + 2 * q + e] = v;
+    }
   __syncthreads();
-  if (threadIdx.x < nbp) {
-    double v = 0.0;
-    for (int w = 0; w < 8; w++) v = fmax(v, wmax[w][threadIdx.x]);
-    atomicMax(&ctl->colmax[threadIdx.x], dbits(v));
+  if (threadIdx.x < NB) {
+    const int col = threadIdx.x;
+    const int half = col >> 5;                 // column col is owned by warps half and half+2
+    const double v = fmax(cmax[half][col & 31], cmax[half + 2][col & 31]);
+    if (col < nbp) atomicMax(&ctl->colmax[col], dbits(v));
   }
 }
 
@@ -279,33 +371,31 @@ __global__ void __launch_bounds__(256) k_panel_accept(int64_t N, double* __restr
   const int nbp = ctl->nbp;
   const int64_t k0 = ctl->k0;
   if (nbp == 0) return;
-  __shared__ int s_p;
   __shared__ double s_r1[NB], s_d[NB];
-  if (threadIdx.x == 0) {
-    int p = 0;
-    while (p < nbp) {
-      const double d = ctl->d[p], cm = bitsd(ctl->colmax[p]);
-      if (!(fabs(d) >= ALPHA_BK * cm)) break;   // (0 >= 0 accepts the exact-zero column)
-      p++;
-    }
-    s_p = p;
-  }
+  __shared__ unsigned s_fail[2];
+  // p = first column failing BK's 1x1-no-interchange test (all columns tested in parallel)
   if (threadIdx.x < NB) {
-    const double d = (threadIdx.x < nbp) ? ctl->d[threadIdx.x] : 0.0;
-    s_d[threadIdx.x] = d;
-    s_r1[threadIdx.x] = (d != 0.0) ? 1.0 / d : 0.0;
+    const int j = threadIdx.x;
+    const double d = (j < nbp) ? ctl->d[j] : 0.0;
+    const double cm = (j < nbp) ? bitsd(ctl->colmax[j]) : 0.0;
+    s_d[j] = d;
+    s_r1[j] = (d != 0.0) ? 1.0 / d : 0.0;
+    const bool fail = (j >= nbp) || !(fabs(d) >= ALPHA_BK * cm);   // (0 >= 0 accepts the exact-zero column)
+    const unsigned b = __ballot_sync(0xffffffffu, fail);
+    s_fail[j >> 5] = b;
   }
   __syncthreads();
-  const int p = s_p;
+  const int p = s_fail[0] ? (__ffs(s_fail[0]) - 1) : (s_fail[1] ? 32 + __ffs(s_fail[1]) - 1 : NB);
   const int64_t r = k0 + (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int j0 = blockIdx.y * (NB / 8), j1 = min(p, j0 + NB / 8);   // 8 column groups per row
   if (r < N) {
-    for (int j = 0; j < p; j++) {
+    for (int j = j0; j < j1; j++) {
       const int64_t k = k0 + j;
       if (r == k) A[r + k * lda] = s_d[j];
       else if (r > k) A[r + k * lda] = f.W[r + j * f.ldw] * s_r1[j];
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
     const double tol = ctl->tol;
     for (int j = 0; j < p; j++) {
       const double d = s_d[j];
@@ -344,10 +434,12 @@ __global__ void __launch_bounds__(1024) k_panel_slow(int64_t N, double* __restri
   const int nbp = ctl->nbp;
   const int64_t k0 = ctl->k0;
   int j = ctl->kb;
-  if (nbp == 0) return;
   const bool last = (k0 + nbp >= N);
   const int jlim = last ? nbp : nbp - 1;
-  if (j >= jlim) return;
+  if (nbp == 0 || j >= jlim) {   // nothing left for the exact path: publish (k0, kb) for the updates
+    if (threadIdx.x == 0) f.pinfo[f.pidx] = make_int2((int)k0, nbp == 0 ? 0 : j);
+    return;
+  }
   __shared__ double wrow[WCOLS];
   __shared__ ArgMax sh[33];
   double* W = f.W;
@@ -457,81 +549,371 @@ __global__ void __launch_bounds__(1024) k_panel_slow(int64_t N, double* __restri
     __syncthreads();
     j += kstep;
   }
-  if (tid == 0) ctl->kb = j;
+  if (tid == 0) {
+    ctl->kb = j;
+    f.pinfo[f.pidx] = make_int2((int)k0, j);
+  }
 }
 
 // ---------------------------------------------------------------------------
 // Trailing update C -= L21 * W21^T on the lower triangle, FP64 tensor cores.
-// 64x64 tile per CTA, 4 warps of 32x32, mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4),
-// full K (= kb <= NB) staged in shared memory, C held in registers.
-constexpr int UT = 64;          // tile edge
-constexpr int US = UT + 4;      // smem row stride (conflict-free fragment loads)
+// Persistent: one 128-thread CTA per SM walks the lower-triangular 64x64 tile
+// list (linear order, so concurrently active tiles share their L21 row panel
+// in L2).  Each tile's operands -- the L tile (64 x kb), the W tile (64 x kb)
+// and the C tile (64 x 64) -- are staged in shared memory with cp.async into a
+// 2-stage ring, so the loads of tile t+1 fly while tile t runs on the DMMA
+// pipe (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4; 4 warps of 32x32, K = kb <= 64
+// in one pass, C accumulated in registers, stored straight back to HBM).
+constexpr int UCS = UT + 2;                         // C tile stride (conflict-free fragment reads)
+constexpr int USTAGE = 2 * NB * US + UT * UCS;      // doubles per stage
 
-__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  const int sz = pred ? 8 : 0;   // src-size 0 -> zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gsrc), "r"(sz) : "memory");
 }
+__device__ __forceinline__ void cp_async16(double* sdst, const double* gsrc, int bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gsrc), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory"); }
 
-__global__ void __launch_bounds__(128) k_update(int64_t N, double* __restrict__ A, int64_t lda, FWork f) {
-  FCtl* ctl = f.ctl;
-  if (ctl->abort) return;
-  const int64_t k0 = ctl->k0;
-  const int kb = ctl->kb;
-  const int64_t s = k0 + kb;
-  const int64_t n2 = N - s;
-  if (n2 <= 0 || kb <= 0) return;
-  const int64_t nt = (n2 + UT - 1) / UT;
-  const int64_t x = blockIdx.x;
-  if (x >= nt * (nt + 1) / 2) return;
-  int64_t bi = (int64_t)((sqrt(8.0 * (double)x + 1.0) - 1.0) * 0.5);
+__device__ __forceinline__ void tri_tile(int64_t x, int64_t& bi, int64_t& bj) {
+  bi = (int64_t)((sqrt(8.0 * (double)x + 1.0) - 1.0) * 0.5);
   while (bi * (bi + 1) / 2 > x) bi--;
   while ((bi + 1) * (bi + 2) / 2 <= x) bi++;
-  const int64_t bj = x - bi * (bi + 1) / 2;
-  const int64_t R0 = s + bi * UT, C0 = s + bj * UT;
-  extern __shared__ double sm[];
-  double* Ls = sm;                 // [t][row]
-  double* Ws = sm + NB * US;       // [t][col]
-  const int kp4 = (kb + 3) & ~3;
-  for (int idx = threadIdx.x; idx < UT * kp4; idx += 128) {
-    const int i = idx % UT, t = idx / UT;
-    const bool tin = t < kb;
-    Ls[t * US + i] = (tin && R0 + i < N) ? A[(R0 + i) + (k0 + t) * lda] : 0.0;
-    Ws[t * US + i] = (tin && C0 + i < N) ? f.W[(C0 + i) + t * f.ldw] : 0.0;
+  bj = x - bi * (bi + 1) / 2;
+}
+
+// Tiles are anchored on the ABSOLUTE 64-grid (tile (BI,BJ) covers rows
+// [64 BI, 64 BI + 64) x cols [64 BJ, 64 BJ + 64)), so with a 16-byte aligned
+// M and even ldm every tile column segment is 16-byte aligned: one 16-byte
+// cp.async moves two doubles.  Rows/cols < s (already factored) are computed
+// on but never stored.
+template <bool V16>
+__device__ __forceinline__ void update_issue(double* st, int64_t R0, int64_t C0, int64_t k0, int kb, int kp4,
+                                             int64_t N, const double* A, int64_t lda, const double* W,
+                                             int64_t ldw) {
+  double* Ls = st;
+  double* Ws = st + NB * US;
+  double* Cs = st + 2 * NB * US;
+  if (V16) {
+    // pairs of rows: idx -> (pair ip = idx & 31, column t = idx >> 5)
+    const int ip = threadIdx.x & 31;
+    const int i = 2 * ip;
+    const int64_t ra = R0 + i, ca = C0 + i;
+    const int64_t dl = N - ra, dw = N - ca;
+    const int nl = (dl >= 2) ? 16 : (dl == 1 ? 8 : 0);
+    const int nw = (dw >= 2) ? 16 : (dw == 1 ? 8 : 0);
+    const double* gl = A + ra + k0 * lda;
+    const double* gw = W + ca;
+    for (int t = threadIdx.x >> 5; t < kp4; t += 4) {
+      const bool tin = t < kb;
+      cp_async16(&Ls[t * US + i], (tin && nl) ? gl + t * lda : A, tin ? nl : 0);
+      cp_async16(&Ws[t * US + i], (tin && nw) ? gw + t * ldw : W, tin ? nw : 0);
+    }
+    const double* gc = A + ra + C0 * lda;
+    for (int c = threadIdx.x >> 5; c < UT; c += 4) {
+      const int nc = (C0 + c < N) ? nl : 0;
+      cp_async16(&Cs[c * UCS + i], nc ? gc + c * lda : A, nc);
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < UT * kp4; idx += 128) {
+      const int i = idx & (UT - 1), t = idx >> 6;
+      const bool tin = t < kb;
+      const bool pl = tin && (R0 + i < N), pw = tin && (C0 + i < N);
+      cp_async8(&Ls[t * US + i], pl ? &A[(R0 + i) + (k0 + t) * lda] : A, pl);
+      cp_async8(&Ws[t * US + i], pw ? &W[(C0 + i) + t * ldw] : W, pw);
+    }
+    for (int idx = threadIdx.x; idx < UT * UT; idx += 128) {
+      const int i = idx & (UT - 1), c = idx >> 6;
+      const bool pc = (R0 + i < N) && (C0 + c < N);
+      cp_async8(&Cs[c * UCS + i], pc ? &A[(R0 + i) + (C0 + c) * lda] : A, pc);
+    }
   }
+}
+
+template <bool V16>
+__global__ void __launch_bounds__(128, 1) k_update(int64_t N, double* __restrict__ A, int64_t lda, FWork f) {
+  FCtl* ctl = f.ctl;
+  if (ctl->abort) return;
+  const int2 pi = f.pinfo[f.pidx];
+  const int64_t k0 = pi.x;
+  const int kb = pi.y;
+  const int64_t s = k0 + kb;
+  if (N - s <= 0 || kb <= 0) return;
+  const int64_t b0 = s / UT;                               // first absolute tile row/col
+  const int64_t nt = (N + UT - 1) / UT - b0;
+  const int64_t ntiles = nt * (nt + 1) / 2;
+  int64_t x = blockIdx.x;
+  if (x >= ntiles) return;
+  extern __shared__ double sm[];
+  const int kp4 = (kb + 3) & ~3;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int g = lane >> 2, q = lane & 3;
-  double acc[4][4][2];
-#pragma unroll
-  for (int a = 0; a < 4; a++)
-#pragma unroll
-    for (int b = 0; b < 4; b++)
-#pragma unroll
-      for (int e = 0; e < 2; e++) {
-        const int64_t row = R0 + wm + 8 * a + g, col = C0 + wn + 8 * b + 2 * q + e;
-        acc[a][b][e] = (row < N && col < N) ? A[row + col * lda] : 0.0;
-      }
-  __syncthreads();
-  for (int t0 = 0; t0 < kp4; t0 += 4) {
-    double av[4], bv[4];
-#pragma unroll
-    for (int a = 0; a < 4; a++) av[a] = -Ls[(t0 + q) * US + wm + 8 * a + g];
-#pragma unroll
-    for (int b = 0; b < 4; b++) bv[b] = Ws[(t0 + q) * US + wn + 8 * b + g];
+  int64_t bi, bj;
+  tri_tile(x, bi, bj);
+  int64_t R0 = (b0 + bi) * UT, C0 = (b0 + bj) * UT;
+  update_issue<V16>(sm, R0, C0, k0, kb, kp4, N, A, lda, f.W, f.ldw);
+  cp_async_commit();
+  for (int it = 0; x < ntiles; it++) {
+    const int64_t xn = x + gridDim.x;
+    double* cur = sm + (size_t)(it & 1) * USTAGE;
+    int64_t Rn = 0, Cn = 0;
+    if (xn < ntiles) {
+      int64_t bin, bjn;
+      tri_tile(xn, bin, bjn);
+      Rn = (b0 + bin) * UT; Cn = (b0 + bjn) * UT;
+      update_issue<V16>(sm + (size_t)((it + 1) & 1) * USTAGE, Rn, Cn, k0, kb, kp4, N, A, lda, f.W, f.ldw);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* Ls = cur;
+    const double* Ws = cur + NB * US;
+    const double* Cs = cur + 2 * NB * US;
+    double acc[4][4][2];
 #pragma unroll
     for (int a = 0; a < 4; a++)
 #pragma unroll
-      for (int b = 0; b < 4; b++) dmma(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+      for (int b = 0; b < 4; b++)
+#pragma unroll
+        for (int e = 0; e < 2; e++) acc[a][b][e] = Cs[(wn + 8 * b + 2 * q + e) * UCS + wm + 8 * a + g];
+#pragma unroll 4
+    for (int t0 = 0; t0 < kp4; t0 += 4) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; a++) av[a] = -Ls[(t0 + q) * US + wm + 8 * a + g];
+#pragma unroll
+      for (int b = 0; b < 4; b++) bv[b] = Ws[(t0 + q) * US + wn + 8 * b + g];
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) dmma(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; a++) {
+      const int64_t row = R0 + wm + 8 * a + g;
+#pragma unroll
+      for (int b = 0; b < 4; b++)
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const int64_t col = C0 + wn + 8 * b + 2 * q + e;
+          if (row < N && col >= s && row >= col) A[row + col * lda] = acc[a][b][e];
+        }
+    }
+    __syncthreads();   // stage `cur` may be refilled by the next iteration's issue
+    x = xn; R0 = Rn; C0 = Cn;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Trailing update, TMA + warp-specialised version (the default when M is
+// 16-byte aligned with an even ldm).  One producer warp issues
+// cp.async.bulk.tensor (TMA, SASS UTMALDG) copies of the L21 and W21 tiles
+// into a 3-stage shared-memory ring (64-byte swizzle: conflict-free DMMA
+// fragment reads), completion tracked by mbarriers; two consumer groups of
+// 4 warps each take alternate tiles ("ping-pong"), so one group's C loads
+// and epilogue stores overlap the other group's DMMA k-loop.
+constexpr int TS = 3;                             // pipeline stages
+constexpr int TOPB = UT * NB * 8;                 // bytes per operand tile (32 KB)
+constexpr int TSTAGEB = 2 * TOPB;                 // L + W
+constexpr int TSMEM = TS * TSTAGEB + 1024 + 64;   // + alignment + barriers
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map, int c0, int c1, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+// byte offset of element (row i in 0..63, k t in 0..63) inside an operand tile:
+// 8 boxes of 8 rows x 64 k (4 KB each), 64-byte swizzle (bits[4:5] ^= bits[7:8])
+__device__ __forceinline__ unsigned tma_off(int i, int t) {
+  const unsigned lin = (unsigned)(t * 64 + (i & 7) * 8);
+  return (unsigned)((i >> 3) * 4096) + (lin ^ (((lin >> 7) & 3u) << 4));
+}
+
+// Tile sets of the look-ahead split: mode 0 = all lower tiles of the trailing
+// matrix, 1 = the two leading tile columns (they hold the next panel), 2 = the rest.
+__device__ __forceinline__ int64_t upd_ntiles(int64_t nt, int mode) {
+  if (mode == 0) return nt * (nt + 1) / 2;
+  if (mode == 1) return nt >= 2 ? 2 * nt - 1 : nt * (nt + 1) / 2;
+  const int64_t r = nt - 2;
+  return r > 0 ? r * (r + 1) / 2 : 0;
+}
+__device__ __forceinline__ void upd_tile(int64_t x, int64_t nt, int mode, int64_t& bi, int64_t& bj) {
+  if (mode == 0) { tri_tile(x, bi, bj); return; }
+  if (mode == 1) {
+    if (nt < 2) { tri_tile(x, bi, bj); return; }
+    if (x < nt) { bi = x; bj = 0; } else { bi = x - nt + 1; bj = 1; }
+    return;
+  }
+  tri_tile(x, bi, bj);
+  bi += 2; bj += 2;
+}
+
+__global__ void __launch_bounds__(288, 1) k_update_tma(int64_t N, double* __restrict__ A, int64_t lda, FWork f,
+                                                       const __grid_constant__ CUtensorMap mapA,
+                                                       const __grid_constant__ CUtensorMap mapW, int mode) {
+  FCtl* ctl = f.ctl;
+  if (ctl->abort) return;
+  const int2 pi = f.pinfo[f.pidx];
+  const int64_t k0 = pi.x;
+  const int kb = pi.y;
+  const int64_t s = k0 + kb;
+  if (N - s <= 0 || kb <= 0) return;
+  const int64_t b0 = s / UT;
+  const int64_t nt = (N + UT - 1) / UT - b0;
+  const int64_t ntiles = upd_ntiles(nt, mode);
+  if ((int64_t)blockIdx.x >= ntiles) return;
+  const int ntile_cta = (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
+  extern __shared__ unsigned char tsm_raw[];
+  unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(tsm + TS * TSTAGEB);
+  const unsigned full0 = smem_u32(bars), empty0 = smem_u32(bars + TS);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < TS; i++) { mbar_init(full0 + 8 * i, 1); mbar_init(empty0 + 8 * i, 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // ---------------- producer: one elected lane issues all TMA copies
+    if (lane == 0) {
+      for (int i = 0; i < ntile_cta; i++) {
+        const int st = i % TS, u = i / TS;
+        if (u > 0) mbar_wait(empty0 + 8 * st, (u - 1) & 1);
+        const int64_t x = blockIdx.x + (int64_t)i * gridDim.x;
+        int64_t bi, bj;
+        upd_tile(x, nt, mode, bi, bj);
+        const int R0 = (int)((b0 + bi) * UT), C0 = (int)((b0 + bj) * UT);
+        const unsigned sL = smem_u32(tsm + st * TSTAGEB), sW = sL + TOPB;
+        const unsigned fb = full0 + 8 * st;
+        mbar_expect_tx(fb, TSTAGEB);
 #pragma unroll
-  for (int a = 0; a < 4; a++)
-#pragma unroll
-    for (int b = 0; b < 4; b++)
-#pragma unroll
-      for (int e = 0; e < 2; e++) {
-        const int64_t row = R0 + wm + 8 * a + g, col = C0 + wn + 8 * b + 2 * q + e;
-        if (row < N && col < N && row >= col) A[row + col * lda] = acc[a][b][e];
+        for (int b = 0; b < 8; b++) {
+          tma_load_2d(sL + b * 4096, &mapA, R0 + 8 * b, (int)k0, fb);
+          tma_load_2d(sW + b * 4096, &mapW, C0 + 8 * b, 0, fb);
+        }
       }
+    }
+    return;
+  }
+  // ---------------- consumers: group grp takes tiles grp, grp+2, ...
+  const int grp = (warp - 1) >> 2, wq = (warp - 1) & 3;
+  const int wm = (wq >> 1) * 32, wn = (wq & 1) * 32;
+  const int g = lane >> 2, q = lane & 3;
+  for (int i = grp; i < ntile_cta; i += 2) {
+    const int st = i % TS, u = i / TS;
+    const int64_t x = blockIdx.x + (int64_t)i * gridDim.x;
+    int64_t bi, bj;
+    upd_tile(x, nt, mode, bi, bj);
+    const int64_t R0 = (b0 + bi) * UT, C0 = (b0 + bj) * UT;
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; a++) {
+      const int64_t row = R0 + wm + 8 * a + g;
+#pragma unroll
+      for (int b = 0; b < 4; b++)
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const int64_t col = C0 + wn + 8 * b + 2 * q + e;
+          acc[a][b][e] = (row < N && col < N && row >= col) ? A[row + col * lda] : 0.0;
+        }
+    }
+    mbar_wait(full0 + 8 * st, u & 1);
+    const unsigned char* Lt = tsm + st * TSTAGEB;
+    const unsigned char* Wt = Lt + TOPB;
+#pragma unroll 4
+    for (int t0 = 0; t0 < NB; t0 += 4) {
+      const int t = t0 + q;
+      double av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; a++) {
+        const double v = *reinterpret_cast<const double*>(Lt + tma_off(wm + 8 * a + g, t));
+        av[a] = (t < kb) ? -v : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < 4; b++) {
+        const double v = *reinterpret_cast<const double*>(Wt + tma_off(wn + 8 * b + g, t));
+        bv[b] = (t < kb) ? v : 0.0;
+      }
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) dmma(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * st);
+#pragma unroll
+    for (int a = 0; a < 4; a++) {
+      const int64_t row = R0 + wm + 8 * a + g;
+#pragma unroll
+      for (int b = 0; b < 4; b++)
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const int64_t col = C0 + wn + 8 * b + 2 * q + e;
+          if (row < N && col >= s && row >= col) A[row + col * lda] = acc[a][b][e];
+        }
+    }
+  }
+}
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+    (void)cudaGetLastError();
+  }
+  return fn;
+}
+
+// 2-D map over a column-major (rows x cols, ld) FP64 matrix; box 8 rows x 64 cols, 64-byte swizzle
+bool make_map(CUtensorMap* m, const double* base, int64_t rows, int64_t cols, int64_t ld) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  cuuint32_t box[2] = {8, 64};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
 }
 
 // ---------------------------------------------------------------------------
@@ -594,9 +976,44 @@ __global__ void k_factor_finalize(int64_t N, double* __restrict__ A, int64_t lda
 }
 }  // namespace
 
+extern "C" int64_t mds_factor_panels(const void* fwork, int64_t N, int32_t* starts_host, int64_t cap) {
+  if (!fwork || N <= 0) return MDS_ERR_ARG;
+  FWork f = carve(const_cast<void*>(fwork), N, nullptr);
+  FCtl c;
+  if (cudaMemcpy(&c, f.ctl, sizeof(FCtl), cudaMemcpyDeviceToHost) != cudaSuccess) return MDS_ERR_CUDA;
+  int64_t n = c.npanel;
+  if (starts_host && cap > 0) {
+    if (cudaMemcpy(starts_host, f.panel_start, sizeof(int32_t) * std::min<int64_t>(n, cap), cudaMemcpyDeviceToHost) !=
+        cudaSuccess)
+      return MDS_ERR_CUDA;
+  }
+  return n;
+}
+
 // read by solve.cu
 double* mds_factor_tol_ptr(const void* fwork) {
   return fwork ? &reinterpret_cast<FCtl*>(const_cast<void*>(fwork))->tol : nullptr;
+}
+
+// side stream (per device) and reusable events for the look-ahead split
+static cudaStream_t side_stream() {
+  static cudaStream_t streams[64] = {nullptr};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  return streams[dev];
+}
+static std::vector<cudaEvent_t>* event_pool(size_t n) {
+  static std::vector<cudaEvent_t> pools[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  auto& v = pools[dev];
+  while (v.size() < n) {
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    v.push_back(e);
+  }
+  return &v;
 }
 
 extern "C" size_t mds_factor_workspace_size(int64_t N) {
@@ -624,42 +1041,93 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   MDS_CUDA_TRY(cudaMemsetAsync(f.sw, 0xff, sizeof(int) * N, st));
   MDS_CUDA_TRY(cudaMemsetAsync(f.bt, 0, sizeof(int) * N, st));
   MDS_CUDA_TRY(cudaMemsetAsync(f.rowsum, 0, sizeof(double) * N, st));
-  k_factor_init<<<1, 1, 0, st>>>(f.ctl, zero_tol);
-  MDS_LAUNCH_CHECK();
+  MDS_LAUNCH(PC_ANORM, st, (k_factor_init<<<1, 1, 0, st>>>(f.ctl, zero_tol)));
   {
     int64_t nt = (N + 31) / 32;
-    k_anorm_tiles<<<(unsigned)(nt * (nt + 1) / 2), 256, 0, st>>>(N, M, ldm, f.rowsum, f.ctl, status);
-    MDS_LAUNCH_CHECK();
-    k_anorm_final<<<1, 1024, 0, st>>>(N, f.rowsum, f.ctl);
-    MDS_LAUNCH_CHECK();
+    MDS_LAUNCH(PC_ANORM, st,
+               (k_anorm_tiles<<<(unsigned)(nt * (nt + 1) / 2), 256, 0, st>>>(N, M, ldm, f.rowsum, f.ctl, status)));
+    MDS_LAUNCH(PC_ANORM, st, (k_anorm_final<<<1, 1024, 0, st>>>(N, f.rowsum, f.ctl)));
   }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB * US * (int)sizeof(double));
+    cudaFuncSetAttribute(k_update_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
+    cudaFuncSetAttribute(k_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * USTAGE * (int)sizeof(double));
+    cudaFuncSetAttribute(k_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * USTAGE * (int)sizeof(double));
+    cudaFuncSetAttribute(k_panel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB * US * (int)sizeof(double));
     attr = true;
   }
   const size_t usmem = 2 * NB * US * sizeof(double);
+  // 16-byte cp.async path needs a 16-byte aligned M, even ldm and a 16-byte aligned W
+  const bool v16 = ((reinterpret_cast<uintptr_t>(M) & 15) == 0) && (ldm % 2 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(f.W) & 15) == 0);
+  CUtensorMap mapA, mapW;
+  const bool use_tma = v16 && std::getenv("MDS_NO_TMA") == nullptr && make_map(&mapA, M, N, N, ldm) &&
+                       make_map(&mapW, f.W, N, NB, f.ldw);
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
   const int64_t npmax = (N + (NB - 2)) / (NB - 1) + 1;
+  // Look-ahead (TMA path): the update after panel p is split into the two
+  // leading tile columns (holding panel p+1; on the main stream, before
+  // panel p+1's fast path) and the rest (on a side stream, overlapping panel
+  // p+1's diag/trsm/accept on the SMs it leaves free).  Panel p+1's exact
+  // BK step (which may interchange anywhere) waits for the rest-update.
+  const bool lookahead = use_tma && std::getenv("MDS_NO_LOOKAHEAD") == nullptr;
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t>* evs = nullptr;
+  if (lookahead) {
+    side = side_stream();
+    evs = event_pool(2 * (size_t)npmax + 2);
+    if (!side || !evs) return MDS_ERR_CUDA;
+  }
+  CUtensorMap mapW1;
+  if (use_tma && !make_map(&mapW1, f.W1, N, NB, f.ldw)) return MDS_ERR_CUDA;
+  const unsigned reserve = 16;   // SMs left to the panel chain while the rest-update runs
+  int64_t plast = -1;
   for (int64_t p = 0; p < npmax; p++) {
     const int64_t kmin = std::min<int64_t>(p * (NB - 1), N);   // lower bound on this panel's k0
     const int64_t rows = N - kmin;
     if (rows <= 0) break;
-    k_panel_diag<<<1, 256, 0, st>>>(N, M, ldm, f);
-    MDS_LAUNCH_CHECK();
+    FWork fp = f;
+    fp.pidx = (int)p;
+    if (p & 1) fp.W = f.W1;
+    MDS_LAUNCH(PC_PANEL_DIAG, st, (k_panel_diag<<<1, 256, 0, st>>>(N, M, ldm, fp)));
     const unsigned g256 = (unsigned)std::max<int64_t>(mds_cdiv(rows, 256), 1);
-    k_panel_trsm<<<g256, 256, 0, st>>>(N, M, ldm, f);
-    MDS_LAUNCH_CHECK();
-    k_panel_accept<<<g256, 256, 0, st>>>(N, M, ldm, f, piv);
-    MDS_LAUNCH_CHECK();
-    k_panel_slow<<<1, 1024, 0, st>>>(N, M, ldm, f, piv);
-    MDS_LAUNCH_CHECK();
+    const unsigned g64 = (unsigned)std::max<int64_t>(mds_cdiv(rows, UT), 1);
+    MDS_LAUNCH(PC_PANEL_TRSM, st, (k_panel_trsm<<<g64, 128, usmem, st>>>(N, M, ldm, fp)));
+    MDS_LAUNCH(PC_PANEL_ACCEPT, st, (k_panel_accept<<<dim3(g256, 8), 256, 0, st>>>(N, M, ldm, fp, piv)));
+    if (lookahead && plast >= 0) MDS_CUDA_TRY(cudaStreamWaitEvent(st, (*evs)[2 * plast + 1], 0));
+    MDS_LAUNCH(PC_PANEL_SLOW, st, (k_panel_slow<<<1, 1024, 0, st>>>(N, M, ldm, fp, piv)));
     const int64_t n2max = std::max<int64_t>(rows - 1, 0);
-    const int64_t nt = mds_cdiv(n2max, UT);
-    if (nt > 0) {
-      k_update<<<(unsigned)(nt * (nt + 1) / 2), 128, usmem, st>>>(N, M, ldm, f);
-      MDS_LAUNCH_CHECK();
+    const int64_t nt = mds_cdiv(n2max, UT) + 1;
+    if (n2max > 0) {
+      const CUtensorMap& mw = (p & 1) ? mapW1 : mapW;
+      if (lookahead) {
+        MDS_CUDA_TRY(cudaEventRecord((*evs)[2 * p], st));
+        const unsigned gn = (unsigned)std::min<int64_t>(2 * nt, sms);
+        MDS_LAUNCH(PC_UPDATE, st, (k_update_tma<<<gn, 288, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, 1)));
+        MDS_CUDA_TRY(cudaStreamWaitEvent(side, (*evs)[2 * p], 0));
+        const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt * (nt + 1) / 2, sms - reserve));
+        MDS_LAUNCH(PC_UPDATE, side, (k_update_tma<<<gr, 288, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, 2)));
+        MDS_CUDA_TRY(cudaEventRecord((*evs)[2 * p + 1], side));
+        plast = p;
+      } else {
+        const unsigned ugrid = (unsigned)std::min<int64_t>(nt * (nt + 1) / 2, sms);
+        if (use_tma)
+          MDS_LAUNCH(PC_UPDATE, st, (k_update_tma<<<ugrid, 288, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, 0)));
+        else if (v16)
+          MDS_LAUNCH(PC_UPDATE, st,
+                     (k_update<true><<<ugrid, 128, 2 * USTAGE * sizeof(double), st>>>(N, M, ldm, fp)));
+        else
+          MDS_LAUNCH(PC_UPDATE, st,
+                     (k_update<false><<<ugrid, 128, 2 * USTAGE * sizeof(double), st>>>(N, M, ldm, fp)));
+      }
     }
   }
+  if (lookahead && plast >= 0) MDS_CUDA_TRY(cudaStreamWaitEvent(st, (*evs)[2 * plast + 1], 0));
   {
     int dev = 0, sms = 148, occ = 0;
     cudaGetDevice(&dev);
@@ -667,7 +1135,8 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_factor_finalize, 256, 0);
     int blocks = sms * std::max(1, std::min(occ, 2));
     void* args[] = {&N, &M, &ldm, &f, &piv, &inertia_dev};
-    MDS_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_factor_finalize, blocks, 256, args, 0, st));
+    MDS_LAUNCH(PC_FINALIZE, st,
+               MDS_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_factor_finalize, blocks, 256, args, 0, st)));
   }
   if (inertia_host) {
     if (!inertia_dev) return MDS_ERR_ARG;

@@ -1,0 +1,66 @@
+// prof.cu — launch counter and per-kernel-class CUDA-event timing (used by
+// bench.py to measure the dominant kernel's average launch duration on the
+// stream it is launched on; off by default, never active during graph capture).
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+bool g_mds_prof = false;
+static std::atomic<unsigned long long> g_launches{0};
+static std::mutex g_mu;
+struct Rec { int cls; cudaEvent_t a, b; };
+static std::vector<Rec> g_recs;
+static std::vector<cudaEvent_t> g_pool;
+static int g_open_cls = -1;
+static cudaEvent_t g_open_ev = nullptr;
+
+static cudaEvent_t get_event() {
+  if (!g_pool.empty()) { cudaEvent_t e = g_pool.back(); g_pool.pop_back(); return e; }
+  cudaEvent_t e; cudaEventCreate(&e); return e;
+}
+
+void mds_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void mds_prof_start(int cls, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_open_cls = cls;
+  g_open_ev = get_event();
+  cudaEventRecord(g_open_ev, st);
+}
+
+void mds_prof_stop(int cls, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaEvent_t b = get_event();
+  cudaEventRecord(b, st);
+  g_recs.push_back(Rec{cls, g_open_ev, b});
+  g_open_ev = nullptr;
+}
+
+extern "C" unsigned long long mds_launch_count(void) { return g_launches.load(); }
+
+extern "C" int mds_profile_begin(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (auto& r : g_recs) { g_pool.push_back(r.a); g_pool.push_back(r.b); }
+  g_recs.clear();
+  g_mds_prof = true;
+  return MDS_OK;
+}
+
+extern "C" int mds_profile_end(double* ms_by_class, int64_t* launches_by_class, int ncls) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_mds_prof = false;
+  if (ncls < PC_COUNT || !ms_by_class || !launches_by_class) return MDS_ERR_ARG;
+  for (int c = 0; c < ncls; c++) { ms_by_class[c] = 0.0; launches_by_class[c] = 0; }
+  for (auto& r : g_recs) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) return MDS_ERR_CUDA;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    ms_by_class[r.cls] += ms;
+    launches_by_class[r.cls] += 1;
+  }
+  for (auto& r : g_recs) { g_pool.push_back(r.a); g_pool.push_back(r.b); }
+  g_recs.clear();
+  return MDS_OK;
+}

@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(ST) k_trsv_bwd(int64_t N, const double* __rest
   double acc[8];
 #pragma unroll
   for (int u = 0; u < 8; u++) acc[u] = 0.0;
-  for (int64_t q = i + 1; q < nblk; q++) {
+  for (int64_t q = nblk - 1; q > i; q--) {   // completion order: last block finishes first
     if (threadIdx.x == 0) {
       while (atomicAdd(&flags[q], 0) == 0) { __nanosleep(32); }
     }
@@ -225,18 +225,15 @@ extern "C" int mds_solve(const mds_plan* plan, int64_t N, const double* LD, int6
     MDS_CUDA_TRY(cudaMemsetAsync(s.tickets, 0, sizeof(int) * 4, st));
     MDS_CUDA_TRY(cudaMemsetAsync(s.flags, 0, sizeof(int) * (nblk + 1), st));
     const unsigned ge = (unsigned)std::min<int64_t>(mds_cdiv(N, 256), 148 * 8);
-    k_gather<<<ge, 256, 0, st>>>(N, piv, rhs_c, s.y);
-    MDS_LAUNCH_CHECK();
-    k_trsv_fwd<<<(unsigned)nblk, ST, 0, st>>>(N, LD, ldm, s.y, s.flags, s.tickets);
-    MDS_LAUNCH_CHECK();
+    MDS_LAUNCH(PC_SOLVE_GATHER, st, (k_gather<<<ge, 256, 0, st>>>(N, piv, rhs_c, s.y)));
+    MDS_LAUNCH(PC_SOLVE_FWD, st, (k_trsv_fwd<<<(unsigned)nblk, ST, 0, st>>>(N, LD, ldm, s.y, s.flags, s.tickets)));
     const double* tolp = (zero_tol < 0.0 && fwork) ? mds_factor_tol_ptr(fwork) : nullptr;
-    k_dsolve<<<ge, 256, 0, st>>>(N, LD, ldm, piv, s.y, tolp, zero_tol < 0.0 ? 0.0 : zero_tol, status);
-    MDS_LAUNCH_CHECK();
+    MDS_LAUNCH(PC_SOLVE_D, st,
+               (k_dsolve<<<ge, 256, 0, st>>>(N, LD, ldm, piv, s.y, tolp, zero_tol < 0.0 ? 0.0 : zero_tol, status)));
     MDS_CUDA_TRY(cudaMemsetAsync(s.flags, 0, sizeof(int) * (nblk + 1), st));
-    k_trsv_bwd<<<(unsigned)nblk, ST, 0, st>>>(N, LD, ldm, s.y, s.flags, s.tickets + 1);
-    MDS_LAUNCH_CHECK();
-    k_scatter<<<ge, 256, 0, st>>>(N, piv, s.y, dxy);
-    MDS_LAUNCH_CHECK();
+    MDS_LAUNCH(PC_SOLVE_BWD, st,
+               (k_trsv_bwd<<<(unsigned)nblk, ST, 0, st>>>(N, LD, ldm, s.y, s.flags, s.tickets + 1)));
+    MDS_LAUNCH(PC_SOLVE_SCATTER, st, (k_scatter<<<ge, 256, 0, st>>>(N, piv, s.y, dxy)));
   }
   if (plan && dx_s) {
     int64_t dims[5];
@@ -246,9 +243,9 @@ extern "C" int mds_solve(const mds_plan* plan, int64_t N, const double* LD, int6
     if (n_s > 0) {
       if (!w || !r_xs || (dims[4] > 0 && !js_val)) return MDS_ERR_ARG;
       const unsigned g = (unsigned)std::min<int64_t>(mds_cdiv(n_s, 256), 148 * 16);
-      k_recover<<<g, 256, 0, st>>>(n_s, mds_plan_rowptr(plan), mds_plan_colidx(plan), js_val, w, r_xs, dxy + n_d,
-                                   dx_s);
-      MDS_LAUNCH_CHECK();
+      MDS_LAUNCH(PC_RECOVER, st,
+                 (k_recover<<<g, 256, 0, st>>>(n_s, mds_plan_rowptr(plan), mds_plan_colidx(plan), js_val, w, r_xs,
+                                               dxy + n_d, dx_s)));
     }
   }
   return MDS_OK;

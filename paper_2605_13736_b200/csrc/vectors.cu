@@ -184,8 +184,9 @@ extern "C" int ipm_step_vectors(int64_t n, const double* x, const double* dx, co
   unsigned int* counter = reinterpret_cast<unsigned int*>(work);
   double* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(work) + 256);
   int grid = vec_grid(n);
-  k_step_vectors<<<grid, VT, 0, (cudaStream_t)stream>>>(n, x, dx, lo, up, zl, zu, dzl, dzu, tau, mu, R, out,
-                                                         sigma_out, status, partials, counter);
-  MDS_LAUNCH_CHECK();
+  cudaStream_t st = (cudaStream_t)stream;
+  MDS_LAUNCH(PC_VECTORS, st,
+             (k_step_vectors<<<grid, VT, 0, st>>>(n, x, dx, lo, up, zl, zu, dzl, dzu, tau, mu, R, out, sigma_out,
+                                                  status, partials, counter)));
   return MDS_OK;
 }
