@@ -427,6 +427,18 @@ __device__ __forceinline__ ArgMax block_argmax(ArgMax a, ArgMax* sh) {
   return sh[32];
 }
 
+// W columns [kb, NB) of rows >= k0 hold speculative / stale values; the TMA
+// update multiplies all NB columns, so they must be exactly zero.
+__device__ __forceinline__ void zero_w_tail(int64_t N, int64_t k0, int kb, const FWork& f) {
+  const int64_t nr = N - k0;
+  const int nc = NB - kb;
+  if (nr <= 0 || nc <= 0) return;
+  for (int64_t idx = threadIdx.x; idx < nr * nc; idx += blockDim.x) {
+    const int64_t r = k0 + idx % nr, c = kb + idx / nr;
+    f.W[r + c * f.ldw] = 0.0;
+  }
+}
+
 __global__ void __launch_bounds__(1024) k_panel_slow(int64_t N, double* __restrict__ A, int64_t lda, FWork f,
                                                      int32_t* piv) {
   FCtl* ctl = f.ctl;
@@ -438,6 +450,7 @@ __global__ void __launch_bounds__(1024) k_panel_slow(int64_t N, double* __restri
   const int jlim = last ? nbp : nbp - 1;
   if (nbp == 0 || j >= jlim) {   // nothing left for the exact path: publish (k0, kb) for the updates
     if (threadIdx.x == 0) f.pinfo[f.pidx] = make_int2((int)k0, nbp == 0 ? 0 : j);
+    if (nbp > 0) zero_w_tail(N, k0, j, f);
     return;
   }
   __shared__ double wrow[WCOLS];
@@ -553,6 +566,7 @@ __global__ void __launch_bounds__(1024) k_panel_slow(int64_t N, double* __restri
     ctl->kb = j;
     f.pinfo[f.pidx] = make_int2((int)k0, j);
   }
+  zero_w_tail(N, k0, j, f);
 }
 
 // ---------------------------------------------------------------------------
@@ -720,9 +734,11 @@ __global__ void __launch_bounds__(128, 1) k_update(int64_t N, double* __restrict
 // fragment reads), completion tracked by mbarriers; two consumer groups of
 // 4 warps each take alternate tiles ("ping-pong"), so one group's C loads
 // and epilogue stores overlap the other group's DMMA k-loop.
-constexpr int TS = 3;                             // pipeline stages
+constexpr int TNG = 2;                            // consumer groups (4 warps each), ping-pong
+constexpr int TS = TNG;                           // pipeline stages (stage i % TS == group of tile i)
+constexpr int TTHREADS = 32 * (1 + 4 * TNG);      // producer warp + consumer warps
 constexpr int TOPB = UT * NB * 8;                 // bytes per operand tile (32 KB)
-constexpr int TSTAGEB = 2 * TOPB;                 // L + W
+constexpr int TSTAGEB = 3 * TOPB;                 // C + L + W
 constexpr int TSMEM = TS * TSTAGEB + 1024 + 64;   // + alignment + barriers
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -776,9 +792,21 @@ __device__ __forceinline__ void upd_tile(int64_t x, int64_t nt, int mode, int64_
   bi += 2; bj += 2;
 }
 
-__global__ void __launch_bounds__(288, 1) k_update_tma(int64_t N, double* __restrict__ A, int64_t lda, FWork f,
-                                                       const __grid_constant__ CUtensorMap mapA,
-                                                       const __grid_constant__ CUtensorMap mapW, int mode) {
+__device__ __forceinline__ double lds_f64(unsigned addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ double dneg(double v) {   // exact sign flip on the integer pipe (not DADD)
+  double r;
+  asm("{\n .reg .b64 t;\n mov.b64 t, %1;\n xor.b64 t, t, 0x8000000000000000;\n mov.b64 %0, t;\n}\n"
+      : "=d"(r) : "d"(v));
+  return r;
+}
+
+__global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* __restrict__ A, int64_t lda, FWork f,
+                                                             const __grid_constant__ CUtensorMap mapA,
+                                                             const __grid_constant__ CUtensorMap mapW, int mode) {
   FCtl* ctl = f.ctl;
   if (ctl->abort) return;
   const int2 pi = f.pinfo[f.pidx];
@@ -792,9 +820,9 @@ __global__ void __launch_bounds__(288, 1) k_update_tma(int64_t N, double* __rest
   if ((int64_t)blockIdx.x >= ntiles) return;
   const int ntile_cta = (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
   extern __shared__ unsigned char tsm_raw[];
-  unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~(uintptr_t)1023);
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(tsm + TS * TSTAGEB);
-  const unsigned full0 = smem_u32(bars), empty0 = smem_u32(bars + TS);
+  // all shared addresses as 32-bit shared-window offsets (keeps LDS, not generic LD)
+  const unsigned tsm = (smem_u32(tsm_raw) + 1023u) & ~1023u;
+  const unsigned full0 = tsm + TS * TSTAGEB, empty0 = full0 + 8 * TS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < TS; i++) { mbar_init(full0 + 8 * i, 1); mbar_init(empty0 + 8 * i, 4); }
@@ -802,7 +830,7 @@ __global__ void __launch_bounds__(288, 1) k_update_tma(int64_t N, double* __rest
   }
   __syncthreads();
   if (warp == 0) {
-    // ---------------- producer: one elected lane issues all TMA copies
+    // ---------------- producer: one lane issues all TMA copies (C, L and W tiles)
     if (lane == 0) {
       for (int i = 0; i < ntile_cta; i++) {
         const int st = i % TS, u = i / TS;
@@ -811,11 +839,12 @@ __global__ void __launch_bounds__(288, 1) k_update_tma(int64_t N, double* __rest
         int64_t bi, bj;
         upd_tile(x, nt, mode, bi, bj);
         const int R0 = (int)((b0 + bi) * UT), C0 = (int)((b0 + bj) * UT);
-        const unsigned sL = smem_u32(tsm + st * TSTAGEB), sW = sL + TOPB;
+        const unsigned sC = tsm + st * TSTAGEB, sL = sC + TOPB, sW = sL + TOPB;
         const unsigned fb = full0 + 8 * st;
         mbar_expect_tx(fb, TSTAGEB);
 #pragma unroll
         for (int b = 0; b < 8; b++) {
+          tma_load_2d(sC + b * 4096, &mapA, R0 + 8 * b, C0, fb);
           tma_load_2d(sL + b * 4096, &mapA, R0 + 8 * b, (int)k0, fb);
           tma_load_2d(sW + b * 4096, &mapW, C0 + 8 * b, 0, fb);
         }
@@ -823,49 +852,52 @@ __global__ void __launch_bounds__(288, 1) k_update_tma(int64_t N, double* __rest
     }
     return;
   }
-  // ---------------- consumers: group grp takes tiles grp, grp+2, ...
+  // ---------------- consumers: group grp takes tiles grp, grp+TNG, ... (stage == group)
   const int grp = (warp - 1) >> 2, wq = (warp - 1) & 3;
   const int wm = (wq >> 1) * 32, wn = (wq & 1) * 32;
   const int g = lane >> 2, q = lane & 3;
-  for (int i = grp; i < ntile_cta; i += 2) {
+  for (int i = grp; i < ntile_cta; i += TNG) {
     const int st = i % TS, u = i / TS;
     const int64_t x = blockIdx.x + (int64_t)i * gridDim.x;
     int64_t bi, bj;
     upd_tile(x, nt, mode, bi, bj);
     const int64_t R0 = (b0 + bi) * UT, C0 = (b0 + bj) * UT;
+    mbar_wait(full0 + 8 * st, u & 1);
+    const unsigned Ct = tsm + st * TSTAGEB;
+    const unsigned Lb = Ct + TOPB + (unsigned)(wm >> 3) * 4096u;
+    const unsigned Wb = Ct + 2 * TOPB + (unsigned)(wn >> 3) * 4096u;
+    // acc = -C ; acc += L W^T ; C_new = -acc   (negations are exact)
     double acc[4][4][2];
 #pragma unroll
-    for (int a = 0; a < 4; a++) {
-      const int64_t row = R0 + wm + 8 * a + g;
+    for (int a = 0; a < 4; a++)
 #pragma unroll
       for (int b = 0; b < 4; b++)
 #pragma unroll
-        for (int e = 0; e < 2; e++) {
-          const int64_t col = C0 + wn + 8 * b + 2 * q + e;
-          acc[a][b][e] = (row < N && col < N && row >= col) ? A[row + col * lda] : 0.0;
-        }
-    }
-    mbar_wait(full0 + 8 * st, u & 1);
-    const unsigned char* Lt = tsm + st * TSTAGEB;
-    const unsigned char* Wt = Lt + TOPB;
-#pragma unroll 4
-    for (int t0 = 0; t0 < NB; t0 += 4) {
-      const int t = t0 + q;
-      double av[4], bv[4];
+        for (int e = 0; e < 2; e++)
+          acc[a][b][e] = dneg(lds_f64(Ct + tma_off(wm + 8 * a + g, wn + 8 * b + 2 * q + e)));
+    // k-loop with register double-buffered fragments (loads of step t+1 overlap the DMMAs of step t)
+    double a0[4], b0v[4], a1[4], b1v[4];
+    auto frag = [&](int ks, double* av, double* bv) {
+      const unsigned t = (unsigned)(4 * ks + q);
+      const unsigned off = (t * 64u + (unsigned)g * 8u) ^ (((t >> 1) & 3u) << 4);
 #pragma unroll
-      for (int a = 0; a < 4; a++) {
-        const double v = *reinterpret_cast<const double*>(Lt + tma_off(wm + 8 * a + g, t));
-        av[a] = (t < kb) ? -v : 0.0;
-      }
+      for (int a = 0; a < 4; a++) av[a] = lds_f64(Lb + (unsigned)a * 4096u + off);
 #pragma unroll
-      for (int b = 0; b < 4; b++) {
-        const double v = *reinterpret_cast<const double*>(Wt + tma_off(wn + 8 * b + g, t));
-        bv[b] = (t < kb) ? v : 0.0;
-      }
+      for (int b = 0; b < 4; b++) bv[b] = lds_f64(Wb + (unsigned)b * 4096u + off);
+    };
+    frag(0, a0, b0v);
+#pragma unroll 1
+    for (int ks = 0; ks < NB / 4; ks += 2) {
+      frag(ks + 1, a1, b1v);
 #pragma unroll
       for (int a = 0; a < 4; a++)
 #pragma unroll
-        for (int b = 0; b < 4; b++) dmma(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+        for (int b = 0; b < 4; b++) dmma(acc[a][b][0], acc[a][b][1], a0[a], b0v[b]);
+      if (ks + 2 < NB / 4) frag(ks + 2, a0, b0v);
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) dmma(acc[a][b][0], acc[a][b][1], a1[a], b1v[b]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * st);
@@ -877,7 +909,7 @@ __global__ void __launch_bounds__(288, 1) k_update_tma(int64_t N, double* __rest
 #pragma unroll
         for (int e = 0; e < 2; e++) {
           const int64_t col = C0 + wn + 8 * b + 2 * q + e;
-          if (row < N && col >= s && row >= col) A[row + col * lda] = acc[a][b][e];
+          if (row < N && col >= s && row >= col) A[row + col * lda] = dneg(acc[a][b][e]);
         }
     }
   }
@@ -1108,16 +1140,16 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
       if (lookahead) {
         MDS_CUDA_TRY(cudaEventRecord((*evs)[2 * p], st));
         const unsigned gn = (unsigned)std::min<int64_t>(2 * nt, sms);
-        MDS_LAUNCH(PC_UPDATE, st, (k_update_tma<<<gn, 288, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, 1)));
+        MDS_LAUNCH(PC_UPDATE, st, (k_update_tma<<<gn, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, 1)));
         MDS_CUDA_TRY(cudaStreamWaitEvent(side, (*evs)[2 * p], 0));
         const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt * (nt + 1) / 2, sms - reserve));
-        MDS_LAUNCH(PC_UPDATE, side, (k_update_tma<<<gr, 288, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, 2)));
+        MDS_LAUNCH(PC_UPDATE, side, (k_update_tma<<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, 2)));
         MDS_CUDA_TRY(cudaEventRecord((*evs)[2 * p + 1], side));
         plast = p;
       } else {
         const unsigned ugrid = (unsigned)std::min<int64_t>(nt * (nt + 1) / 2, sms);
         if (use_tma)
-          MDS_LAUNCH(PC_UPDATE, st, (k_update_tma<<<ugrid, 288, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, 0)));
+          MDS_LAUNCH(PC_UPDATE, st, (k_update_tma<<<ugrid, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, 0)));
         else if (v16)
           MDS_LAUNCH(PC_UPDATE, st,
                      (k_update<true><<<ugrid, 128, 2 * USTAGE * sizeof(double), st>>>(N, M, ldm, fp)));
