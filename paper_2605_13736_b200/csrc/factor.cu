@@ -30,6 +30,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -1027,25 +1029,31 @@ double* mds_factor_tol_ptr(const void* fwork) {
   return fwork ? &reinterpret_cast<FCtl*>(const_cast<void*>(fwork))->tol : nullptr;
 }
 
-// side stream (per device) and reusable events for the look-ahead split
-static cudaStream_t side_stream() {
-  static cudaStream_t streams[64] = {nullptr};
+// Side stream + reusable events for the look-ahead split, one set per CALLER
+// stream (so concurrent factorizations on different streams never share
+// events; a call on stream s always orders its side work through s).
+struct LookaheadCtx {
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> ev;
+};
+static std::mutex g_la_mu;
+static std::map<std::pair<int, cudaStream_t>, LookaheadCtx*> g_la;
+
+static LookaheadCtx* lookahead_ctx(cudaStream_t st, size_t nev) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-  return streams[dev];
-}
-static std::vector<cudaEvent_t>* event_pool(size_t n) {
-  static std::vector<cudaEvent_t> pools[64];
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  auto& v = pools[dev];
-  while (v.size() < n) {
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(g_la_mu);
+  LookaheadCtx*& c = g_la[std::make_pair(dev, st)];
+  if (!c) {
+    c = new LookaheadCtx();
+    if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) { delete c; c = nullptr; return nullptr; }
+  }
+  while (c->ev.size() < nev) {
     cudaEvent_t e;
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
-    v.push_back(e);
+    c->ev.push_back(e);
   }
-  return &v;
+  return c;
 }
 
 extern "C" size_t mds_factor_workspace_size(int64_t N) {
@@ -1111,9 +1119,10 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   cudaStream_t side = nullptr;
   std::vector<cudaEvent_t>* evs = nullptr;
   if (lookahead) {
-    side = side_stream();
-    evs = event_pool(2 * (size_t)npmax + 2);
-    if (!side || !evs) return MDS_ERR_CUDA;
+    LookaheadCtx* c = lookahead_ctx(st, 2 * (size_t)npmax + 2);
+    if (!c) return MDS_ERR_CUDA;
+    side = c->side;
+    evs = &c->ev;
   }
   CUtensorMap mapW1;
   if (use_tma && !make_map(&mapW1, f.W1, N, NB, f.ldw)) return MDS_ERR_CUDA;

@@ -22,6 +22,7 @@ constexpr int PERM_MASK = (1 << 29) - 1;
 
 struct SWork {
   double* y;
+  double* binv;   // [nblk][TB*TB] inverses of the unit-lower diagonal blocks (column-major)
   int* flags;     // [nblk]
   int* tickets;   // [2]
 };
@@ -35,6 +36,7 @@ SWork carve(void* work, int64_t N, size_t* total) {
   s.tickets = reinterpret_cast<int*>(take(sizeof(int) * 4));
   s.flags = reinterpret_cast<int*>(take(sizeof(int) * (N / TB + 2)));
   s.y = reinterpret_cast<double*>(take(sizeof(double) * std::max<int64_t>(N, 1)));
+  s.binv = reinterpret_cast<double*>(take(sizeof(double) * TB * TB * (N / TB + 1)));
   if (total) *total = off;
   return s;
 }
@@ -47,54 +49,104 @@ __global__ void k_gather(int64_t N, const int32_t* __restrict__ piv, const doubl
     y[i] = b[piv[N + i] & PERM_MASK];
 }
 
-// forward: L y = y (unit lower; 2x2 D off-diagonals were moved out of L by the factor)
+// Inverses of the unit-lower TB x TB diagonal blocks of L (one CTA per block,
+// row-by-row: Binv[r][c] = -sum_{k=c}^{r-1} L[r][k] Binv[k][c]).  With them the
+// dependent chain of the triangular sweeps is two small GEMVs per block.
+__global__ void __launch_bounds__(256) k_inv_blocks(int64_t N, const double* __restrict__ L, int64_t lda,
+                                                    double* __restrict__ binv) {
+  extern __shared__ double ism[];
+  double* Ls = ism;                      // Ls[k*(TB+1) + r] = L[r][k]
+  double* Bs = ism + TB * (TB + 1);      // Bs[c*(TB+1) + r] = Binv[r][c]
+  const int64_t i = blockIdx.x;
+  const int64_t r0 = i * TB;
+  const int nr = (int)((N - r0) < TB ? (N - r0) : TB);
+  for (int idx = threadIdx.x; idx < TB * TB; idx += blockDim.x) {
+    const int r = idx % TB, c = idx / TB;
+    Ls[c * (TB + 1) + r] = (r < nr && c < nr && r > c) ? L[(r0 + r) + (r0 + c) * lda] : 0.0;
+    Bs[c * (TB + 1) + r] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  // 4 threads per column c split the dot product; rows r sequential
+  const int c = threadIdx.x >> 2, part = threadIdx.x & 3;
+  for (int r = 1; r < nr; r++) {
+    double sacc = 0.0;
+    if (c < r) {
+      for (int k = c + part; k < r; k += 4) sacc += Ls[k * (TB + 1) + r] * Bs[c * (TB + 1) + k];
+    }
+    sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+    sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+    if (c < r && part == 0) Bs[c * (TB + 1) + r] = -sacc;
+    __syncthreads();
+  }
+  double* out = binv + (size_t)i * TB * TB;
+  for (int idx = threadIdx.x; idx < TB * TB; idx += blockDim.x) {
+    const int r = idx % TB, cc = idx / TB;
+    out[idx] = Bs[cc * (TB + 1) + r];
+  }
+}
+
+// forward: L y = y (unit lower; 2x2 D off-diagonals were moved out of L by the factor).
+// CTA i (ticket order) streams its row block of L against the published y_q, the
+// loads of L for block q+1 issued before waiting on block q's flag; then
+// y_i = Binv_i (b_i - acc).
 __global__ void __launch_bounds__(ST) k_trsv_fwd(int64_t N, const double* __restrict__ L, int64_t lda, double* y,
-                                                 int* flags, int* ticket) {
+                                                 const double* __restrict__ binv, int* flags, int* ticket) {
   __shared__ int s_i;
   __shared__ double part[ST / TB][TB];
-  __shared__ double Ld[TB * (TB + 1)];
+  __shared__ double v[TB];
   if (threadIdx.x == 0) s_i = atomicAdd(ticket, 1);
   __syncthreads();
   const int64_t i = s_i;
   const int64_t r0 = i * TB;
   const int nr = (int)((N - r0) < TB ? (N - r0) : TB);
   const int r = threadIdx.x & (TB - 1), cgp = threadIdx.x / TB;   // 4 column groups of 16
-  // stage the diagonal block while waiting
-  for (int idx = threadIdx.x; idx < TB * TB; idx += ST) {
-    const int rr = idx % TB, cc = idx / TB;
-    Ld[cc * (TB + 1) + rr] = (rr < nr && cc < nr && rr > cc) ? L[(r0 + rr) + (r0 + cc) * lda] : 0.0;
-  }
   double acc = 0.0;
+  double lv[16], ln[16];
+  const double* Lr = L + (r0 + r);
+  auto loadL = [&](int64_t q, double* dst) {
+    const int64_t c0 = q * TB + cgp * 16;
+#pragma unroll
+    for (int c = 0; c < 16; c++) dst[c] = (r < nr) ? Lr[(c0 + c) * lda] : 0.0;
+  };
+  if (i > 0) loadL(0, lv);
   for (int64_t q = 0; q < i; q++) {
+    if (q + 1 < i) loadL(q + 1, ln);
     if (threadIdx.x == 0) {
-      while (atomicAdd(&flags[q], 0) == 0) { __nanosleep(32); }
+      while (*((volatile int*)&flags[q]) == 0) { }
+      __threadfence();
     }
     __syncthreads();
-    const int64_t c0 = q * TB + cgp * 16;
-    if (r < nr) {
+    const double* yq = y + q * TB + cgp * 16;
 #pragma unroll
-      for (int c = 0; c < 16; c++) acc += L[(r0 + r) + (c0 + c) * lda] * ld_cg(&y[c0 + c]);
-    }
+    for (int c = 0; c < 16; c++) acc += lv[c] * ld_cg(&yq[c]);
+#pragma unroll
+    for (int c = 0; c < 16; c++) lv[c] = ln[c];
   }
   part[cgp][r] = acc;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    double v0 = 0.0, v1 = 0.0;
-    if (lane < nr) v0 = ld_cg(&y[r0 + lane]) - (part[0][lane] + part[1][lane] + part[2][lane] + part[3][lane]);
-    if (lane + 32 < nr)
-      v1 = ld_cg(&y[r0 + lane + 32]) -
-           (part[0][lane + 32] + part[1][lane + 32] + part[2][lane + 32] + part[3][lane + 32]);
-    for (int c = 0; c < nr; c++) {
-      const double yc = __shfl_sync(0xffffffffu, c < 32 ? v0 : v1, c & 31);
-      if (lane > c) v0 -= Ld[c * (TB + 1) + lane] * yc;
-      if (lane + 32 > c) v1 -= Ld[c * (TB + 1) + lane + 32] * yc;
-    }
-    if (lane < nr) y[r0 + lane] = v0;
-    if (lane + 32 < nr) y[r0 + lane + 32] = v1;
+  if (threadIdx.x < TB) {
+    const int rr = threadIdx.x;
+    v[rr] = (rr < nr) ? ld_cg(&y[r0 + rr]) - (part[0][rr] + part[1][rr] + part[2][rr] + part[3][rr]) : 0.0;
+  }
+  __syncthreads();
+  // y_i = Binv v : thread (r, cgp) sums 16 columns, reduce over the 4 groups
+  const double* B = binv + (size_t)i * TB * TB;
+  double sacc = 0.0;
+#pragma unroll
+  for (int c = 0; c < 16; c++) {
+    const int cc = cgp * 16 + c;
+    sacc += B[r + cc * TB] * v[cc];
+  }
+  part[cgp][r] = sacc;
+  __syncthreads();
+  if (threadIdx.x < TB) {
+    const int rr = threadIdx.x;
+    if (rr < nr) y[r0 + rr] = part[0][rr] + part[1][rr] + part[2][rr] + part[3][rr];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
     __threadfence();
-    __syncwarp();
-    if (lane == 0) atomicExch(&flags[i], 1);
+    atomicExch(&flags[i], 1);
   }
 }
 
@@ -121,69 +173,85 @@ __global__ void k_dsolve(int64_t N, const double* __restrict__ LD, int64_t lda, 
   }
 }
 
-// backward: L^T x = z, blocks from the bottom
+// backward: L^T x = z, blocks from the bottom.  CTA i accumulates
+// sum_{q>i} L[q rows, i cols]^T x_q (threads run down contiguous column
+// segments: thread (k, cg) owns row k of every later block and 16 columns),
+// then x_i = Binv_i^T (z_i - acc).
 __global__ void __launch_bounds__(ST) k_trsv_bwd(int64_t N, const double* __restrict__ L, int64_t lda, double* y,
-                                                 int* flags, int* ticket) {
+                                                 const double* __restrict__ binv, int* flags, int* ticket) {
   __shared__ int s_i;
-  __shared__ double Ld[TB * (TB + 1)];
-  __shared__ double colsum[TB];
+  __shared__ double red[ST / 32][TB];
+  __shared__ double v[TB];
   const int64_t nblk = (N + TB - 1) / TB;
   if (threadIdx.x == 0) s_i = atomicAdd(ticket, 1);
   __syncthreads();
   const int64_t i = nblk - 1 - s_i;
   const int64_t r0 = i * TB;
   const int nr = (int)((N - r0) < TB ? (N - r0) : TB);
-  for (int idx = threadIdx.x; idx < TB * TB; idx += ST) {
-    const int rr = idx % TB, cc = idx / TB;
-    Ld[cc * (TB + 1) + rr] = (rr < nr && cc < nr && rr > cc) ? L[(r0 + rr) + (r0 + cc) * lda] : 0.0;
-  }
+  const int k = threadIdx.x & (TB - 1), cgp = threadIdx.x / TB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // warp w owns columns c = w + 8*u (u < 8) of this block; lanes stride rows of later blocks
-  double acc[8];
+  double acc[16];
 #pragma unroll
-  for (int u = 0; u < 8; u++) acc[u] = 0.0;
+  for (int c = 0; c < 16; c++) acc[c] = 0.0;
+  double lv[16], ln[16];
+  auto loadL = [&](int64_t q, double* dst) {
+    const int64_t row = q * TB + k;
+    const bool ok = row < N;
+#pragma unroll
+    for (int c = 0; c < 16; c++) {
+      const int cc = cgp * 16 + c;
+      dst[c] = (ok && cc < nr) ? L[row + (r0 + cc) * lda] : 0.0;
+    }
+  };
+  if (nblk - 1 > i) loadL(nblk - 1, lv);
   for (int64_t q = nblk - 1; q > i; q--) {   // completion order: last block finishes first
+    if (q - 1 > i) loadL(q - 1, ln);
     if (threadIdx.x == 0) {
-      while (atomicAdd(&flags[q], 0) == 0) { __nanosleep(32); }
+      while (*((volatile int*)&flags[q]) == 0) { }
+      __threadfence();
     }
     __syncthreads();
-    const int64_t q0 = q * TB;
-    const int qn = (int)((N - q0) < TB ? (N - q0) : TB);
-    const double x0 = (lane < qn) ? ld_cg(&y[q0 + lane]) : 0.0;
-    const double x1 = (lane + 32 < qn) ? ld_cg(&y[q0 + lane + 32]) : 0.0;
+    const int64_t row = q * TB + k;
+    const double xq = (row < N) ? ld_cg(&y[row]) : 0.0;
 #pragma unroll
-    for (int u = 0; u < 8; u++) {
-      const int c = warp + 8 * u;
-      if (c < nr) {
-        const double* Lc = L + (r0 + c) * lda + q0;
-        double s = 0.0;
-        if (lane < qn) s += Lc[lane] * x0;
-        if (lane + 32 < qn) s += Lc[lane + 32] * x1;
-        acc[u] += s;
-      }
-    }
+    for (int c = 0; c < 16; c++) acc[c] += lv[c] * xq;
+#pragma unroll
+    for (int c = 0; c < 16; c++) lv[c] = ln[c];
   }
+  // reduce acc over the 64 rows k: warp shuffle (32 rows) then the 2 warps of each column group
 #pragma unroll
-  for (int u = 0; u < 8; u++) {
-    const double v = warp_sum(acc[u]);
-    if (lane == 0) colsum[warp + 8 * u] = v;
+  for (int c = 0; c < 16; c++) {
+    double t = acc[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) red[warp][c] = t;
   }
   __syncthreads();
-  if (warp == 0) {
-    double v0 = 0.0, v1 = 0.0;
-    if (lane < nr) v0 = ld_cg(&y[r0 + lane]) - colsum[lane];
-    if (lane + 32 < nr) v1 = ld_cg(&y[r0 + lane + 32]) - colsum[lane + 32];
-    for (int c = nr - 1; c >= 0; c--) {
-      const double xc = __shfl_sync(0xffffffffu, c < 32 ? v0 : v1, c & 31);
-      // row c of L (columns < c) : v_{c'} -= L[c, c'] * x_c
-      if (lane < c) v0 -= Ld[lane * (TB + 1) + c] * xc;
-      if (lane + 32 < c) v1 -= Ld[(lane + 32) * (TB + 1) + c] * xc;
-    }
-    if (lane < nr) y[r0 + lane] = v0;
-    if (lane + 32 < nr) y[r0 + lane + 32] = v1;
+  if (threadIdx.x < TB) {
+    const int cc = threadIdx.x;
+    const int grp = cc >> 4, c = cc & 15;
+    const double sum = red[2 * grp][c] + red[2 * grp + 1][c];
+    v[cc] = (cc < nr) ? ld_cg(&y[r0 + cc]) - sum : 0.0;
+  }
+  __syncthreads();
+  // x_i = Binv^T v : x[c] = sum_r Binv[r][c] v[r]; thread (c = k, group cgp) sums 16 rows
+  const double* B = binv + (size_t)i * TB * TB;
+  double sacc = 0.0;
+#pragma unroll
+  for (int rr = 0; rr < 16; rr++) {
+    const int r = cgp * 16 + rr;
+    sacc += B[r + k * TB] * v[r];
+  }
+  red[cgp][k] = sacc;
+  __syncthreads();
+  if (threadIdx.x < TB) {
+    const int cc = threadIdx.x;
+    if (cc < nr) y[r0 + cc] = red[0][cc] + red[1][cc] + red[2][cc] + red[3][cc];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
     __threadfence();
-    __syncwarp();
-    if (lane == 0) atomicExch(&flags[i], 1);
+    atomicExch(&flags[i], 1);
   }
 }
 
@@ -226,13 +294,21 @@ extern "C" int mds_solve(const mds_plan* plan, int64_t N, const double* LD, int6
     MDS_CUDA_TRY(cudaMemsetAsync(s.flags, 0, sizeof(int) * (nblk + 1), st));
     const unsigned ge = (unsigned)std::min<int64_t>(mds_cdiv(N, 256), 148 * 8);
     MDS_LAUNCH(PC_SOLVE_GATHER, st, (k_gather<<<ge, 256, 0, st>>>(N, piv, rhs_c, s.y)));
-    MDS_LAUNCH(PC_SOLVE_FWD, st, (k_trsv_fwd<<<(unsigned)nblk, ST, 0, st>>>(N, LD, ldm, s.y, s.flags, s.tickets)));
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_inv_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TB * (TB + 1) * 8);
+      attr = true;
+    }
+    MDS_LAUNCH(PC_SOLVE_FWD, st,
+               (k_inv_blocks<<<(unsigned)nblk, 256, 2 * TB * (TB + 1) * sizeof(double), st>>>(N, LD, ldm, s.binv)));
+    MDS_LAUNCH(PC_SOLVE_FWD, st,
+               (k_trsv_fwd<<<(unsigned)nblk, ST, 0, st>>>(N, LD, ldm, s.y, s.binv, s.flags, s.tickets)));
     const double* tolp = (zero_tol < 0.0 && fwork) ? mds_factor_tol_ptr(fwork) : nullptr;
     MDS_LAUNCH(PC_SOLVE_D, st,
                (k_dsolve<<<ge, 256, 0, st>>>(N, LD, ldm, piv, s.y, tolp, zero_tol < 0.0 ? 0.0 : zero_tol, status)));
     MDS_CUDA_TRY(cudaMemsetAsync(s.flags, 0, sizeof(int) * (nblk + 1), st));
     MDS_LAUNCH(PC_SOLVE_BWD, st,
-               (k_trsv_bwd<<<(unsigned)nblk, ST, 0, st>>>(N, LD, ldm, s.y, s.flags, s.tickets + 1)));
+               (k_trsv_bwd<<<(unsigned)nblk, ST, 0, st>>>(N, LD, ldm, s.y, s.binv, s.flags, s.tickets + 1)));
     MDS_LAUNCH(PC_SOLVE_SCATTER, st, (k_scatter<<<ge, 256, 0, st>>>(N, piv, s.y, dxy)));
   }
   if (plan && dx_s) {
