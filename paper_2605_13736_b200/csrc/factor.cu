@@ -97,6 +97,14 @@ FWork carve(void* work, int64_t N, size_t* total) {
   return f;
 }
 
+// reciprocal for the pivot multipliers: MUFU seed + 2 Newton steps (off the
+// correctly-rounded slow path; the oracle's 1/d differs by <= 1 ulp)
+__device__ __forceinline__ double fast_rcp(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  const double e = fma(-d, r, 1.0);          // r (1 + e + e^2): 3 dependent FP64 ops after the seed
+  return fma(r, fma(e, e, e), r);
+}
 __device__ __forceinline__ unsigned long long dbits(double v) { return (unsigned long long)__double_as_longlong(v); }
 __device__ __forceinline__ double bitsd(unsigned long long b) { return __longlong_as_double((long long)b); }
 
@@ -168,23 +176,81 @@ __global__ void __launch_bounds__(1024) k_anorm_final(int64_t N, const double* r
 }
 
 // ---------------------------------------------------------------------------
-// F1: unpivoted LDL^T of the NB x NB diagonal block, register-blocked: a
-// 16x16 thread grid, each thread owning a 4x4 sub-block (rows tr+16a, cols
-// tc+16b) in registers; column j and row j of L^{-1} are broadcast through
-// shared memory once per elimination step (one __syncthreads per column).
-// The same elimination is applied to an identity block, accumulating
-// Linv = L11^{-1} (Gauss-Jordan style), so F2 can form W21 = A21 L11^{-T} as a
-// GEMM on the FP64 tensor cores (explicit inverted diagonal blocks, as MAGMA's
-// GPU trsm does).  Leaves W11 (updated, unscaled columns) in W, X = L11^{-T}
-// (row-major [t][j]) in Lblk, d and the in-block part of colmax in ctl.
-// A is NOT modified (rejected columns need their original values).
+// F1: unpivoted LDL^T of the NB x NB diagonal block (shared memory), blocked
+// right-looking with 16-column blocks: inside a block one column step per
+// __syncthreads touches only the block's 16 columns; the rest of the block
+// is updated once per 16 columns (rank-16).  Then L11^{-1} by a blocked
+// triangular inversion (16x16 diagonal blocks by one warp each, off-diagonal
+// blocks by small GEMMs), so F2 forms W21 = A21 L11^{-T} as a GEMM on the
+// FP64 tensor cores (explicit inverted diagonal blocks, as MAGMA's GPU trsm).
+// Leaves W11 (updated, unscaled columns) in W, X = L11^{-T} (row-major [t][j])
+// in Lblk, d and the in-block part of colmax in ctl.  A is NOT modified
+// (rejected columns need their original values).
+#ifdef MDS_F1_TIMING
+__device__ long long g_f1t[8];
+#define F1T(i) do { __syncthreads(); if (threadIdx.x == 0) g_f1t[i] = clock64(); } while (0)
+#else
+#define F1T(i) do { } while (0)
+#endif
+constexpr int F1S = NB + 1;                     // smem column stride
+constexpr int F1SMEM = 4 * NB * F1S * 8 + 2 * NB * 8;
+
+// One warp factors a 16-column panel (rows cb..nbp-1) held in registers: lane
+// owns rows cb+lane (+32); pivots and column values broadcast by shuffles.
+template <int SLOTS>
+__device__ __forceinline__ void f1_panel(double* As, double* Lm, double* rcp, int cb, int ce, int nbp, int lane) {
+  double pv[SLOTS][16];
+  int rr[SLOTS];
+#pragma unroll
+  for (int sl = 0; sl < SLOTS; sl++) {
+    rr[sl] = cb + 32 * sl + lane;
+#pragma unroll
+    for (int c = 0; c < 16; c++) pv[sl][c] = (rr[sl] < nbp && cb + c < ce) ? As[(cb + c) * F1S + rr[sl]] : 0.0;
+  }
+#pragma unroll
+  for (int jj = 0; jj < 16; jj++) {
+    const int j = cb + jj;
+    if (j < ce) {
+      const double d = __shfl_sync(0xffffffffu, pv[0][jj], jj);
+      const double r1 = (d != 0.0) ? fast_rcp(d) : 0.0;
+      double l[SLOTS];
+#pragma unroll
+      for (int sl = 0; sl < SLOTS; sl++) l[sl] = (rr[sl] > j) ? pv[sl][jj] * r1 : 0.0;
+#pragma unroll
+      for (int c = 1; c < 16; c++) {
+        if (c > jj) {
+          const double v = __shfl_sync(0xffffffffu, pv[0][jj], c);   // A(cb+c, j)
+#pragma unroll
+          for (int sl = 0; sl < SLOTS; sl++)
+            if (rr[sl] >= cb + c) pv[sl][c] -= l[sl] * v;
+        }
+      }
+      if (lane == 0) rcp[j] = r1;
+#pragma unroll
+      for (int sl = 0; sl < SLOTS; sl++)
+        if (rr[sl] < NB) Lm[j * F1S + rr[sl]] = l[sl];   // scaled multipliers of column j
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 16; c++) {
+    if (cb + c < ce) {
+#pragma unroll
+      for (int sl = 0; sl < SLOTS; sl++)
+        if (rr[sl] < nbp && rr[sl] >= cb + c) As[(cb + c) * F1S + rr[sl]] = pv[sl][c];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_panel_diag(int64_t N, const double* __restrict__ A, int64_t lda,
                                                     FWork f) {
   FCtl* ctl = f.ctl;
   if (ctl->abort) return;
-  __shared__ double colj[2][NB];
-  __shared__ double rowj[2][NB];
-  __shared__ double Wsh[NB * (NB + 1)];   // W11, column-major, stride NB+1
+  extern __shared__ double f1sm[];
+  double* As = f1sm;                 // As[c*F1S + r] : the block, updated in place (lower)
+  double* Li = As + NB * F1S;        // Li[c*F1S + r] = Linv[r][c]
+  double* Tm = Li + NB * F1S;        // temp GEMM block
+  double* Lm = Tm + NB * F1S;        // Lm[c*F1S + r] = L[r][c] (unit lower multipliers, r > c)
+  double* rcp = Lm + NB * F1S;       // 1/d_j (0 for an exactly zero pivot)
   __shared__ int s_k0;
   if (threadIdx.x == 0) s_k0 = ctl->k0 + ctl->kb;
   __syncthreads();
@@ -194,85 +260,185 @@ __global__ void __launch_bounds__(256) k_panel_diag(int64_t N, const double* __r
     return;
   }
   const int nbp = (int)((N - k0) < NB ? (N - k0) : NB);
-  constexpr int S = NB + 1;
-  const int tr = threadIdx.x & 15, tc = threadIdx.x >> 4;
-  double a[4][4], li[4][4];
+  const int tid = threadIdx.x;
+  F1T(0);
+  {
+    // all 16 loads of a thread in flight at once
+    double v[16];
+    const int r = tid & (NB - 1), c0 = tid >> 6;
+    const double* src = A + (k0 + r) + (k0 + c0) * lda;
 #pragma unroll
-  for (int ai = 0; ai < 4; ai++)
-#pragma unroll
-    for (int bi = 0; bi < 4; bi++) {
-      const int r = tr + 16 * ai, c = tc + 16 * bi;
-      a[ai][bi] = (r >= c && r < nbp && c < nbp) ? A[(k0 + r) + (k0 + c) * lda] : 0.0;
-      li[ai][bi] = (r == c) ? 1.0 : 0.0;
+    for (int u = 0; u < 16; u++) {
+      const int c = c0 + 4 * u;
+      v[u] = (r >= c && r < nbp && c < nbp) ? src[(int64_t)(4 * u) * lda] : 0.0;
     }
-  // j = 16*js + jj with js a compile-time constant (keeps a/li in registers)
 #pragma unroll
-  for (int js = 0; js < 4; js++) {
-    for (int jj = 0; jj < 16; jj++) {
-      const int j = 16 * js + jj;
-      if (j >= nbp) break;
-      const int buf = j & 1;
-      if (tc == jj) {
-#pragma unroll
-        for (int ai = 0; ai < 4; ai++) {
-          const int r = tr + 16 * ai;
-          const double v = (r >= j && r < nbp) ? a[ai][js] : 0.0;
-          colj[buf][r] = v;
-          if (r >= j) Wsh[j * S + r] = v;
-        }
-      }
-      if (tr == jj) {
-#pragma unroll
-        for (int bi = 0; bi < 4; bi++) rowj[buf][tc + 16 * bi] = li[js][bi];
-      }
-      __syncthreads();
-      const double d = colj[buf][j];
-      const double r1 = (d != 0.0) ? 1.0 / d : 0.0;
-#pragma unroll
-      for (int ai = 0; ai < 4; ai++) {
-        const int r = tr + 16 * ai;
-        if (r > j) {
-          const double l = colj[buf][r] * r1;
-#pragma unroll
-          for (int bi = 0; bi < 4; bi++) {
-            const int c = tc + 16 * bi;
-            if (c > j && r >= c) a[ai][bi] -= l * colj[buf][c];
-            if (c <= j) li[ai][bi] -= l * rowj[buf][c];
-          }
-        }
-      }
-    }
+    for (int u = 0; u < 16; u++) As[(c0 + 4 * u) * F1S + r] = v[u];
   }
   __syncthreads();
-  // X[t][j] = Linv[j][t]  (row-major, NB x NB, zero outside nbp)
-#pragma unroll
-  for (int ai = 0; ai < 4; ai++)
-#pragma unroll
-    for (int bi = 0; bi < 4; bi++) {
-      const int r = tr + 16 * ai, c = tc + 16 * bi;   // Linv[r][c]
-      f.Lblk[c * NB + r] = (r < nbp && c < nbp) ? li[ai][bi] : 0.0;
+  F1T(1);
+  // ---- factorization, 16-column blocks.  Panel (rows cb.., 16 columns) by warp 0
+  // in registers (lane owns rows cb+lane, cb+32+lane; broadcasts by shuffles,
+  // no block barriers); the trailing part by all threads, register-blocked.
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int cb = 0; cb < nbp; cb += 16) {
+    const int ce = min(cb + 16, nbp);
+    if (warp == 0) {
+      if (nbp - cb > 32) f1_panel<2>(As, Lm, rcp, cb, ce, nbp, lane);
+      else f1_panel<1>(As, Lm, rcp, cb, ce, nbp, lane);
     }
-  for (int idx = threadIdx.x; idx < nbp * nbp; idx += blockDim.x) {
-    const int r = idx % nbp, j = idx / nbp;
-    if (r >= j) f.W[(k0 + r) + j * f.ldw] = Wsh[j * S + r];
+    __syncthreads();
+    if (cb == 0) F1T(6);
+    // rank-(ce-cb) update of the trailing part (rows/cols >= ce, lower): 16x16 threads x 3x3 blocks
+    if (ce < nbp) {
+      const int tr = tid & 15, tc = tid >> 4;
+      double acc[3][3];
+#pragma unroll
+      for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++) {
+          const int r = ce + tr + 16 * a, c = ce + tc + 16 * b;
+          acc[a][b] = (r < nbp && c < nbp && r >= c) ? As[c * F1S + r] : 0.0;
+        }
+      for (int t = 0; t < ce - cb; t++) {
+        double lr[3], wc[3];
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+          const int r = ce + tr + 16 * a;
+          lr[a] = (r < NB) ? Lm[(cb + t) * F1S + r] : 0.0;
+        }
+#pragma unroll
+        for (int b = 0; b < 3; b++) {
+          const int c = ce + tc + 16 * b;
+          wc[b] = (c < NB) ? As[(cb + t) * F1S + c] : 0.0;
+        }
+#pragma unroll
+        for (int a = 0; a < 3; a++)
+#pragma unroll
+          for (int b = 0; b < 3; b++) acc[a][b] -= lr[a] * wc[b];
+      }
+#pragma unroll
+      for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++) {
+          const int r = ce + tr + 16 * a, c = ce + tc + 16 * b;
+          if (r < nbp && c < nbp && r >= c) As[c * F1S + r] = acc[a][b];
+        }
+    }
+    __syncthreads();
+    if (cb == 0) F1T(5);
   }
-  // in-block colmax of column j: warp w handles columns w, w+8, ...
+  F1T(2);
+  // ---- L11^{-1}: Lunit[r][c] = As[c][r] * rcp[c] (r > c)
+  // (1) diagonal 16x16 blocks: warp w<4 inverts block w; lane c<16 owns column c.
+  //     Right-looking: once x_k is final, s_r += L[r][k] x_k for all r > k (independent FMAs),
+  //     so the dependent chain is one FMA per row.
+  //     (the strictly upper blocks of Li are never read; off-diagonal lower blocks are written in (2))
+  if (warp < 4 && lane < 16) {
+    const int o = warp * 16, c = lane;
+    double x[16];
+#pragma unroll
+    for (int r = 0; r < 16; r++) x[r] = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < 15; k++) {
+      const double xk = x[k];
+#pragma unroll
+      for (int r = k + 1; r < 16; r++) {
+        const double lrk = (o + r < nbp) ? Lm[(o + k) * F1S + o + r] : 0.0;
+        x[r] = (r > c) ? fma(-lrk, xk, x[r]) : x[r];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 16; r++) Li[(o + c) * F1S + o + r] = (o + r < nbp && o + c < nbp) ? x[r] : 0.0;
+  }
+  __syncthreads();
+  F1T(7);
+  // (2) off-diagonal blocks by distance dd: Linv_ij = -Linv_ii * sum_{k=j}^{i-1} L_ik Linv_kj
+  //     (4 independent partial sums per dot, all blocks of a distance interleaved)
+  const int er = tid & 15, ec = tid >> 4;   // element (er, ec) of a 16x16 block
+#pragma unroll
+  for (int dd = 1; dd < 4; dd++) {
+    double tv[3];
+#pragma unroll
+    for (int bj = 0; bj < 3; bj++) {
+      if (bj + dd < 4) {
+        const int bi = bj + dd;
+        double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+#pragma unroll
+        for (int kb2 = bj; kb2 < bi; kb2++)
+#pragma unroll
+          for (int k = 0; k < 16; k += 4) {
+            const int kk = kb2 * 16 + k;
+            const double* lr = Lm + bi * 16 + er;
+            const double* lc = Li + (bj * 16 + ec) * F1S;
+            p0 = fma(lr[(kk + 0) * F1S], lc[kk + 0], p0);
+            p1 = fma(lr[(kk + 1) * F1S], lc[kk + 1], p1);
+            p2 = fma(lr[(kk + 2) * F1S], lc[kk + 2], p2);
+            p3 = fma(lr[(kk + 3) * F1S], lc[kk + 3], p3);
+          }
+        tv[bj] = (p0 + p1) + (p2 + p3);
+      }
+    }
+#pragma unroll
+    for (int bj = 0; bj < 3; bj++)
+      if (bj + dd < 4) Tm[(bj * 16 + ec) * F1S + (bj + dd) * 16 + er] = tv[bj];
+    __syncthreads();
+#pragma unroll
+    for (int bj = 0; bj < 3; bj++) {
+      if (bj + dd < 4) {
+        const int bi = bj + dd;
+        double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+        const double* li = Li + bi * 16 + er;
+        const double* tc = Tm + (bj * 16 + ec) * F1S + bi * 16;
+#pragma unroll
+        for (int k = 0; k < 16; k += 4) {
+          p0 = fma(li[(bi * 16 + k + 0) * F1S], tc[k + 0], p0);
+          p1 = fma(li[(bi * 16 + k + 1) * F1S], tc[k + 1], p1);
+          p2 = fma(li[(bi * 16 + k + 2) * F1S], tc[k + 2], p2);
+          p3 = fma(li[(bi * 16 + k + 3) * F1S], tc[k + 3], p3);
+        }
+        tv[bj] = (p0 + p1) + (p2 + p3);
+      }
+    }
+#pragma unroll
+    for (int bj = 0; bj < 3; bj++) {
+      if (bj + dd < 4) {
+        const int r = (bj + dd) * 16 + er, c = bj * 16 + ec;
+        Li[c * F1S + r] = (r < nbp && c < nbp) ? -tv[bj] : 0.0;
+      }
+    }
+    __syncthreads();
+  }
+  F1T(3);
+  // ---- outputs: X[t][j] = Linv[j][t] (row-major), W11, d, in-block colmax
   {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int j = warp; j < nbp; j += 8) {
-      double cm = 0.0;
-      for (int r = j + 1 + lane; r < nbp; r += 32) cm = fmax(cm, fabs(Wsh[j * S + r]));
-      cm = warp_max(cm);
-      if (lane == 0) { ctl->colmax[j] = dbits(cm); ctl->d[j] = Wsh[j * S + j]; }
+    const int j = tid & (NB - 1), t0 = tid >> 6;
+    double* Xg = f.Lblk;
+    double* Wg = f.W + k0;
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const int t = t0 + 4 * u;                 // X[t][j] = Linv[j][t] (0 above the diagonal)
+      Xg[t * NB + j] = (j >= t) ? Li[t * F1S + j] : 0.0;
+      if (j >= t && j < nbp && t < nbp) Wg[j + t * f.ldw] = As[t * F1S + j];   // W11 (r=j, col=t)
     }
   }
-  if (threadIdx.x == 0) {
+  {
+    // in-block colmax of column j: 4 threads per column, shuffle-reduced
+    const int j = tid >> 2, part = tid & 3;
+    double cm = 0.0;
+    for (int r = j + 1 + part; r < nbp; r += 4) cm = fmax(cm, fabs(As[j * F1S + r]));
+    cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
+    cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
+    if (part == 0 && j < nbp) { ctl->colmax[j] = dbits(cm); ctl->d[j] = As[j * F1S + j]; }
+  }
+  if (tid == 0) {
     ctl->k0 = (int)k0;
     ctl->kb = 0;
     ctl->nbp = nbp;
-    f.panel_start[ctl->npanel] = (int)k0;
-    ctl->npanel += 1;
+    f.panel_start[f.pidx] = (int)k0;
+    ctl->npanel = f.pidx + 1;
   }
+  F1T(4);
 }
 
 // FP64 tensor-core fragment op: mma.sync m8n8k4 f64 (SASS DMMA.8x8x4).
@@ -1091,6 +1257,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_update_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
+    cudaFuncSetAttribute(k_panel_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, F1SMEM);
     cudaFuncSetAttribute(k_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * USTAGE * (int)sizeof(double));
     cudaFuncSetAttribute(k_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * USTAGE * (int)sizeof(double));
     cudaFuncSetAttribute(k_panel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB * US * (int)sizeof(double));
@@ -1135,7 +1302,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     FWork fp = f;
     fp.pidx = (int)p;
     if (p & 1) fp.W = f.W1;
-    MDS_LAUNCH(PC_PANEL_DIAG, st, (k_panel_diag<<<1, 256, 0, st>>>(N, M, ldm, fp)));
+    MDS_LAUNCH(PC_PANEL_DIAG, st, (k_panel_diag<<<1, 256, F1SMEM, st>>>(N, M, ldm, fp)));
     const unsigned g256 = (unsigned)std::max<int64_t>(mds_cdiv(rows, 256), 1);
     const unsigned g64 = (unsigned)std::max<int64_t>(mds_cdiv(rows, UT), 1);
     MDS_LAUNCH(PC_PANEL_TRSM, st, (k_panel_trsm<<<g64, 128, usmem, st>>>(N, M, ldm, fp)));
@@ -1147,9 +1314,9 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     if (n2max > 0) {
       const CUtensorMap& mw = (p & 1) ? mapW1 : mapW;
       if (lookahead) {
-        MDS_CUDA_TRY(cudaEventRecord((*evs)[2 * p], st));
         const unsigned gn = (unsigned)std::min<int64_t>(2 * nt, sms);
         MDS_LAUNCH(PC_UPDATE, st, (k_update_tma<<<gn, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, 1)));
+        MDS_CUDA_TRY(cudaEventRecord((*evs)[2 * p], st));
         MDS_CUDA_TRY(cudaStreamWaitEvent(side, (*evs)[2 * p], 0));
         const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt * (nt + 1) / 2, sms - reserve));
         MDS_LAUNCH(PC_UPDATE, side, (k_update_tma<<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, 2)));
