@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=1536, help="oracle factor sample size (leading block)")
+    ap.add_argument("--scenarios", type=int, default=256, help="C4: total SCOPF scenarios (strong scaling)")
+    ap.add_argument("--streams", type=int, default=8, help="C4: concurrent CUDA streams per GPU")
     return ap.parse_args()
 
 
@@ -350,6 +352,78 @@ def run_ours(args, rank, world):
         print(json.dumps(line), flush=True)
 
 
+def run_scopf(args, rank, world):
+    """C4: SCOPF scenario batch, scenarios round-robin over ranks; per Newton step
+    every local scenario's KKT step on concurrent streams + ONE small NCCL
+    all-reduce pair for the global stopping test (read on the host)."""
+    import torch
+    import torch.distributed as dist
+
+    import mdsgen
+    import paper_2605_13736_b200 as mds
+    from paper_2605_13736_b200 import scopf
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    base = mdsgen.scopf_base()
+    fn = lambda s_: mdsgen.scopf_scenario(base, s_)
+    svf = lambda p_, s_: mdsgen.step_vectors_for(p_, seed=100 + s_)
+    ids = scopf.partition(args.scenarios, world, rank)
+    t0 = time.time()
+    l0 = mds.launch_count()
+    batch = scopf.ScopfBatch(base, fn, ids, svf, n_streams=args.streams)
+    setup_s = time.time() - t0
+    for _ in range(args.warmup):
+        batch.newton_step()
+        batch.stop_test()
+    torch.cuda.synchronize()
+    # launches per Newton step = per-scenario step launches x local scenarios
+    l1 = mds.launch_count()
+    batch.steps[0].run()
+    torch.cuda.synchronize()
+    per_scen = mds.launch_count() - l1
+    if world > 1:
+        dist.barrier()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            batch.newton_step()
+            st = batch.stop_test()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    recs = scopf.gather_records(batch.records, args.scenarios)
+    value = args.scenarios * args.steps / (ms_max / 1e3)
+    if rank == 0:
+        N = base.N
+        fl = args.scenarios * args.steps * (N ** 3 / 3.0 + 2.0 * N * N)
+        line = {"metric": METRIC, "value": value, "unit": "scenario_newton_iters/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": "C4 " + f"SCOPF {args.scenarios} contingency scenarios, N=2048 each "
+                           "(n_d=1024, m_E=m_I=512, n_s=131072, shared pattern), round-robin over ranks",
+                           "N": N, "scenarios": args.scenarios, "streams_per_gpu": args.streams,
+                           "parallelism": f"scenario-dp{world}", "cuda_graph": True},
+                "gpu_launches": per_scen * len(ids) * args.steps,
+                "factor_solve_fp64_tflops_aggregate": fl / (ms_max * 1e-3) / 1e12,
+                "stop_test": st, "records_gathered": int(recs.shape[0]),
+                "all_inertia_ok": bool(st["n_bad_inertia"] == 0), "setup_s": setup_s,
+                "clocks": clk.summary(), "e2e": None, "cpu_baseline": None}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -364,7 +438,10 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         dist.init_process_group("nccl")
-    run_ours(args, rank, world)
+    if args.config == "C4":
+        run_scopf(args, rank, world)
+    else:
+        run_ours(args, rank, world)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -294,3 +294,28 @@ def step_vectors_for(prob: MDSProblem, seed: int, mu=0.1):
     """K1 inputs for the primal block (x_s, x_d): n_b = n_s + n_d components
     (the primal direction itself comes from the solve)."""
     return step_vectors(prob.n_s + prob.n_d, seed, mu=mu)
+
+
+def scopf_base(seed=4000, n_s=131_072, n_d=1024, m_E=512, m_I=512, pattern="local"):
+    """C4 base case: one G1 instance whose sparsity pattern all contingency
+    scenarios share (SCOPF: the same network with one element altered)."""
+    return g1_quasidefinite(n_s, n_d, m_E, m_I, seed, pattern=pattern)
+
+
+def scopf_scenario(base: MDSProblem, s: int, seed: int = 4000):
+    """Contingency scenario s of a SCOPF batch: same pattern
+    as `base`, values re-drawn with seed (seed, s) so that the G1 structure --
+    hence the closed-form inertia (n_d, 0, m) -- is preserved:
+      J_s values scaled by U[0.8,1.2] (private entries kept at 1.0), h_ss, sigma_s,
+      sigma_d, d_h, r re-drawn, H_dd + diag(U[0,0.1]), J_d scaled by U[0.9,1.1]."""
+    rng = np.random.default_rng([seed, s])
+    n_s, n_d, m = base.n_s, base.n_d, base.m
+    scale = rng.uniform(0.8, 1.2, base.nnz)
+    val = np.where(base.val == 1.0, 1.0, base.val * scale)
+    H = np.array(base.H_dd, order="F", copy=True)
+    H[np.diag_indices(n_d)] += rng.uniform(0.0, 0.1, n_d)
+    J_d = np.asfortranarray(np.asarray(base.J_d) * rng.uniform(0.9, 1.1, (m, n_d)))
+    return MDSProblem(n_s, n_d, base.m_E, base.m_I, base.rowptr, base.colidx, val,
+                      rng.uniform(0.0, 1.0, n_s), rng.uniform(0.5, 2.0, n_s), H, rng.uniform(0.1, 1.0, n_d),
+                      J_d, rng.uniform(1.0, 10.0, base.m_I), 0.0, 0.0, rng.standard_normal(n_s + n_d + m),
+                      expected_inertia=(n_d, 0, m), meta=dict(gen="SCOPF", seed=seed, scenario=s))
