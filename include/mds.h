@@ -188,6 +188,10 @@ enum {
     MDS_PROF_SOLVE_SCATTER, MDS_PROF_RECOVER, MDS_PROF_VECTORS, MDS_PROF_COUNT
 };
 unsigned long long mds_launch_count(void);
+/* Tuning knob (process-wide): cap the CTA count of mds_factor's persistent
+ * trailing-update kernels (0 = one per SM, the default).  Used when several
+ * factorizations run concurrently on different streams (SCOPF batches). */
+int mds_factor_set_grid_cap(int ctas);
 int mds_profile_begin(void);
 int mds_profile_end(double *ms_by_class, int64_t *launches_by_class, int ncls);
 int64_t mds_factor_panels(const void *fwork, int64_t N, int32_t *starts_host, int64_t cap);

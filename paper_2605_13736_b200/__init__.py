@@ -56,7 +56,7 @@ for _f in ("mds_plan_create", "mds_plan_destroy", "mds_plan_dims", "mds_condense
 EXPORTS = ["mds_version", "mds_plan_create", "mds_plan_destroy", "mds_plan_dims", "mds_condense",
            "mds_factor_workspace_size", "mds_factor", "mds_solve_workspace_size", "mds_solve",
            "ipm_step_vectors_workspace_size", "ipm_step_vectors", "mds_launch_count", "mds_profile_begin",
-           "mds_profile_end", "mds_factor_panels"]
+           "mds_profile_end", "mds_factor_panels", "mds_factor_set_grid_cap"]
 
 PROF_CLASSES = ["condense_w", "condense_dense", "condense_yy", "anorm", "panel_diag", "panel_trsm", "panel_accept",
                 "panel_slow", "update", "finalize", "solve_gather", "solve_fwd", "solve_d", "solve_bwd",
@@ -189,6 +189,12 @@ def step_vectors(n, x, dx, lo, up, zl, zu, dzl, dzu, tau, mu, out, sigma_out, st
                                  _f64(dzu), float(tau), float(mu), nres, arr_p, arr_l, _f64(out), _f64(sigma_out),
                                  _ptr(status), _ptr(work), work.numel() * work.element_size(), _stream(stream))
     _check(code, "ipm_step_vectors")
+
+
+def set_grid_cap(ctas: int):
+    """Cap the persistent update kernels' CTAs (0 = all SMs); for concurrent streams."""
+    _lib.mds_factor_set_grid_cap.argtypes = [ctypes.c_int]
+    _check(_lib.mds_factor_set_grid_cap(int(ctas)), "mds_factor_set_grid_cap")
 
 
 def launch_count() -> int:

@@ -1190,6 +1190,15 @@ extern "C" int64_t mds_factor_panels(const void* fwork, int64_t N, int32_t* star
   return n;
 }
 
+// Optional cap on the CTAs of the persistent update kernels (0 = all SMs);
+// lets several factorizations on different streams share the GPU.
+static int g_grid_cap = 0;
+extern "C" int mds_factor_set_grid_cap(int ctas) {
+  if (ctas < 0) return MDS_ERR_ARG;
+  g_grid_cap = ctas;
+  return MDS_OK;
+}
+
 // read by solve.cu
 double* mds_factor_tol_ptr(const void* fwork) {
   return fwork ? &reinterpret_cast<FCtl*>(const_cast<void*>(fwork))->tol : nullptr;
@@ -1293,7 +1302,8 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   }
   CUtensorMap mapW1;
   if (use_tma && !make_map(&mapW1, f.W1, N, NB, f.ldw)) return MDS_ERR_CUDA;
-  const unsigned reserve = 16;   // SMs left to the panel chain while the rest-update runs
+  unsigned reserve = 16;         // SMs left to the panel chain while the rest-update runs
+  if (g_grid_cap > 0 && g_grid_cap < sms) { sms = g_grid_cap; reserve = 0; }
   int64_t plast = -1;
   for (int64_t p = 0; p < npmax; p++) {
     const int64_t kmin = std::min<int64_t>(p * (NB - 1), N);   // lower bound on this panel's k0
@@ -1341,7 +1351,9 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_factor_finalize, 256, 0);
-    int blocks = sms * std::max(1, std::min(occ, 2));
+    // a small cooperative grid (grid-stride loops): co-resident even while other
+    // streams' factorizations occupy most SMs (SCOPF batches)
+    int blocks = std::min(32, sms * std::max(1, std::min(occ, 2)));
     void* args[] = {&N, &M, &ldm, &f, &piv, &inertia_dev};
     MDS_LAUNCH(PC_FINALIZE, st,
                MDS_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_factor_finalize, blocks, 256, args, 0, st)));

@@ -20,7 +20,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import Plan
+from . import Plan, set_grid_cap
 from .step import DeviceProblem, KKTStep
 
 REC = 8   # record: [scenario, pos, zero, neg, alpha_p, alpha_d, res_inf, compl_inf]
@@ -93,20 +93,43 @@ class ScopfBatch:
             st = KKTStep(DeviceProblem(prob, plan=self.plan), sv=sv_fn(prob, s))
             self.steps.append(st)
         self.streams = [torch.cuda.Stream() for _ in range(max(1, min(n_streams, n)))]
-        self.graphs = [st.capture() for st in self.steps]
+        # concurrent factorizations share the SMs: cap each persistent update grid
+        sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        set_grid_cap(max(8, sms // len(self.streams)) if len(self.streams) > 1 else 0)
         self._ids_t = torch.tensor(self.ids, dtype=torch.float64, device=device)
+        self.graph = self._capture_all()
+        set_grid_cap(0)
 
-    def newton_step(self):
-        """One Newton step's KKT work for every local scenario (concurrent streams)."""
+    def _run_all(self):
         cur = torch.cuda.current_stream()
         for s in self.streams:
             s.wait_stream(cur)
-        for i, g in enumerate(self.graphs):
-            with torch.cuda.stream(self.streams[i % len(self.streams)]):
-                g.replay()
+        for i, st in enumerate(self.steps):
+            s = self.streams[i % len(self.streams)]
+            with torch.cuda.stream(s):
+                st.run(stream=s)
         for s in self.streams:
             cur.wait_stream(s)
         self._fill_records()
+
+    def _capture_all(self):
+        """ONE CUDA graph for the whole local batch: the capture forks onto the
+        stream pool (one branch per stream) and joins back, so a Newton step is a
+        single graph launch."""
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self._run_all()                       # warm-up (workspaces, look-ahead contexts)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._run_all()
+        return g
+
+    def newton_step(self):
+        """One Newton step's KKT work for every local scenario (one graph launch)."""
+        self.graph.replay()
 
     def _fill_records(self):
         r = self.records
