@@ -183,7 +183,7 @@ int ipm_step_vectors(int64_t n, const double *x, const double *dx, const double 
  * the caller can compute the trailing update's algorithmic flops exactly. */
 enum {
     MDS_PROF_CONDENSE_W = 0, MDS_PROF_CONDENSE_DENSE, MDS_PROF_CONDENSE_YY, MDS_PROF_ANORM,
-    MDS_PROF_PANEL_DIAG, MDS_PROF_PANEL_TRSM, MDS_PROF_PANEL_ACCEPT, MDS_PROF_PANEL_SLOW, MDS_PROF_UPDATE,
+    MDS_PROF_PANEL_DIAG, MDS_PROF_PANEL_TRSM, MDS_PROF_PANEL_STORE, MDS_PROF_PANEL_SLOW, MDS_PROF_UPDATE,
     MDS_PROF_FINALIZE, MDS_PROF_SOLVE_GATHER, MDS_PROF_SOLVE_FWD, MDS_PROF_SOLVE_D, MDS_PROF_SOLVE_BWD,
     MDS_PROF_SOLVE_SCATTER, MDS_PROF_RECOVER, MDS_PROF_VECTORS, MDS_PROF_COUNT
 };
@@ -195,6 +195,10 @@ int mds_factor_set_grid_cap(int ctas);
 int mds_profile_begin(void);
 int mds_profile_end(double *ms_by_class, int64_t *launches_by_class, int ncls);
 int64_t mds_factor_panels(const void *fwork, int64_t N, int32_t *starts_host, int64_t cap);
+/* Per-launch timeline of the last mds_profile_begin/end region: out3[3*i..] =
+ * (class, start_ms, end_ms) relative to the first profiled launch; returns the
+ * number of launches (copies at most cap). */
+int64_t mds_profile_timeline(double *out3, int64_t cap);
 
 #ifdef __cplusplus
 }

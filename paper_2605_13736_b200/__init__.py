@@ -56,9 +56,9 @@ for _f in ("mds_plan_create", "mds_plan_destroy", "mds_plan_dims", "mds_condense
 EXPORTS = ["mds_version", "mds_plan_create", "mds_plan_destroy", "mds_plan_dims", "mds_condense",
            "mds_factor_workspace_size", "mds_factor", "mds_solve_workspace_size", "mds_solve",
            "ipm_step_vectors_workspace_size", "ipm_step_vectors", "mds_launch_count", "mds_profile_begin",
-           "mds_profile_end", "mds_factor_panels", "mds_factor_set_grid_cap"]
+           "mds_profile_end", "mds_factor_panels", "mds_factor_set_grid_cap", "mds_profile_timeline"]
 
-PROF_CLASSES = ["condense_w", "condense_dense", "condense_yy", "anorm", "panel_diag", "panel_trsm", "panel_accept",
+PROF_CLASSES = ["condense_w", "condense_dense", "condense_yy", "anorm", "panel_diag", "panel_trsm", "panel_store",
                 "panel_slow", "update", "finalize", "solve_gather", "solve_fwd", "solve_d", "solve_bwd",
                 "solve_scatter", "recover", "vectors"]
 
@@ -214,6 +214,17 @@ def profile_end():
     cnt = np.zeros(n, dtype=np.int64)
     _check(_lib.mds_profile_end(ms.ctypes.data, cnt.ctypes.data, n), "mds_profile_end")
     return {c: (float(ms[i]), int(cnt[i])) for i, c in enumerate(PROF_CLASSES)}
+
+
+def profile_timeline():
+    """[(class, start_ms, end_ms)] of every launch in the last profiled region."""
+    import numpy as np
+    _lib.mds_profile_timeline.restype = ctypes.c_int64
+    _lib.mds_profile_timeline.argtypes = [_P, _I64]
+    n = int(_lib.mds_profile_timeline(None, 0))
+    buf = np.zeros(3 * max(n, 1))
+    _lib.mds_profile_timeline(buf.ctypes.data, n)
+    return [(PROF_CLASSES[int(buf[3 * i])], buf[3 * i + 1], buf[3 * i + 2]) for i in range(n)]
 
 
 def factor_panels(fwork, N):

@@ -63,7 +63,7 @@ static inline int64_t mds_cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // launch accounting + optional per-class CUDA-event profiling (prof.cu)
 enum MdsProfClass {
   PC_CONDENSE_W = 0, PC_CONDENSE_DENSE, PC_CONDENSE_YY, PC_ANORM, PC_PANEL_DIAG, PC_PANEL_TRSM,
-  PC_PANEL_ACCEPT, PC_PANEL_SLOW, PC_UPDATE, PC_FINALIZE, PC_SOLVE_GATHER, PC_SOLVE_FWD, PC_SOLVE_D,
+  PC_PANEL_STORE, PC_PANEL_SLOW, PC_UPDATE, PC_FINALIZE, PC_SOLVE_GATHER, PC_SOLVE_FWD, PC_SOLVE_D,
   PC_SOLVE_BWD, PC_SOLVE_SCATTER, PC_RECOVER, PC_VECTORS, PC_COUNT
 };
 extern bool g_mds_prof;

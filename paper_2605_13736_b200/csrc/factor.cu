@@ -9,11 +9,13 @@
 //                     pivoting (in shared memory),
 //   F2 k_panel_trsm   all SMs form W21 = A21 L11^{-T} (the fully updated
 //                     panel columns) and the per-column BK colmax,
-//   F3 k_panel_accept accepts the longest prefix of columns that pass BK's
+//   F4 k_panel_slow   accepts the longest prefix of columns that pass BK's
 //                     1x1-no-interchange test |d_k| >= alpha*colmax_k (the test
-//                     BK itself applies to exactly these numbers), stores L.
-// Columns after the first failing one are recomputed by the exact sequential
-// BK panel (F4 k_panel_slow, dlasyf semantics: rowmax, 1x1 / 2x2 / interchange).
+//                     BK itself applies to exactly these numbers),
+// and recomputes the columns after the first failing one with the exact
+// sequential BK panel (dlasyf semantics: rowmax, 1x1 / 2x2 / interchange).
+// The panel's D + L live in a side buffer Lb until k_panel_store copies them
+// into M (off the critical path, on the look-ahead stream).
 // So the pivot sequence is Bunch-Kaufman's; only the operation order differs
 // (reading R7: parity is on inertia and x).  Quasi-definite KKT matrices take
 // the fast path almost always, so the per-column global pivot search costs
@@ -68,6 +70,8 @@ struct FWork {
   double* Lblk;       // [NB*NB]
   double* W;          // [ldw * WCOLS]  W panel of the current panel (host picks W0/W1 by panel parity)
   double* W1;         // second W buffer (look-ahead: panel p+1 is formed while p's update still reads W)
+  double* Lb;         // [ldw * WCOLS]  the panel's D + L columns (speculative, fixed up by k_panel_slow);
+  double* Lb1;        //   copied into M by k_panel_store; double-buffered like W
   int2* pinfo;        // [N+2] per-panel (k0, kb), written by k_panel_slow, read by the updates
   int pidx;           // panel index of this launch (host loop counter)
   int64_t ldw;
@@ -91,6 +95,8 @@ FWork carve(void* work, int64_t N, size_t* total) {
   f.ldw = align_up(std::max<int64_t>(N, 1), 8);
   f.W = reinterpret_cast<double*>(take(sizeof(double) * f.ldw * WCOLS));
   f.W1 = reinterpret_cast<double*>(take(sizeof(double) * f.ldw * WCOLS));
+  f.Lb = reinterpret_cast<double*>(take(sizeof(double) * f.ldw * WCOLS));
+  f.Lb1 = reinterpret_cast<double*>(take(sizeof(double) * f.ldw * WCOLS));
   f.pinfo = reinterpret_cast<int2*>(take(sizeof(int2) * (N + 2)));
   f.pidx = 0;
   if (total) *total = off;
@@ -419,7 +425,10 @@ __global__ void __launch_bounds__(256) k_panel_diag(int64_t N, const double* __r
     for (int u = 0; u < 16; u++) {
       const int t = t0 + 4 * u;                 // X[t][j] = Linv[j][t] (0 above the diagonal)
       Xg[t * NB + j] = (j >= t) ? Li[t * F1S + j] : 0.0;
-      if (j >= t && j < nbp && t < nbp) Wg[j + t * f.ldw] = As[t * F1S + j];   // W11 (r=j, col=t)
+      if (j >= t && j < nbp && t < nbp) {
+        Wg[j + t * f.ldw] = As[t * F1S + j];                                   // W11 (r=j, col=t)
+        f.Lb[(k0 + j) + t * f.ldw] = (j == t) ? As[t * F1S + t] : Lm[t * F1S + j];   // D / L11
+      }
     }
   }
   {
@@ -464,6 +473,11 @@ __global__ void __launch_bounds__(128) k_panel_trsm(int64_t N, const double* __r
   double* As = dsm;                 // [t][row]
   double* Xs = dsm + NB * US;       // [t][j]
   __shared__ double cmax[4][32];
+  __shared__ double r1s[NB];
+  if (threadIdx.x < NB) {
+    const double d = (threadIdx.x < nbp) ? ctl->d[threadIdx.x] : 0.0;
+    r1s[threadIdx.x] = (d != 0.0) ? fast_rcp(d) : 0.0;
+  }
   for (int idx = threadIdx.x; idx < UT * NB; idx += 128) {
     const int i = idx % UT, t = idx / UT;
     As[t * US + i] = (t < nbp && R0 + i < N) ? A[(R0 + i) + (k0 + t) * lda] : 0.0;
@@ -505,6 +519,7 @@ __global__ void __launch_bounds__(128) k_panel_trsm(int64_t N, const double* __r
           const int col = wn + 8 * b + 2 * q + e;
           if (col < nbp) {
             f.W[row + col * f.ldw] = acc[a][b][e];
+            f.Lb[row + col * f.ldw] = acc[a][b][e] * r1s[col];      // speculative L21
             cm[b][e] = fmax(cm[b][e], fabs(acc[a][b][e]));
           }
         }
@@ -527,52 +542,6 @@ __global__ void __launch_bounds__(128) k_panel_trsm(int64_t N, const double* __r
     const int half = col >> 5;                 // column col is owned by warps half and half+2
     const double v = fmax(cmax[half][col & 31], cmax[half + 2][col & 31]);
     if (col < nbp) atomicMax(&ctl->colmax[col], dbits(v));
-  }
-}
-
-// F3: accept the longest prefix of columns that pass BK's 1x1-no-interchange
-// test, write L (= W * 1/d) and D for them; counts inertia; sets ctl->kb.
-__global__ void __launch_bounds__(256) k_panel_accept(int64_t N, double* __restrict__ A, int64_t lda, FWork f,
-                                                      int32_t* piv) {
-  FCtl* ctl = f.ctl;
-  if (ctl->abort) return;
-  const int nbp = ctl->nbp;
-  const int64_t k0 = ctl->k0;
-  if (nbp == 0) return;
-  __shared__ double s_r1[NB], s_d[NB];
-  __shared__ unsigned s_fail[2];
-  // p = first column failing BK's 1x1-no-interchange test (all columns tested in parallel)
-  if (threadIdx.x < NB) {
-    const int j = threadIdx.x;
-    const double d = (j < nbp) ? ctl->d[j] : 0.0;
-    const double cm = (j < nbp) ? bitsd(ctl->colmax[j]) : 0.0;
-    s_d[j] = d;
-    s_r1[j] = (d != 0.0) ? 1.0 / d : 0.0;
-    const bool fail = (j >= nbp) || !(fabs(d) >= ALPHA_BK * cm);   // (0 >= 0 accepts the exact-zero column)
-    const unsigned b = __ballot_sync(0xffffffffu, fail);
-    s_fail[j >> 5] = b;
-  }
-  __syncthreads();
-  const int p = s_fail[0] ? (__ffs(s_fail[0]) - 1) : (s_fail[1] ? 32 + __ffs(s_fail[1]) - 1 : NB);
-  const int64_t r = k0 + (int64_t)blockIdx.x * 256 + threadIdx.x;
-  const int j0 = blockIdx.y * (NB / 8), j1 = min(p, j0 + NB / 8);   // 8 column groups per row
-  if (r < N) {
-    for (int j = j0; j < j1; j++) {
-      const int64_t k = k0 + j;
-      if (r == k) A[r + k * lda] = s_d[j];
-      else if (r > k) A[r + k * lda] = f.W[r + j * f.ldw] * s_r1[j];
-    }
-  }
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
-    const double tol = ctl->tol;
-    for (int j = 0; j < p; j++) {
-      const double d = s_d[j];
-      if (d > tol) ctl->inertia[0]++;
-      else if (d < -tol) ctl->inertia[2]++;
-      else ctl->inertia[1]++;
-      piv[k0 + j] = (int32_t)(k0 + j + 1);
-    }
-    ctl->kb = p;
   }
 }
 
@@ -604,6 +573,7 @@ __device__ __forceinline__ void zero_w_tail(int64_t N, int64_t k0, int kb, const
   for (int64_t idx = threadIdx.x; idx < nr * nc; idx += blockDim.x) {
     const int64_t r = k0 + idx % nr, c = kb + idx / nr;
     f.W[r + c * f.ldw] = 0.0;
+    f.Lb[r + c * f.ldw] = 0.0;
   }
 }
 
@@ -613,17 +583,50 @@ __global__ void __launch_bounds__(1024) k_panel_slow(int64_t N, double* __restri
   if (ctl->abort) return;
   const int nbp = ctl->nbp;
   const int64_t k0 = ctl->k0;
-  int j = ctl->kb;
+  if (nbp == 0) {
+    if (threadIdx.x == 0) f.pinfo[f.pidx] = make_int2((int)k0, 0);
+    return;
+  }
+  // accept the longest prefix of columns that pass BK's 1x1-no-interchange test
+  // |d_j| >= alpha * colmax_j on the speculatively updated values (all tested in parallel)
+  __shared__ unsigned s_fail[2], s_pos[2], s_neg[2];
+  double dj = 0.0;
+  if (threadIdx.x < NB) {
+    const int jj = threadIdx.x;
+    dj = (jj < nbp) ? ctl->d[jj] : 0.0;
+    const double cm = (jj < nbp) ? bitsd(ctl->colmax[jj]) : 0.0;
+    const bool fail = (jj >= nbp) || !(fabs(dj) >= ALPHA_BK * cm);   // (0 >= 0 accepts the exact-zero column)
+    const double tol = ctl->tol;
+    const unsigned b = __ballot_sync(0xffffffffu, fail);
+    const unsigned bp = __ballot_sync(0xffffffffu, dj > tol);
+    const unsigned bn = __ballot_sync(0xffffffffu, dj < -tol);
+    if ((jj & 31) == 0) { s_fail[jj >> 5] = b; s_pos[jj >> 5] = bp; s_neg[jj >> 5] = bn; }
+  }
+  __syncthreads();
+  const int p = s_fail[0] ? (__ffs(s_fail[0]) - 1) : (s_fail[1] ? 32 + __ffs(s_fail[1]) - 1 : NB);
+  if (threadIdx.x < p) piv[k0 + threadIdx.x] = (int32_t)(k0 + threadIdx.x + 1);
+  if (threadIdx.x == 0 && p > 0) {
+    // inertia of the accepted prefix: popcounts of the sign masks below p
+    const unsigned long long m = (p >= 64) ? ~0ull : ((1ull << p) - 1ull);
+    const unsigned long long pos = ((unsigned long long)s_pos[1] << 32 | s_pos[0]) & m;
+    const unsigned long long neg = ((unsigned long long)s_neg[1] << 32 | s_neg[0]) & m;
+    const int np = __popcll(pos), nn = __popcll(neg);
+    ctl->inertia[0] += np;
+    ctl->inertia[2] += nn;
+    ctl->inertia[1] += p - np - nn;
+  }
+  int j = p;
   const bool last = (k0 + nbp >= N);
   const int jlim = last ? nbp : nbp - 1;
-  if (nbp == 0 || j >= jlim) {   // nothing left for the exact path: publish (k0, kb) for the updates
-    if (threadIdx.x == 0) f.pinfo[f.pidx] = make_int2((int)k0, nbp == 0 ? 0 : j);
-    if (nbp > 0) zero_w_tail(N, k0, j, f);
+  if (j >= jlim) {   // nothing left for the exact path: publish (k0, kb) for the updates
+    if (threadIdx.x == 0) { ctl->kb = j; f.pinfo[f.pidx] = make_int2((int)k0, j); }
+    zero_w_tail(N, k0, j, f);
     return;
   }
   __shared__ double wrow[WCOLS];
   __shared__ ArgMax sh[33];
   double* W = f.W;
+  double* Lb = f.Lb;
   const int64_t ldw = f.ldw;
   const int tid = threadIdx.x, nth = blockDim.x;
   const double tol = ctl->tol;
@@ -635,7 +638,7 @@ __global__ void __launch_bounds__(1024) k_panel_slow(int64_t N, double* __restri
     ArgMax am{-1.0, 0x7fffffff};
     for (int64_t r = k + tid; r < N; r += nth) {
       double v = A[r + k * lda];
-      for (int t = 0; t < j; t++) v -= A[r + (k0 + t) * lda] * wrow[t];
+      for (int t = 0; t < j; t++) v -= Lb[r + t * ldw] * wrow[t];
       W[r + j * ldw] = v;
       if (r > k) am = am_better(am, ArgMax{fabs(v), (int)r});
     }
@@ -657,7 +660,7 @@ __global__ void __launch_bounds__(1024) k_panel_slow(int64_t N, double* __restri
       ArgMax rm{-1.0, 0x7fffffff};
       for (int64_t r = k + tid; r < N; r += nth) {
         double v = (r < imax) ? A[imax + r * lda] : A[r + imax * lda];
-        for (int t = 0; t < j; t++) v -= A[r + (k0 + t) * lda] * wrow[t];
+        for (int t = 0; t < j; t++) v -= Lb[r + t * ldw] * wrow[t];
         W[r + (j + 1) * ldw] = v;
         if (r != imax) rm = am_better(rm, ArgMax{fabs(v), (int)r});
       }
@@ -684,8 +687,8 @@ __global__ void __launch_bounds__(1024) k_panel_slow(int64_t N, double* __restri
       }
       if (tid == 0) A[kp + kp * lda] = A[kk + kk * lda];
       // rows kk <-> kp of the panel's finished L columns and of W
-      for (int64_t c = k0 + tid; c < kk; c += nth) {
-        double t = A[kk + c * lda]; A[kk + c * lda] = A[kp + c * lda]; A[kp + c * lda] = t;
+      for (int64_t c = tid; c < kk - k0; c += nth) {
+        double t = Lb[kk + c * ldw]; Lb[kk + c * ldw] = Lb[kp + c * ldw]; Lb[kp + c * ldw] = t;
       }
       for (int64_t t = tid; t <= kk - k0; t += nth) {
         double u = W[kk + t * ldw]; W[kk + t * ldw] = W[kp + t * ldw]; W[kp + t * ldw] = u;
@@ -696,9 +699,9 @@ __global__ void __launch_bounds__(1024) k_panel_slow(int64_t N, double* __restri
     if (kstep == 1) {
       const double d = W[k + j * ldw];
       const double r1 = zero ? 0.0 : 1.0 / d;
-      for (int64_t r = k + 1 + tid; r < N; r += nth) A[r + k * lda] = zero ? W[r + j * ldw] : W[r + j * ldw] * r1;
+      for (int64_t r = k + 1 + tid; r < N; r += nth) Lb[r + j * ldw] = zero ? W[r + j * ldw] : W[r + j * ldw] * r1;
       if (tid == 0) {
-        A[k + k * lda] = d;
+        Lb[k + j * ldw] = d;
         if (d > tol) ctl->inertia[0]++;
         else if (d < -tol) ctl->inertia[2]++;
         else ctl->inertia[1]++;
@@ -713,13 +716,13 @@ __global__ void __launch_bounds__(1024) k_panel_slow(int64_t N, double* __restri
       d21 = tt / d21;
       for (int64_t r = k + 2 + tid; r < N; r += nth) {
         const double wk = W[r + j * ldw], wk1 = W[r + (j + 1) * ldw];
-        A[r + k * lda] = d21 * (d11 * wk - wk1);
-        A[r + (k + 1) * lda] = d21 * (d22 * wk1 - wk);
+        Lb[r + j * ldw] = d21 * (d11 * wk - wk1);
+        Lb[r + (j + 1) * ldw] = d21 * (d22 * wk1 - wk);
       }
       if (tid == 0) {
-        A[k + k * lda] = W[k + j * ldw];
-        A[(k + 1) + k * lda] = W[(k + 1) + j * ldw];
-        A[(k + 1) + (k + 1) * lda] = W[(k + 1) + (j + 1) * ldw];
+        Lb[k + j * ldw] = W[k + j * ldw];
+        Lb[(k + 1) + j * ldw] = W[(k + 1) + j * ldw];             // D21 (moved to the upper slot at finalize)
+        Lb[(k + 1) + (j + 1) * ldw] = W[(k + 1) + (j + 1) * ldw];
         ctl->inertia[0]++;
         ctl->inertia[2]++;
         piv[k] = piv[k + 1] = (int32_t)(-(kp + 1));
@@ -735,6 +738,19 @@ __global__ void __launch_bounds__(1024) k_panel_slow(int64_t N, double* __restri
     f.pinfo[f.pidx] = make_int2((int)k0, j);
   }
   zero_w_tail(N, k0, j, f);
+}
+
+// Copy the finished panel (D + L columns, rows >= the diagonal) from Lb into M.
+__global__ void __launch_bounds__(256) k_panel_store(int64_t N, double* __restrict__ A, int64_t lda, FWork f) {
+  if (f.ctl->abort) return;
+  const int2 pi = f.pinfo[f.pidx];
+  const int64_t k0 = pi.x;
+  const int kb = pi.y;
+  const int64_t r = k0 + (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (kb <= 0 || r >= N) return;
+  const int t0 = blockIdx.y * (NB / 8), t1 = min(kb, t0 + NB / 8);
+  for (int t = t0; t < t1; t++)
+    if (r >= k0 + t) A[r + (k0 + t) * lda] = f.Lb[r + t * f.ldw];
 }
 
 // ---------------------------------------------------------------------------
@@ -777,7 +793,7 @@ __device__ __forceinline__ void tri_tile(int64_t x, int64_t& bi, int64_t& bj) {
 template <bool V16>
 __device__ __forceinline__ void update_issue(double* st, int64_t R0, int64_t C0, int64_t k0, int kb, int kp4,
                                              int64_t N, const double* A, int64_t lda, const double* W,
-                                             int64_t ldw) {
+                                             int64_t ldw, const double* Lp) {
   double* Ls = st;
   double* Ws = st + NB * US;
   double* Cs = st + 2 * NB * US;
@@ -789,11 +805,11 @@ __device__ __forceinline__ void update_issue(double* st, int64_t R0, int64_t C0,
     const int64_t dl = N - ra, dw = N - ca;
     const int nl = (dl >= 2) ? 16 : (dl == 1 ? 8 : 0);
     const int nw = (dw >= 2) ? 16 : (dw == 1 ? 8 : 0);
-    const double* gl = A + ra + k0 * lda;
+    const double* gl = Lp + ra;
     const double* gw = W + ca;
     for (int t = threadIdx.x >> 5; t < kp4; t += 4) {
       const bool tin = t < kb;
-      cp_async16(&Ls[t * US + i], (tin && nl) ? gl + t * lda : A, tin ? nl : 0);
+      cp_async16(&Ls[t * US + i], (tin && nl) ? gl + t * ldw : Lp, tin ? nl : 0);
       cp_async16(&Ws[t * US + i], (tin && nw) ? gw + t * ldw : W, tin ? nw : 0);
     }
     const double* gc = A + ra + C0 * lda;
@@ -806,7 +822,7 @@ __device__ __forceinline__ void update_issue(double* st, int64_t R0, int64_t C0,
       const int i = idx & (UT - 1), t = idx >> 6;
       const bool tin = t < kb;
       const bool pl = tin && (R0 + i < N), pw = tin && (C0 + i < N);
-      cp_async8(&Ls[t * US + i], pl ? &A[(R0 + i) + (k0 + t) * lda] : A, pl);
+      cp_async8(&Ls[t * US + i], pl ? &Lp[(R0 + i) + t * ldw] : Lp, pl);
       cp_async8(&Ws[t * US + i], pw ? &W[(C0 + i) + t * ldw] : W, pw);
     }
     for (int idx = threadIdx.x; idx < UT * UT; idx += 128) {
@@ -839,7 +855,7 @@ __global__ void __launch_bounds__(128, 1) k_update(int64_t N, double* __restrict
   int64_t bi, bj;
   tri_tile(x, bi, bj);
   int64_t R0 = (b0 + bi) * UT, C0 = (b0 + bj) * UT;
-  update_issue<V16>(sm, R0, C0, k0, kb, kp4, N, A, lda, f.W, f.ldw);
+  update_issue<V16>(sm, R0, C0, k0, kb, kp4, N, A, lda, f.W, f.ldw, f.Lb);
   cp_async_commit();
   for (int it = 0; x < ntiles; it++) {
     const int64_t xn = x + gridDim.x;
@@ -849,7 +865,7 @@ __global__ void __launch_bounds__(128, 1) k_update(int64_t N, double* __restrict
       int64_t bin, bjn;
       tri_tile(xn, bin, bjn);
       Rn = (b0 + bin) * UT; Cn = (b0 + bjn) * UT;
-      update_issue<V16>(sm + (size_t)((it + 1) & 1) * USTAGE, Rn, Cn, k0, kb, kp4, N, A, lda, f.W, f.ldw);
+      update_issue<V16>(sm + (size_t)((it + 1) & 1) * USTAGE, Rn, Cn, k0, kb, kp4, N, A, lda, f.W, f.ldw, f.Lb);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
@@ -903,10 +919,10 @@ __global__ void __launch_bounds__(128, 1) k_update(int64_t N, double* __restrict
 // 4 warps each take alternate tiles ("ping-pong"), so one group's C loads
 // and epilogue stores overlap the other group's DMMA k-loop.
 constexpr int TNG = 2;                            // consumer groups (4 warps each), ping-pong
-constexpr int TS = TNG;                           // pipeline stages (stage i % TS == group of tile i)
+constexpr int TS = 3;                             // pipeline stages (L + W tiles)
 constexpr int TTHREADS = 32 * (1 + 4 * TNG);      // producer warp + consumer warps
 constexpr int TOPB = UT * NB * 8;                 // bytes per operand tile (32 KB)
-constexpr int TSTAGEB = 3 * TOPB;                 // C + L + W
+constexpr int TSTAGEB = 2 * TOPB;                 // L + W
 constexpr int TSMEM = TS * TSTAGEB + 1024 + 64;   // + alignment + barriers
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -972,9 +988,25 @@ __device__ __forceinline__ double dneg(double v) {   // exact sign flip on the i
   return r;
 }
 
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, int c0, int c1, unsigned src) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map),
+               "r"(c0), "r"(c1), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void sts_f64(unsigned addr, double v) {
+  asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(addr), "d"(v) : "memory");
+}
+
+// The update no longer reads C at all: each group computes P = L21 W21^T for
+// its tile from zero, writes -P (0 where the tile must not change: rows < s,
+// cols < s, upper triangle) into the stage it just consumed, and one thread
+// issues a TMA REDUCE-ADD of that tile into M (SASS UTMAREDG: the
+// read-modify-write happens in L2).  The stage is released to the producer
+// once the TMA engine has read it.
 __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* __restrict__ A, int64_t lda, FWork f,
                                                              const __grid_constant__ CUtensorMap mapA,
-                                                             const __grid_constant__ CUtensorMap mapW, int mode) {
+                                                             const __grid_constant__ CUtensorMap mapW,
+                                                             const __grid_constant__ CUtensorMap mapL, int mode) {
   FCtl* ctl = f.ctl;
   if (ctl->abort) return;
   const int2 pi = f.pinfo[f.pidx];
@@ -993,12 +1025,12 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
   const unsigned full0 = tsm + TS * TSTAGEB, empty0 = full0 + 8 * TS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < TS; i++) { mbar_init(full0 + 8 * i, 1); mbar_init(empty0 + 8 * i, 4); }
+    for (int i = 0; i < TS; i++) { mbar_init(full0 + 8 * i, 1); mbar_init(empty0 + 8 * i, 1); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
   if (warp == 0) {
-    // ---------------- producer: one lane issues all TMA copies (C, L and W tiles)
+    // ---------------- producer: one lane issues all TMA loads (L and W tiles)
     if (lane == 0) {
       for (int i = 0; i < ntile_cta; i++) {
         const int st = i % TS, u = i / TS;
@@ -1007,42 +1039,38 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
         int64_t bi, bj;
         upd_tile(x, nt, mode, bi, bj);
         const int R0 = (int)((b0 + bi) * UT), C0 = (int)((b0 + bj) * UT);
-        const unsigned sC = tsm + st * TSTAGEB, sL = sC + TOPB, sW = sL + TOPB;
+        const unsigned sL = tsm + st * TSTAGEB, sW = sL + TOPB;
         const unsigned fb = full0 + 8 * st;
         mbar_expect_tx(fb, TSTAGEB);
 #pragma unroll
         for (int b = 0; b < 8; b++) {
-          tma_load_2d(sC + b * 4096, &mapA, R0 + 8 * b, C0, fb);
-          tma_load_2d(sL + b * 4096, &mapA, R0 + 8 * b, (int)k0, fb);
+          tma_load_2d(sL + b * 4096, &mapL, R0 + 8 * b, 0, fb);
           tma_load_2d(sW + b * 4096, &mapW, C0 + 8 * b, 0, fb);
         }
       }
     }
     return;
   }
-  // ---------------- consumers: group grp takes tiles grp, grp+TNG, ... (stage == group)
+  // ---------------- consumers: group grp takes tiles grp, grp+TNG, ...
   const int grp = (warp - 1) >> 2, wq = (warp - 1) & 3;
   const int wm = (wq >> 1) * 32, wn = (wq & 1) * 32;
   const int g = lane >> 2, q = lane & 3;
+  const bool leader = (wq == 0 && lane == 0);
   for (int i = grp; i < ntile_cta; i += TNG) {
     const int st = i % TS, u = i / TS;
     const int64_t x = blockIdx.x + (int64_t)i * gridDim.x;
     int64_t bi, bj;
     upd_tile(x, nt, mode, bi, bj);
     const int64_t R0 = (b0 + bi) * UT, C0 = (b0 + bj) * UT;
-    mbar_wait(full0 + 8 * st, u & 1);
-    const unsigned Ct = tsm + st * TSTAGEB;
-    const unsigned Lb = Ct + TOPB + (unsigned)(wm >> 3) * 4096u;
-    const unsigned Wb = Ct + 2 * TOPB + (unsigned)(wn >> 3) * 4096u;
-    // acc = -C ; acc += L W^T ; C_new = -acc   (negations are exact)
     double acc[4][4][2];
 #pragma unroll
     for (int a = 0; a < 4; a++)
 #pragma unroll
-      for (int b = 0; b < 4; b++)
-#pragma unroll
-        for (int e = 0; e < 2; e++)
-          acc[a][b][e] = dneg(lds_f64(Ct + tma_off(wm + 8 * a + g, wn + 8 * b + 2 * q + e)));
+      for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+    mbar_wait(full0 + 8 * st, u & 1);
+    const unsigned Lt = tsm + st * TSTAGEB;
+    const unsigned Lb = Lt + (unsigned)(wm >> 3) * 4096u;
+    const unsigned Wb = Lt + TOPB + (unsigned)(wn >> 3) * 4096u;
     // k-loop with register double-buffered fragments (loads of step t+1 overlap the DMMAs of step t)
     double a0[4], b0v[4], a1[4], b1v[4];
     auto frag = [&](int ks, double* av, double* bv) {
@@ -1067,8 +1095,9 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
 #pragma unroll
         for (int b = 0; b < 4; b++) dmma(acc[a][b][0], acc[a][b][1], a1[a], b1v[b]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty0 + 8 * st);
+    // the whole group has finished reading L/W of this stage
+    asm volatile("bar.sync %0, 128;\n" ::"r"(grp + 1) : "memory");
+    // -P (masked) into the stage's L area, same swizzled box layout as the loads
 #pragma unroll
     for (int a = 0; a < 4; a++) {
       const int64_t row = R0 + wm + 8 * a + g;
@@ -1076,11 +1105,23 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
       for (int b = 0; b < 4; b++)
 #pragma unroll
         for (int e = 0; e < 2; e++) {
-          const int64_t col = C0 + wn + 8 * b + 2 * q + e;
-          if (row < N && col >= s && row >= col) A[row + col * lda] = dneg(acc[a][b][e]);
+          const int cl = wn + 8 * b + 2 * q + e;
+          const int64_t col = C0 + cl;
+          const bool upd = (row < N && col >= s && row >= col);
+          sts_f64(Lt + tma_off(wm + 8 * a + g, cl), upd ? dneg(acc[a][b][e]) : 0.0);
         }
     }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("bar.sync %0, 128;\n" ::"r"(grp + 1) : "memory");
+    if (leader) {
+#pragma unroll
+      for (int b = 0; b < 8; b++) tma_reduce_add_2d(&mapA, (int)(R0 + 8 * b), (int)C0, Lt + b * 4096);
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");   // smem source consumed
+      mbar_arrive(empty0 + 8 * st);
+    }
   }
+  if (leader) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // reductions complete before exit
 }
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1208,7 +1249,8 @@ double* mds_factor_tol_ptr(const void* fwork) {
 // stream (so concurrent factorizations on different streams never share
 // events; a call on stream s always orders its side work through s).
 struct LookaheadCtx {
-  cudaStream_t side = nullptr;
+  cudaStream_t side = nullptr;    // rest-of-matrix trailing updates
+  cudaStream_t store = nullptr;   // panel copies Lb -> M (nothing but the finalize waits on them)
   std::vector<cudaEvent_t> ev;
 };
 static std::mutex g_la_mu;
@@ -1221,7 +1263,12 @@ static LookaheadCtx* lookahead_ctx(cudaStream_t st, size_t nev) {
   LookaheadCtx*& c = g_la[std::make_pair(dev, st)];
   if (!c) {
     c = new LookaheadCtx();
-    if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) { delete c; c = nullptr; return nullptr; }
+    if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->store, cudaStreamNonBlocking) != cudaSuccess) {
+      delete c;
+      c = nullptr;
+      return nullptr;
+    }
   }
   while (c->ev.size() < nev) {
     cudaEvent_t e;
@@ -1292,16 +1339,19 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   // p+1's diag/trsm/accept on the SMs it leaves free).  Panel p+1's exact
   // BK step (which may interchange anywhere) waits for the rest-update.
   const bool lookahead = use_tma && std::getenv("MDS_NO_LOOKAHEAD") == nullptr;
-  cudaStream_t side = nullptr;
+  cudaStream_t side = nullptr, sstore = nullptr;
   std::vector<cudaEvent_t>* evs = nullptr;
   if (lookahead) {
-    LookaheadCtx* c = lookahead_ctx(st, 2 * (size_t)npmax + 2);
+    LookaheadCtx* c = lookahead_ctx(st, 3 * (size_t)npmax + 3);
     if (!c) return MDS_ERR_CUDA;
     side = c->side;
+    sstore = c->store;
     evs = &c->ev;
   }
-  CUtensorMap mapW1;
-  if (use_tma && !make_map(&mapW1, f.W1, N, NB, f.ldw)) return MDS_ERR_CUDA;
+  CUtensorMap mapW1, mapL0, mapL1;
+  if (use_tma && !(make_map(&mapW1, f.W1, N, NB, f.ldw) && make_map(&mapL0, f.Lb, N, NB, f.ldw) &&
+                   make_map(&mapL1, f.Lb1, N, NB, f.ldw)))
+    return MDS_ERR_CUDA;
   unsigned reserve = 16;         // SMs left to the panel chain while the rest-update runs
   if (g_grid_cap > 0 && g_grid_cap < sms) { sms = g_grid_cap; reserve = 0; }
   int64_t plast = -1;
@@ -1311,31 +1361,42 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     if (rows <= 0) break;
     FWork fp = f;
     fp.pidx = (int)p;
-    if (p & 1) fp.W = f.W1;
+    if (p & 1) { fp.W = f.W1; fp.Lb = f.Lb1; }
     MDS_LAUNCH(PC_PANEL_DIAG, st, (k_panel_diag<<<1, 256, F1SMEM, st>>>(N, M, ldm, fp)));
     const unsigned g256 = (unsigned)std::max<int64_t>(mds_cdiv(rows, 256), 1);
     const unsigned g64 = (unsigned)std::max<int64_t>(mds_cdiv(rows, UT), 1);
     MDS_LAUNCH(PC_PANEL_TRSM, st, (k_panel_trsm<<<g64, 128, usmem, st>>>(N, M, ldm, fp)));
-    MDS_LAUNCH(PC_PANEL_ACCEPT, st, (k_panel_accept<<<dim3(g256, 8), 256, 0, st>>>(N, M, ldm, fp, piv)));
-    if (lookahead && plast >= 0) MDS_CUDA_TRY(cudaStreamWaitEvent(st, (*evs)[2 * plast + 1], 0));
+    if (lookahead && plast >= 0) MDS_CUDA_TRY(cudaStreamWaitEvent(st, (*evs)[3 * plast + 1], 0));
     MDS_LAUNCH(PC_PANEL_SLOW, st, (k_panel_slow<<<1, 1024, 0, st>>>(N, M, ldm, fp, piv)));
     const int64_t n2max = std::max<int64_t>(rows - 1, 0);
     const int64_t nt = mds_cdiv(n2max, UT) + 1;
-    if (n2max > 0) {
-      const CUtensorMap& mw = (p & 1) ? mapW1 : mapW;
-      if (lookahead) {
+    const CUtensorMap& mw = (p & 1) ? mapW1 : mapW;
+    const CUtensorMap& ml = (p & 1) ? mapL1 : mapL0;
+    if (lookahead) {
+      if (n2max > 0) {
         const unsigned gn = (unsigned)std::min<int64_t>(2 * nt, sms);
-        MDS_LAUNCH(PC_UPDATE, st, (k_update_tma<<<gn, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, 1)));
-        MDS_CUDA_TRY(cudaEventRecord((*evs)[2 * p], st));
-        MDS_CUDA_TRY(cudaStreamWaitEvent(side, (*evs)[2 * p], 0));
+        MDS_LAUNCH(PC_UPDATE, st, (k_update_tma<<<gn, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, 1)));
+      }
+      MDS_CUDA_TRY(cudaEventRecord((*evs)[3 * p], st));
+      MDS_CUDA_TRY(cudaStreamWaitEvent(side, (*evs)[3 * p], 0));
+      // the panel copy into M runs on its own stream, off every critical path; it
+      // follows U_next, the only update touching the tile columns that hold cols < s
+      MDS_CUDA_TRY(cudaStreamWaitEvent(sstore, (*evs)[3 * p], 0));
+      MDS_LAUNCH(PC_PANEL_STORE, sstore, (k_panel_store<<<dim3(g256, 8), 256, 0, sstore>>>(N, M, ldm, fp)));
+      if (n2max > 0) {
         const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt * (nt + 1) / 2, sms - reserve));
-        MDS_LAUNCH(PC_UPDATE, side, (k_update_tma<<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, 2)));
-        MDS_CUDA_TRY(cudaEventRecord((*evs)[2 * p + 1], side));
-        plast = p;
-      } else {
+        MDS_LAUNCH(PC_UPDATE, side,
+                   (k_update_tma<<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, 2)));
+      }
+      MDS_CUDA_TRY(cudaEventRecord((*evs)[3 * p + 1], side));
+      plast = p;
+    } else {
+      MDS_LAUNCH(PC_PANEL_STORE, st, (k_panel_store<<<dim3(g256, 8), 256, 0, st>>>(N, M, ldm, fp)));
+      if (n2max > 0) {
         const unsigned ugrid = (unsigned)std::min<int64_t>(nt * (nt + 1) / 2, sms);
         if (use_tma)
-          MDS_LAUNCH(PC_UPDATE, st, (k_update_tma<<<ugrid, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, 0)));
+          MDS_LAUNCH(PC_UPDATE, st,
+                     (k_update_tma<<<ugrid, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, 0)));
         else if (v16)
           MDS_LAUNCH(PC_UPDATE, st,
                      (k_update<true><<<ugrid, 128, 2 * USTAGE * sizeof(double), st>>>(N, M, ldm, fp)));
@@ -1345,7 +1406,11 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
       }
     }
   }
-  if (lookahead && plast >= 0) MDS_CUDA_TRY(cudaStreamWaitEvent(st, (*evs)[2 * plast + 1], 0));
+  if (lookahead && plast >= 0) {
+    MDS_CUDA_TRY(cudaStreamWaitEvent(st, (*evs)[3 * plast + 1], 0));
+    MDS_CUDA_TRY(cudaEventRecord((*evs)[3 * npmax], sstore));   // last panel copy
+    MDS_CUDA_TRY(cudaStreamWaitEvent(st, (*evs)[3 * npmax], 0));
+  }
   {
     int dev = 0, sms = 148, occ = 0;
     cudaGetDevice(&dev);

@@ -1,6 +1,7 @@
 // prof.cu — launch counter and per-kernel-class CUDA-event timing (used by
 // bench.py to measure the dominant kernel's average launch duration on the
 // stream it is launched on; off by default, never active during graph capture).
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <vector>
@@ -13,7 +14,6 @@ static std::mutex g_mu;
 struct Rec { int cls; cudaEvent_t a, b; };
 static std::vector<Rec> g_recs;
 static std::vector<cudaEvent_t> g_pool;
-static int g_open_cls = -1;
 static cudaEvent_t g_open_ev = nullptr;
 
 static cudaEvent_t get_event() {
@@ -25,7 +25,6 @@ void mds_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void mds_prof_start(int cls, cudaStream_t st) {
   std::lock_guard<std::mutex> lk(g_mu);
-  g_open_cls = cls;
   g_open_ev = get_event();
   cudaEventRecord(g_open_ev, st);
 }
@@ -48,17 +47,32 @@ extern "C" int mds_profile_begin(void) {
   return MDS_OK;
 }
 
+// per-launch timeline of the last profiled region: (class, start_ms, end_ms) relative to the first event
+static std::vector<double> g_timeline;
+extern "C" int64_t mds_profile_timeline(double* out3, int64_t cap) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  const int64_t n = (int64_t)g_timeline.size() / 3;
+  for (int64_t i = 0; i < std::min(n, cap) * 3; i++) out3[i] = g_timeline[i];
+  return n;
+}
+
 extern "C" int mds_profile_end(double* ms_by_class, int64_t* launches_by_class, int ncls) {
   std::lock_guard<std::mutex> lk(g_mu);
   g_mds_prof = false;
   if (ncls < PC_COUNT || !ms_by_class || !launches_by_class) return MDS_ERR_ARG;
   for (int c = 0; c < ncls; c++) { ms_by_class[c] = 0.0; launches_by_class[c] = 0; }
+  g_timeline.clear();
   for (auto& r : g_recs) {
     if (cudaEventSynchronize(r.b) != cudaSuccess) return MDS_ERR_CUDA;
-    float ms = 0.f;
+    float ms = 0.f, t0 = 0.f, t1 = 0.f;
     cudaEventElapsedTime(&ms, r.a, r.b);
+    cudaEventElapsedTime(&t0, g_recs[0].a, r.a);
+    cudaEventElapsedTime(&t1, g_recs[0].a, r.b);
     ms_by_class[r.cls] += ms;
     launches_by_class[r.cls] += 1;
+    g_timeline.push_back((double)r.cls);
+    g_timeline.push_back((double)t0);
+    g_timeline.push_back((double)t1);
   }
   for (auto& r : g_recs) { g_pool.push_back(r.a); g_pool.push_back(r.b); }
   g_recs.clear();
