@@ -148,6 +148,27 @@ __global__ void k_condense_dense(int64_t n_d, int64_t m, const double* __restric
 // diagonal term (s = 0, every lane hits it) is a warp sum; off-diagonal lanes
 // that collide on the same c1 are serialised via __match_any_sync (no FP64
 // shared-memory atomics, which are CAS loops on sm_100a).  Deterministic.
+// L2 cache policies: the J_s row gathers (colidx, val, w, r_xs: ~70 MB at C3)
+// are re-read ~5x and must stay L2-resident while M (268 MB) streams out.
+__device__ __forceinline__ unsigned long long pol_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ldg_el(const double* a, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int ldg_el(const int32_t* a, unsigned long long pol) {
+  int v;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void stg_ef(double* a, double v) {   // streaming store (evict-first)
+  asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(a), "d"(v) : "memory");
+}
+
 constexpr int YY_U = 2;      // list entries per lane per iteration
 constexpr int YY_SMAX = 8;   // suffix entries gathered up front (longer suffixes take a slow loop)
 constexpr unsigned TKP_PMASK = (1u << 27) - 1u;
@@ -167,6 +188,7 @@ k_condense_yy(int64_t n_d, int64_t m_E, int64_t m, int64_t acc_len,
   const int64_t ntask = (m + 1) / 2;
   if (task >= ntask) return;
   const unsigned lanemask_lt = (1u << lane) - 1u;
+  const unsigned long long pol = pol_evict_last();
   for (int half = 0; half < 2; half++) {
     const int64_t c = half ? (m - 1 - task) : task;
     if (half && c == task) break;
@@ -178,61 +200,94 @@ k_condense_yy(int64_t n_d, int64_t m_E, int64_t m, int64_t acc_len,
       for (int64_t i = lane; i < clen; i += 32) acc[i] = 0.0;
       __syncwarp();
       double diag = 0.0;
-      for (int32_t e = e0; e < e1; e += 32 * YY_U) {
-        int kk[YY_U], pp[YY_U], ln[YY_U];
-        double tt[YY_U];
-        int cs[YY_U][YY_SMAX];
-        double vs[YY_U][YY_SMAX];
+      // software pipeline over iterations: the transpose entries two iterations ahead
+      // and the row gathers one iteration ahead are in flight while this iteration
+      // scatters (the loop is otherwise bound by dependent L2/HBM latency)
+      struct KP { int k[YY_U], p[YY_U], l[YY_U]; };
+      struct GA { int cs[YY_U][YY_SMAX]; double vs[YY_U][YY_SMAX]; double wk[YY_U], rr[YY_U]; int l[YY_U]; };
+      auto load_kp = [&](int32_t e, KP& o) {
 #pragma unroll
         for (int u = 0; u < YY_U; u++) {
           const int32_t my = e + u * 32 + lane;
-          ln[u] = 0; kk[u] = 0; pp[u] = 0;
+          o.l[u] = 0; o.k[u] = 0; o.p[u] = 0;
           if (my < e1) {
             const int2 kp = tkp[my];
-            kk[u] = kp.x;
-            pp[u] = (int)((unsigned)kp.y & TKP_PMASK);
-            ln[u] = (int)((unsigned)kp.y >> 27);
-            if (ln[u] == 31) ln[u] = rowptr[kk[u] + 1] - pp[u];
+            o.k[u] = kp.x;
+            o.p[u] = (int)((unsigned)kp.y & TKP_PMASK);
+            o.l[u] = (int)((unsigned)kp.y >> 27);
           }
         }
+      };
+      auto gather = [&](KP& kp, GA& g) {
 #pragma unroll
         for (int u = 0; u < YY_U; u++) {
+          if (kp.l[u] == 31) kp.l[u] = rowptr[kp.k[u] + 1] - kp.p[u];
+          g.l[u] = kp.l[u];
 #pragma unroll
-          for (int s = 0; s < YY_SMAX; s++) {
-            cs[u][s] = -1;
-            vs[u][s] = 0.0;
-            if (s < ln[u]) { cs[u][s] = colidx[pp[u] + s]; vs[u][s] = val[pp[u] + s]; }
+          for (int s2 = 0; s2 < YY_SMAX; s2++) {
+            g.cs[u][s2] = -1;
+            g.vs[u][s2] = 0.0;
+            if (s2 < kp.l[u]) {
+              g.cs[u][s2] = ldg_el(colidx + kp.p[u] + s2, pol);
+              g.vs[u][s2] = ldg_el(val + kp.p[u] + s2, pol);
+            }
           }
-          const double wk = (ln[u] > 0) ? w[kk[u]] : 0.0;
-          tt[u] = vs[u][0] * wk;
-          if (base == 0 && r && ln[u] > 0) rsum += tt[u] * r[kk[u]];
+          g.wk[u] = (kp.l[u] > 0) ? ldg_el(w + kp.k[u], pol) : 0.0;
+          g.rr[u] = (base == 0 && r && kp.l[u] > 0) ? ldg_el(r + kp.k[u], pol) : 0.0;
+        }
+      };
+      KP kpn, kpnn;
+      GA ga, gb;
+      int kcur[YY_U], pcur[YY_U], kn[YY_U], pn[YY_U];
+      load_kp(e0, kpn);
+#pragma unroll
+      for (int u = 0; u < YY_U; u++) { kcur[u] = kpn.k[u]; pcur[u] = kpn.p[u]; }
+      gather(kpn, ga);
+      load_kp(e0 + 32 * YY_U, kpnn);
+      for (int32_t e = e0; e < e1; e += 32 * YY_U) {
+        const bool more = (e + 32 * YY_U) < e1;
+        if (more) {
+#pragma unroll
+          for (int u = 0; u < YY_U; u++) { kn[u] = kpnn.k[u]; pn[u] = kpnn.p[u]; }
+          gather(kpnn, gb);
+          load_kp(e + 64 * YY_U, kpnn);
+        }
+        double tt[YY_U];
+#pragma unroll
+        for (int u = 0; u < YY_U; u++) {
+          tt[u] = ga.vs[u][0] * ga.wk[u];
+          rsum += tt[u] * ga.rr[u];
         }
         // s = 0: the diagonal (c1 == c) -- every lane hits it: warp sum, no scatter
 #pragma unroll
-        for (int u = 0; u < YY_U; u++) diag += tt[u] * vs[u][0];
+        for (int u = 0; u < YY_U; u++) diag += tt[u] * ga.vs[u][0];
         // s >= 1: off-diagonal scatter into the private column
 #pragma unroll
         for (int u = 0; u < YY_U; u++) {
 #pragma unroll
-          for (int s = 1; s < YY_SMAX; s++) {
+          for (int s2 = 1; s2 < YY_SMAX; s2++) {
             int64_t c1 = -1;
-            if (s < ln[u]) {
-              c1 = (int64_t)cs[u][s] - c - base;
+            if (s2 < ga.l[u]) {
+              c1 = (int64_t)ga.cs[u][s2] - c - base;
               if (c1 < 0 || c1 >= clen) c1 = -1;
             }
             const bool go = c1 >= 0;
             const unsigned gomask = __ballot_sync(0xffffffffu, go);
             if (gomask == 0u) continue;
-            const double upd = tt[u] * vs[u][s];
+            const double upd = tt[u] * ga.vs[u][s2];
             if (go) {
+#ifdef MDS_YY_NOMATCH
+              const unsigned peers = 1u << lane;   // timing experiment only (wrong on collisions)
+#else
               const unsigned peers = __match_any_sync(gomask, (int)c1);
+#endif
               if (peers == (1u << lane)) {
                 acc[c1] -= upd;
               } else {
                 const int rank = __popc(peers & lanemask_lt);
                 const int gs = __popc(peers);
-                for (int q = 0; q < gs; q++) {
-                  if (rank == q) acc[c1] -= upd;
+                for (int qq = 0; qq < gs; qq++) {
+                  if (rank == qq) acc[c1] -= upd;
                   __syncwarp(peers);
                 }
               }
@@ -240,12 +295,12 @@ k_condense_yy(int64_t n_d, int64_t m_E, int64_t m, int64_t acc_len,
             __syncwarp();
           }
           // rare: suffix longer than YY_SMAX
-          for (int s = YY_SMAX; __any_sync(0xffffffffu, s < ln[u]); s++) {
+          for (int s2 = YY_SMAX; __any_sync(0xffffffffu, s2 < ga.l[u]); s2++) {
             int64_t c1 = -1;
             double upd = 0.0;
-            if (s < ln[u]) {
-              c1 = (int64_t)colidx[pp[u] + s] - c - base;
-              upd = tt[u] * val[pp[u] + s];
+            if (s2 < ga.l[u]) {
+              c1 = (int64_t)colidx[pcur[u] + s2] - c - base;
+              upd = tt[u] * val[pcur[u] + s2];
               if (c1 < 0 || c1 >= clen) c1 = -1;
             }
             const bool go = c1 >= 0;
@@ -254,15 +309,21 @@ k_condense_yy(int64_t n_d, int64_t m_E, int64_t m, int64_t acc_len,
               const unsigned peers = __match_any_sync(gomask, (int)c1);
               const int rank = __popc(peers & lanemask_lt);
               const int gs = __popc(peers);
-              for (int q = 0; q < gs; q++) {
-                if (rank == q) acc[c1] -= upd;
+              for (int qq = 0; qq < gs; qq++) {
+                if (rank == qq) acc[c1] -= upd;
                 __syncwarp(peers);
               }
             }
             __syncwarp();
           }
         }
+        if (more) {
+          ga = gb;
+#pragma unroll
+          for (int u = 0; u < YY_U; u++) { kcur[u] = kn[u]; pcur[u] = pn[u]; }
+        }
       }
+      (void)kcur;
       diag = warp_sum(diag);
       __syncwarp();
       // diagonal terms -diag(0_{m_E}, 1/d_h) - delta_c I, then one coalesced column write
@@ -277,7 +338,7 @@ k_condense_yy(int64_t n_d, int64_t m_E, int64_t m, int64_t acc_len,
             v = v - 1.0 / dh;
           }
         }
-        Mc[i] = v;
+        stg_ef(Mc + i, v);
       }
       __syncwarp();
     }
