@@ -180,7 +180,8 @@ __global__ void k_dsolve(int64_t N, const double* __restrict__ LD, int64_t lda, 
 __global__ void __launch_bounds__(ST) k_trsv_bwd(int64_t N, const double* __restrict__ L, int64_t lda, double* y,
                                                  const double* __restrict__ binv, int* flags, int* ticket) {
   __shared__ int s_i;
-  __shared__ double red[ST / 32][TB];
+  __shared__ double redt[TB][TB + 1];
+  __shared__ double part4[4][TB];
   __shared__ double v[TB];
   const int64_t nblk = (N + TB - 1) / TB;
   if (threadIdx.x == 0) s_i = atomicAdd(ticket, 1);
@@ -218,19 +219,21 @@ __global__ void __launch_bounds__(ST) k_trsv_bwd(int64_t N, const double* __rest
 #pragma unroll
     for (int c = 0; c < 16; c++) lv[c] = ln[c];
   }
-  // reduce acc over the 64 rows k: warp shuffle (32 rows) then the 2 warps of each column group
+  // reduce acc over the 64 rows k: transpose through shared memory (no shuffle chains)
 #pragma unroll
-  for (int c = 0; c < 16; c++) {
-    double t = acc[c];
+  for (int c = 0; c < 16; c++) redt[k][cgp * 16 + c] = acc[c];
+  __syncthreads();
+  {
+    const int c = threadIdx.x & (TB - 1), part = threadIdx.x / TB;   // 4 threads per column, 16 rows each
+    double sacc = 0.0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (lane == 0) red[warp][c] = t;
+    for (int kk = 0; kk < 16; kk++) sacc += redt[part * 16 + kk][c];
+    part4[part][c] = sacc;
   }
   __syncthreads();
   if (threadIdx.x < TB) {
     const int cc = threadIdx.x;
-    const int grp = cc >> 4, c = cc & 15;
-    const double sum = red[2 * grp][c] + red[2 * grp + 1][c];
+    const double sum = part4[0][cc] + part4[1][cc] + part4[2][cc] + part4[3][cc];
     v[cc] = (cc < nr) ? ld_cg(&y[r0 + cc]) - sum : 0.0;
   }
   __syncthreads();
@@ -242,11 +245,11 @@ __global__ void __launch_bounds__(ST) k_trsv_bwd(int64_t N, const double* __rest
     const int r = cgp * 16 + rr;
     sacc += B[r + k * TB] * v[r];
   }
-  red[cgp][k] = sacc;
+  part4[cgp][k] = sacc;
   __syncthreads();
   if (threadIdx.x < TB) {
     const int cc = threadIdx.x;
-    if (cc < nr) y[r0 + cc] = red[0][cc] + red[1][cc] + red[2][cc] + red[3][cc];
+    if (cc < nr) y[r0 + cc] = part4[0][cc] + part4[1][cc] + part4[2][cc] + part4[3][cc];
   }
   __syncthreads();
   if (threadIdx.x == 0) {
