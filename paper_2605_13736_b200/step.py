@@ -91,20 +91,29 @@ class KKTStep:
         self.vwork = torch.zeros(step_vectors_workspace_size(n), dtype=torch.uint8, device=self.M.device)
 
     # -- the hot path ------------------------------------------------------
-    def run(self, stream=None, sync_inertia=False):
+    def run(self, stream=None, sync_inertia=False, marks=None):
+        """One Newton step.  `marks`: optional list of 5 CUDA events recorded on the
+        stream between the four calls (wall-clock phase timing)."""
         p = self.p
+        ev = (lambda i: marks[i].record(stream) if stream is not None else marks[i].record()) if marks else \
+            (lambda i: None)
         self.status.zero_()
+        ev(0)
         condense(p.plan, p.val, p.h_ss, p.sigma_s, p.H_dd, p.ldh, p.sigma_d, p.J_d, p.ldj, p.d_h, p.delta_w,
                  p.delta_c, p.r, self.M, self.ldm, self.rhs, self.w, self.status, stream)
+        ev(1)
         ine = factor(self.N, self.M, self.ldm, self.piv, self.zero_tol, self.inertia, self.status, self.fwork,
                      sync=sync_inertia, stream=stream)
+        ev(2)
         solve(p.plan, self.N, self.M, self.ldm, self.piv, self.rhs, p.val, self.w, p.r[:p.n_s] if p.n_s else None,
               self.dxy, self.dx_s, self.zero_tol, self.fwork, self.status, self.swork, stream)
+        ev(3)
         if self.sv is not None:
             s = self.sv
             step_vectors(self.nb, s["x"], self.dirn[:self.nb], s["lo"], s["up"], s["zl"], s["zu"], s["dzl"],
                          s["dzu"], s["tau"], s["mu"], self.vout, self.sigma, self.status, self.vwork,
                          res=(p.r,), stream=stream)
+        ev(4)
         return ine
 
     def capture(self, warmup=1):

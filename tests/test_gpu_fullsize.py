@@ -1,0 +1,98 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (CUDA-graph replay of the whole step):
+  C2 (N=1024, n_s=100k): every output against the oracle.
+  C3 (N=8192, n_s=1M): condensed M element by element against the oracle;
+    inertia against the closed form; the solve through properties that hold at
+    any size (relative residual of the condensed system against the oracle's
+    M <= 1e-10, dx_s equal to the recovery formula applied to the GPU's dy);
+    step vectors against the oracle on the GPU's direction."""
+import numpy as np
+import pytest
+
+import mdsgen
+import oracle
+from tests.helpers import rel_inf
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2605_13736_b200 as mds  # noqa: E402
+
+
+def graph_step(prob, sv):
+    st = mds.KKTStep(mds.DeviceProblem(prob), sv=sv)
+    g = st.capture()
+    g.replay()
+    torch.cuda.synchronize()
+    return st, st.results()
+
+
+def sym_matvec_lower(M, x):
+    L = np.tril(M)
+    return L @ x + np.tril(M, -1).T @ x
+
+
+def test_c2_full_step_vs_oracle():
+    prob = mdsgen.config_problem("C2")
+    sv = mdsgen.step_vectors_for(prob, seed=7)
+    st, out = graph_step(prob, sv)
+    ref = oracle.newton_step(prob)
+    assert out["status"] == 0
+    assert out["inertia"] == ref["inertia"] == prob.expected_inertia
+    assert rel_inf(out["dxy"], ref["dxy"]) <= 1e-8
+    assert rel_inf(out["dx_s"], ref["dx_s"]) <= 1e-8
+    res = np.abs(sym_matvec_lower(ref["M"], out["dxy"]) - ref["rhs_c"]).max() / np.abs(ref["rhs_c"]).max()
+    assert res <= 1e-10
+
+
+def test_c3_full_size_properties():
+    prob = mdsgen.config_problem("C3")
+    sv = mdsgen.step_vectors_for(prob, seed=7)
+    dp = mds.DeviceProblem(prob)
+    st = mds.KKTStep(dp, sv=sv)
+    # condensation alone, element by element
+    mds.condense(dp.plan, dp.val, dp.h_ss, dp.sigma_s, dp.H_dd, dp.ldh, dp.sigma_d, dp.J_d, dp.ldj, dp.d_h,
+                 dp.delta_w, dp.delta_c, dp.r, st.M, st.ldm, st.rhs, st.w, st.status)
+    torch.cuda.synchronize()
+    M_or, rhs_or, w_or = oracle.condense(prob)
+    Mg = st.M_host()
+    scale = np.abs(np.tril(M_or)).max()
+    assert np.abs(np.tril(Mg) - np.tril(M_or)).max() <= 1e-13 * scale
+    np.testing.assert_array_equal(st.w[:prob.n_s].cpu().numpy(), w_or)
+    assert rel_inf(st.rhs[:prob.N].cpu().numpy(), rhs_or) <= 1e-13
+    del Mg
+    # the whole step as bench.py runs it (graph replay)
+    g = st.capture()
+    g.replay()
+    out = st.results()
+    assert out["status"] == 0
+    assert out["inertia"] == prob.expected_inertia == (4096, 0, 4096)
+    res = np.abs(sym_matvec_lower(M_or, out["dxy"]) - rhs_or).max() / np.abs(rhs_or).max()
+    assert res <= 1e-10, res
+    dy = out["dxy"][prob.n_d:]
+    dxs_ref = oracle.recover(prob, w_or, prob.r[:prob.n_s], dy)
+    assert rel_inf(out["dx_s"], dxs_ref) <= 1e-12
+    dx = np.concatenate([out["dx_s"], out["dxy"][:prob.n_d]])
+    s, v, sig = oracle.step_vectors(sv.x, dx, sv.lo, sv.up, sv.zl, sv.zu, sv.dzl, sv.dzu, sv.tau, sv.mu)
+    assert out["vec"]["alpha_p"] == v["alpha_p"] and out["vec"]["alpha_d"] == v["alpha_d"]
+    assert out["vec"]["compl_inf"] == v["compl_inf"]
+    np.testing.assert_array_equal(out["sigma"], sig)
+
+
+@pytest.mark.parametrize("N,n2", [(1500, 300), (2111, 500)])
+def test_pivoting_heavy_multi_panel(N, n2):
+    # prescribed-spectrum matrices: many 2x2 pivots and interchanges across ~30 panels
+    A, ine = mdsgen.g3_prescribed(N, seed=N, n2x2=n2)
+    b = np.random.default_rng(N).standard_normal(N)
+    LD, ipiv, _ = oracle.bk_factor(A)
+    tol = oracle.default_tol(A)
+    x_or = oracle.bk_solve(LD, ipiv, b, tol)
+    from tests.test_gpu_parity import factor_solve_dense
+    g_ine, x, status, _ = factor_solve_dense(A, b)
+    assert status == 0
+    assert g_ine == oracle.inertia(LD, ipiv, tol) == ine
+    As = np.tril(A) + np.tril(A, -1).T
+    assert np.abs(As @ x - b).max() / np.abs(b).max() <= 1e-10
+    assert rel_inf(x, x_or) <= 1e-8
