@@ -7,7 +7,7 @@
 // tcgen05 kind on Blackwell).  Each panel first tries a SPECULATIVE fast path:
 //   F1 k_panel_diag   one CTA factors the NB x NB diagonal block without
 //                     pivoting (in shared memory),
-//   F2 k_panel_trsm   all SMs form W21 = A21 L11^{-T} (the fully updated
+//   F2 k_panel_trsm   all free SMs form W21 = A21 L11^{-T} (the fully updated
 //                     panel columns) and the per-column BK colmax,
 //   F4 k_panel_slow   accepts the longest prefix of columns that pass BK's
 //                     1x1-no-interchange test |d_k| >= alpha*colmax_k (the test
@@ -73,6 +73,10 @@ struct FWork {
   double* Lb;         // [ldw * WCOLS]  the panel's D + L columns (speculative, fixed up by k_panel_slow);
   double* Lb1;        //   copied into M by k_panel_store; double-buffered like W
   int2* pinfo;        // [N+2] per-panel (k0, kb), written by k_panel_slow, read by the updates
+  unsigned long long* ucount;   // [2N+4] per-(panel, launch) tile counters of the updates (dynamic scheduling)
+  const double* Wprev;          // the previous panel's W / Lb (the other parity buffers), for the
+  const double* Lbprev;         //   deferred update of this panel's columns
+  int fuse;           // 1: this panel's columns still lack the previous panel's update (look-ahead)
   int pidx;           // panel index of this launch (host loop counter)
   int64_t ldw;
 };
@@ -98,6 +102,10 @@ FWork carve(void* work, int64_t N, size_t* total) {
   f.Lb = reinterpret_cast<double*>(take(sizeof(double) * f.ldw * WCOLS));
   f.Lb1 = reinterpret_cast<double*>(take(sizeof(double) * f.ldw * WCOLS));
   f.pinfo = reinterpret_cast<int2*>(take(sizeof(int2) * (N + 2)));
+  f.ucount = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * 2 * (N + 2)));
+  f.Wprev = f.W1;
+  f.Lbprev = f.Lb1;
+  f.fuse = 0;
   f.pidx = 0;
   if (total) *total = off;
   return f;
@@ -182,116 +190,199 @@ __global__ void __launch_bounds__(1024) k_anorm_final(int64_t N, const double* r
 }
 
 // ---------------------------------------------------------------------------
-// F1: unpivoted LDL^T of the NB x NB diagonal block (shared memory), blocked
-// right-looking with 16-column blocks: inside a block one column step per
-// __syncthreads touches only the block's 16 columns; the rest of the block
-// is updated once per 16 columns (rank-16).  Then L11^{-1} by a blocked
-// triangular inversion (16x16 diagonal blocks by one warp each, off-diagonal
-// blocks by small GEMMs), so F2 forms W21 = A21 L11^{-T} as a GEMM on the
-// FP64 tensor cores (explicit inverted diagonal blocks, as MAGMA's GPU trsm).
-// Leaves W11 (updated, unscaled columns) in W, X = L11^{-T} (row-major [t][j])
-// in Lblk, d and the in-block part of colmax in ctl.  A is NOT modified
-// (rejected columns need their original values).
+// Panel fast path.
+//   F1 k_panel_diag (1 CTA): apply the previous panel's rank-kb update to the
+//       64x64 diagonal block (with look-ahead the trailing update of panel p
+//       never touches it, so F1 starts right after panel p's exact step),
+//       unpivoted LDL^T of the block in shared memory (16-column blocks:
+//       warp-register panels + register-blocked rank-16 trailing updates),
+//       L11^{-1} by blocked inversion.  Leaves X = L11^{-T} (row-major
+//       [t][j]) in Lblk, W11 / D + L11 in W / Lb, d and the in-block colmax.
+//   F2 k_panel_trsm (all free SMs): W21 = A21 X (DMMA), speculative
+//       L21 = W21 D^{-1}, per-column colmax.
 #ifdef MDS_F1_TIMING
 __device__ long long g_f1t[8];
 #define F1T(i) do { __syncthreads(); if (threadIdx.x == 0) g_f1t[i] = clock64(); } while (0)
 #else
 #define F1T(i) do { } while (0)
 #endif
-constexpr int F1S = NB + 1;                     // smem column stride
-constexpr int F1SMEM = 4 * NB * F1S * 8 + 2 * NB * 8;
+#ifdef MDS_F1_TRACE   // tools/factor_trace.cu: per-panel F1 wall time and SM cycles
+__device__ unsigned long long g_f1trace[4096][8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define F1TRACE(k) do { if (threadIdx.x == 0 && f.pidx < 4096) { g_f1trace[f.pidx][2 * (k)] = gtimer(); g_f1trace[f.pidx][2 * (k) + 1] = clock64(); } } while (0)
+#else
+#define F1TRACE(k) do { } while (0)
+#endif
+constexpr int F1S = NB + 1;                     // F1 smem column stride
+constexpr int UT = 64;                          // DMMA tile edge
+constexpr int US = UT + 4;                      // F2 smem row stride (conflict-free fragment loads)
+constexpr int PF_BUF = NB * US;                 // doubles per shared buffer (>= NB * F1S)
+constexpr int F1SMEM = (3 * PF_BUF + NB) * 8;   // 3 buffers + 1/d
 
-// One warp factors a 16-column panel (rows cb..nbp-1) held in registers: lane
+// FP64 tensor-core fragment op: mma.sync m8n8k4 f64 (SASS DMMA.8x8x4).
+// a0 = A[g][q], b0 = B[q][g], {c0,c1} = C[g][2q], C[g][2q+1]  (g = lane>>2, q = lane&3)
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+// first column of this launch's panel: end of the previous panel (written by its k_panel_slow)
+__device__ __forceinline__ int64_t panel_k0(const FWork& f) {
+  if (f.pidx == 0) return 0;
+  const int2 pp = f.pinfo[f.pidx - 1];
+  return (int64_t)pp.x + pp.y;
+}
+
+// One warp factors a 16-column panel (rows cb..63) held in registers: lane
 // owns rows cb+lane (+32); pivots and column values broadcast by shuffles.
+// The block is padded with the identity beyond nbp, so every block has 16
+// columns and nothing is predicated: entries above the diagonal are updated
+// with garbage that is never read (only the lower triangle, the diagonal and
+// the multipliers below it feed later steps).
 template <int SLOTS>
-__device__ __forceinline__ void f1_panel(double* As, double* Lm, double* rcp, int cb, int ce, int nbp, int lane) {
+__device__ __forceinline__ void f1_panel(double* As, double* Lm, double* rcp, int cb, int lane) {
+  // register window pv[sl][c] = column cb+jj+c of row rr[sl]; shifted by one column per step,
+  // so the loop body is the same every step (a rolled loop: small code, i-cache resident)
   double pv[SLOTS][16];
   int rr[SLOTS];
 #pragma unroll
   for (int sl = 0; sl < SLOTS; sl++) {
     rr[sl] = cb + 32 * sl + lane;
 #pragma unroll
-    for (int c = 0; c < 16; c++) pv[sl][c] = (rr[sl] < nbp && cb + c < ce) ? As[(cb + c) * F1S + rr[sl]] : 0.0;
+    for (int c = 0; c < 16; c++) pv[sl][c] = (rr[sl] < NB) ? As[(cb + c) * F1S + rr[sl]] : 0.0;
   }
-#pragma unroll
+#pragma unroll 1
   for (int jj = 0; jj < 16; jj++) {
     const int j = cb + jj;
-    if (j < ce) {
-      const double d = __shfl_sync(0xffffffffu, pv[0][jj], jj);
-      const double r1 = (d != 0.0) ? fast_rcp(d) : 0.0;
-      double l[SLOTS];
+    const double d = __shfl_sync(0xffffffffu, pv[0][0], jj);
+    const double rd = fast_rcp(d);               // branch-free (keeps the shuffles convergent)
+    const double r1 = (d != 0.0) ? rd : 0.0;
+    double l[SLOTS];
 #pragma unroll
-      for (int sl = 0; sl < SLOTS; sl++) l[sl] = (rr[sl] > j) ? pv[sl][jj] * r1 : 0.0;
+    for (int sl = 0; sl < SLOTS; sl++) l[sl] = pv[sl][0] * r1;
 #pragma unroll
-      for (int c = 1; c < 16; c++) {
-        if (c > jj) {
-          const double v = __shfl_sync(0xffffffffu, pv[0][jj], c);   // A(cb+c, j)
+    for (int c = 1; c < 16; c++) {
+      const double v = __shfl_sync(0xffffffffu, pv[0][0], jj + c);   // A(cb+jj+c, j)
 #pragma unroll
-          for (int sl = 0; sl < SLOTS; sl++)
-            if (rr[sl] >= cb + c) pv[sl][c] -= l[sl] * v;
-        }
-      }
-      if (lane == 0) rcp[j] = r1;
-#pragma unroll
-      for (int sl = 0; sl < SLOTS; sl++)
-        if (rr[sl] < NB) Lm[j * F1S + rr[sl]] = l[sl];   // scaled multipliers of column j
+      for (int sl = 0; sl < SLOTS; sl++) pv[sl][c] -= l[sl] * v;
     }
-  }
+    if (lane == 0) rcp[j] = r1;
 #pragma unroll
-  for (int c = 0; c < 16; c++) {
-    if (cb + c < ce) {
+    for (int sl = 0; sl < SLOTS; sl++) {
+      if (SLOTS == 1 || rr[sl] < NB) Lm[j * F1S + rr[sl]] = l[sl];        // multipliers of column j
+      if (rr[sl] < NB && rr[sl] >= j) As[j * F1S + rr[sl]] = pv[sl][0];   // column j is final
+    }
 #pragma unroll
-      for (int sl = 0; sl < SLOTS; sl++)
-        if (rr[sl] < nbp && rr[sl] >= cb + c) As[(cb + c) * F1S + rr[sl]] = pv[sl][c];
+    for (int sl = 0; sl < SLOTS; sl++) {
+#pragma unroll
+      for (int c = 0; c < 15; c++) pv[sl][c] = pv[sl][c + 1];
+      pv[sl][15] = 0.0;
     }
   }
 }
 
-__global__ void __launch_bounds__(256) k_panel_diag(int64_t N, const double* __restrict__ A, int64_t lda,
-                                                    FWork f) {
+__global__ void __launch_bounds__(256) k_panel_diag(int64_t N, double* __restrict__ A, int64_t lda, FWork f) {
   FCtl* ctl = f.ctl;
   if (ctl->abort) return;
-  extern __shared__ double f1sm[];
-  double* As = f1sm;                 // As[c*F1S + r] : the block, updated in place (lower)
-  double* Li = As + NB * F1S;        // Li[c*F1S + r] = Linv[r][c]
-  double* Tm = Li + NB * F1S;        // temp GEMM block
-  double* Lm = Tm + NB * F1S;        // Lm[c*F1S + r] = L[r][c] (unit lower multipliers, r > c)
-  double* rcp = Lm + NB * F1S;       // 1/d_j (0 for an exactly zero pivot)
-  __shared__ int s_k0;
-  if (threadIdx.x == 0) s_k0 = ctl->k0 + ctl->kb;
-  __syncthreads();
-  const int64_t k0 = s_k0;
+  const int64_t k0 = panel_k0(f);
   if (k0 >= N) {
     if (threadIdx.x == 0) { ctl->k0 = (int)N; ctl->kb = 0; ctl->nbp = 0; }
     return;
   }
   const int nbp = (int)((N - k0) < NB ? (N - k0) : NB);
+  const bool fprev = f.fuse && f.pidx > 0;
+  extern __shared__ double sm[];
+  double* As = sm;                   // As[c*F1S + r] : the block, updated in place (lower)
+  double* Lm = sm + PF_BUF;          // Lm[c*F1S + r] = L[r][c] (unit lower multipliers, r > c); staging: Lprev
+  double* Li = sm + 2 * PF_BUF;      // Li[c*F1S + r] = Linv[r][c];                              staging: Wprev
+  double* Tm = As;                   // temp GEMM block of the inversion (As is dead by then)
+  double* rcp = sm + 3 * PF_BUF;     // 1/d_j (0 for an exactly zero pivot)
   const int tid = threadIdx.x;
+  const int64_t ldw = f.ldw;
   F1T(0);
+  F1TRACE(0);
   {
-    // all 16 loads of a thread in flight at once
+    // all loads of a thread in flight at once
     double v[16];
     const int r = tid & (NB - 1), c0 = tid >> 6;
     const double* src = A + (k0 + r) + (k0 + c0) * lda;
 #pragma unroll
     for (int u = 0; u < 16; u++) {
       const int c = c0 + 4 * u;
-      v[u] = (r >= c && r < nbp && c < nbp) ? src[(int64_t)(4 * u) * lda] : 0.0;
+      v[u] = (r >= c && r < nbp && c < nbp) ? src[(int64_t)(4 * u) * lda] : (r == c ? 1.0 : 0.0);   // identity pad
     }
+    if (fprev) {
+      double lp[16];
 #pragma unroll
-    for (int u = 0; u < 16; u++) As[(c0 + 4 * u) * F1S + r] = v[u];
+      for (int u = 0; u < 16; u++) lp[u] = (r < nbp) ? f.Lbprev[(k0 + r) + (c0 + 4 * u) * ldw] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 16; u++) As[(c0 + 4 * u) * F1S + r] = v[u];
+#pragma unroll
+      for (int u = 0; u < 16; u++) v[u] = (r < nbp) ? f.Wprev[(k0 + r) + (c0 + 4 * u) * ldw] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 16; u++) Lm[(c0 + 4 * u) * F1S + r] = lp[u];
+#pragma unroll
+      for (int u = 0; u < 16; u++) Li[(c0 + 4 * u) * F1S + r] = v[u];
+    } else {
+#pragma unroll
+      for (int u = 0; u < 16; u++) As[(c0 + 4 * u) * F1S + r] = v[u];
+    }
   }
   __syncthreads();
+  if (fprev) {
+    // deferred update of the previous panel on the FP64 tensor cores:
+    // A11 -= Lprev(k0:k0+64, :) Wprev(k0:k0+64, :)^T; warp w owns rows 32(w&1).., cols 16(w>>1)..
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+    double acc[4][2][2];
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+      for (int b = 0; b < 2; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+    if (wm + 31 >= wn) {   // warps entirely above the diagonal have nothing to do
+#pragma unroll 4
+      for (int t0 = 0; t0 < NB; t0 += 4) {
+        double av[4], bv[2];
+#pragma unroll
+        for (int a = 0; a < 4; a++) av[a] = Lm[(t0 + q) * F1S + wm + 8 * a + g];
+#pragma unroll
+        for (int b = 0; b < 2; b++) bv[b] = Li[(t0 + q) * F1S + wn + 8 * b + g];
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+#pragma unroll
+          for (int b = 0; b < 2; b++) dmma(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+      for (int b = 0; b < 2; b++)
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const int r = wm + 8 * a + g, c = wn + 8 * b + 2 * q + e;
+          if (r >= c && r < nbp && c < nbp) {
+            const double nv = As[c * F1S + r] - acc[a][b][e];
+            As[c * F1S + r] = nv;
+            A[(k0 + r) + (k0 + c) * lda] = nv;   // updated values for the exact path
+          }
+        }
+    __syncthreads();
+  }
   F1T(1);
+  F1TRACE(1);
   // ---- factorization, 16-column blocks.  Panel (rows cb.., 16 columns) by warp 0
   // in registers (lane owns rows cb+lane, cb+32+lane; broadcasts by shuffles,
   // no block barriers); the trailing part by all threads, register-blocked.
   const int warp = tid >> 5, lane = tid & 31;
-  for (int cb = 0; cb < nbp; cb += 16) {
-    const int ce = min(cb + 16, nbp);
+#pragma unroll 1
+  for (int cb = 0; cb < NB; cb += 16) {
+    const int ce = cb + 16;   // (the identity pad makes every block 16 wide)
     if (warp == 0) {
-      if (nbp - cb > 32) f1_panel<2>(As, Lm, rcp, cb, ce, nbp, lane);
-      else f1_panel<1>(As, Lm, rcp, cb, ce, nbp, lane);
+      if (cb < 32) f1_panel<2>(As, Lm, rcp, cb, lane);
+      else f1_panel<1>(As, Lm, rcp, cb, lane);
     }
     __syncthreads();
     if (cb == 0) F1T(6);
@@ -306,7 +397,8 @@ __global__ void __launch_bounds__(256) k_panel_diag(int64_t N, const double* __r
           const int r = ce + tr + 16 * a, c = ce + tc + 16 * b;
           acc[a][b] = (r < nbp && c < nbp && r >= c) ? As[c * F1S + r] : 0.0;
         }
-      for (int t = 0; t < ce - cb; t++) {
+#pragma unroll 4
+      for (int t = 0; t < 16; t++) {
         double lr[3], wc[3];
 #pragma unroll
         for (int a = 0; a < 3; a++) {
@@ -335,6 +427,30 @@ __global__ void __launch_bounds__(256) k_panel_diag(int64_t N, const double* __r
     if (cb == 0) F1T(5);
   }
   F1T(2);
+  F1TRACE(2);
+  // ---- outputs that need As / Lm: W11 (updated, unscaled), D + L11 into Lb, d, in-block colmax
+  {
+    const int j = tid & (NB - 1), t0 = tid >> 6;
+    double* Wg = f.W + k0;
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const int t = t0 + 4 * u;
+      if (j >= t && j < nbp && t < nbp) {
+        Wg[j + t * ldw] = As[t * F1S + j];                                           // W11 (r=j, col=t)
+        f.Lb[(k0 + j) + t * ldw] = (j == t) ? As[t * F1S + t] : Lm[t * F1S + j];     // D / L11
+      }
+    }
+  }
+  {
+    // in-block colmax of column j: 4 threads per column, shuffle-reduced
+    const int j = tid >> 2, part = tid & 3;
+    double cm = 0.0;
+    for (int r = j + 1 + part; r < nbp; r += 4) cm = fmax(cm, fabs(As[j * F1S + r]));
+    cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
+    cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
+    if (part == 0 && j < nbp) { ctl->colmax[j] = dbits(cm); ctl->d[j] = As[j * F1S + j]; }
+  }
+  __syncthreads();   // As becomes the inversion's temp block
   // ---- L11^{-1}: Lunit[r][c] = As[c][r] * rcp[c] (r > c)
   // (1) diagonal 16x16 blocks: warp w<4 inverts block w; lane c<16 owns column c.
   //     Right-looking: once x_k is final, s_r += L[r][k] x_k for all r > k (independent FMAs),
@@ -350,8 +466,7 @@ __global__ void __launch_bounds__(256) k_panel_diag(int64_t N, const double* __r
       const double xk = x[k];
 #pragma unroll
       for (int r = k + 1; r < 16; r++) {
-        const double lrk = (o + r < nbp) ? Lm[(o + k) * F1S + o + r] : 0.0;
-        x[r] = (r > c) ? fma(-lrk, xk, x[r]) : x[r];
+        x[r] = fma(-Lm[(o + k) * F1S + o + r], xk, x[r]);   // (x[k] = 0 for k < c: rows <= c stay e_c)
       }
     }
 #pragma unroll
@@ -416,29 +531,14 @@ __global__ void __launch_bounds__(256) k_panel_diag(int64_t N, const double* __r
     __syncthreads();
   }
   F1T(3);
-  // ---- outputs: X[t][j] = Linv[j][t] (row-major), W11, d, in-block colmax
+  // ---- X[t][j] = Linv[j][t] (row-major, 0 above the diagonal)
   {
     const int j = tid & (NB - 1), t0 = tid >> 6;
-    double* Xg = f.Lblk;
-    double* Wg = f.W + k0;
 #pragma unroll
     for (int u = 0; u < 16; u++) {
-      const int t = t0 + 4 * u;                 // X[t][j] = Linv[j][t] (0 above the diagonal)
-      Xg[t * NB + j] = (j >= t) ? Li[t * F1S + j] : 0.0;
-      if (j >= t && j < nbp && t < nbp) {
-        Wg[j + t * f.ldw] = As[t * F1S + j];                                   // W11 (r=j, col=t)
-        f.Lb[(k0 + j) + t * f.ldw] = (j == t) ? As[t * F1S + t] : Lm[t * F1S + j];   // D / L11
-      }
+      const int t = t0 + 4 * u;
+      f.Lblk[t * NB + j] = (j >= t) ? Li[t * F1S + j] : 0.0;
     }
-  }
-  {
-    // in-block colmax of column j: 4 threads per column, shuffle-reduced
-    const int j = tid >> 2, part = tid & 3;
-    double cm = 0.0;
-    for (int r = j + 1 + part; r < nbp; r += 4) cm = fmax(cm, fabs(As[j * F1S + r]));
-    cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
-    cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
-    if (part == 0 && j < nbp) { ctl->colmax[j] = dbits(cm); ctl->d[j] = As[j * F1S + j]; }
   }
   if (tid == 0) {
     ctl->k0 = (int)k0;
@@ -448,16 +548,8 @@ __global__ void __launch_bounds__(256) k_panel_diag(int64_t N, const double* __r
     ctl->npanel = f.pidx + 1;
   }
   F1T(4);
+  F1TRACE(3);
 }
-
-// FP64 tensor-core fragment op: mma.sync m8n8k4 f64 (SASS DMMA.8x8x4).
-// a0 = A[g][q], b0 = B[q][g], {c0,c1} = C[g][2q], C[g][2q+1]  (g = lane>>2, q = lane&3)
-__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
-}
-constexpr int UT = 64;          // DMMA tile edge
-constexpr int US = UT + 4;      // smem row stride (conflict-free fragment loads)
 
 // F2: W21 = A21 * X (X = L11^{-T}) on the FP64 tensor cores, 64-row tiles,
 // K = 64; writes W21 and atomically max-reduces |W21| per column (colmax).
@@ -923,7 +1015,7 @@ constexpr int TS = 3;                             // pipeline stages (L + W tile
 constexpr int TTHREADS = 32 * (1 + 4 * TNG);      // producer warp + consumer warps
 constexpr int TOPB = UT * NB * 8;                 // bytes per operand tile (32 KB)
 constexpr int TSTAGEB = 2 * TOPB;                 // L + W
-constexpr int TSMEM = TS * TSTAGEB + 1024 + 64;   // + alignment + barriers
+constexpr int TSMEM = TS * TSTAGEB + 1024 + 16 * TS + 8 * TS;   // + alignment + barriers + tile slots
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
@@ -957,23 +1049,31 @@ __device__ __forceinline__ unsigned tma_off(int i, int t) {
   return (unsigned)((i >> 3) * 4096) + (lin ^ (((lin >> 7) & 3u) << 4));
 }
 
-// Tile sets of the look-ahead split: mode 0 = all lower tiles of the trailing
-// matrix, 1 = the two leading tile columns (they hold the next panel), 2 = the rest.
+// Tile sets: mode 0 = all lower tiles of the trailing matrix (columns >= s).
+// Look-ahead split (nbn = width of the next panel, which starts at column s):
+// mode 1 = the next panel's columns [s, s+nbn) below its diagonal block (two
+// leading tile columns, the diagonal block itself is updated inside
+// k_panel_diag); mode 3 = everything right of the next panel (cols >= s+nbn).
 __device__ __forceinline__ int64_t upd_ntiles(int64_t nt, int mode) {
   if (mode == 0) return nt * (nt + 1) / 2;
-  if (mode == 1) return nt >= 2 ? 2 * nt - 1 : nt * (nt + 1) / 2;
-  const int64_t r = nt - 2;
+  if (mode == 1) return nt >= 2 ? 2 * nt - 1 : nt;
+  const int64_t r = nt - 1;
   return r > 0 ? r * (r + 1) / 2 : 0;
 }
 __device__ __forceinline__ void upd_tile(int64_t x, int64_t nt, int mode, int64_t& bi, int64_t& bj) {
-  if (mode == 0) { tri_tile(x, bi, bj); return; }
   if (mode == 1) {
-    if (nt < 2) { tri_tile(x, bi, bj); return; }
     if (x < nt) { bi = x; bj = 0; } else { bi = x - nt + 1; bj = 1; }
     return;
   }
   tri_tile(x, bi, bj);
-  bi += 2; bj += 2;
+  if (mode == 3) { bi += 1; bj += 1; }
+}
+// entries (row, col) a launch of this mode may change
+__device__ __forceinline__ bool upd_mask(int64_t row, int64_t col, int64_t N, int64_t s, int64_t nbn, int mode) {
+  if (row >= N || row < col) return false;
+  if (mode == 0) return col >= s;
+  if (mode == 1) return col < s + nbn && row >= s + nbn;   // (col >= s: tiles start at column b0*64 <= s)
+  return col >= s + nbn;
 }
 
 __device__ __forceinline__ double lds_f64(unsigned addr) {
@@ -1003,10 +1103,11 @@ __device__ __forceinline__ void sts_f64(unsigned addr, double v) {
 // issues a TMA REDUCE-ADD of that tile into M (SASS UTMAREDG: the
 // read-modify-write happens in L2).  The stage is released to the producer
 // once the TMA engine has read it.
+template <int mode>
 __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* __restrict__ A, int64_t lda, FWork f,
                                                              const __grid_constant__ CUtensorMap mapA,
                                                              const __grid_constant__ CUtensorMap mapW,
-                                                             const __grid_constant__ CUtensorMap mapL, int mode) {
+                                                             const __grid_constant__ CUtensorMap mapL, int sched) {
   FCtl* ctl = f.ctl;
   if (ctl->abort) return;
   const int2 pi = f.pinfo[f.pidx];
@@ -1018,11 +1119,13 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
   const int64_t nt = (N + UT - 1) / UT - b0;
   const int64_t ntiles = upd_ntiles(nt, mode);
   if ((int64_t)blockIdx.x >= ntiles) return;
-  const int ntile_cta = (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
+  const int64_t nbn = (N - s) < NB ? (N - s) : NB;
+  unsigned long long* counter = f.ucount + 2 * f.pidx + (mode == 1 ? 1 : 0);
   extern __shared__ unsigned char tsm_raw[];
   // all shared addresses as 32-bit shared-window offsets (keeps LDS, not generic LD)
   const unsigned tsm = (smem_u32(tsm_raw) + 1023u) & ~1023u;
   const unsigned full0 = tsm + TS * TSTAGEB, empty0 = full0 + 8 * TS;
+  volatile long long* stile = reinterpret_cast<volatile long long*>(tsm_raw + (empty0 + 8 * TS - smem_u32(tsm_raw)));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < TS; i++) { mbar_init(full0 + 8 * i, 1); mbar_init(empty0 + 8 * i, 1); }
@@ -1030,44 +1133,57 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
   }
   __syncthreads();
   if (warp == 0) {
-    // ---------------- producer: one lane issues all TMA loads (L and W tiles)
+    // ---------------- producer: one lane claims tiles from the launch's counter (dynamic
+    // scheduling: CTAs that start late, e.g. behind the panel kernels, just take fewer tiles)
+    // and issues their TMA loads; -1 in a stage's tile slot ends its consumer group
     if (lane == 0) {
-      for (int i = 0; i < ntile_cta; i++) {
+      int ends = 0;
+      const bool dyn = (sched == 0);
+      unsigned long long xnext = dyn ? atomicAdd(counter, 1ull) : blockIdx.x;   // claimed one tile ahead
+      for (int i = 0; ends < TNG; i++) {
         const int st = i % TS, u = i / TS;
         if (u > 0) mbar_wait(empty0 + 8 * st, (u - 1) & 1);
-        const int64_t x = blockIdx.x + (int64_t)i * gridDim.x;
+        const unsigned long long xc = xnext;
+        const unsigned fb = full0 + 8 * st;
+        if (xc >= (unsigned long long)ntiles) {
+          stile[st] = -1;
+          mbar_arrive(fb);
+          ends++;
+          continue;
+        }
+        const int64_t x = (int64_t)xc;
         int64_t bi, bj;
         upd_tile(x, nt, mode, bi, bj);
         const int R0 = (int)((b0 + bi) * UT), C0 = (int)((b0 + bj) * UT);
+        stile[st] = (long long)(((unsigned long long)(unsigned)C0 << 32) | (unsigned)R0);   // tile origin for the consumers
         const unsigned sL = tsm + st * TSTAGEB, sW = sL + TOPB;
-        const unsigned fb = full0 + 8 * st;
         mbar_expect_tx(fb, TSTAGEB);
 #pragma unroll
         for (int b = 0; b < 8; b++) {
           tma_load_2d(sL + b * 4096, &mapL, R0 + 8 * b, 0, fb);
           tma_load_2d(sW + b * 4096, &mapW, C0 + 8 * b, 0, fb);
         }
+        xnext = dyn ? atomicAdd(counter, 1ull) : xnext + gridDim.x;
       }
     }
     return;
   }
-  // ---------------- consumers: group grp takes tiles grp, grp+TNG, ...
+  // ---------------- consumers: group grp takes stages grp, grp+TNG, ...
   const int grp = (warp - 1) >> 2, wq = (warp - 1) & 3;
   const int wm = (wq >> 1) * 32, wn = (wq & 1) * 32;
   const int g = lane >> 2, q = lane & 3;
   const bool leader = (wq == 0 && lane == 0);
-  for (int i = grp; i < ntile_cta; i += TNG) {
+  for (int i = grp;; i += TNG) {
     const int st = i % TS, u = i / TS;
-    const int64_t x = blockIdx.x + (int64_t)i * gridDim.x;
-    int64_t bi, bj;
-    upd_tile(x, nt, mode, bi, bj);
-    const int64_t R0 = (b0 + bi) * UT, C0 = (b0 + bj) * UT;
+    mbar_wait(full0 + 8 * st, u & 1);
+    const long long x = stile[st];
+    if (x < 0) break;
+    const int64_t R0 = (int64_t)(unsigned)(x & 0xffffffffll), C0 = (int64_t)(x >> 32);
     double acc[4][4][2];
 #pragma unroll
     for (int a = 0; a < 4; a++)
 #pragma unroll
       for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
-    mbar_wait(full0 + 8 * st, u & 1);
     const unsigned Lt = tsm + st * TSTAGEB;
     const unsigned Lb = Lt + (unsigned)(wm >> 3) * 4096u;
     const unsigned Wb = Lt + TOPB + (unsigned)(wn >> 3) * 4096u;
@@ -1107,7 +1223,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
         for (int e = 0; e < 2; e++) {
           const int cl = wn + 8 * b + 2 * q + e;
           const int64_t col = C0 + cl;
-          const bool upd = (row < N && col >= s && row >= col);
+          const bool upd = upd_mask(row, col, N, s, nbn, mode) && col >= s;
           sts_f64(Lt + tma_off(wm + 8 * a + g, cl), upd ? dneg(acc[a][b][e]) : 0.0);
         }
     }
@@ -1312,14 +1428,15 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_update_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
+    cudaFuncSetAttribute(k_update_tma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
+    cudaFuncSetAttribute(k_update_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
+    cudaFuncSetAttribute(k_update_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
     cudaFuncSetAttribute(k_panel_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, F1SMEM);
+    cudaFuncSetAttribute(k_panel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB * US * (int)sizeof(double));
     cudaFuncSetAttribute(k_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * USTAGE * (int)sizeof(double));
     cudaFuncSetAttribute(k_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * USTAGE * (int)sizeof(double));
-    cudaFuncSetAttribute(k_panel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB * US * (int)sizeof(double));
     attr = true;
   }
-  const size_t usmem = 2 * NB * US * sizeof(double);
   // 16-byte cp.async path needs a 16-byte aligned M, even ldm and a 16-byte aligned W
   const bool v16 = ((reinterpret_cast<uintptr_t>(M) & 15) == 0) && (ldm % 2 == 0) &&
                    ((reinterpret_cast<uintptr_t>(f.W) & 15) == 0);
@@ -1333,27 +1450,34 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int64_t npmax = (N + (NB - 2)) / (NB - 1) + 1;
-  // Look-ahead (TMA path): the update after panel p is split into the two
-  // leading tile columns (holding panel p+1; on the main stream, before
-  // panel p+1's fast path) and the rest (on a side stream, overlapping panel
-  // p+1's diag/trsm/accept on the SMs it leaves free).  Panel p+1's exact
-  // BK step (which may interchange anywhere) waits for the rest-update.
+  MDS_CUDA_TRY(cudaMemsetAsync(f.ucount, 0, sizeof(unsigned long long) * 2 * (N + 2), st));
+  // Look-ahead (TMA path).  Panel p's trailing update runs on a side stream in
+  // two launches: U_next (panel p+1's columns below its diagonal block, all
+  // SMs, short) and U_rest (everything right of panel p+1, all but `reserve`
+  // SMs).  Panel p+1's F1 applies panel p's update to its own diagonal block,
+  // so it starts right after panel p's exact step, concurrently with U_next;
+  // F2 waits for U_next, F4 (which may interchange anywhere) for U_rest.
+  // Panel copies Lb -> M run on a third stream.
   const bool lookahead = use_tma && std::getenv("MDS_NO_LOOKAHEAD") == nullptr;
+  constexpr int EVP = 4;   // events per panel: F4 done, U_next done, U_rest done, store done
   cudaStream_t side = nullptr, sstore = nullptr;
   std::vector<cudaEvent_t>* evs = nullptr;
   if (lookahead) {
-    LookaheadCtx* c = lookahead_ctx(st, 3 * (size_t)npmax + 3);
+    LookaheadCtx* c = lookahead_ctx(st, EVP * (size_t)npmax + EVP);
     if (!c) return MDS_ERR_CUDA;
     side = c->side;
     sstore = c->store;
     evs = &c->ev;
   }
+  auto ev = [&](int64_t p, int k) { return (*evs)[EVP * p + k]; };
   CUtensorMap mapW1, mapL0, mapL1;
   if (use_tma && !(make_map(&mapW1, f.W1, N, NB, f.ldw) && make_map(&mapL0, f.Lb, N, NB, f.ldw) &&
                    make_map(&mapL1, f.Lb1, N, NB, f.ldw)))
     return MDS_ERR_CUDA;
-  unsigned reserve = 16;         // SMs left to the panel chain while the rest-update runs
-  if (g_grid_cap > 0 && g_grid_cap < sms) { sms = g_grid_cap; reserve = 0; }
+  const int g_sched = std::getenv("MDS_STATIC_SCHED") ? 1 : 0;
+  const bool capped = (g_grid_cap > 0 && g_grid_cap < sms);
+  if (capped) sms = g_grid_cap;
+  const size_t usmem = 2 * NB * US * sizeof(double);
   int64_t plast = -1;
   for (int64_t p = 0; p < npmax; p++) {
     const int64_t kmin = std::min<int64_t>(p * (NB - 1), N);   // lower bound on this panel's k0
@@ -1361,34 +1485,39 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     if (rows <= 0) break;
     FWork fp = f;
     fp.pidx = (int)p;
-    if (p & 1) { fp.W = f.W1; fp.Lb = f.Lb1; }
-    MDS_LAUNCH(PC_PANEL_DIAG, st, (k_panel_diag<<<1, 256, F1SMEM, st>>>(N, M, ldm, fp)));
+    fp.fuse = lookahead ? 1 : 0;
+    if (p & 1) { fp.W = f.W1; fp.Lb = f.Lb1; fp.Wprev = f.W; fp.Lbprev = f.Lb; }
+    else { fp.Wprev = f.W1; fp.Lbprev = f.Lb1; }
     const unsigned g256 = (unsigned)std::max<int64_t>(mds_cdiv(rows, 256), 1);
     const unsigned g64 = (unsigned)std::max<int64_t>(mds_cdiv(rows, UT), 1);
-    MDS_LAUNCH(PC_PANEL_TRSM, st, (k_panel_trsm<<<g64, 128, usmem, st>>>(N, M, ldm, fp)));
-    if (lookahead && plast >= 0) MDS_CUDA_TRY(cudaStreamWaitEvent(st, (*evs)[3 * plast + 1], 0));
-    MDS_LAUNCH(PC_PANEL_SLOW, st, (k_panel_slow<<<1, 1024, 0, st>>>(N, M, ldm, fp, piv)));
     const int64_t n2max = std::max<int64_t>(rows - 1, 0);
     const int64_t nt = mds_cdiv(n2max, UT) + 1;
+    if (lookahead && p >= 2)   // panel p-2's copy has finished reading this parity's Lb
+      MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(p - 2, 3), 0));
+    MDS_LAUNCH(PC_PANEL_DIAG, st, (k_panel_diag<<<1, 256, F1SMEM, st>>>(N, M, ldm, fp)));
+    if (lookahead && plast >= 0) MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(plast, 1), 0));
+    MDS_LAUNCH(PC_PANEL_TRSM, st, (k_panel_trsm<<<g64, 128, usmem, st>>>(N, M, ldm, fp)));
+    if (lookahead && plast >= 0) MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(plast, 2), 0));
+    MDS_LAUNCH(PC_PANEL_SLOW, st, (k_panel_slow<<<1, 1024, 0, st>>>(N, M, ldm, fp, piv)));
     const CUtensorMap& mw = (p & 1) ? mapW1 : mapW;
     const CUtensorMap& ml = (p & 1) ? mapL1 : mapL0;
     if (lookahead) {
-      if (n2max > 0) {
-        const unsigned gn = (unsigned)std::min<int64_t>(2 * nt, sms);
-        MDS_LAUNCH(PC_UPDATE, st, (k_update_tma<<<gn, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, 1)));
+      MDS_CUDA_TRY(cudaEventRecord(ev(p, 0), st));
+      MDS_CUDA_TRY(cudaStreamWaitEvent(side, ev(p, 0), 0));
+      if (nt >= 1) {
+        const unsigned gn = (unsigned)std::max<int64_t>(1, std::min<int64_t>(2 * nt, sms - 1));
+        MDS_LAUNCH(PC_UPDATE, side, (k_update_tma<1><<<gn, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, g_sched)));
       }
-      MDS_CUDA_TRY(cudaEventRecord((*evs)[3 * p], st));
-      MDS_CUDA_TRY(cudaStreamWaitEvent(side, (*evs)[3 * p], 0));
-      // the panel copy into M runs on its own stream, off every critical path; it
-      // follows U_next, the only update touching the tile columns that hold cols < s
-      MDS_CUDA_TRY(cudaStreamWaitEvent(sstore, (*evs)[3 * p], 0));
+      MDS_CUDA_TRY(cudaEventRecord(ev(p, 1), side));
+      const int reserve = capped ? std::max(1, sms / 8) : 16;   // SMs left to the panel chain
+      if (nt >= 2) {
+        const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt * (nt - 1) / 2, sms - reserve));
+        MDS_LAUNCH(PC_UPDATE, side, (k_update_tma<3><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, g_sched)));
+      }
+      MDS_CUDA_TRY(cudaEventRecord(ev(p, 2), side));
+      MDS_CUDA_TRY(cudaStreamWaitEvent(sstore, ev(p, 0), 0));
       MDS_LAUNCH(PC_PANEL_STORE, sstore, (k_panel_store<<<dim3(g256, 8), 256, 0, sstore>>>(N, M, ldm, fp)));
-      if (n2max > 0) {
-        const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt * (nt + 1) / 2, sms - reserve));
-        MDS_LAUNCH(PC_UPDATE, side,
-                   (k_update_tma<<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, 2)));
-      }
-      MDS_CUDA_TRY(cudaEventRecord((*evs)[3 * p + 1], side));
+      MDS_CUDA_TRY(cudaEventRecord(ev(p, 3), sstore));
       plast = p;
     } else {
       MDS_LAUNCH(PC_PANEL_STORE, st, (k_panel_store<<<dim3(g256, 8), 256, 0, st>>>(N, M, ldm, fp)));
@@ -1396,7 +1525,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
         const unsigned ugrid = (unsigned)std::min<int64_t>(nt * (nt + 1) / 2, sms);
         if (use_tma)
           MDS_LAUNCH(PC_UPDATE, st,
-                     (k_update_tma<<<ugrid, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, 0)));
+                     (k_update_tma<0><<<ugrid, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, g_sched)));
         else if (v16)
           MDS_LAUNCH(PC_UPDATE, st,
                      (k_update<true><<<ugrid, 128, 2 * USTAGE * sizeof(double), st>>>(N, M, ldm, fp)));
@@ -1407,9 +1536,8 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     }
   }
   if (lookahead && plast >= 0) {
-    MDS_CUDA_TRY(cudaStreamWaitEvent(st, (*evs)[3 * plast + 1], 0));
-    MDS_CUDA_TRY(cudaEventRecord((*evs)[3 * npmax], sstore));   // last panel copy
-    MDS_CUDA_TRY(cudaStreamWaitEvent(st, (*evs)[3 * npmax], 0));
+    MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(plast, 2), 0));
+    MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(plast, 3), 0));   // stores are ordered on sstore
   }
   {
     int dev = 0, sms = 148, occ = 0;
