@@ -52,7 +52,8 @@ struct FCtl {
   int npanel;      // panels started
   int nswap;       // interchanges performed (kp != kk)
   int abort;       // non-finite input: nothing is factored
-  int pad[2];
+  unsigned xready; // q+1 once panel q's F1 has published X, d and the in-block colmax
+  int pad;
   double anorm, tol;
   long long inertia[3];
   unsigned long long colmax[NB];   // bit patterns of non-negative doubles (atomicMax-able)
@@ -73,7 +74,9 @@ struct FWork {
   double* Lb;         // [ldw * WCOLS]  the panel's D + L columns (speculative, fixed up by k_panel_slow);
   double* Lb1;        //   copied into M by k_panel_store; double-buffered like W
   int2* pinfo;        // [N+2] per-panel (k0, kb), written by k_panel_slow, read by the updates
-  unsigned long long* ucount;   // [2N+4] per-(panel, launch) tile counters of the updates (dynamic scheduling)
+  unsigned long long* ucount;   // [3(N+2)] per-panel tile counters: [3q] rest/full update, [3q+1] next-panel
+                                //   update, [3q+2] F2 tiles of panel q (claimed by k_panel_trsm and k_update_tma<3>)
+  unsigned* t1flag;             // [2(N/64+4)] p+1 once panel p's update of tile (row BI, column b0+c) has landed
   const double* Wprev;          // the previous panel's W / Lb (the other parity buffers), for the
   const double* Lbprev;         //   deferred update of this panel's columns
   int fuse;           // 1: this panel's columns still lack the previous panel's update (look-ahead)
@@ -102,7 +105,8 @@ FWork carve(void* work, int64_t N, size_t* total) {
   f.Lb = reinterpret_cast<double*>(take(sizeof(double) * f.ldw * WCOLS));
   f.Lb1 = reinterpret_cast<double*>(take(sizeof(double) * f.ldw * WCOLS));
   f.pinfo = reinterpret_cast<int2*>(take(sizeof(int2) * (N + 2)));
-  f.ucount = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * 2 * (N + 2)));
+  f.ucount = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * 3 * (N + 2)));
+  f.t1flag = reinterpret_cast<unsigned*>(take(sizeof(unsigned) * 2 * (N / 64 + 4)));
   f.Wprev = f.W1;
   f.Lbprev = f.Lb1;
   f.fuse = 0;
@@ -214,7 +218,24 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 #define F1TRACE(k) do { if (threadIdx.x == 0 && f.pidx < 4096) { g_f1trace[f.pidx][2 * (k)] = gtimer(); g_f1trace[f.pidx][2 * (k) + 1] = clock64(); } } while (0)
+// [0] U start (min), [1] U end (max), [2] F2 tiles done in U, [3] trsm start, [4] trsm end, [5] trsm tiles
+__device__ unsigned long long g_utrace[4096][6];
+__device__ unsigned long long g_usm[512][160][2];   // per panel, per SM: U CTA start / end
+__device__ unsigned g_f1sm[4096];
+__device__ __forceinline__ unsigned smid() { unsigned r; asm volatile("mov.u32 %0, %smid;" : "=r"(r)); return r; }
+#define USM_START(p) do { if ((p) < 512) atomicMin(&g_usm[p][smid()][0], gtimer()); } while (0)
+#define USM_END(p) do { if ((p) < 512) atomicMax(&g_usm[p][smid()][1], gtimer()); } while (0)
+#define F1SM() do { if (threadIdx.x == 0 && f.pidx < 4096) g_f1sm[f.pidx] = smid(); } while (0)
+#define UTRACE_MIN(p, k) atomicMin(&g_utrace[p][k], gtimer())
+#define UTRACE_MAX(p, k) atomicMax(&g_utrace[p][k], gtimer())
+#define UTRACE_ADD(p, k) atomicAdd(&g_utrace[p][k], 1ull)
 #else
+#define UTRACE_MIN(p, k) do { } while (0)
+#define UTRACE_MAX(p, k) do { } while (0)
+#define UTRACE_ADD(p, k) do { } while (0)
+#define USM_START(p) do { } while (0)
+#define USM_END(p) do { } while (0)
+#define F1SM() do { } while (0)
 #define F1TRACE(k) do { } while (0)
 #endif
 constexpr int F1S = NB + 1;                     // F1 smem column stride
@@ -228,6 +249,14 @@ constexpr int F1SMEM = (3 * PF_BUF + NB) * 8;   // 3 buffers + 1/d
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 // first column of this launch's panel: end of the previous panel (written by its k_panel_slow)
 __device__ __forceinline__ int64_t panel_k0(const FWork& f) {
@@ -304,6 +333,7 @@ __global__ void __launch_bounds__(256) k_panel_diag(int64_t N, double* __restric
   const int64_t ldw = f.ldw;
   F1T(0);
   F1TRACE(0);
+  F1SM();
   {
     // all loads of a thread in flight at once
     double v[16];
@@ -547,76 +577,107 @@ __global__ void __launch_bounds__(256) k_panel_diag(int64_t N, double* __restric
     f.panel_start[f.pidx] = (int)k0;
     ctl->npanel = f.pidx + 1;
   }
+  __syncthreads();
+  if (tid == 0) {   // publish X / d / colmax to the F2 tiles run inside the concurrent trailing update
+    __threadfence();
+    st_release_u32(&ctl->xready, (unsigned)(f.pidx + 1));
+  }
   F1T(4);
   F1TRACE(3);
 }
 
 // F2: W21 = A21 * X (X = L11^{-T}) on the FP64 tensor cores, 64-row tiles,
-// K = 64; writes W21 and atomically max-reduces |W21| per column (colmax).
+// K = 64; writes W21, speculative L21 = W21 D^{-1}, and atomically
+// max-reduces |W21| per column (colmax).  Tiles are claimed from the panel's
+// F2 counter, which the concurrent trailing update (k_update_tma<3>) also
+// draws from once this panel's X is published: whatever it has not taken is
+// done here.
 __global__ void __launch_bounds__(128) k_panel_trsm(int64_t N, const double* __restrict__ A, int64_t lda, FWork f) {
   FCtl* ctl = f.ctl;
   if (ctl->abort) return;
   const int nbp = ctl->nbp;
   const int64_t k0 = ctl->k0;
   if (nbp == 0) return;
-  const int64_t R0 = k0 + nbp + (int64_t)blockIdx.x * UT;
-  if (R0 >= N) return;
+  const int64_t rb = k0 + nbp;
+  // tiles on the absolute 64-row grid (the same tiling as the F2 tiles of k_update_tma<3>,
+  // which claims from the same counter); rows < rb are masked
+  const int64_t rbase = (rb / UT) * UT;
+  const int64_t ntile = (N > rb) ? (N + UT - 1) / UT - rb / UT : 0;
+  if ((int64_t)blockIdx.x >= ntile) return;
+  unsigned long long* counter = f.ucount + 3 * f.pidx + 2;
   extern __shared__ double dsm[];
   double* As = dsm;                 // [t][row]
   double* Xs = dsm + NB * US;       // [t][j]
   __shared__ double cmax[4][32];
   __shared__ double r1s[NB];
-  if (threadIdx.x < NB) {
-    const double d = (threadIdx.x < nbp) ? ctl->d[threadIdx.x] : 0.0;
-    r1s[threadIdx.x] = (d != 0.0) ? fast_rcp(d) : 0.0;
+  __shared__ long long s_x;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_x = (long long)atomicAdd(counter, 1ull);
+  __syncthreads();
+  long long x = s_x;
+  if (tid == 0) UTRACE_MIN(f.pidx, 3);
+  if (x >= ntile) { if (tid == 0) UTRACE_MAX(f.pidx, 4); return; }
+  if (tid < NB) {
+    const double d = (tid < nbp) ? ctl->d[tid] : 0.0;
+    r1s[tid] = (d != 0.0) ? fast_rcp(d) : 0.0;
   }
-  for (int idx = threadIdx.x; idx < UT * NB; idx += 128) {
+  for (int idx = tid; idx < UT * NB; idx += 128) {
     const int i = idx % UT, t = idx / UT;
-    As[t * US + i] = (t < nbp && R0 + i < N) ? A[(R0 + i) + (k0 + t) * lda] : 0.0;
     Xs[t * US + i] = f.Lblk[t * NB + i];   // X[t][j=i]
   }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = tid >> 5, lane = tid & 31;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int g = lane >> 2, q = lane & 3;
-  double acc[4][4][2];
-#pragma unroll
-  for (int a = 0; a < 4; a++)
-#pragma unroll
-    for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
-#pragma unroll 4
-  for (int t0 = 0; t0 < NB; t0 += 4) {
-    double av[4], bv[4];
-#pragma unroll
-    for (int a = 0; a < 4; a++) av[a] = As[(t0 + q) * US + wm + 8 * a + g];
-#pragma unroll
-    for (int b = 0; b < 4; b++) bv[b] = Xs[(t0 + q) * US + wn + 8 * b + g];
-#pragma unroll
-    for (int a = 0; a < 4; a++)
-#pragma unroll
-      for (int b = 0; b < 4; b++) dmma(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
-  }
-  // store W21 and per-column max |W|
   double cm[4][2];
 #pragma unroll
   for (int b = 0; b < 4; b++) cm[b][0] = cm[b][1] = 0.0;
-#pragma unroll
-  for (int a = 0; a < 4; a++) {
-    const int64_t row = R0 + wm + 8 * a + g;
-    if (row < N) {
-#pragma unroll
-      for (int b = 0; b < 4; b++)
-#pragma unroll
-        for (int e = 0; e < 2; e++) {
-          const int col = wn + 8 * b + 2 * q + e;
-          if (col < nbp) {
-            f.W[row + col * f.ldw] = acc[a][b][e];
-            f.Lb[row + col * f.ldw] = acc[a][b][e] * r1s[col];      // speculative L21
-            cm[b][e] = fmax(cm[b][e], fabs(acc[a][b][e]));
-          }
-        }
+  while (x < ntile) {
+    const int64_t R0 = rbase + x * UT;
+    for (int idx = tid; idx < UT * NB; idx += 128) {
+      const int i = idx % UT, t = idx / UT;
+      As[t * US + i] = (t < nbp && R0 + i < N && R0 + i >= rb) ? A[(R0 + i) + (k0 + t) * lda] : 0.0;
     }
+    __syncthreads();
+    if (tid == 0) s_x = (long long)atomicAdd(counter, 1ull);   // next claim (read after the closing barrier)
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+      for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll 4
+    for (int t0 = 0; t0 < NB; t0 += 4) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; a++) av[a] = As[(t0 + q) * US + wm + 8 * a + g];
+#pragma unroll
+      for (int b = 0; b < 4; b++) bv[b] = Xs[(t0 + q) * US + wn + 8 * b + g];
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) dmma(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; a++) {
+      const int64_t row = R0 + wm + 8 * a + g;
+      if (row < N && row >= rb) {
+#pragma unroll
+        for (int b = 0; b < 4; b++)
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            const int col = wn + 8 * b + 2 * q + e;
+            if (col < nbp) {
+              f.W[row + col * f.ldw] = acc[a][b][e];
+              f.Lb[row + col * f.ldw] = acc[a][b][e] * r1s[col];      // speculative L21
+              cm[b][e] = fmax(cm[b][e], fabs(acc[a][b][e]));
+            }
+          }
+      }
+    }
+    __syncthreads();   // As is refilled; s_x holds the next claim
+    if (tid == 0) UTRACE_ADD(f.pidx, 5);
+    x = s_x;
   }
+  if (tid == 0) UTRACE_MAX(f.pidx, 4);
   // reduce over the 8 row-groups g (lanes with equal q share columns)
 #pragma unroll
   for (int b = 0; b < 4; b++)
@@ -629,8 +690,8 @@ __global__ void __launch_bounds__(128) k_panel_trsm(int64_t N, const double* __r
       if (g == 0) cmax[warp][8 * b + 2 * q + e] = v;
     }
   __syncthreads();
-  if (threadIdx.x < NB) {
-    const int col = threadIdx.x;
+  if (tid < NB) {
+    const int col = tid;
     const int half = col >> 5;                 // column col is owned by warps half and half+2
     const double v = fmax(cmax[half][col & 31], cmax[half + 2][col & 31]);
     if (col < nbp) atomicMax(&ctl->colmax[col], dbits(v));
@@ -1050,30 +1111,28 @@ __device__ __forceinline__ unsigned tma_off(int i, int t) {
 }
 
 // Tile sets: mode 0 = all lower tiles of the trailing matrix (columns >= s).
-// Look-ahead split (nbn = width of the next panel, which starts at column s):
-// mode 1 = the next panel's columns [s, s+nbn) below its diagonal block (two
-// leading tile columns, the diagonal block itself is updated inside
-// k_panel_diag); mode 3 = everything right of the next panel (cols >= s+nbn).
+// Look-ahead (mode 3; nbn = width of the next panel, which starts at column
+// s): the same set minus the next panel's diagonal block (k_panel_diag
+// updates that itself), in the order: tile column b0, tile column b0+1 (the
+// "T1" tiles, which hold the next panel's columns), then the rest -- so the
+// dynamic queue finishes the next panel's columns first.
+__device__ __forceinline__ int64_t upd_nt1(int64_t nt) { return nt >= 2 ? 2 * nt - 1 : nt; }
 __device__ __forceinline__ int64_t upd_ntiles(int64_t nt, int mode) {
   if (mode == 0) return nt * (nt + 1) / 2;
-  if (mode == 1) return nt >= 2 ? 2 * nt - 1 : nt;
-  const int64_t r = nt - 1;
-  return r > 0 ? r * (r + 1) / 2 : 0;
+  const int64_t r = nt - 2;
+  return upd_nt1(nt) + (r > 0 ? r * (r + 1) / 2 : 0);
 }
 __device__ __forceinline__ void upd_tile(int64_t x, int64_t nt, int mode, int64_t& bi, int64_t& bj) {
-  if (mode == 1) {
-    if (x < nt) { bi = x; bj = 0; } else { bi = x - nt + 1; bj = 1; }
-    return;
-  }
-  tri_tile(x, bi, bj);
-  if (mode == 3) { bi += 1; bj += 1; }
+  if (mode == 0) { tri_tile(x, bi, bj); return; }
+  if (x < nt) { bi = x; bj = 0; return; }
+  if (x < upd_nt1(nt)) { bi = x - nt + 1; bj = 1; return; }
+  tri_tile(x - upd_nt1(nt), bi, bj);
+  bi += 2; bj += 2;
 }
 // entries (row, col) a launch of this mode may change
 __device__ __forceinline__ bool upd_mask(int64_t row, int64_t col, int64_t N, int64_t s, int64_t nbn, int mode) {
-  if (row >= N || row < col) return false;
-  if (mode == 0) return col >= s;
-  if (mode == 1) return col < s + nbn && row >= s + nbn;   // (col >= s: tiles start at column b0*64 <= s)
-  return col >= s + nbn;
+  if (row >= N || row < col || col < s) return false;
+  return mode == 0 || !(col < s + nbn && row < s + nbn);
 }
 
 __device__ __forceinline__ double lds_f64(unsigned addr) {
@@ -1107,20 +1166,33 @@ template <int mode>
 __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* __restrict__ A, int64_t lda, FWork f,
                                                              const __grid_constant__ CUtensorMap mapA,
                                                              const __grid_constant__ CUtensorMap mapW,
-                                                             const __grid_constant__ CUtensorMap mapL, int sched) {
+                                                             const __grid_constant__ CUtensorMap mapL,
+                                                             const __grid_constant__ CUtensorMap mapX, int sched) {
   FCtl* ctl = f.ctl;
   if (ctl->abort) return;
   const int2 pi = f.pinfo[f.pidx];
   const int64_t k0 = pi.x;
   const int kb = pi.y;
   const int64_t s = k0 + kb;
-  if (N - s <= 0 || kb <= 0) return;
+  if (kb <= 0 || (mode != 3 && N - s <= 0)) return;   // (mode 3 still copies the last panel)
   const int64_t b0 = s / UT;
-  const int64_t nt = (N + UT - 1) / UT - b0;
-  const int64_t ntiles = upd_ntiles(nt, mode);
-  if ((int64_t)blockIdx.x >= ntiles) return;
+  const int64_t nt = (N - s > 0) ? (N + UT - 1) / UT - b0 : 0;
+  const int64_t ntiles = (nt > 0) ? upd_ntiles(nt, mode) : 0;
   const int64_t nbn = (N - s) < NB ? (N - s) : NB;
-  unsigned long long* counter = f.ucount + 2 * f.pidx + (mode == 1 ? 1 : 0);
+  // mode 3 also runs the NEXT panel's F2 tiles (W21 = A21 X, rows >= s + nbn)
+  // as soon as that panel's F1 has published X: claimed before any update
+  // tile, never waited for (the leftovers are k_panel_trsm's).
+  // (tiles on the absolute 64-row grid: TMA box starts stay 16-byte aligned; rows < s + nbn are masked)
+  const int64_t f2r0 = s + nbn;
+  const int64_t f2base = (f2r0 / UT) * UT;
+  const int64_t nf2 = (mode == 3 && N > f2r0) ? (N + UT - 1) / UT - f2r0 / UT : 0;
+  if ((int64_t)blockIdx.x >= ntiles + nf2 + ((mode == 3) ? (N + UT - 1) / UT - k0 / UT : 0)) return;
+  unsigned long long* counter = f.ucount + 3 * f.pidx;
+  const int64_t nT1 = (mode == 3) ? upd_nt1(nt) : 0;
+  // mode 3 also copies this panel's D + L from Lb into M (64-row "S" tiles, queued after T1)
+  const int64_t nS = (mode == 3) ? (N + UT - 1) / UT - k0 / UT : 0;
+  const int64_t nall = ntiles + nS;
+  unsigned long long* f2counter = f.ucount + 3 * (f.pidx + 1) + 2;
   extern __shared__ unsigned char tsm_raw[];
   // all shared addresses as 32-bit shared-window offsets (keeps LDS, not generic LD)
   const unsigned tsm = (smem_u32(tsm_raw) + 1023u) & ~1023u;
@@ -1137,26 +1209,67 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
     // scheduling: CTAs that start late, e.g. behind the panel kernels, just take fewer tiles)
     // and issues their TMA loads; -1 in a stage's tile slot ends its consumer group
     if (lane == 0) {
+      if (mode == 3) { UTRACE_MIN(f.pidx, 0); USM_START(f.pidx); }
       int ends = 0;
       const bool dyn = (sched == 0);
       unsigned long long xnext = dyn ? atomicAdd(counter, 1ull) : blockIdx.x;   // claimed one tile ahead
+      bool f2open = nf2 > 0, xready = false;
       for (int i = 0; ends < TNG; i++) {
         const int st = i % TS, u = i / TS;
         if (u > 0) mbar_wait(empty0 + 8 * st, (u - 1) & 1);
-        const unsigned long long xc = xnext;
         const unsigned fb = full0 + 8 * st;
-        if (xc >= (unsigned long long)ntiles) {
+        const unsigned sL = tsm + st * TSTAGEB, sW = sL + TOPB;
+        if (f2open && xnext >= (unsigned long long)nT1) {   // (never while holding an unissued T1 tile)
+          if (!xready) xready = ld_acquire_u32(&ctl->xready) >= (unsigned)(f.pidx + 2);
+          if (xready) {
+            const unsigned long long x2 = atomicAdd(f2counter, 1ull);
+            if (x2 < (unsigned long long)nf2) {
+              const int R0 = (int)(f2base + (int64_t)x2 * UT);
+              // the rows' T1 tiles (this launch's update of the next panel's columns) must have landed;
+              // they were all claimed before any other tile and their CTAs never wait, so this is bounded
+              const int64_t rlast = ((int64_t)R0 + UT - 1 < N - 1) ? (int64_t)R0 + UT - 1 : N - 1;
+              for (int64_t BI = R0 / UT; BI <= rlast / UT; BI++) {
+                const unsigned want = (unsigned)(f.pidx + 1);
+                while (ld_acquire_u32(&f.t1flag[2 * BI]) < want) __nanosleep(64);
+                if (nt >= 2 && BI > b0)
+                  while (ld_acquire_u32(&f.t1flag[2 * BI + 1]) < want) __nanosleep(64);
+              }
+              stile[st] = (long long)((0xfffffffeull << 32) | (unsigned)R0);   // C0 = -2: F2 tile
+              asm volatile("fence.proxy.async.global;\n" ::: "memory");     // X was written by the generic proxy
+              mbar_expect_tx(fb, TSTAGEB);
+#pragma unroll
+              for (int b = 0; b < 8; b++) {
+                tma_load_2d(sL + b * 4096, &mapA, R0 + 8 * b, (int)s, fb);   // A21 (updated by U_next)
+                tma_load_2d(sW + b * 4096, &mapX, 8 * b, 0, fb);            // L11^{-1}
+              }
+              continue;
+            }
+            f2open = false;
+          }
+        }
+        const unsigned long long xc = xnext;
+        if (xc >= (unsigned long long)nall) {
+          f2open = false;          // never wait for X: the rest of the F2 tiles go to k_panel_trsm
           stile[st] = -1;
           mbar_arrive(fb);
           ends++;
           continue;
         }
-        const int64_t x = (int64_t)xc;
+        int64_t x = (int64_t)xc;
+        if (mode == 3 && x >= nT1 && x < nT1 + nS) {   // S tile: Lb rows -> M
+          const int R0 = (int)((k0 / UT + (x - nT1)) * UT);
+          stile[st] = (long long)((0xfffffffdull << 32) | (unsigned)R0);   // C0 = -3
+          mbar_expect_tx(fb, TOPB);
+#pragma unroll
+          for (int b = 0; b < 8; b++) tma_load_2d(sL + b * 4096, &mapL, R0 + 8 * b, 0, fb);
+          xnext = dyn ? atomicAdd(counter, 1ull) : xnext + gridDim.x;
+          continue;
+        }
+        if (mode == 3 && x >= nT1) x -= nS;
         int64_t bi, bj;
         upd_tile(x, nt, mode, bi, bj);
         const int R0 = (int)((b0 + bi) * UT), C0 = (int)((b0 + bj) * UT);
         stile[st] = (long long)(((unsigned long long)(unsigned)C0 << 32) | (unsigned)R0);   // tile origin for the consumers
-        const unsigned sL = tsm + st * TSTAGEB, sW = sL + TOPB;
         mbar_expect_tx(fb, TSTAGEB);
 #pragma unroll
         for (int b = 0; b < 8; b++) {
@@ -1177,8 +1290,23 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
     const int st = i % TS, u = i / TS;
     mbar_wait(full0 + 8 * st, u & 1);
     const long long x = stile[st];
-    if (x < 0) break;
+    if (x == -1) break;
     const int64_t R0 = (int64_t)(unsigned)(x & 0xffffffffll), C0 = (int64_t)(x >> 32);
+    if (mode == 3 && C0 == -3) {
+      // S tile: panel rows R0..R0+63 of D + L (columns < kb, on/below the diagonal) into M
+      const unsigned Lt = tsm + st * TSTAGEB;
+      const int tq = (int)threadIdx.x - 32 - grp * 128;   // 0..127 within the group
+      const int i = tq & 63;
+      const int64_t row = R0 + i;
+#pragma unroll 4
+      for (int c = tq >> 6; c < NB; c += 2) {
+        const double v = lds_f64(Lt + tma_off(i, c));
+        if (c < kb && row < N && row >= k0 + c) A[row + (k0 + c) * lda] = v;
+      }
+      asm volatile("bar.sync %0, 128;\n" ::"r"(grp + 1) : "memory");
+      if (leader) mbar_arrive(empty0 + 8 * st);
+      continue;
+    }
     double acc[4][4][2];
 #pragma unroll
     for (int a = 0; a < 4; a++)
@@ -1213,6 +1341,38 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
     }
     // the whole group has finished reading L/W of this stage
     asm volatile("bar.sync %0, 128;\n" ::"r"(grp + 1) : "memory");
+    if (mode == 3 && C0 == -2) {
+      // F2 tile of the next panel: W21 = acc, L21 = acc D^{-1}, colmax (the stage is free already)
+      if (leader) { mbar_arrive(empty0 + 8 * st); UTRACE_ADD(f.pidx, 2); }
+      double* W2 = const_cast<double*>(f.Wprev);
+      double* L2 = const_cast<double*>(f.Lbprev);
+      double cm[4][2];
+#pragma unroll
+      for (int b = 0; b < 4; b++)
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const int c = wn + 8 * b + 2 * q + e;
+          const double d = (c < nbn) ? __ldcg(&ctl->d[c]) : 0.0;
+          const double rd = fast_rcp(d);
+          const double r1 = (d != 0.0) ? rd : 0.0;
+          cm[b][e] = 0.0;
+#pragma unroll
+          for (int a = 0; a < 4; a++) {
+            const int64_t row = R0 + wm + 8 * a + g;
+            if (row < N && row >= f2r0 && c < nbn) {
+              W2[row + c * f.ldw] = acc[a][b][e];
+              L2[row + c * f.ldw] = acc[a][b][e] * r1;
+              cm[b][e] = fmax(cm[b][e], fabs(acc[a][b][e]));
+            }
+          }
+          double v = cm[b][e];
+          v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 4));
+          v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 8));
+          v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 16));
+          if (g == 0 && c < nbn) atomicMax(&ctl->colmax[c], dbits(v));
+        }
+      continue;
+    }
     // -P (masked) into the stage's L area, same swizzled box layout as the loads
 #pragma unroll
     for (int a = 0; a < 4; a++) {
@@ -1235,9 +1395,17 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");   // smem source consumed
       mbar_arrive(empty0 + 8 * st);
+      if (mode == 3 && C0 < (b0 + 2) * UT && nf2 > 0) {
+        // T1 tile: publish its completion to the F2 tiles of the next panel
+        asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        __threadfence();
+        st_release_u32(&f.t1flag[2 * (R0 / UT) + (C0 / UT - b0)], (unsigned)(f.pidx + 1));
+      }
     }
   }
   if (leader) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // reductions complete before exit
+  if (mode == 3 && leader) { UTRACE_MAX(f.pidx, 1); USM_END(f.pidx); }
 }
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1365,8 +1533,7 @@ double* mds_factor_tol_ptr(const void* fwork) {
 // stream (so concurrent factorizations on different streams never share
 // events; a call on stream s always orders its side work through s).
 struct LookaheadCtx {
-  cudaStream_t side = nullptr;    // rest-of-matrix trailing updates
-  cudaStream_t store = nullptr;   // panel copies Lb -> M (nothing but the finalize waits on them)
+  cudaStream_t side = nullptr;    // trailing updates
   std::vector<cudaEvent_t> ev;
 };
 static std::mutex g_la_mu;
@@ -1379,8 +1546,7 @@ static LookaheadCtx* lookahead_ctx(cudaStream_t st, size_t nev) {
   LookaheadCtx*& c = g_la[std::make_pair(dev, st)];
   if (!c) {
     c = new LookaheadCtx();
-    if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&c->store, cudaStreamNonBlocking) != cudaSuccess) {
+    if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) {
       delete c;
       c = nullptr;
       return nullptr;
@@ -1429,7 +1595,6 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_update_tma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
-    cudaFuncSetAttribute(k_update_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
     cudaFuncSetAttribute(k_update_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
     cudaFuncSetAttribute(k_panel_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, F1SMEM);
     cudaFuncSetAttribute(k_panel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB * US * (int)sizeof(double));
@@ -1450,29 +1615,30 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int64_t npmax = (N + (NB - 2)) / (NB - 1) + 1;
-  MDS_CUDA_TRY(cudaMemsetAsync(f.ucount, 0, sizeof(unsigned long long) * 2 * (N + 2), st));
-  // Look-ahead (TMA path).  Panel p's trailing update runs on a side stream in
-  // two launches: U_next (panel p+1's columns below its diagonal block, all
-  // SMs, short) and U_rest (everything right of panel p+1, all but `reserve`
-  // SMs).  Panel p+1's F1 applies panel p's update to its own diagonal block,
-  // so it starts right after panel p's exact step, concurrently with U_next;
-  // F2 waits for U_next, F4 (which may interchange anywhere) for U_rest.
-  // Panel copies Lb -> M run on a third stream.
+  MDS_CUDA_TRY(cudaMemsetAsync(f.ucount, 0, sizeof(unsigned long long) * 3 * (N + 2), st));
+  MDS_CUDA_TRY(cudaMemsetAsync(f.t1flag, 0, sizeof(unsigned) * 2 * (N / 64 + 4), st));
+  // Look-ahead (TMA path).  Panel p's trailing update U(p) runs on a side
+  // stream on all SMs but one, its dynamic tile queue starting with panel
+  // p+1's columns.  Panel p+1's F1 applies panel p's update to its own
+  // diagonal block, so it starts right after panel p's exact step,
+  // concurrently with U(p); once F1 has published X, U(p)'s CTAs take panel
+  // p+1's F2 tiles before any further update tile, and k_panel_trsm (after
+  // U(p)) does whatever is left.  F4 (which may interchange anywhere) runs
+  // after U(p).  U(p) also copies panel p's D + L from Lb into M (S tiles).
   const bool lookahead = use_tma && std::getenv("MDS_NO_LOOKAHEAD") == nullptr;
-  constexpr int EVP = 4;   // events per panel: F4 done, U_next done, U_rest done, store done
-  cudaStream_t side = nullptr, sstore = nullptr;
+  constexpr int EVP = 2;   // events per panel: F4 done, U done
+  cudaStream_t side = nullptr;
   std::vector<cudaEvent_t>* evs = nullptr;
   if (lookahead) {
     LookaheadCtx* c = lookahead_ctx(st, EVP * (size_t)npmax + EVP);
     if (!c) return MDS_ERR_CUDA;
     side = c->side;
-    sstore = c->store;
     evs = &c->ev;
   }
   auto ev = [&](int64_t p, int k) { return (*evs)[EVP * p + k]; };
-  CUtensorMap mapW1, mapL0, mapL1;
+  CUtensorMap mapW1, mapL0, mapL1, mapX;
   if (use_tma && !(make_map(&mapW1, f.W1, N, NB, f.ldw) && make_map(&mapL0, f.Lb, N, NB, f.ldw) &&
-                   make_map(&mapL1, f.Lb1, N, NB, f.ldw)))
+                   make_map(&mapL1, f.Lb1, N, NB, f.ldw) && make_map(&mapX, f.Lblk, NB, NB, NB)))
     return MDS_ERR_CUDA;
   const int g_sched = std::getenv("MDS_STATIC_SCHED") ? 1 : 0;
   const bool capped = (g_grid_cap > 0 && g_grid_cap < sms);
@@ -1492,32 +1658,21 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     const unsigned g64 = (unsigned)std::max<int64_t>(mds_cdiv(rows, UT), 1);
     const int64_t n2max = std::max<int64_t>(rows - 1, 0);
     const int64_t nt = mds_cdiv(n2max, UT) + 1;
-    if (lookahead && p >= 2)   // panel p-2's copy has finished reading this parity's Lb
-      MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(p - 2, 3), 0));
     MDS_LAUNCH(PC_PANEL_DIAG, st, (k_panel_diag<<<1, 256, F1SMEM, st>>>(N, M, ldm, fp)));
     if (lookahead && plast >= 0) MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(plast, 1), 0));
     MDS_LAUNCH(PC_PANEL_TRSM, st, (k_panel_trsm<<<g64, 128, usmem, st>>>(N, M, ldm, fp)));
-    if (lookahead && plast >= 0) MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(plast, 2), 0));
     MDS_LAUNCH(PC_PANEL_SLOW, st, (k_panel_slow<<<1, 1024, 0, st>>>(N, M, ldm, fp, piv)));
     const CUtensorMap& mw = (p & 1) ? mapW1 : mapW;
     const CUtensorMap& ml = (p & 1) ? mapL1 : mapL0;
     if (lookahead) {
       MDS_CUDA_TRY(cudaEventRecord(ev(p, 0), st));
       MDS_CUDA_TRY(cudaStreamWaitEvent(side, ev(p, 0), 0));
-      if (nt >= 1) {
-        const unsigned gn = (unsigned)std::max<int64_t>(1, std::min<int64_t>(2 * nt, sms - 1));
-        MDS_LAUNCH(PC_UPDATE, side, (k_update_tma<1><<<gn, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, g_sched)));
+      const int reserve = capped ? std::max(1, sms / 8) : 1;   // SMs left to the panel chain (F1)
+      {
+        const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt * (nt + 1) / 2 + 2 * nt, sms - reserve));
+        MDS_LAUNCH(PC_UPDATE, side, (k_update_tma<3><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
       }
       MDS_CUDA_TRY(cudaEventRecord(ev(p, 1), side));
-      const int reserve = capped ? std::max(1, sms / 8) : 16;   // SMs left to the panel chain
-      if (nt >= 2) {
-        const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt * (nt - 1) / 2, sms - reserve));
-        MDS_LAUNCH(PC_UPDATE, side, (k_update_tma<3><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, g_sched)));
-      }
-      MDS_CUDA_TRY(cudaEventRecord(ev(p, 2), side));
-      MDS_CUDA_TRY(cudaStreamWaitEvent(sstore, ev(p, 0), 0));
-      MDS_LAUNCH(PC_PANEL_STORE, sstore, (k_panel_store<<<dim3(g256, 8), 256, 0, sstore>>>(N, M, ldm, fp)));
-      MDS_CUDA_TRY(cudaEventRecord(ev(p, 3), sstore));
       plast = p;
     } else {
       MDS_LAUNCH(PC_PANEL_STORE, st, (k_panel_store<<<dim3(g256, 8), 256, 0, st>>>(N, M, ldm, fp)));
@@ -1525,7 +1680,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
         const unsigned ugrid = (unsigned)std::min<int64_t>(nt * (nt + 1) / 2, sms);
         if (use_tma)
           MDS_LAUNCH(PC_UPDATE, st,
-                     (k_update_tma<0><<<ugrid, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, g_sched)));
+                     (k_update_tma<0><<<ugrid, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
         else if (v16)
           MDS_LAUNCH(PC_UPDATE, st,
                      (k_update<true><<<ugrid, 128, 2 * USTAGE * sizeof(double), st>>>(N, M, ldm, fp)));
@@ -1536,8 +1691,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     }
   }
   if (lookahead && plast >= 0) {
-    MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(plast, 2), 0));
-    MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(plast, 3), 0));   // stores are ordered on sstore
+    MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(plast, 1), 0));
   }
   {
     int dev = 0, sms = 148, occ = 0;

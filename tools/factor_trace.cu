@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <random>
 #include <vector>
+#include <algorithm>
 int main(int argc, char** argv) {
   const int64_t N = argc > 1 ? atoll(argv[1]) : 8192, ld = N;
   std::vector<double> h(N * ld);
@@ -21,13 +22,46 @@ int main(int argc, char** argv) {
   mds_inertia* ine; cudaMalloc(&ine, sizeof(mds_inertia));
   int32_t* status; cudaMalloc(&status, 4);
   cudaStream_t st; cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-  for (int rep = 0; rep < 2; rep++) {
-    cudaMemcpy(A, h.data(), sizeof(double) * N * ld, cudaMemcpyHostToDevice);
-    cudaMemset(status, 0, 4);
+  const bool graph = argc > 2 && atoi(argv[2]) == 1;
+  static unsigned long long uinit[4096][6];
+  for (int i = 0; i < 4096; i++) { uinit[i][0] = uinit[i][3] = ~0ull; for (int k : {1, 2, 4, 5}) uinit[i][k] = 0; }
+  double* A0; cudaMalloc(&A0, sizeof(double) * N * ld);
+  cudaMemcpy(A0, h.data(), sizeof(double) * N * ld, cudaMemcpyHostToDevice);
+  cudaGraphExec_t gexec = nullptr;
+  if (graph) {
+    cudaGraph_t g;
+    cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
+    cudaMemcpyAsync(A, A0, sizeof(double) * N * ld, cudaMemcpyDeviceToDevice, st);
     int rc = mds_factor(N, A, ld, piv, -1.0, ine, nullptr, status, work, wb, st);
-    cudaStreamSynchronize(st);
-    if (rc) printf("rc %d\n", rc);
+    cudaStreamEndCapture(st, &g);
+    cudaGraphInstantiate(&gexec, g, 0);
+    if (rc) printf("capture rc %d\n", rc);
   }
+  static unsigned long long usinit[512][160][2];
+  for (int i = 0; i < 512; i++) for (int j = 0; j < 160; j++) { usinit[i][j][0] = ~0ull; usinit[i][j][1] = 0; }
+  for (int rep = 0; rep < 3; rep++) {
+    cudaMemcpyToSymbol(g_utrace, uinit, sizeof(uinit));
+    cudaMemcpyToSymbol(g_usm, usinit, sizeof(usinit));
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    if (graph) {
+      cudaEventRecord(a, st); cudaGraphLaunch(gexec, st); cudaEventRecord(b, st);
+    } else {
+      cudaMemcpyAsync(A, A0, sizeof(double) * N * ld, cudaMemcpyDeviceToDevice, st);
+      cudaEventRecord(a, st);
+      int rc = mds_factor(N, A, ld, piv, -1.0, ine, nullptr, status, work, wb, st);
+      cudaEventRecord(b, st);
+      if (rc) printf("rc %d\n", rc);
+    }
+    cudaStreamSynchronize(st);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    printf("rep %d (%s): %.3f ms\n", rep, graph ? "graph" : "eager", ms);
+  }
+  static unsigned long long ut[4096][6];
+  cudaMemcpyFromSymbol(ut, g_utrace, sizeof(ut));
+  static unsigned long long usm[512][160][2];
+  cudaMemcpyFromSymbol(usm, g_usm, sizeof(usm));
+  static unsigned f1sm[4096];
+  cudaMemcpyFromSymbol(f1sm, g_f1sm, sizeof(f1sm));
   static unsigned long long tr[4096][8];
   cudaMemcpyFromSymbol(tr, g_f1trace, sizeof(tr));
   const int np = (int)((N + 62) / 63) + 1;
@@ -37,9 +71,21 @@ int main(int argc, char** argv) {
   for (int p = 0; p < np; p++) {
     if (!tr[p][0] || !tr[p][6]) continue;
     const double us = (tr[p][6] - tr[p][0]) * 1e-3, cyc = (double)(tr[p][7] - tr[p][1]);
-    if (p % 8 == 0)
-      printf("panel %3d start %8.1f us  F1 %6.1f us  %7.0f cycles (%.0f MHz): load+defer %llu fact %llu inv+out %llu\n", p,
-             (tr[p][0] - t0) * 1e-3, us, cyc, cyc / us, tr[p][3] - tr[p][1], tr[p][5] - tr[p][3], tr[p][7] - tr[p][5]);
+    if (p < 12 || p % 8 == 0) {
+      auto ab = [&](unsigned long long t) { return (t == ~0ull || t == 0) ? -1.0 : ((double)t - (double)t0) * 1e-3; };
+      printf("  abs: F1 [%.1f, %.1f] on SM %u  trsm [%.1f, %.1f]  U [%.1f, %.1f]", ab(tr[p][0]), ab(tr[p][6]), f1sm[p], ab(ut[p][3]), ab(ut[p][4]), ab(ut[p][0]), ab(ut[p][1]));
+      if (p > 0 && p < 512) {
+        int nsm = 0; double late = 0;
+        for (int k = 0; k < 160; k++) if (usm[p - 1][k][0] != ~0ull) { nsm++; late = std::max(late, ab(usm[p - 1][k][0])); }
+        const unsigned sm = f1sm[p];
+        printf(" | U(p-1): %d SMs, last CTA start %.1f; U(p-1) on F1's SM: [%.1f, %.1f]", nsm, late, ab(usm[p - 1][sm][0]), ab(usm[p - 1][sm][1]));
+      }
+      printf("\n");
+      auto rel = [&](unsigned long long t) { return (t == ~0ull || t == 0) ? -1.0 : ((double)t - (double)tr[p][0]) * 1e-3; };
+      printf("panel %3d start %8.1f us  F1 %5.1f us (%.0f MHz; defer %llu fact %llu inv %llu cyc) | U(p) [%.1f, %.1f] F2-in-U(p) %llu | trsm [%.1f, %.1f] tiles %llu\n", p,
+             (tr[p][0] - t0) * 1e-3, us, cyc / us, tr[p][3] - tr[p][1], tr[p][5] - tr[p][3], tr[p][7] - tr[p][5],
+             rel(ut[p][0]), rel(ut[p][1]), p > 0 ? ut[p - 1][2] : 0ull, rel(ut[p][3]), rel(ut[p][4]), ut[p][5]);
+    }
     sum_us += us; sum_cyc += cyc; n++;
   }
   printf("avg F1 %.1f us %.0f cycles over %d panels; err=%s\n", sum_us / n, sum_cyc / n, n, cudaGetErrorString(cudaGetLastError()));
