@@ -75,7 +75,7 @@ struct FWork {
   double* Lb1;        //   copied into M by k_panel_store; double-buffered like W
   int2* pinfo;        // [N+2] per-panel (k0, kb), written by k_panel_slow, read by the updates
   unsigned long long* ucount;   // [3(N+2)] per-panel tile counters: [3q] rest/full update, [3q+1] next-panel
-                                //   update, [3q+2] F2 tiles of panel q (claimed by k_panel_trsm and k_update_tma<3>)
+                                //   update, [3q+2] F2 tiles of panel q (claimed by k_panel_trsm and k_update_tma<3, true>)
   unsigned* t1flag;             // [2(N/64+4)] p+1 once panel p's update of tile (row BI, column b0+c) has landed
   const double* Wprev;          // the previous panel's W / Lb (the other parity buffers), for the
   const double* Lbprev;         //   deferred update of this panel's columns
@@ -249,6 +249,14 @@ constexpr int F1SMEM = (3 * PF_BUF + NB) * 8;   // 3 buffers + 1/d
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+// plain (non-warp-aggregated) 64-bit fetch-add: the compiler's atomicAdd from a single
+// lane becomes a match/popc/shuffle sequence that consumes the result at once,
+// which would serialise the producer's one-ahead tile claim
+__device__ __forceinline__ unsigned long long atom_add_u64(unsigned long long* p, unsigned long long v) {
+  unsigned long long r;
+  asm volatile("atom.global.add.u64 %0, [%1], %2;\n" : "=l"(r) : "l"(p), "l"(v) : "memory");
+  return r;
 }
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -589,7 +597,7 @@ __global__ void __launch_bounds__(256) k_panel_diag(int64_t N, double* __restric
 // F2: W21 = A21 * X (X = L11^{-T}) on the FP64 tensor cores, 64-row tiles,
 // K = 64; writes W21, speculative L21 = W21 D^{-1}, and atomically
 // max-reduces |W21| per column (colmax).  Tiles are claimed from the panel's
-// F2 counter, which the concurrent trailing update (k_update_tma<3>) also
+// F2 counter, which the concurrent trailing update (k_update_tma<3, true>) also
 // draws from once this panel's X is published: whatever it has not taken is
 // done here.
 __global__ void __launch_bounds__(128) k_panel_trsm(int64_t N, const double* __restrict__ A, int64_t lda, FWork f) {
@@ -599,7 +607,7 @@ __global__ void __launch_bounds__(128) k_panel_trsm(int64_t N, const double* __r
   const int64_t k0 = ctl->k0;
   if (nbp == 0) return;
   const int64_t rb = k0 + nbp;
-  // tiles on the absolute 64-row grid (the same tiling as the F2 tiles of k_update_tma<3>,
+  // tiles on the absolute 64-row grid (the same tiling as the F2 tiles of k_update_tma<3, true>,
   // which claims from the same counter); rows < rb are masked
   const int64_t rbase = (rb / UT) * UT;
   const int64_t ntile = (N > rb) ? (N + UT - 1) / UT - rb / UT : 0;
@@ -1072,11 +1080,14 @@ __global__ void __launch_bounds__(128, 1) k_update(int64_t N, double* __restrict
 // 4 warps each take alternate tiles ("ping-pong"), so one group's C loads
 // and epilogue stores overlap the other group's DMMA k-loop.
 constexpr int TNG = 2;                            // consumer groups (4 warps each), ping-pong
-constexpr int TS = 3;                             // pipeline stages (L + W tiles)
+constexpr int TSMAX = 3;                          // pipeline stages (L + W tiles) -- in-place staging variant
 constexpr int TTHREADS = 32 * (1 + 4 * TNG);      // producer warp + consumer warps
 constexpr int TOPB = UT * NB * 8;                 // bytes per operand tile (32 KB)
 constexpr int TSTAGEB = 2 * TOPB;                 // L + W
-constexpr int TSMEM = TS * TSTAGEB + 1024 + 16 * TS + 8 * TS;   // + alignment + barriers + tile slots
+// OUTB variant: 2 stages + one 32 KB output buffer per consumer group (a stage is released as soon as
+// its k-loop is done); in-place variant: 3 stages, -P staged in the consumed stage (released after the
+// TMA reduce has read it).  Both use 192 KB.
+constexpr int TSMEM = TSMAX * TSTAGEB + 1024 + 16 * TSMAX + 8 * TSMAX;   // + alignment + barriers + tile slots
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
@@ -1162,7 +1173,7 @@ __device__ __forceinline__ void sts_f64(unsigned addr, double v) {
 // issues a TMA REDUCE-ADD of that tile into M (SASS UTMAREDG: the
 // read-modify-write happens in L2).  The stage is released to the producer
 // once the TMA engine has read it.
-template <int mode>
+template <int mode, bool OUTB>
 __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* __restrict__ A, int64_t lda, FWork f,
                                                              const __grid_constant__ CUtensorMap mapA,
                                                              const __grid_constant__ CUtensorMap mapW,
@@ -1196,8 +1207,10 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
   extern __shared__ unsigned char tsm_raw[];
   // all shared addresses as 32-bit shared-window offsets (keeps LDS, not generic LD)
   const unsigned tsm = (smem_u32(tsm_raw) + 1023u) & ~1023u;
-  const unsigned full0 = tsm + TS * TSTAGEB, empty0 = full0 + 8 * TS;
-  volatile long long* stile = reinterpret_cast<volatile long long*>(tsm_raw + (empty0 + 8 * TS - smem_u32(tsm_raw)));
+  constexpr int TS = OUTB ? 2 : 3;
+  const unsigned full0 = tsm + TSMAX * TSTAGEB, empty0 = full0 + 8 * TSMAX;
+  volatile long long* stile = reinterpret_cast<volatile long long*>(tsm_raw + (empty0 + 8 * TSMAX - smem_u32(tsm_raw)));
+  const unsigned outb0 = tsm + 2 * TSTAGEB;   // OUTB: group g stages -P at outb0 + g * TOPB
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < TS; i++) { mbar_init(full0 + 8 * i, 1); mbar_init(empty0 + 8 * i, 1); }
@@ -1212,7 +1225,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
       if (mode == 3) { UTRACE_MIN(f.pidx, 0); USM_START(f.pidx); }
       int ends = 0;
       const bool dyn = (sched == 0);
-      unsigned long long xnext = dyn ? atomicAdd(counter, 1ull) : blockIdx.x;   // claimed one tile ahead
+      unsigned long long xnext = dyn ? atom_add_u64(counter, 1ull) : blockIdx.x;   // claimed one tile ahead
       bool f2open = nf2 > 0, xready = false;
       for (int i = 0; ends < TNG; i++) {
         const int st = i % TS, u = i / TS;
@@ -1222,7 +1235,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
         if (f2open && xnext >= (unsigned long long)nT1) {   // (never while holding an unissued T1 tile)
           if (!xready) xready = ld_acquire_u32(&ctl->xready) >= (unsigned)(f.pidx + 2);
           if (xready) {
-            const unsigned long long x2 = atomicAdd(f2counter, 1ull);
+            const unsigned long long x2 = atom_add_u64(f2counter, 1ull);
             if (x2 < (unsigned long long)nf2) {
               const int R0 = (int)(f2base + (int64_t)x2 * UT);
               // the rows' T1 tiles (this launch's update of the next panel's columns) must have landed;
@@ -1262,7 +1275,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
           mbar_expect_tx(fb, TOPB);
 #pragma unroll
           for (int b = 0; b < 8; b++) tma_load_2d(sL + b * 4096, &mapL, R0 + 8 * b, 0, fb);
-          xnext = dyn ? atomicAdd(counter, 1ull) : xnext + gridDim.x;
+          xnext = dyn ? atom_add_u64(counter, 1ull) : xnext + gridDim.x;
           continue;
         }
         if (mode == 3 && x >= nT1) x -= nS;
@@ -1276,7 +1289,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
           tma_load_2d(sL + b * 4096, &mapL, R0 + 8 * b, 0, fb);
           tma_load_2d(sW + b * 4096, &mapW, C0 + 8 * b, 0, fb);
         }
-        xnext = dyn ? atomicAdd(counter, 1ull) : xnext + gridDim.x;
+        xnext = dyn ? atom_add_u64(counter, 1ull) : xnext + gridDim.x;
       }
     }
     return;
@@ -1373,7 +1386,17 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
         }
       continue;
     }
-    // -P (masked) into the stage's L area, same swizzled box layout as the loads
+    // -P (masked) into the staging tile (OUTB: the group's own buffer, once its previous reduce has
+    // read it, and the stage is released now; else the stage's L area), same swizzled box layout
+    unsigned Ot = Lt;
+    if (OUTB) {
+      Ot = outb0 + (unsigned)grp * TOPB;
+      if (leader) {
+        mbar_arrive(empty0 + 8 * st);
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      }
+      asm volatile("bar.sync %0, 128;\n" ::"r"(grp + 1) : "memory");
+    }
 #pragma unroll
     for (int a = 0; a < 4; a++) {
       const int64_t row = R0 + wm + 8 * a + g;
@@ -1384,17 +1407,19 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
           const int cl = wn + 8 * b + 2 * q + e;
           const int64_t col = C0 + cl;
           const bool upd = upd_mask(row, col, N, s, nbn, mode) && col >= s;
-          sts_f64(Lt + tma_off(wm + 8 * a + g, cl), upd ? dneg(acc[a][b][e]) : 0.0);
+          sts_f64(Ot + tma_off(wm + 8 * a + g, cl), upd ? dneg(acc[a][b][e]) : 0.0);
         }
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     asm volatile("bar.sync %0, 128;\n" ::"r"(grp + 1) : "memory");
     if (leader) {
 #pragma unroll
-      for (int b = 0; b < 8; b++) tma_reduce_add_2d(&mapA, (int)(R0 + 8 * b), (int)C0, Lt + b * 4096);
+      for (int b = 0; b < 8; b++) tma_reduce_add_2d(&mapA, (int)(R0 + 8 * b), (int)C0, Ot + b * 4096);
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");   // smem source consumed
-      mbar_arrive(empty0 + 8 * st);
+      if (!OUTB) {
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");   // smem source consumed
+        mbar_arrive(empty0 + 8 * st);
+      }
       if (mode == 3 && C0 < (b0 + 2) * UT && nf2 > 0) {
         // T1 tile: publish its completion to the F2 tiles of the next panel
         asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
@@ -1594,8 +1619,10 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_update_tma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
-    cudaFuncSetAttribute(k_update_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
+    cudaFuncSetAttribute(k_update_tma<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
+    cudaFuncSetAttribute(k_update_tma<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
+    cudaFuncSetAttribute(k_update_tma<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
+    cudaFuncSetAttribute(k_update_tma<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
     cudaFuncSetAttribute(k_panel_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, F1SMEM);
     cudaFuncSetAttribute(k_panel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB * US * (int)sizeof(double));
     cudaFuncSetAttribute(k_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * USTAGE * (int)sizeof(double));
@@ -1641,6 +1668,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
                    make_map(&mapL1, f.Lb1, N, NB, f.ldw) && make_map(&mapX, f.Lblk, NB, NB, NB)))
     return MDS_ERR_CUDA;
   const int g_sched = std::getenv("MDS_STATIC_SCHED") ? 1 : 0;
+  const bool g_inplace = std::getenv("MDS_UPD_INPLACE") != nullptr;
   const bool capped = (g_grid_cap > 0 && g_grid_cap < sms);
   if (capped) sms = g_grid_cap;
   const size_t usmem = 2 * NB * US * sizeof(double);
@@ -1670,7 +1698,12 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
       const int reserve = capped ? std::max(1, sms / 8) : 1;   // SMs left to the panel chain (F1)
       {
         const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt * (nt + 1) / 2 + 2 * nt, sms - reserve));
-        MDS_LAUNCH(PC_UPDATE, side, (k_update_tma<3><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
+        if (g_inplace)
+          MDS_LAUNCH(PC_UPDATE, side,
+                     (k_update_tma<3, false><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
+        else
+          MDS_LAUNCH(PC_UPDATE, side,
+                     (k_update_tma<3, true><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
       }
       MDS_CUDA_TRY(cudaEventRecord(ev(p, 1), side));
       plast = p;
@@ -1678,9 +1711,12 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
       MDS_LAUNCH(PC_PANEL_STORE, st, (k_panel_store<<<dim3(g256, 8), 256, 0, st>>>(N, M, ldm, fp)));
       if (n2max > 0) {
         const unsigned ugrid = (unsigned)std::min<int64_t>(nt * (nt + 1) / 2, sms);
-        if (use_tma)
+        if (use_tma && g_inplace)
           MDS_LAUNCH(PC_UPDATE, st,
-                     (k_update_tma<0><<<ugrid, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
+                     (k_update_tma<0, false><<<ugrid, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
+        else if (use_tma)
+          MDS_LAUNCH(PC_UPDATE, st,
+                     (k_update_tma<0, true><<<ugrid, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
         else if (v16)
           MDS_LAUNCH(PC_UPDATE, st,
                      (k_update<true><<<ugrid, 128, 2 * USTAGE * sizeof(double), st>>>(N, M, ldm, fp)));

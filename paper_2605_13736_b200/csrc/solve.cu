@@ -5,8 +5,14 @@
 //
 // Triangular sweeps are single "sync-free" launches: CTA i (row block of 64,
 // index taken from an atomic ticket so lower blocks always run first) streams
-// its part of L against already-published blocks (per-block ready flags), then
-// solves its 64x64 diagonal block in one warp and publishes.
+// its part of L against already-published blocks, then finishes its block.
+// The dependent chain between consecutive blocks is one 64x64 GEMV: with
+// Binv_i = L_ii^{-1} and G_i = Binv_i L_{i,i-1} precomputed (k_inv_blocks),
+//   y_i = Binv_i (b_i - sum_{q<i-1} L_iq y_q) - G_i y_{i-1},
+// where the first term is ready before y_{i-1} is.  Published values are
+// their own ready flags: the output vectors are pre-filled with an all-ones
+// bit pattern (never produced: NaN results are canonicalised on store) and a
+// consumer polls the values it needs.
 #include <algorithm>
 
 #include "common.cuh"
@@ -21,11 +27,15 @@ constexpr int ST = 256;       // threads
 constexpr int PERM_MASK = (1 << 29) - 1;
 
 struct SWork {
-  double* y;
+  double* b;      // [N] P rhs
+  double* y;      // [N] forward result, then D^{-1} applied in place (published values, sentinel-filled)
+  double* x;      // [N] backward result (published values, sentinel-filled)
   double* binv;   // [nblk][TB*TB] inverses of the unit-lower diagonal blocks (column-major)
-  int* flags;     // [nblk]
+  double* gf;     // [nblk][TB*TB] Binv_i L_{i,i-1}            (column-major)
+  double* gb;     // [nblk][TB*TB] (L_{i+1,i} Binv_i)^T        (column-major)
   int* tickets;   // [2]
 };
+constexpr unsigned long long SENT = ~0ull;   // "not yet published" (a NaN payload never stored)
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 SWork carve(void* work, int64_t N, size_t* total) {
@@ -34,14 +44,78 @@ SWork carve(void* work, int64_t N, size_t* total) {
   char* b = reinterpret_cast<char*>(work);
   auto take = [&](size_t bytes) { char* p = b + off; off = align_up(off + bytes, 256); return p; };
   s.tickets = reinterpret_cast<int*>(take(sizeof(int) * 4));
-  s.flags = reinterpret_cast<int*>(take(sizeof(int) * (N / TB + 2)));
+  s.b = reinterpret_cast<double*>(take(sizeof(double) * std::max<int64_t>(N, 1)));
   s.y = reinterpret_cast<double*>(take(sizeof(double) * std::max<int64_t>(N, 1)));
+  s.x = reinterpret_cast<double*>(take(sizeof(double) * std::max<int64_t>(N, 1)));
   s.binv = reinterpret_cast<double*>(take(sizeof(double) * TB * TB * (N / TB + 1)));
+  s.gf = reinterpret_cast<double*>(take(sizeof(double) * TB * TB * (N / TB + 1)));
+  s.gb = reinterpret_cast<double*>(take(sizeof(double) * TB * TB * (N / TB + 1)));
   if (total) *total = off;
   return s;
 }
 
-__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const double* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// wait until the n published values at p are all present, return them
+template <int NV>
+__device__ __forceinline__ void poll_values(const double* p, double* out) {
+  unsigned long long v[NV];
+  bool ready;
+  do {
+    ready = true;
+#pragma unroll
+    for (int c = 0; c < NV; c++) {
+      v[c] = ld_relaxed_u64(p + c);
+      ready &= (v[c] != SENT);
+    }
+  } while (!ready);
+#pragma unroll
+  for (int c = 0; c < NV; c++) out[c] = __longlong_as_double((long long)v[c]);
+}
+// prefetch NV values (may still be sentinels); complete them later with finish_values
+template <int NV>
+__device__ __forceinline__ void load_values(const double* p, unsigned long long* v) {
+#pragma unroll
+  for (int c = 0; c < NV; c++) v[c] = ld_relaxed_u64(p + c);
+}
+template <int NV>
+__device__ __forceinline__ void finish_values(const double* p, unsigned long long* v, double* out) {
+  bool ready = true;
+#pragma unroll
+  for (int c = 0; c < NV; c++) ready &= (v[c] != SENT);
+  while (!ready) {
+    ready = true;
+#pragma unroll
+    for (int c = 0; c < NV; c++) {
+      if (v[c] == SENT) v[c] = ld_relaxed_u64(p + c);
+      ready &= (v[c] != SENT);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NV; c++) out[c] = __longlong_as_double((long long)v[c]);
+}
+// 16 published values p[0..16) needed by every lane of the warp: lane l fetches
+// p[l & 15] only (prefetched raw value `raw`, completed by polling if it was not
+// yet published), then the warp exchanges them by shuffles -- 16x fewer polling
+// loads on the line the producer is about to write.  `valid` = how many exist.
+__device__ __forceinline__ void warp_values16(const double* p, unsigned long long raw, int valid, double* out) {
+  const int lane = threadIdx.x & 31, c = lane & 15;
+  double mine = 0.0;
+  if (c < valid) finish_values<1>(p + c, &raw, &mine);
+#pragma unroll
+  for (int u = 0; u < 16; u++) out[u] = __shfl_sync(0xffffffffu, mine, u);
+}
+__device__ __forceinline__ unsigned long long prefetch16(const double* p, int valid) {
+  const int c = threadIdx.x & 15;
+  return (c < valid) ? ld_relaxed_u64(p + c) : 0ull;
+}
+__device__ __forceinline__ void publish(double* p, double v) {
+  if (v != v) v = __longlong_as_double(0x7ff8000000000000ll);   // canonical NaN, never the sentinel
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;\n" ::"l"(p), "l"((unsigned long long)__double_as_longlong(v)) : "memory");
+}
 
 __global__ void k_gather(int64_t N, const int32_t* __restrict__ piv, const double* __restrict__ b,
                          double* __restrict__ y) {
@@ -50,56 +124,141 @@ __global__ void k_gather(int64_t N, const int32_t* __restrict__ piv, const doubl
 }
 
 // Inverses of the unit-lower TB x TB diagonal blocks of L (one CTA per block,
-// row-by-row: Binv[r][c] = -sum_{k=c}^{r-1} L[r][k] Binv[k][c]).  With them the
-// dependent chain of the triangular sweeps is two small GEMVs per block.
+// row-by-row: Binv[r][c] = -sum_{k=c}^{r-1} L[r][k] Binv[k][c]), and the
+// one-step chain operators Gf_i = Binv_i L_{i,i-1}, Gb_i = (L_{i+1,i} Binv_i)^T.
+constexpr int TBP = TB + 1;
+constexpr int IBSMEM = (2 * TB * TBP + 4 * 16 * 17) * 8;   // L block, Binv, 16x16 temporaries
 __global__ void __launch_bounds__(256) k_inv_blocks(int64_t N, const double* __restrict__ L, int64_t lda,
-                                                    double* __restrict__ binv) {
+                                                    double* __restrict__ binv, double* __restrict__ gf,
+                                                    double* __restrict__ gb) {
   extern __shared__ double ism[];
-  double* Ls = ism;                      // Ls[k*(TB+1) + r] = L[r][k]
-  double* Bs = ism + TB * (TB + 1);      // Bs[c*(TB+1) + r] = Binv[r][c]
+  double* Ls = ism;                      // Ls[k*TBP + r] = L[r][k]  (diagonal block, later the off-diagonal ones)
+  double* Bs = ism + TB * TBP;           // Bs[c*TBP + r] = Binv[r][c]
+  const int64_t nblk = (N + TB - 1) / TB;
   const int64_t i = blockIdx.x;
   const int64_t r0 = i * TB;
   const int nr = (int)((N - r0) < TB ? (N - r0) : TB);
   for (int idx = threadIdx.x; idx < TB * TB; idx += blockDim.x) {
     const int r = idx % TB, c = idx / TB;
-    Ls[c * (TB + 1) + r] = (r < nr && c < nr && r > c) ? L[(r0 + r) + (r0 + c) * lda] : 0.0;
-    Bs[c * (TB + 1) + r] = (r == c) ? 1.0 : 0.0;
+    Ls[c * TBP + r] = (r < nr && c < nr && r > c) ? L[(r0 + r) + (r0 + c) * lda] : 0.0;
+    Bs[c * TBP + r] = (r == c) ? 1.0 : 0.0;
   }
   __syncthreads();
-  // 4 threads per column c split the dot product; rows r sequential
-  const int c = threadIdx.x >> 2, part = threadIdx.x & 3;
-  for (int r = 1; r < nr; r++) {
-    double sacc = 0.0;
-    if (c < r) {
-      for (int k = c + part; k < r; k += 4) sacc += Ls[k * (TB + 1) + r] * Bs[c * (TB + 1) + k];
+  // blocked inversion of the unit-lower block: (1) the four 16x16 diagonal
+  // blocks, one warp each (lane c < 16 owns column c, right-looking so each
+  // row's update is one FMA); (2) off-diagonal 16x16 blocks by distance dd:
+  // Binv_{bi,bj} = -Binv_{bi,bi} sum_{k=bj}^{bi-1} L_{bi,k} Binv_{k,bj}.
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < 4 && lane < 16) {
+    const int o = warp * 16, c = lane;
+    double xv[16];
+#pragma unroll
+    for (int rr = 0; rr < 16; rr++) xv[rr] = (rr == c) ? 1.0 : 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 15; kk++) {
+      const double xk = xv[kk];
+#pragma unroll
+      for (int rr = kk + 1; rr < 16; rr++) xv[rr] = fma(-Ls[(o + kk) * TBP + o + rr], xk, xv[rr]);
     }
-    sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
-    sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
-    if (c < r && part == 0) Bs[c * (TB + 1) + r] = -sacc;
-    __syncthreads();
+#pragma unroll
+    for (int rr = 0; rr < 16; rr++) Bs[(o + c) * TBP + o + rr] = xv[rr];   // (zero above the diagonal)
+  }
+  __syncthreads();
+  {
+    double* Ts = Bs + TB * TBP;          // temp 16x16 blocks (third buffer)
+    const int er = threadIdx.x & 15, ec = threadIdx.x >> 4;
+    for (int dd = 1; dd < 4; dd++) {
+      for (int bj = 0; bj + dd < 4; bj++) {
+        const int bi = bj + dd;
+        double t = 0.0;
+        for (int kk = bj * 16; kk < bi * 16; kk++) t = fma(Ls[kk * TBP + bi * 16 + er], Bs[(bj * 16 + ec) * TBP + kk], t);
+        Ts[(bj * 16 + ec) * 17 + er] = t;
+      }
+      __syncthreads();
+      for (int bj = 0; bj + dd < 4; bj++) {
+        const int bi = bj + dd;
+        double t = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 16; kk++) t = fma(Bs[(bi * 16 + kk) * TBP + bi * 16 + er], Ts[(bj * 16 + ec) * 17 + kk], t);
+        Bs[(bj * 16 + ec) * TBP + bi * 16 + er] = -t;
+      }
+      __syncthreads();
+    }
   }
   double* out = binv + (size_t)i * TB * TB;
   for (int idx = threadIdx.x; idx < TB * TB; idx += blockDim.x) {
     const int r = idx % TB, cc = idx / TB;
-    out[idx] = Bs[cc * (TB + 1) + r];
+    out[idx] = Bs[cc * TBP + r];
+  }
+  // thread (r = tid & 63, column group cg = tid >> 6) computes 16 outputs of each G
+  const int r = threadIdx.x & (TB - 1), cg = threadIdx.x >> 6;
+  if (i >= 1) {
+    // Gf[r][c] = sum_k Binv[r][k] L_{i,i-1}[k][c]
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < TB * TB; idx += blockDim.x) {
+      const int rr = idx % TB, c = idx / TB;
+      Ls[c * TBP + rr] = (rr < nr) ? L[(r0 + rr) + (r0 - TB + c) * lda] : 0.0;
+    }
+    __syncthreads();
+    double acc[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++) acc[u] = 0.0;
+    for (int k = 0; k < TB; k++) {
+      const double bk = Bs[k * TBP + r];
+#pragma unroll
+      for (int u = 0; u < 16; u++) acc[u] += bk * Ls[(cg * 16 + u) * TBP + k];
+    }
+    double* go = gf + (size_t)i * TB * TB;
+#pragma unroll
+    for (int u = 0; u < 16; u++) go[r + (cg * 16 + u) * TB] = acc[u];
+  }
+  if (i + 1 < nblk) {
+    // Gb[c][k] = sum_m L_{i+1,i}[k][m] Binv[m][c]   (thread: c = r, k = cg*16+u)
+    const int nr1 = (int)((N - r0 - TB) < TB ? (N - r0 - TB) : TB);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < TB * TB; idx += blockDim.x) {
+      const int kk = idx % TB, m = idx / TB;
+      Ls[m * TBP + kk] = (kk < nr1 && m < nr) ? L[(r0 + TB + kk) + (r0 + m) * lda] : 0.0;
+    }
+    __syncthreads();
+    double acc[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++) acc[u] = 0.0;
+    for (int m = 0; m < TB; m++) {
+      const double bmc = Bs[r * TBP + m];   // Binv[m][c=r]
+#pragma unroll
+      for (int u = 0; u < 16; u++) acc[u] += Ls[m * TBP + cg * 16 + u] * bmc;
+    }
+    double* go = gb + (size_t)i * TB * TB;
+#pragma unroll
+    for (int u = 0; u < 16; u++) go[r + (cg * 16 + u) * TB] = acc[u];   // Gb[c=r][k] at (r, k) column-major
   }
 }
 
-// forward: L y = y (unit lower; 2x2 D off-diagonals were moved out of L by the factor).
-// CTA i (ticket order) streams its row block of L against the published y_q, the
-// loads of L for block q+1 issued before waiting on block q's flag; then
-// y_i = Binv_i (b_i - acc).
-__global__ void __launch_bounds__(ST) k_trsv_fwd(int64_t N, const double* __restrict__ L, int64_t lda, double* y,
-                                                 const double* __restrict__ binv, int* flags, int* ticket) {
+// forward: L y = b (unit lower; 2x2 D off-diagonals were moved out of L by the factor).
+constexpr int SWSMEM = 2 * TB * TB * 8;   // Binv_i and G_i in shared memory
+__global__ void __launch_bounds__(ST) k_trsv_fwd(int64_t N, const double* __restrict__ L, int64_t lda,
+                                                 const double* __restrict__ b, double* y,
+                                                 const double* __restrict__ binv, const double* __restrict__ gf,
+                                                 int* ticket) {
+  extern __shared__ double fsm[];
+  double* Bs = fsm;             // Binv_i, column-major
+  double* Gs = fsm + TB * TB;   // Gf_i, column-major
   __shared__ int s_i;
   __shared__ double part[ST / TB][TB];
   __shared__ double v[TB];
+  __shared__ double cvec[TB];
   if (threadIdx.x == 0) s_i = atomicAdd(ticket, 1);
   __syncthreads();
   const int64_t i = s_i;
   const int64_t r0 = i * TB;
   const int nr = (int)((N - r0) < TB ? (N - r0) : TB);
   const int r = threadIdx.x & (TB - 1), cgp = threadIdx.x / TB;   // 4 column groups of 16
+  for (int idx = threadIdx.x; idx < TB * TB; idx += ST) {
+    Bs[idx] = binv[(size_t)i * TB * TB + idx];
+    Gs[idx] = (i >= 1) ? gf[(size_t)i * TB * TB + idx] : 0.0;
+  }
+  const double bi = (threadIdx.x < TB && r < nr) ? b[r0 + r] : 0.0;   // off the chain
   double acc = 0.0;
   double lv[16], ln[16];
   const double* Lr = L + (r0 + r);
@@ -108,45 +267,57 @@ __global__ void __launch_bounds__(ST) k_trsv_fwd(int64_t N, const double* __rest
 #pragma unroll
     for (int c = 0; c < 16; c++) dst[c] = (r < nr) ? Lr[(c0 + c) * lda] : 0.0;
   };
-  if (i > 0) loadL(0, lv);
-  for (int64_t q = 0; q < i; q++) {
-    if (q + 1 < i) loadL(q + 1, ln);
-    if (threadIdx.x == 0) {
-      while (*((volatile int*)&flags[q]) == 0) { }
-      __threadfence();
-    }
-    __syncthreads();
-    const double* yq = y + q * TB + cgp * 16;
+  const int64_t qend = i - 1;   // blocks streamed here; block i-1 goes through G_i
+  // y_q is prefetched together with L's block q (one block ahead), so a published
+  // value costs no extra round trip; only values not yet published are polled
+  unsigned long long yv = 0ull, yn = 0ull;
+  if (qend > 0) { loadL(0, lv); yv = prefetch16(y + cgp * 16, 16); }
+  for (int64_t q = 0; q < qend; q++) {
+    if (q + 1 < qend) { loadL(q + 1, ln); yn = prefetch16(y + (q + 1) * TB + cgp * 16, 16); }
+    double yq[16];
+    warp_values16(y + q * TB + cgp * 16, yv, 16, yq);
 #pragma unroll
-    for (int c = 0; c < 16; c++) acc += lv[c] * ld_cg(&yq[c]);
+    for (int c = 0; c < 16; c++) acc += lv[c] * yq[c];
 #pragma unroll
     for (int c = 0; c < 16; c++) lv[c] = ln[c];
+    yv = yn;
   }
   part[cgp][r] = acc;
   __syncthreads();
   if (threadIdx.x < TB) {
     const int rr = threadIdx.x;
-    v[rr] = (rr < nr) ? ld_cg(&y[r0 + rr]) - (part[0][rr] + part[1][rr] + part[2][rr] + part[3][rr]) : 0.0;
+    v[rr] = (rr < nr) ? bi - (part[0][rr] + part[1][rr] + part[2][rr] + part[3][rr]) : 0.0;
   }
   __syncthreads();
-  // y_i = Binv v : thread (r, cgp) sums 16 columns, reduce over the 4 groups
-  const double* B = binv + (size_t)i * TB * TB;
+  // c_i = Binv_i v
   double sacc = 0.0;
 #pragma unroll
   for (int c = 0; c < 16; c++) {
     const int cc = cgp * 16 + c;
-    sacc += B[r + cc * TB] * v[cc];
+    sacc += Bs[r + cc * TB] * v[cc];
   }
+  __syncthreads();
   part[cgp][r] = sacc;
   __syncthreads();
   if (threadIdx.x < TB) {
     const int rr = threadIdx.x;
-    if (rr < nr) y[r0 + rr] = part[0][rr] + part[1][rr] + part[2][rr] + part[3][rr];
+    cvec[rr] = part[0][rr] + part[1][rr] + part[2][rr] + part[3][rr];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicExch(&flags[i], 1);
+  // the chain step: y_i = c_i - G_i y_{i-1}
+  double g = 0.0;
+  if (i >= 1) {
+    double yp[16];
+    const double* pp = y + (i - 1) * TB + cgp * 16;
+    warp_values16(pp, prefetch16(pp, 16), 16, yp);
+#pragma unroll
+    for (int c = 0; c < 16; c++) g += Gs[r + (cgp * 16 + c) * TB] * yp[c];
+  }
+  part[cgp][r] = g;
+  __syncthreads();
+  if (threadIdx.x < TB) {
+    const int rr = threadIdx.x;
+    if (rr < nr) publish(&y[r0 + rr], cvec[rr] - ((part[0][rr] + part[1][rr]) + (part[2][rr] + part[3][rr])));
   }
 }
 
@@ -174,15 +345,21 @@ __global__ void k_dsolve(int64_t N, const double* __restrict__ LD, int64_t lda, 
 }
 
 // backward: L^T x = z, blocks from the bottom.  CTA i accumulates
-// sum_{q>i} L[q rows, i cols]^T x_q (threads run down contiguous column
+// sum_{q>i+1} L[q rows, i cols]^T x_q (threads run down contiguous column
 // segments: thread (k, cg) owns row k of every later block and 16 columns),
-// then x_i = Binv_i^T (z_i - acc).
-__global__ void __launch_bounds__(ST) k_trsv_bwd(int64_t N, const double* __restrict__ L, int64_t lda, double* y,
-                                                 const double* __restrict__ binv, int* flags, int* ticket) {
+// then x_i = Binv_i^T (z_i - acc) - Gb_i x_{i+1}.
+__global__ void __launch_bounds__(ST) k_trsv_bwd(int64_t N, const double* __restrict__ L, int64_t lda,
+                                                 const double* __restrict__ z, double* x,
+                                                 const double* __restrict__ binv, const double* __restrict__ gb,
+                                                 int* ticket) {
+  extern __shared__ double fsm[];
+  double* Bs = fsm;             // Binv_i, column-major
+  double* Gs = fsm + TB * TB;   // Gb_i, column-major: Gs[c + k*TB] = Gb[c][k]
   __shared__ int s_i;
   __shared__ double redt[TB][TB + 1];
   __shared__ double part4[4][TB];
   __shared__ double v[TB];
+  __shared__ double cvec[TB];
   const int64_t nblk = (N + TB - 1) / TB;
   if (threadIdx.x == 0) s_i = atomicAdd(ticket, 1);
   __syncthreads();
@@ -190,7 +367,11 @@ __global__ void __launch_bounds__(ST) k_trsv_bwd(int64_t N, const double* __rest
   const int64_t r0 = i * TB;
   const int nr = (int)((N - r0) < TB ? (N - r0) : TB);
   const int k = threadIdx.x & (TB - 1), cgp = threadIdx.x / TB;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int idx = threadIdx.x; idx < TB * TB; idx += ST) {
+    Bs[idx] = binv[(size_t)i * TB * TB + idx];
+    Gs[idx] = (i + 1 < nblk) ? gb[(size_t)i * TB * TB + idx] : 0.0;
+  }
+  const double zi = (threadIdx.x < TB && k < nr) ? z[r0 + k] : 0.0;   // off the chain
   double acc[16];
 #pragma unroll
   for (int c = 0; c < 16; c++) acc[c] = 0.0;
@@ -204,20 +385,24 @@ __global__ void __launch_bounds__(ST) k_trsv_bwd(int64_t N, const double* __rest
       dst[c] = (ok && cc < nr) ? L[row + (r0 + cc) * lda] : 0.0;
     }
   };
-  if (nblk - 1 > i) loadL(nblk - 1, lv);
-  for (int64_t q = nblk - 1; q > i; q--) {   // completion order: last block finishes first
-    if (q - 1 > i) loadL(q - 1, ln);
-    if (threadIdx.x == 0) {
-      while (*((volatile int*)&flags[q]) == 0) { }
-      __threadfence();
-    }
-    __syncthreads();
+  const int64_t qlo = i + 2;   // blocks streamed here (block i+1 goes through Gb_i)
+  // x_q is prefetched together with L's block q (one block ahead)
+  const unsigned long long ZERO = 0ull;
+  unsigned long long xv = ZERO, xn = ZERO;
+  if (nblk - 1 >= qlo) {
+    loadL(nblk - 1, lv);
+    if ((nblk - 1) * TB + k < N) load_values<1>(x + (nblk - 1) * TB + k, &xv);
+  }
+  for (int64_t q = nblk - 1; q >= qlo; q--) {   // completion order: last block finishes first
+    if (q - 1 >= qlo) { loadL(q - 1, ln); load_values<1>(x + (q - 1) * TB + k, &xn); }
     const int64_t row = q * TB + k;
-    const double xq = (row < N) ? ld_cg(&y[row]) : 0.0;
+    double xq = 0.0;
+    if (row < N) finish_values<1>(x + row, &xv, &xq);
 #pragma unroll
     for (int c = 0; c < 16; c++) acc[c] += lv[c] * xq;
 #pragma unroll
     for (int c = 0; c < 16; c++) lv[c] = ln[c];
+    xv = xn;
   }
   // reduce acc over the 64 rows k: transpose through shared memory (no shuffle chains)
 #pragma unroll
@@ -234,27 +419,38 @@ __global__ void __launch_bounds__(ST) k_trsv_bwd(int64_t N, const double* __rest
   if (threadIdx.x < TB) {
     const int cc = threadIdx.x;
     const double sum = part4[0][cc] + part4[1][cc] + part4[2][cc] + part4[3][cc];
-    v[cc] = (cc < nr) ? ld_cg(&y[r0 + cc]) - sum : 0.0;
+    v[cc] = (cc < nr) ? zi - sum : 0.0;
   }
   __syncthreads();
-  // x_i = Binv^T v : x[c] = sum_r Binv[r][c] v[r]; thread (c = k, group cgp) sums 16 rows
-  const double* B = binv + (size_t)i * TB * TB;
+  // c'_i = Binv^T v : c'[c] = sum_r Binv[r][c] v[r]; thread (c = k, group cgp) sums 16 rows
   double sacc = 0.0;
 #pragma unroll
   for (int rr = 0; rr < 16; rr++) {
     const int r = cgp * 16 + rr;
-    sacc += B[r + k * TB] * v[r];
+    sacc += Bs[r + k * TB] * v[r];
   }
   part4[cgp][k] = sacc;
   __syncthreads();
   if (threadIdx.x < TB) {
     const int cc = threadIdx.x;
-    if (cc < nr) y[r0 + cc] = part4[0][cc] + part4[1][cc] + part4[2][cc] + part4[3][cc];
+    cvec[cc] = part4[0][cc] + part4[1][cc] + part4[2][cc] + part4[3][cc];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicExch(&flags[i], 1);
+  // the chain step: x_i = c'_i - Gb_i x_{i+1}; thread (c = k, group cgp) sums 16 k's
+  double g = 0.0;
+  if (i + 1 < nblk) {
+    const int64_t rb1 = (i + 1) * TB + cgp * 16;
+    double xp[16];
+    const int valid = (int)((N - rb1) < 16 ? ((N - rb1) > 0 ? (N - rb1) : 0) : 16);   // ragged last block
+    warp_values16(x + rb1, prefetch16(x + rb1, valid), valid, xp);
+#pragma unroll
+    for (int u = 0; u < 16; u++) g += Gs[k + (cgp * 16 + u) * TB] * xp[u];
+  }
+  part4[cgp][k] = g;
+  __syncthreads();
+  if (threadIdx.x < TB) {
+    const int cc = threadIdx.x;
+    if (cc < nr) publish(&x[r0 + cc], cvec[cc] - ((part4[0][cc] + part4[1][cc]) + (part4[2][cc] + part4[3][cc])));
   }
 }
 
@@ -294,25 +490,28 @@ extern "C" int mds_solve(const mds_plan* plan, int64_t N, const double* LD, int6
     SWork s = carve(work, N, nullptr);
     const int64_t nblk = (N + TB - 1) / TB;
     MDS_CUDA_TRY(cudaMemsetAsync(s.tickets, 0, sizeof(int) * 4, st));
-    MDS_CUDA_TRY(cudaMemsetAsync(s.flags, 0, sizeof(int) * (nblk + 1), st));
+    MDS_CUDA_TRY(cudaMemsetAsync(s.y, 0xff, sizeof(double) * N, st));   // SENT: not yet published
+    MDS_CUDA_TRY(cudaMemsetAsync(s.x, 0xff, sizeof(double) * N, st));
     const unsigned ge = (unsigned)std::min<int64_t>(mds_cdiv(N, 256), 148 * 8);
-    MDS_LAUNCH(PC_SOLVE_GATHER, st, (k_gather<<<ge, 256, 0, st>>>(N, piv, rhs_c, s.y)));
+    MDS_LAUNCH(PC_SOLVE_GATHER, st, (k_gather<<<ge, 256, 0, st>>>(N, piv, rhs_c, s.b)));
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_inv_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * TB * (TB + 1) * 8);
+      cudaFuncSetAttribute(k_inv_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, IBSMEM);
+      cudaFuncSetAttribute(k_trsv_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SWSMEM);
+      cudaFuncSetAttribute(k_trsv_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SWSMEM);
       attr = true;
     }
     MDS_LAUNCH(PC_SOLVE_FWD, st,
-               (k_inv_blocks<<<(unsigned)nblk, 256, 2 * TB * (TB + 1) * sizeof(double), st>>>(N, LD, ldm, s.binv)));
+               (k_inv_blocks<<<(unsigned)nblk, 256, IBSMEM, st>>>(N, LD, ldm, s.binv, s.gf,
+                                                                                         s.gb)));
     MDS_LAUNCH(PC_SOLVE_FWD, st,
-               (k_trsv_fwd<<<(unsigned)nblk, ST, 0, st>>>(N, LD, ldm, s.y, s.binv, s.flags, s.tickets)));
+               (k_trsv_fwd<<<(unsigned)nblk, ST, SWSMEM, st>>>(N, LD, ldm, s.b, s.y, s.binv, s.gf, s.tickets)));
     const double* tolp = (zero_tol < 0.0 && fwork) ? mds_factor_tol_ptr(fwork) : nullptr;
     MDS_LAUNCH(PC_SOLVE_D, st,
                (k_dsolve<<<ge, 256, 0, st>>>(N, LD, ldm, piv, s.y, tolp, zero_tol < 0.0 ? 0.0 : zero_tol, status)));
-    MDS_CUDA_TRY(cudaMemsetAsync(s.flags, 0, sizeof(int) * (nblk + 1), st));
     MDS_LAUNCH(PC_SOLVE_BWD, st,
-               (k_trsv_bwd<<<(unsigned)nblk, ST, 0, st>>>(N, LD, ldm, s.y, s.binv, s.flags, s.tickets + 1)));
-    MDS_LAUNCH(PC_SOLVE_SCATTER, st, (k_scatter<<<ge, 256, 0, st>>>(N, piv, s.y, dxy)));
+               (k_trsv_bwd<<<(unsigned)nblk, ST, SWSMEM, st>>>(N, LD, ldm, s.y, s.x, s.binv, s.gb, s.tickets + 1)));
+    MDS_LAUNCH(PC_SOLVE_SCATTER, st, (k_scatter<<<ge, 256, 0, st>>>(N, piv, s.x, dxy)));
   }
   if (plan && dx_s) {
     int64_t dims[5];
