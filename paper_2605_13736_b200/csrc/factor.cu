@@ -281,8 +281,9 @@ __device__ __forceinline__ int64_t panel_k0(const FWork& f) {
 // the multipliers below it feed later steps).
 template <int SLOTS>
 __device__ __forceinline__ void f1_panel(double* As, double* Lm, double* rcp, int cb, int lane) {
-  // register window pv[sl][c] = column cb+jj+c of row rr[sl]; shifted by one column per step,
-  // so the loop body is the same every step (a rolled loop: small code, i-cache resident)
+  // fully unrolled (column index compile-time, so pv stays in registers and the
+  // triangular loop does only the live updates); no per-element predicates, so
+  // the straight-line code stays small enough for the instruction cache
   double pv[SLOTS][16];
   int rr[SLOTS];
 #pragma unroll
@@ -291,32 +292,26 @@ __device__ __forceinline__ void f1_panel(double* As, double* Lm, double* rcp, in
 #pragma unroll
     for (int c = 0; c < 16; c++) pv[sl][c] = (rr[sl] < NB) ? As[(cb + c) * F1S + rr[sl]] : 0.0;
   }
-#pragma unroll 1
+#pragma unroll
   for (int jj = 0; jj < 16; jj++) {
     const int j = cb + jj;
-    const double d = __shfl_sync(0xffffffffu, pv[0][0], jj);
+    const double d = __shfl_sync(0xffffffffu, pv[0][jj], jj);
     const double rd = fast_rcp(d);               // branch-free (keeps the shuffles convergent)
     const double r1 = (d != 0.0) ? rd : 0.0;
     double l[SLOTS];
 #pragma unroll
-    for (int sl = 0; sl < SLOTS; sl++) l[sl] = pv[sl][0] * r1;
+    for (int sl = 0; sl < SLOTS; sl++) l[sl] = pv[sl][jj] * r1;
 #pragma unroll
-    for (int c = 1; c < 16; c++) {
-      const double v = __shfl_sync(0xffffffffu, pv[0][0], jj + c);   // A(cb+jj+c, j)
+    for (int c = jj + 1; c < 16; c++) {
+      const double v = __shfl_sync(0xffffffffu, pv[0][jj], c);   // A(cb+c, j)
 #pragma unroll
       for (int sl = 0; sl < SLOTS; sl++) pv[sl][c] -= l[sl] * v;
     }
     if (lane == 0) rcp[j] = r1;
 #pragma unroll
     for (int sl = 0; sl < SLOTS; sl++) {
-      if (SLOTS == 1 || rr[sl] < NB) Lm[j * F1S + rr[sl]] = l[sl];        // multipliers of column j
-      if (rr[sl] < NB && rr[sl] >= j) As[j * F1S + rr[sl]] = pv[sl][0];   // column j is final
-    }
-#pragma unroll
-    for (int sl = 0; sl < SLOTS; sl++) {
-#pragma unroll
-      for (int c = 0; c < 15; c++) pv[sl][c] = pv[sl][c + 1];
-      pv[sl][15] = 0.0;
+      if (SLOTS == 1 || rr[sl] < NB) Lm[j * F1S + rr[sl]] = l[sl];         // multipliers of column j
+      if (rr[sl] < NB && rr[sl] >= j) As[j * F1S + rr[sl]] = pv[sl][jj];   // column j is final
     }
   }
 }
