@@ -316,17 +316,9 @@ __device__ __forceinline__ void f1_panel(double* As, double* Lm, double* rcp, in
   }
 }
 
-__global__ void __launch_bounds__(256) k_panel_diag(int64_t N, double* __restrict__ A, int64_t lda, FWork f) {
+__device__ __forceinline__ void f1_body(int64_t N, double* __restrict__ A, int64_t lda, const FWork& f, int64_t k0,
+                                        int nbp, bool fprev, double* sm) {
   FCtl* ctl = f.ctl;
-  if (ctl->abort) return;
-  const int64_t k0 = panel_k0(f);
-  if (k0 >= N) {
-    if (threadIdx.x == 0) { ctl->k0 = (int)N; ctl->kb = 0; ctl->nbp = 0; }
-    return;
-  }
-  const int nbp = (int)((N - k0) < NB ? (N - k0) : NB);
-  const bool fprev = f.fuse && f.pidx > 0;
-  extern __shared__ double sm[];
   double* As = sm;                   // As[c*F1S + r] : the block, updated in place (lower)
   double* Lm = sm + PF_BUF;          // Lm[c*F1S + r] = L[r][c] (unit lower multipliers, r > c); staging: Lprev
   double* Li = sm + 2 * PF_BUF;      // Li[c*F1S + r] = Linv[r][c];                              staging: Wprev
@@ -587,6 +579,188 @@ __global__ void __launch_bounds__(256) k_panel_diag(int64_t N, double* __restric
   }
   F1T(4);
   F1TRACE(3);
+}
+
+__global__ void __launch_bounds__(256) k_panel_diag(int64_t N, double* __restrict__ A, int64_t lda, FWork f) {
+  FCtl* ctl = f.ctl;
+  if (ctl->abort) return;
+  const int64_t k0 = panel_k0(f);
+  if (k0 >= N) {
+    if (threadIdx.x == 0) { ctl->k0 = (int)N; ctl->kb = 0; ctl->nbp = 0; }
+    return;
+  }
+  extern __shared__ double sm[];
+  f1_body(N, A, lda, f, k0, (int)((N - k0) < NB ? (N - k0) : NB), f.fuse && f.pidx > 0, sm);
+}
+
+// Tail-phase panel (the trailing update is short, SMs are free): one launch.
+// The first CTA to arrive (ticket 0) takes the F1 role; every other CTA takes
+// 64-row tiles below the diagonal block and, while F1 runs, applies the
+// previous panel's deferred update to them (A21 -= Lprev Wprev^T, DMMA;
+// written back to M for the exact path), then waits for F1's X (the F1 role
+// never waits on anything, so this cannot deadlock) and forms W21 = A21 X,
+// L21 and colmax.  The concurrent trailing update skips these columns.
+__device__ __forceinline__ void f2_role(int64_t N, double* __restrict__ A, int64_t lda, const FWork& f, int64_t k0,
+                                        int nbp, bool fprev, int role, int nrole, double* sm) {
+  FCtl* ctl = f.ctl;
+  const int64_t rb = k0 + nbp;
+  const int64_t rbase = (rb / UT) * UT;
+  const int64_t ntile = (N > rb) ? (N + UT - 1) / UT - rb / UT : 0;
+  int64_t tix = role - 1;
+  if (tix >= ntile) return;
+  double* S0 = sm;                   // Lprev tile [t][row], then A21 (updated) [col][row]
+  double* S1 = sm + PF_BUF;          // Wprev rows of the block [t][c]
+  double* S2 = sm + 2 * PF_BUF;      // X [t][j]
+  double* r1s = sm + 3 * PF_BUF;
+  __shared__ double cmx[8][16];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+  const int64_t ldw = f.ldw;
+  if (fprev)
+    for (int idx = tid; idx < NB * NB; idx += 256) {
+      const int i = idx & (NB - 1), t = idx >> 6;
+      S1[t * US + i] = (i < nbp) ? f.Wprev[(k0 + i) + t * ldw] : 0.0;
+    }
+  double cm[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  bool haveX = false;
+  for (; tix < ntile; tix += nrole) {
+    const int64_t R0 = rbase + tix * UT;
+    if (fprev) {
+      for (int idx = tid; idx < NB * UT; idx += 256) {
+        const int i = idx & (UT - 1), t = idx >> 6;
+        S0[t * US + i] = (R0 + i < N && R0 + i >= rb) ? f.Lbprev[(R0 + i) + t * ldw] : 0.0;
+      }
+      double acc[4][2][2];
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 2; b++)
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            const int64_t row = R0 + wm + 8 * a + g;
+            const int col = wn + 8 * b + 2 * q + e;
+            acc[a][b][e] = (row < N && row >= rb && col < nbp) ? A[row + (k0 + col) * lda] : 0.0;
+          }
+      __syncthreads();
+#pragma unroll 4
+      for (int t0 = 0; t0 < NB; t0 += 4) {
+        double av[4], bv[2];
+#pragma unroll
+        for (int a = 0; a < 4; a++) av[a] = -S0[(t0 + q) * US + wm + 8 * a + g];
+#pragma unroll
+        for (int b = 0; b < 2; b++) bv[b] = S1[(t0 + q) * US + wn + 8 * b + g];
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+#pragma unroll
+          for (int b = 0; b < 2; b++) dmma(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+      }
+      __syncthreads();   // every warp is done with the Lprev tile
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 2; b++)
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            const int r = wm + 8 * a + g, c = wn + 8 * b + 2 * q + e;
+            S0[c * US + r] = acc[a][b][e];
+            if (R0 + r < N && R0 + r >= rb && c < nbp) A[(R0 + r) + (k0 + c) * lda] = acc[a][b][e];
+          }
+    } else {
+      for (int idx = tid; idx < NB * UT; idx += 256) {
+        const int i = idx & (UT - 1), t = idx >> 6;
+        S0[t * US + i] = (t < nbp && R0 + i < N && R0 + i >= rb) ? A[(R0 + i) + (k0 + t) * lda] : 0.0;
+      }
+    }
+    if (!haveX) {
+      if (tid == 0) {
+        while (ld_acquire_u32(&ctl->xready) < (unsigned)(f.pidx + 1)) __nanosleep(32);
+      }
+      __syncthreads();
+      for (int idx = tid; idx < NB * NB; idx += 256) {
+        const int j = idx & (NB - 1), t = idx >> 6;
+        S2[t * US + j] = __ldcg(&f.Lblk[t * NB + j]);
+      }
+      if (tid < NB) {
+        const double d = (tid < nbp) ? __ldcg(&ctl->d[tid]) : 0.0;
+        const double rd = fast_rcp(d);
+        r1s[tid] = (d != 0.0) ? rd : 0.0;
+      }
+      haveX = true;
+    }
+    __syncthreads();
+    double acc[4][2][2];
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+      for (int b = 0; b < 2; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll 4
+    for (int t0 = 0; t0 < NB; t0 += 4) {
+      double av[4], bv[2];
+#pragma unroll
+      for (int a = 0; a < 4; a++) av[a] = S0[(t0 + q) * US + wm + 8 * a + g];
+#pragma unroll
+      for (int b = 0; b < 2; b++) bv[b] = S2[(t0 + q) * US + wn + 8 * b + g];
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 2; b++) dmma(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; a++) {
+      const int64_t row = R0 + wm + 8 * a + g;
+      if (row < N && row >= rb) {
+#pragma unroll
+        for (int b = 0; b < 2; b++)
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            const int col = wn + 8 * b + 2 * q + e;
+            if (col < nbp) {
+              f.W[row + col * ldw] = acc[a][b][e];
+              f.Lb[row + col * ldw] = acc[a][b][e] * r1s[col];      // speculative L21
+              cm[b][e] = fmax(cm[b][e], fabs(acc[a][b][e]));
+            }
+          }
+      }
+    }
+    __syncthreads();   // S0 is refilled by the next tile
+  }
+  // per-column max |W21| over this CTA's tiles: reduce over g, then over the two row halves
+#pragma unroll
+  for (int b = 0; b < 2; b++)
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+      double v = cm[b][e];
+      v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 4));
+      v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 8));
+      v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 16));
+      if (g == 0) cmx[warp][8 * b + 2 * q + e] = v;
+    }
+  __syncthreads();
+  if (tid < NB) {
+    const int c = tid, w0 = 2 * (c >> 4);
+    const double v = fmax(cmx[w0][c & 15], cmx[w0 + 1][c & 15]);
+    if (c < nbp) atomicMax(&ctl->colmax[c], dbits(v));
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) k_panel_fast(int64_t N, double* __restrict__ A, int64_t lda, FWork f) {
+  FCtl* ctl = f.ctl;
+  if (ctl->abort) return;
+  __shared__ int s_role;
+  if (threadIdx.x == 0) s_role = (int)atomicAdd(&f.ucount[3 * f.pidx + 1], 1ull);   // (slot 3q+1: tickets)
+  __syncthreads();
+  const int role = s_role;
+  const int64_t k0 = panel_k0(f);
+  if (k0 >= N) {
+    if (role == 0 && threadIdx.x == 0) { ctl->k0 = (int)N; ctl->kb = 0; ctl->nbp = 0; }
+    return;
+  }
+  const int nbp = (int)((N - k0) < NB ? (N - k0) : NB);
+  const bool fprev = f.fuse && f.pidx > 0;
+  extern __shared__ double sm[];
+  if (role == 0) f1_body(N, A, lda, f, k0, nbp, fprev, sm);
+  else f2_role(N, A, lda, f, k0, nbp, fprev, role, (int)gridDim.x - 1, sm);
 }
 
 // F2: W21 = A21 * X (X = L11^{-T}) on the FP64 tensor cores, 64-row tiles,
@@ -1122,23 +1296,34 @@ __device__ __forceinline__ unsigned tma_off(int i, int t) {
 // updates that itself), in the order: tile column b0, tile column b0+1 (the
 // "T1" tiles, which hold the next panel's columns), then the rest -- so the
 // dynamic queue finishes the next panel's columns first.
-__device__ __forceinline__ int64_t upd_nt1(int64_t nt) { return nt >= 2 ? 2 * nt - 1 : nt; }
+// mode 4 (tail panels, whose F2 tiles apply the deferred update themselves):
+// tile column b0+1, then the rest; columns >= s+nbn only.
+__device__ __forceinline__ int64_t upd_nt1(int64_t nt, int mode) {
+  if (mode == 4) return nt >= 2 ? nt - 1 : 0;
+  return nt >= 2 ? 2 * nt - 1 : nt;
+}
 __device__ __forceinline__ int64_t upd_ntiles(int64_t nt, int mode) {
   if (mode == 0) return nt * (nt + 1) / 2;
   const int64_t r = nt - 2;
-  return upd_nt1(nt) + (r > 0 ? r * (r + 1) / 2 : 0);
+  return upd_nt1(nt, mode) + (r > 0 ? r * (r + 1) / 2 : 0);
 }
 __device__ __forceinline__ void upd_tile(int64_t x, int64_t nt, int mode, int64_t& bi, int64_t& bj) {
   if (mode == 0) { tri_tile(x, bi, bj); return; }
-  if (x < nt) { bi = x; bj = 0; return; }
-  if (x < upd_nt1(nt)) { bi = x - nt + 1; bj = 1; return; }
-  tri_tile(x - upd_nt1(nt), bi, bj);
+  if (mode == 3) {
+    if (x < nt) { bi = x; bj = 0; return; }
+    if (x < upd_nt1(nt, 3)) { bi = x - nt + 1; bj = 1; return; }
+  } else {
+    if (x < upd_nt1(nt, 4)) { bi = x + 1; bj = 1; return; }
+  }
+  tri_tile(x - upd_nt1(nt, mode), bi, bj);
   bi += 2; bj += 2;
 }
 // entries (row, col) a launch of this mode may change
 __device__ __forceinline__ bool upd_mask(int64_t row, int64_t col, int64_t N, int64_t s, int64_t nbn, int mode) {
   if (row >= N || row < col || col < s) return false;
-  return mode == 0 || !(col < s + nbn && row < s + nbn);
+  if (mode == 0) return true;
+  if (mode == 4) return col >= s + nbn;
+  return !(col < s + nbn && row < s + nbn);
 }
 
 __device__ __forceinline__ double lds_f64(unsigned addr) {
@@ -1180,7 +1365,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
   const int64_t k0 = pi.x;
   const int kb = pi.y;
   const int64_t s = k0 + kb;
-  if (kb <= 0 || (mode != 3 && N - s <= 0)) return;   // (mode 3 still copies the last panel)
+  if (kb <= 0 || (mode == 0 && N - s <= 0)) return;   // (look-ahead modes still copy the last panel)
   const int64_t b0 = s / UT;
   const int64_t nt = (N - s > 0) ? (N + UT - 1) / UT - b0 : 0;
   const int64_t ntiles = (nt > 0) ? upd_ntiles(nt, mode) : 0;
@@ -1192,11 +1377,12 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
   const int64_t f2r0 = s + nbn;
   const int64_t f2base = (f2r0 / UT) * UT;
   const int64_t nf2 = (mode == 3 && N > f2r0) ? (N + UT - 1) / UT - f2r0 / UT : 0;
-  if ((int64_t)blockIdx.x >= ntiles + nf2 + ((mode == 3) ? (N + UT - 1) / UT - k0 / UT : 0)) return;
+  constexpr bool LA = (mode == 3 || mode == 4);   // look-ahead modes (also copy the panel: S tiles)
+  if ((int64_t)blockIdx.x >= ntiles + nf2 + (LA ? (N + UT - 1) / UT - k0 / UT : 0)) return;
   unsigned long long* counter = f.ucount + 3 * f.pidx;
-  const int64_t nT1 = (mode == 3) ? upd_nt1(nt) : 0;
+  const int64_t nT1 = (LA && nt > 0) ? upd_nt1(nt, mode) : 0;
   // mode 3 also copies this panel's D + L from Lb into M (64-row "S" tiles, queued after T1)
-  const int64_t nS = (mode == 3) ? (N + UT - 1) / UT - k0 / UT : 0;
+  const int64_t nS = LA ? (N + UT - 1) / UT - k0 / UT : 0;
   const int64_t nall = ntiles + nS;
   unsigned long long* f2counter = f.ucount + 3 * (f.pidx + 1) + 2;
   extern __shared__ unsigned char tsm_raw[];
@@ -1217,7 +1403,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
     // scheduling: CTAs that start late, e.g. behind the panel kernels, just take fewer tiles)
     // and issues their TMA loads; -1 in a stage's tile slot ends its consumer group
     if (lane == 0) {
-      if (mode == 3) { UTRACE_MIN(f.pidx, 0); USM_START(f.pidx); }
+      if (LA) { UTRACE_MIN(f.pidx, 0); USM_START(f.pidx); }
       int ends = 0;
       const bool dyn = (sched == 0);
       unsigned long long xnext = dyn ? atom_add_u64(counter, 1ull) : blockIdx.x;   // claimed one tile ahead
@@ -1264,7 +1450,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
           continue;
         }
         int64_t x = (int64_t)xc;
-        if (mode == 3 && x >= nT1 && x < nT1 + nS) {   // S tile: Lb rows -> M
+        if (LA && x >= nT1 && x < nT1 + nS) {   // S tile: Lb rows -> M
           const int R0 = (int)((k0 / UT + (x - nT1)) * UT);
           stile[st] = (long long)((0xfffffffdull << 32) | (unsigned)R0);   // C0 = -3
           mbar_expect_tx(fb, TOPB);
@@ -1273,7 +1459,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
           xnext = dyn ? atom_add_u64(counter, 1ull) : xnext + gridDim.x;
           continue;
         }
-        if (mode == 3 && x >= nT1) x -= nS;
+        if (LA && x >= nT1) x -= nS;
         int64_t bi, bj;
         upd_tile(x, nt, mode, bi, bj);
         const int R0 = (int)((b0 + bi) * UT), C0 = (int)((b0 + bj) * UT);
@@ -1300,7 +1486,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
     const long long x = stile[st];
     if (x == -1) break;
     const int64_t R0 = (int64_t)(unsigned)(x & 0xffffffffll), C0 = (int64_t)(x >> 32);
-    if (mode == 3 && C0 == -3) {
+    if (LA && C0 == -3) {
       // S tile: panel rows R0..R0+63 of D + L (columns < kb, on/below the diagonal) into M
       const unsigned Lt = tsm + st * TSTAGEB;
       const int tq = (int)threadIdx.x - 32 - grp * 128;   // 0..127 within the group
@@ -1425,7 +1611,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
     }
   }
   if (leader) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // reductions complete before exit
-  if (mode == 3 && leader) { UTRACE_MAX(f.pidx, 1); USM_END(f.pidx); }
+  if (LA && leader) { UTRACE_MAX(f.pidx, 1); USM_END(f.pidx); }
 }
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1617,6 +1803,8 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     cudaFuncSetAttribute(k_update_tma<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
     cudaFuncSetAttribute(k_update_tma<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
     cudaFuncSetAttribute(k_update_tma<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
+    cudaFuncSetAttribute(k_update_tma<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
+    cudaFuncSetAttribute(k_panel_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, F1SMEM);
     cudaFuncSetAttribute(k_update_tma<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
     cudaFuncSetAttribute(k_panel_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, F1SMEM);
     cudaFuncSetAttribute(k_panel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB * US * (int)sizeof(double));
@@ -1664,45 +1852,103 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     return MDS_ERR_CUDA;
   const int g_sched = std::getenv("MDS_STATIC_SCHED") ? 1 : 0;
   const bool g_inplace = std::getenv("MDS_UPD_INPLACE") != nullptr;
+  const bool upd_main = std::getenv("MDS_UPD_MAIN") != nullptr;   // measured slower (A/B), off by default
+  // panels with at most this many remaining rows use the one-launch fast path
+  const int64_t tail_rows = std::getenv("MDS_TAIL_ROWS") ? std::atoll(std::getenv("MDS_TAIL_ROWS")) : 4800;
   const bool capped = (g_grid_cap > 0 && g_grid_cap < sms);
   if (capped) sms = g_grid_cap;
   const size_t usmem = 2 * NB * US * sizeof(double);
-  int64_t plast = -1;
-  for (int64_t p = 0; p < npmax; p++) {
-    const int64_t kmin = std::min<int64_t>(p * (NB - 1), N);   // lower bound on this panel's k0
-    const int64_t rows = N - kmin;
-    if (rows <= 0) break;
+  auto fwork_for = [&](int64_t p) {
     FWork fp = f;
     fp.pidx = (int)p;
     fp.fuse = lookahead ? 1 : 0;
     if (p & 1) { fp.W = f.W1; fp.Lb = f.Lb1; fp.Wprev = f.W; fp.Lbprev = f.Lb; }
     else { fp.Wprev = f.W1; fp.Lbprev = f.Lb1; }
-    const unsigned g256 = (unsigned)std::max<int64_t>(mds_cdiv(rows, 256), 1);
-    const unsigned g64 = (unsigned)std::max<int64_t>(mds_cdiv(rows, UT), 1);
-    const int64_t n2max = std::max<int64_t>(rows - 1, 0);
-    const int64_t nt = mds_cdiv(n2max, UT) + 1;
-    MDS_LAUNCH(PC_PANEL_DIAG, st, (k_panel_diag<<<1, 256, F1SMEM, st>>>(N, M, ldm, fp)));
-    if (lookahead && plast >= 0) MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(plast, 1), 0));
-    MDS_LAUNCH(PC_PANEL_TRSM, st, (k_panel_trsm<<<g64, 128, usmem, st>>>(N, M, ldm, fp)));
-    MDS_LAUNCH(PC_PANEL_SLOW, st, (k_panel_slow<<<1, 1024, 0, st>>>(N, M, ldm, fp, piv)));
-    const CUtensorMap& mw = (p & 1) ? mapW1 : mapW;
-    const CUtensorMap& ml = (p & 1) ? mapL1 : mapL0;
-    if (lookahead) {
-      MDS_CUDA_TRY(cudaEventRecord(ev(p, 0), st));
-      MDS_CUDA_TRY(cudaStreamWaitEvent(side, ev(p, 0), 0));
-      const int reserve = capped ? std::max(1, sms / 8) : 1;   // SMs left to the panel chain (F1)
-      {
-        const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt * (nt + 1) / 2 + 2 * nt, sms - reserve));
-        if (g_inplace)
-          MDS_LAUNCH(PC_UPDATE, side,
-                     (k_update_tma<3, false><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
-        else
-          MDS_LAUNCH(PC_UPDATE, side,
-                     (k_update_tma<3, true><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
-      }
-      MDS_CUDA_TRY(cudaEventRecord(ev(p, 1), side));
-      plast = p;
+    return fp;
+  };
+  auto rows_of = [&](int64_t p) { return N - std::min<int64_t>(p * (NB - 1), N); };   // upper bound
+  const int reserve = capped ? std::max(1, sms / 8) : 1;   // SMs left to the panel chain (F1)
+  if (lookahead) {
+    // Stream roles.  Update-bound panels: U(p) runs on the main stream right after
+    // F4(p) (no cross-stream hop on the critical path) and F1(p+1) on the side
+    // stream; tail panels (chain-bound): F1+F2 of p+1 (k_panel_fast) on the main
+    // stream right after F4(p), U(p) on the side stream.
+    // ev(p, 0): F4(p) done; ev(p, 1): the side-stream work launched after F4(p) done.
+    auto launch_fast = [&](int64_t p) {
+      const FWork fp = fwork_for(p);
+      const unsigned g64 = (unsigned)std::max<int64_t>(mds_cdiv(rows_of(p), UT), 1);
+      const unsigned gf = (unsigned)(1 + std::max<int64_t>(1, std::min<int64_t>(g64, 4 * (int64_t)sms)));
+      MDS_LAUNCH(PC_PANEL_DIAG, st, (k_panel_fast<<<gf, 256, F1SMEM, st>>>(N, M, ldm, fp)));
+      return MDS_OK;
+    };
+    int64_t p = 0;
+    bool tail = rows_of(0) <= tail_rows;
+    if (tail) {
+      if (int rc = launch_fast(0)) return rc;
     } else {
+      const FWork fp = fwork_for(0);
+      MDS_LAUNCH(PC_PANEL_DIAG, st, (k_panel_diag<<<1, 256, F1SMEM, st>>>(N, M, ldm, fp)));
+    }
+    for (;; p++) {
+      const int64_t rows = rows_of(p);
+      const FWork fp = fwork_for(p);
+      if (!tail) {
+        if (p > 0) MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(p - 1, 1), 0));   // F1(p) (or U(p-1)) on the side stream
+        const unsigned g64 = (unsigned)std::max<int64_t>(mds_cdiv(rows, UT), 1);
+        MDS_LAUNCH(PC_PANEL_TRSM, st, (k_panel_trsm<<<g64, 128, usmem, st>>>(N, M, ldm, fp)));
+      } else if (p > 0) {
+        MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(p - 1, 1), 0));   // U(p-1) on the side stream
+      }
+      MDS_LAUNCH(PC_PANEL_SLOW, st, (k_panel_slow<<<1, 1024, 0, st>>>(N, M, ldm, fp, piv)));
+      MDS_CUDA_TRY(cudaEventRecord(ev(p, 0), st));
+      const int64_t n2max = std::max<int64_t>(rows - 1, 0);
+      const int64_t nt = mds_cdiv(n2max, UT) + 1;
+      const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt * (nt + 1) / 2 + 2 * nt, sms - reserve));
+      const CUtensorMap& mw = (p & 1) ? mapW1 : mapW;
+      const CUtensorMap& ml = (p & 1) ? mapL1 : mapL0;
+      const bool last = rows_of(p + 1) <= 0;
+      const bool next_tail = last || rows_of(p + 1) <= tail_rows;
+      MDS_CUDA_TRY(cudaStreamWaitEvent(side, ev(p, 0), 0));
+      if (next_tail) {
+        MDS_LAUNCH(PC_UPDATE, side,
+                   (k_update_tma<4, true><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
+        MDS_CUDA_TRY(cudaEventRecord(ev(p, 1), side));
+        if (last) break;
+        if (int rc = launch_fast(p + 1)) return rc;
+      } else if (!upd_main) {   // (A/B variant: U on the side stream, F1 on the main stream)
+        MDS_LAUNCH(PC_UPDATE, side,
+                   (k_update_tma<3, true><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
+        MDS_CUDA_TRY(cudaEventRecord(ev(p, 1), side));
+        const FWork fn = fwork_for(p + 1);
+        MDS_LAUNCH(PC_PANEL_DIAG, st, (k_panel_diag<<<1, 256, F1SMEM, st>>>(N, M, ldm, fn)));
+      } else {
+        const FWork fn = fwork_for(p + 1);
+        MDS_LAUNCH(PC_PANEL_DIAG, side, (k_panel_diag<<<1, 256, F1SMEM, side>>>(N, M, ldm, fn)));
+        MDS_CUDA_TRY(cudaEventRecord(ev(p, 1), side));
+        if (g_inplace)
+          MDS_LAUNCH(PC_UPDATE, st,
+                     (k_update_tma<3, false><<<gr, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
+        else
+          MDS_LAUNCH(PC_UPDATE, st,
+                     (k_update_tma<3, true><<<gr, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
+      }
+      tail = next_tail;
+    }
+    MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(p, 1), 0));
+  } else {
+    for (int64_t p = 0; p < npmax; p++) {
+      const int64_t rows = rows_of(p);
+      if (rows <= 0) break;
+      const FWork fp = fwork_for(p);
+      const unsigned g256 = (unsigned)std::max<int64_t>(mds_cdiv(rows, 256), 1);
+      const unsigned g64 = (unsigned)std::max<int64_t>(mds_cdiv(rows, UT), 1);
+      const int64_t n2max = std::max<int64_t>(rows - 1, 0);
+      const int64_t nt = mds_cdiv(n2max, UT) + 1;
+      MDS_LAUNCH(PC_PANEL_DIAG, st, (k_panel_diag<<<1, 256, F1SMEM, st>>>(N, M, ldm, fp)));
+      MDS_LAUNCH(PC_PANEL_TRSM, st, (k_panel_trsm<<<g64, 128, usmem, st>>>(N, M, ldm, fp)));
+      MDS_LAUNCH(PC_PANEL_SLOW, st, (k_panel_slow<<<1, 1024, 0, st>>>(N, M, ldm, fp, piv)));
+      const CUtensorMap& mw = (p & 1) ? mapW1 : mapW;
+      const CUtensorMap& ml = (p & 1) ? mapL1 : mapL0;
       MDS_LAUNCH(PC_PANEL_STORE, st, (k_panel_store<<<dim3(g256, 8), 256, 0, st>>>(N, M, ldm, fp)));
       if (n2max > 0) {
         const unsigned ugrid = (unsigned)std::min<int64_t>(nt * (nt + 1) / 2, sms);
@@ -1720,9 +1966,6 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
                      (k_update<false><<<ugrid, 128, 2 * USTAGE * sizeof(double), st>>>(N, M, ldm, fp)));
       }
     }
-  }
-  if (lookahead && plast >= 0) {
-    MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(plast, 1), 0));
   }
   {
     int dev = 0, sms = 148, occ = 0;
