@@ -1359,6 +1359,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
                                                              const __grid_constant__ CUtensorMap mapW,
                                                              const __grid_constant__ CUtensorMap mapL,
                                                              const __grid_constant__ CUtensorMap mapX, int sched) {
+  const bool snake = (sched & 2) != 0;
   FCtl* ctl = f.ctl;
   if (ctl->abort) return;
   const int2 pi = f.pinfo[f.pidx];
@@ -1405,7 +1406,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
     if (lane == 0) {
       if (LA) { UTRACE_MIN(f.pidx, 0); USM_START(f.pidx); }
       int ends = 0;
-      const bool dyn = (sched == 0);
+      const bool dyn = (sched & 1) == 0;
       unsigned long long xnext = dyn ? atom_add_u64(counter, 1ull) : blockIdx.x;   // claimed one tile ahead
       bool f2open = nf2 > 0, xready = false;
       for (int i = 0; ends < TNG; i++) {
@@ -1459,7 +1460,12 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
           xnext = dyn ? atom_add_u64(counter, 1ull) : xnext + gridDim.x;
           continue;
         }
-        if (LA && x >= nT1) x -= nS;
+        if (LA && x >= nT1) {
+          x -= nS;
+          // the bulk of the tiles runs in alternating direction from panel to panel, so
+          // a pass starts on the tiles the previous pass touched last (still in L2)
+          if (snake && (f.pidx & 1)) x = nT1 + (ntiles - 1 - x);
+        }
         int64_t bi, bj;
         upd_tile(x, nt, mode, bi, bj);
         const int R0 = (int)((b0 + bi) * UT), C0 = (int)((b0 + bj) * UT);
@@ -1850,7 +1856,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   if (use_tma && !(make_map(&mapW1, f.W1, N, NB, f.ldw) && make_map(&mapL0, f.Lb, N, NB, f.ldw) &&
                    make_map(&mapL1, f.Lb1, N, NB, f.ldw) && make_map(&mapX, f.Lblk, NB, NB, NB)))
     return MDS_ERR_CUDA;
-  const int g_sched = std::getenv("MDS_STATIC_SCHED") ? 1 : 0;
+  const int g_sched = (std::getenv("MDS_STATIC_SCHED") ? 1 : 0) | (std::getenv("MDS_NO_SNAKE") ? 0 : 2);
   const bool g_inplace = std::getenv("MDS_UPD_INPLACE") != nullptr;
   const bool upd_main = std::getenv("MDS_UPD_MAIN") != nullptr;   // measured slower (A/B), off by default
   // panels with at most this many remaining rows use the one-launch fast path
