@@ -1,6 +1,7 @@
 // common.cuh — shared device helpers of the product path (NOT shared with oracle/).
 #pragma once
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <stdint.h>
 #include "../../include/mds.h"
 
@@ -58,6 +59,29 @@ __device__ __forceinline__ ArgMax warp_argmax(ArgMax a) {
   } while (0)
 
 static inline int64_t mds_cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Programmatic dependent launch: a kernel launched with launch_pdl may be
+// scheduled before its stream predecessor has finished; it calls pdl_wait()
+// before touching the predecessor's results.  pdl_trigger() lets the
+// successor be scheduled once every CTA of this grid has started (so waiting
+// successors can never block this grid's own CTAs).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t st, Args... args) {
+  static const bool off = std::getenv("MDS_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = off ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
 
 // ---------------------------------------------------------------------------
 // launch accounting + optional per-class CUDA-event profiling (prof.cu)

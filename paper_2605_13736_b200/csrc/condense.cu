@@ -111,6 +111,8 @@ const int32_t* mds_plan_colidx(const mds_plan* P) { return P->colidx; }
 // w_k = 1/q_k, q_k = h_ss + sigma_s + delta_w  (Q_{x_s}^{-1}, A2 PAPER.md:121)
 __global__ void k_condense_w(int64_t n_s, const double* __restrict__ h_ss, const double* __restrict__ sigma_s,
                              double delta_w, double* __restrict__ w, int32_t* status) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n_s; k += (int64_t)gridDim.x * blockDim.x) {
     double q = h_ss[k] + sigma_s[k] + delta_w;
     if (!(q > 0.0)) mds_set_status(status, MDS_ERR_NONPOSITIVE);
@@ -125,6 +127,8 @@ __global__ void k_condense_dense(int64_t n_d, int64_t m, const double* __restric
                                  const double* __restrict__ Jd, int64_t ldj,
                                  double* __restrict__ M, int64_t ldm,
                                  const double* __restrict__ r_xd, double* __restrict__ rhs_c) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t j = blockIdx.x; j < n_d; j += gridDim.x) {
     double* Mj = M + j * ldm;
     const double* Hj = H + j * ldh;
@@ -181,6 +185,8 @@ k_condense_yy(int64_t n_d, int64_t m_E, int64_t m, int64_t acc_len,
               const double* __restrict__ w, const double* __restrict__ d_h, double delta_c,
               const double* __restrict__ r, int64_t n_s, double* __restrict__ M, int64_t ldm,
               double* __restrict__ rhs_c, int32_t* status) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* acc = smem + (size_t)warp * acc_len;
@@ -366,13 +372,14 @@ extern "C" int mds_condense(const mds_plan* P, const double* js_val, const doubl
   if (n_s > 0) {
     int64_t blocks = std::min<int64_t>(mds_cdiv(n_s, 256), 148 * 16);
     MDS_LAUNCH(PC_CONDENSE_W, st,
-               (k_condense_w<<<(unsigned)blocks, 256, 0, st>>>(n_s, h_ss, sigma_s, delta_w, w_out, status)));
+               MDS_CUDA_TRY(launch_pdl(k_condense_w, dim3((unsigned)blocks), dim3(256), 0, st, n_s, h_ss, sigma_s, delta_w,
+                                       w_out, status)));
   }
   if (n_d > 0) {
     int64_t blocks = std::min<int64_t>(n_d, 148 * 8);
     MDS_LAUNCH(PC_CONDENSE_DENSE, st,
-               (k_condense_dense<<<(unsigned)blocks, 256, 0, st>>>(n_d, m, H_dd, ldh, sigma_d, delta_w, J_d, ldj, M,
-                                                                 ldm, r ? r + n_s : nullptr, rhs_c)));
+               MDS_CUDA_TRY(launch_pdl(k_condense_dense, dim3((unsigned)blocks), dim3(256), 0, st, n_d, m, H_dd, ldh, sigma_d,
+                                       delta_w, J_d, ldj, M, ldm, r ? r + n_s : nullptr, rhs_c)));
   }
   if (m > 0) {
     // warp-private accumulator columns: <= 4096 doubles each; warps per CTA sized to ~192 KB
@@ -389,14 +396,14 @@ extern "C" int mds_condense(const mds_plan* P, const double* js_val, const doubl
       constexpr int W = 6;
       size_t smem = sizeof(double) * acc_len * W;
       MDS_LAUNCH(PC_CONDENSE_YY, st,
-                 (k_condense_yy<W><<<(unsigned)mds_cdiv(ntask, W), W * 32, smem, st>>>(
+                 MDS_CUDA_TRY(launch_pdl(k_condense_yy<W>, dim3((unsigned)mds_cdiv(ntask, W)), dim3(W * 32), smem, st,
                      n_d, P->m_E, m, acc_len, P->rowptr, P->colidx, js_val, P->tptr, P->tkp, w_out, d_h, delta_c,
                      r, n_s, M, ldm, rhs_c, status)));
     } else {
       constexpr int W = 8;
       size_t smem = sizeof(double) * acc_len * W;
       MDS_LAUNCH(PC_CONDENSE_YY, st,
-                 (k_condense_yy<W><<<(unsigned)mds_cdiv(ntask, W), W * 32, smem, st>>>(
+                 MDS_CUDA_TRY(launch_pdl(k_condense_yy<W>, dim3((unsigned)mds_cdiv(ntask, W)), dim3(W * 32), smem, st,
                      n_d, P->m_E, m, acc_len, P->rowptr, P->colidx, js_val, P->tptr, P->tkp, w_out, d_h, delta_c,
                      r, n_s, M, ldm, rhs_c, status)));
     }

@@ -127,14 +127,30 @@ __device__ __forceinline__ unsigned long long dbits(double v) { return (unsigned
 __device__ __forceinline__ double bitsd(unsigned long long b) { return __longlong_as_double((long long)b); }
 
 // ---------------------------------------------------------------------------
-__global__ void k_factor_init(FCtl* ctl, double zero_tol) {
-  ctl->tol = zero_tol;
+// zero the per-call control state (one kernel instead of several memsets, so
+// the launch chain stays programmatic-dependent-launch friendly)
+__global__ void k_factor_init(int64_t N, FWork f, double zero_tol) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gth = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = gtid; i < N; i += gth) { f.sw[i] = -1; f.bt[i] = 0; f.rowsum[i] = 0.0; }
+  for (int64_t i = gtid; i < 3 * (N + 2); i += gth) f.ucount[i] = 0ull;
+  for (int64_t i = gtid; i < 2 * (N / 64 + 4); i += gth) f.t1flag[i] = 0u;
+  if (blockIdx.x == 0) {
+    int* c = reinterpret_cast<int*>(f.ctl);
+    for (int i = threadIdx.x; i < (int)(sizeof(FCtl) / sizeof(int)); i += blockDim.x) c[i] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) f.ctl->tol = zero_tol;
+  }
 }
 
 // ||M||_inf (row abs-sums via symmetry, lower storage) + non-finite scan.
 // One CTA per 32x32 lower tile; row partials atomically added to rowsum.
 __global__ void __launch_bounds__(256) k_anorm_tiles(int64_t N, const double* __restrict__ A, int64_t lda,
                                                      double* rowsum, FCtl* ctl, int32_t* status) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t nt = (N + 31) / 32;
   const int64_t x = blockIdx.x;
   int64_t bi = (int64_t)((sqrt(8.0 * (double)x + 1.0) - 1.0) * 0.5);
@@ -179,6 +195,8 @@ __global__ void __launch_bounds__(256) k_anorm_tiles(int64_t N, const double* __
 }
 
 __global__ void __launch_bounds__(1024) k_anorm_final(int64_t N, const double* rowsum, FCtl* ctl) {
+  pdl_wait();
+  pdl_trigger();
   double m = 0.0;
   for (int64_t i = threadIdx.x; i < N; i += blockDim.x) m = fmax(m, rowsum[i]);
   m = warp_max(m);
@@ -582,6 +600,7 @@ __device__ __forceinline__ void f1_body(int64_t N, double* __restrict__ A, int64
 }
 
 __global__ void __launch_bounds__(256) k_panel_diag(int64_t N, double* __restrict__ A, int64_t lda, FWork f) {
+  pdl_wait();
   FCtl* ctl = f.ctl;
   if (ctl->abort) return;
   const int64_t k0 = panel_k0(f);
@@ -745,6 +764,7 @@ __device__ __forceinline__ void f2_role(int64_t N, double* __restrict__ A, int64
 }
 
 __global__ void __launch_bounds__(256, 1) k_panel_fast(int64_t N, double* __restrict__ A, int64_t lda, FWork f) {
+  pdl_wait();
   FCtl* ctl = f.ctl;
   if (ctl->abort) return;
   __shared__ int s_role;
@@ -770,6 +790,7 @@ __global__ void __launch_bounds__(256, 1) k_panel_fast(int64_t N, double* __rest
 // draws from once this panel's X is published: whatever it has not taken is
 // done here.
 __global__ void __launch_bounds__(128) k_panel_trsm(int64_t N, const double* __restrict__ A, int64_t lda, FWork f) {
+  pdl_trigger();   // let k_panel_slow launch and wait (griddepcontrol.wait) behind us
   FCtl* ctl = f.ctl;
   if (ctl->abort) return;
   const int nbp = ctl->nbp;
@@ -909,6 +930,8 @@ __device__ __forceinline__ void zero_w_tail(int64_t N, int64_t k0, int kb, const
 
 __global__ void __launch_bounds__(1024) k_panel_slow(int64_t N, double* __restrict__ A, int64_t lda, FWork f,
                                                      int32_t* piv) {
+  pdl_wait();
+  pdl_trigger();
   FCtl* ctl = f.ctl;
   if (ctl->abort) return;
   const int nbp = ctl->nbp;
@@ -1601,7 +1624,8 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
     asm volatile("bar.sync %0, 128;\n" ::"r"(grp + 1) : "memory");
     if (leader) {
 #pragma unroll
-      for (int b = 0; b < 8; b++) tma_reduce_add_2d(&mapA, (int)(R0 + 8 * b), (int)C0, Ot + b * 4096);
+      for (int b = 0; b < 8; b++)
+        if (!(sched & 4)) tma_reduce_add_2d(&mapA, (int)(R0 + 8 * b), (int)C0, Ot + b * 4096);   // (bit 2: timing experiment)
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       if (!OUTB) {
         asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");   // smem source consumed
@@ -1793,16 +1817,15 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   if (!work || work_bytes < need) return MDS_ERR_WORKSPACE;
   FWork f = carve(work, N, nullptr);
   // zero control + arrays (sw = -1)
-  MDS_CUDA_TRY(cudaMemsetAsync(f.ctl, 0, sizeof(FCtl), st));
-  MDS_CUDA_TRY(cudaMemsetAsync(f.sw, 0xff, sizeof(int) * N, st));
-  MDS_CUDA_TRY(cudaMemsetAsync(f.bt, 0, sizeof(int) * N, st));
-  MDS_CUDA_TRY(cudaMemsetAsync(f.rowsum, 0, sizeof(double) * N, st));
-  MDS_LAUNCH(PC_ANORM, st, (k_factor_init<<<1, 1, 0, st>>>(f.ctl, zero_tol)));
+  MDS_LAUNCH(PC_ANORM, st,
+             MDS_CUDA_TRY(launch_pdl(k_factor_init, dim3((unsigned)std::min<int64_t>(mds_cdiv(3 * (N + 2), 256), 1184)),
+                                     dim3(256), 0, st, N, f, zero_tol)));
   {
     int64_t nt = (N + 31) / 32;
     MDS_LAUNCH(PC_ANORM, st,
-               (k_anorm_tiles<<<(unsigned)(nt * (nt + 1) / 2), 256, 0, st>>>(N, M, ldm, f.rowsum, f.ctl, status)));
-    MDS_LAUNCH(PC_ANORM, st, (k_anorm_final<<<1, 1024, 0, st>>>(N, f.rowsum, f.ctl)));
+               MDS_CUDA_TRY(launch_pdl(k_anorm_tiles, dim3((unsigned)(nt * (nt + 1) / 2)), dim3(256), 0, st, N, M, ldm,
+                                       f.rowsum, f.ctl, status)));
+    MDS_LAUNCH(PC_ANORM, st, MDS_CUDA_TRY(launch_pdl(k_anorm_final, dim3(1), dim3(1024), 0, st, N, f.rowsum, f.ctl)));
   }
   static bool attr = false;
   if (!attr) {
@@ -1831,8 +1854,6 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int64_t npmax = (N + (NB - 2)) / (NB - 1) + 1;
-  MDS_CUDA_TRY(cudaMemsetAsync(f.ucount, 0, sizeof(unsigned long long) * 3 * (N + 2), st));
-  MDS_CUDA_TRY(cudaMemsetAsync(f.t1flag, 0, sizeof(unsigned) * 2 * (N / 64 + 4), st));
   // Look-ahead (TMA path).  Panel p's trailing update U(p) runs on a side
   // stream on all SMs but one, its dynamic tile queue starting with panel
   // p+1's columns.  Panel p+1's F1 applies panel p's update to its own
@@ -1856,7 +1877,8 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   if (use_tma && !(make_map(&mapW1, f.W1, N, NB, f.ldw) && make_map(&mapL0, f.Lb, N, NB, f.ldw) &&
                    make_map(&mapL1, f.Lb1, N, NB, f.ldw) && make_map(&mapX, f.Lblk, NB, NB, NB)))
     return MDS_ERR_CUDA;
-  const int g_sched = (std::getenv("MDS_STATIC_SCHED") ? 1 : 0) | (std::getenv("MDS_NO_SNAKE") ? 0 : 2);
+  const int g_sched = (std::getenv("MDS_STATIC_SCHED") ? 1 : 0) | (std::getenv("MDS_NO_SNAKE") ? 0 : 2) |
+                      (std::getenv("MDS_XP_NOREDUCE") ? 4 : 0);   // (bit 2: timing experiment only, wrong results)
   const bool g_inplace = std::getenv("MDS_UPD_INPLACE") != nullptr;
   const bool upd_main = std::getenv("MDS_UPD_MAIN") != nullptr;   // measured slower (A/B), off by default
   // panels with at most this many remaining rows use the one-launch fast path
@@ -1884,7 +1906,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
       const FWork fp = fwork_for(p);
       const unsigned g64 = (unsigned)std::max<int64_t>(mds_cdiv(rows_of(p), UT), 1);
       const unsigned gf = (unsigned)(1 + std::max<int64_t>(1, std::min<int64_t>(g64, 4 * (int64_t)sms)));
-      MDS_LAUNCH(PC_PANEL_DIAG, st, (k_panel_fast<<<gf, 256, F1SMEM, st>>>(N, M, ldm, fp)));
+      MDS_LAUNCH(PC_PANEL_DIAG, st, MDS_CUDA_TRY(launch_pdl(k_panel_fast, dim3(gf), dim3(256), F1SMEM, st, N, M, ldm, fp)));
       return MDS_OK;
     };
     int64_t p = 0;
@@ -1893,7 +1915,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
       if (int rc = launch_fast(0)) return rc;
     } else {
       const FWork fp = fwork_for(0);
-      MDS_LAUNCH(PC_PANEL_DIAG, st, (k_panel_diag<<<1, 256, F1SMEM, st>>>(N, M, ldm, fp)));
+      MDS_LAUNCH(PC_PANEL_DIAG, st, MDS_CUDA_TRY(launch_pdl(k_panel_diag, dim3(1), dim3(256), F1SMEM, st, N, M, ldm, fp)));
     }
     for (;; p++) {
       const int64_t rows = rows_of(p);
@@ -1905,7 +1927,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
       } else if (p > 0) {
         MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(p - 1, 1), 0));   // U(p-1) on the side stream
       }
-      MDS_LAUNCH(PC_PANEL_SLOW, st, (k_panel_slow<<<1, 1024, 0, st>>>(N, M, ldm, fp, piv)));
+      MDS_LAUNCH(PC_PANEL_SLOW, st, MDS_CUDA_TRY(launch_pdl(k_panel_slow, dim3(1), dim3(1024), 0, st, N, M, ldm, fp, piv)));
       MDS_CUDA_TRY(cudaEventRecord(ev(p, 0), st));
       const int64_t n2max = std::max<int64_t>(rows - 1, 0);
       const int64_t nt = mds_cdiv(n2max, UT) + 1;
@@ -1926,7 +1948,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
                    (k_update_tma<3, true><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
         MDS_CUDA_TRY(cudaEventRecord(ev(p, 1), side));
         const FWork fn = fwork_for(p + 1);
-        MDS_LAUNCH(PC_PANEL_DIAG, st, (k_panel_diag<<<1, 256, F1SMEM, st>>>(N, M, ldm, fn)));
+        MDS_LAUNCH(PC_PANEL_DIAG, st, MDS_CUDA_TRY(launch_pdl(k_panel_diag, dim3(1), dim3(256), F1SMEM, st, N, M, ldm, fn)));
       } else {
         const FWork fn = fwork_for(p + 1);
         MDS_LAUNCH(PC_PANEL_DIAG, side, (k_panel_diag<<<1, 256, F1SMEM, side>>>(N, M, ldm, fn)));

@@ -118,9 +118,16 @@ __device__ __forceinline__ void publish(double* p, double v) {
 }
 
 __global__ void k_gather(int64_t N, const int32_t* __restrict__ piv, const double* __restrict__ b,
-                         double* __restrict__ y) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = b[piv[N + i] & PERM_MASK];
+                         double* __restrict__ bp, double* y, double* x, int* tickets) {
+  pdl_wait();
+  pdl_trigger();
+  if (blockIdx.x == 0 && threadIdx.x < 4) tickets[threadIdx.x] = 0;
+  const double sent = __longlong_as_double((long long)SENT);   // "not yet published"
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    bp[i] = b[piv[N + i] & PERM_MASK];
+    y[i] = sent;
+    x[i] = sent;
+  }
 }
 
 // Inverses of the unit-lower TB x TB diagonal blocks of L (one CTA per block,
@@ -131,6 +138,8 @@ constexpr int IBSMEM = (2 * TB * TBP + 4 * 16 * 17) * 8;   // L block, Binv, 16x
 __global__ void __launch_bounds__(256) k_inv_blocks(int64_t N, const double* __restrict__ L, int64_t lda,
                                                     double* __restrict__ binv, double* __restrict__ gf,
                                                     double* __restrict__ gb) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ double ism[];
   double* Ls = ism;                      // Ls[k*TBP + r] = L[r][k]  (diagonal block, later the off-diagonal ones)
   double* Bs = ism + TB * TBP;           // Bs[c*TBP + r] = Binv[r][c]
@@ -241,6 +250,8 @@ __global__ void __launch_bounds__(ST) k_trsv_fwd(int64_t N, const double* __rest
                                                  const double* __restrict__ b, double* y,
                                                  const double* __restrict__ binv, const double* __restrict__ gf,
                                                  int* ticket) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ double fsm[];
   double* Bs = fsm;             // Binv_i, column-major
   double* Gs = fsm + TB * TB;   // Gf_i, column-major
@@ -324,6 +335,8 @@ __global__ void __launch_bounds__(ST) k_trsv_fwd(int64_t N, const double* __rest
 // D solve: 1x1 and 2x2 blocks (LAPACK dsytrs scaled 2x2 formula); 2x2 off-diagonal at (k, k+1) (upper slot)
 __global__ void k_dsolve(int64_t N, const double* __restrict__ LD, int64_t lda, const int32_t* __restrict__ piv,
                          double* y, const double* tolp, double tolv, int32_t* status) {
+  pdl_wait();
+  pdl_trigger();
   const double tol = tolp ? *tolp : tolv;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N; k += (int64_t)gridDim.x * blockDim.x) {
     const int bt = (piv[N + k] >> 29) & 3;
@@ -352,6 +365,8 @@ __global__ void __launch_bounds__(ST) k_trsv_bwd(int64_t N, const double* __rest
                                                  const double* __restrict__ z, double* x,
                                                  const double* __restrict__ binv, const double* __restrict__ gb,
                                                  int* ticket) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ double fsm[];
   double* Bs = fsm;             // Binv_i, column-major
   double* Gs = fsm + TB * TB;   // Gb_i, column-major: Gs[c + k*TB] = Gb[c][k]
@@ -456,6 +471,8 @@ __global__ void __launch_bounds__(ST) k_trsv_bwd(int64_t N, const double* __rest
 
 __global__ void k_scatter(int64_t N, const int32_t* __restrict__ piv, const double* __restrict__ y,
                           double* __restrict__ x) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
     x[piv[N + i] & PERM_MASK] = y[i];
 }
@@ -465,6 +482,8 @@ __global__ void k_recover(int64_t n_s, const int32_t* __restrict__ rowptr, const
                           const double* __restrict__ val, const double* __restrict__ w,
                           const double* __restrict__ r_xs, const double* __restrict__ dy,
                           double* __restrict__ dx_s) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n_s; k += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int p = rowptr[k]; p < rowptr[k + 1]; p++) s += val[p] * dy[colidx[p]];
@@ -489,11 +508,8 @@ extern "C" int mds_solve(const mds_plan* plan, int64_t N, const double* LD, int6
   if (N > 0) {
     SWork s = carve(work, N, nullptr);
     const int64_t nblk = (N + TB - 1) / TB;
-    MDS_CUDA_TRY(cudaMemsetAsync(s.tickets, 0, sizeof(int) * 4, st));
-    MDS_CUDA_TRY(cudaMemsetAsync(s.y, 0xff, sizeof(double) * N, st));   // SENT: not yet published
-    MDS_CUDA_TRY(cudaMemsetAsync(s.x, 0xff, sizeof(double) * N, st));
     const unsigned ge = (unsigned)std::min<int64_t>(mds_cdiv(N, 256), 148 * 8);
-    MDS_LAUNCH(PC_SOLVE_GATHER, st, (k_gather<<<ge, 256, 0, st>>>(N, piv, rhs_c, s.b)));
+    MDS_LAUNCH(PC_SOLVE_GATHER, st, MDS_CUDA_TRY(launch_pdl(k_gather, dim3(ge), dim3(256), 0, st, N, piv, rhs_c, s.b, s.y, s.x, s.tickets)));
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_inv_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, IBSMEM);
@@ -502,16 +518,15 @@ extern "C" int mds_solve(const mds_plan* plan, int64_t N, const double* LD, int6
       attr = true;
     }
     MDS_LAUNCH(PC_SOLVE_FWD, st,
-               (k_inv_blocks<<<(unsigned)nblk, 256, IBSMEM, st>>>(N, LD, ldm, s.binv, s.gf,
-                                                                                         s.gb)));
+               MDS_CUDA_TRY(launch_pdl(k_inv_blocks, dim3((unsigned)nblk), dim3(256), IBSMEM, st, N, LD, ldm, s.binv, s.gf, s.gb)));
     MDS_LAUNCH(PC_SOLVE_FWD, st,
-               (k_trsv_fwd<<<(unsigned)nblk, ST, SWSMEM, st>>>(N, LD, ldm, s.b, s.y, s.binv, s.gf, s.tickets)));
+               MDS_CUDA_TRY(launch_pdl(k_trsv_fwd, dim3((unsigned)nblk), dim3(ST), SWSMEM, st, N, LD, ldm, s.b, s.y, s.binv, s.gf, s.tickets)));
     const double* tolp = (zero_tol < 0.0 && fwork) ? mds_factor_tol_ptr(fwork) : nullptr;
     MDS_LAUNCH(PC_SOLVE_D, st,
-               (k_dsolve<<<ge, 256, 0, st>>>(N, LD, ldm, piv, s.y, tolp, zero_tol < 0.0 ? 0.0 : zero_tol, status)));
+               MDS_CUDA_TRY(launch_pdl(k_dsolve, dim3(ge), dim3(256), 0, st, N, LD, ldm, piv, s.y, tolp, zero_tol < 0.0 ? 0.0 : zero_tol, status)));
     MDS_LAUNCH(PC_SOLVE_BWD, st,
-               (k_trsv_bwd<<<(unsigned)nblk, ST, SWSMEM, st>>>(N, LD, ldm, s.y, s.x, s.binv, s.gb, s.tickets + 1)));
-    MDS_LAUNCH(PC_SOLVE_SCATTER, st, (k_scatter<<<ge, 256, 0, st>>>(N, piv, s.x, dxy)));
+               MDS_CUDA_TRY(launch_pdl(k_trsv_bwd, dim3((unsigned)nblk), dim3(ST), SWSMEM, st, N, LD, ldm, s.y, s.x, s.binv, s.gb, s.tickets + 1)));
+    MDS_LAUNCH(PC_SOLVE_SCATTER, st, MDS_CUDA_TRY(launch_pdl(k_scatter, dim3(ge), dim3(256), 0, st, N, piv, s.x, dxy)));
   }
   if (plan && dx_s) {
     int64_t dims[5];
@@ -522,8 +537,8 @@ extern "C" int mds_solve(const mds_plan* plan, int64_t N, const double* LD, int6
       if (!w || !r_xs || (dims[4] > 0 && !js_val)) return MDS_ERR_ARG;
       const unsigned g = (unsigned)std::min<int64_t>(mds_cdiv(n_s, 256), 148 * 16);
       MDS_LAUNCH(PC_RECOVER, st,
-                 (k_recover<<<g, 256, 0, st>>>(n_s, mds_plan_rowptr(plan), mds_plan_colidx(plan), js_val, w, r_xs,
-                                               dxy + n_d, dx_s)));
+                 MDS_CUDA_TRY(launch_pdl(k_recover, dim3(g), dim3(256), 0, st, n_s, mds_plan_rowptr(plan),
+                                         mds_plan_colidx(plan), js_val, w, r_xs, dxy + n_d, dx_s)));
     }
   }
   return MDS_OK;

@@ -61,6 +61,8 @@ k_step_vectors(int64_t n, const double* __restrict__ x, const double* __restrict
                const double* __restrict__ dzl, const double* __restrict__ dzu,
                double tau, double mu, ResPtrs R, double* __restrict__ out, double* __restrict__ sigma,
                int32_t* status, double* __restrict__ partials, unsigned int* counter) {
+  pdl_wait();
+  pdl_trigger();
   Part P;
   P.ap = 1.0; P.ad = 1.0; P.cinf = 0.0; P.csum = 0.0; P.nc = 0.0; P.bad = LLONG_MAX;
 #pragma unroll
@@ -186,7 +188,7 @@ extern "C" int ipm_step_vectors(int64_t n, const double* x, const double* dx, co
   int grid = vec_grid(n);
   cudaStream_t st = (cudaStream_t)stream;
   MDS_LAUNCH(PC_VECTORS, st,
-             (k_step_vectors<<<grid, VT, 0, st>>>(n, x, dx, lo, up, zl, zu, dzl, dzu, tau, mu, R, out, sigma_out,
-                                                  status, partials, counter)));
+             MDS_CUDA_TRY(launch_pdl(k_step_vectors, dim3(grid), dim3(VT), 0, st, n, x, dx, lo, up, zl, zu, dzl, dzu, tau,
+                                     mu, R, out, sigma_out, status, partials, counter)));
   return MDS_OK;
 }
