@@ -96,3 +96,45 @@ def test_pivoting_heavy_multi_panel(N, n2):
     As = np.tril(A) + np.tril(A, -1).T
     assert np.abs(As @ x - b).max() / np.abs(b).max() <= 1e-10
     assert rel_inf(x, x_or) <= 1e-8
+
+
+# The factorization has several launch-structure variants chosen by size or
+# environment; each must give the same BK answer.  (Env knobs are read on every
+# mds_factor call.)  "odd ldm" disables the TMA path (16-byte alignment), so the
+# cp.async update kernel without look-ahead runs.
+@pytest.mark.parametrize("variant", ["tail_always", "tail_never", "no_lookahead", "no_tma", "odd_ldm", "no_pdl",
+                                     "static_sched", "upd_main", "inplace"])
+def test_factor_variants_pivoting(variant, monkeypatch):
+    env = {"tail_always": {"MDS_TAIL_ROWS": "100000000"}, "tail_never": {"MDS_TAIL_ROWS": "0"},
+           "no_lookahead": {"MDS_NO_LOOKAHEAD": "1"}, "no_tma": {"MDS_NO_TMA": "1"}, "odd_ldm": {},
+           "no_pdl": {"MDS_NO_PDL": "1"}, "static_sched": {"MDS_STATIC_SCHED": "1"},
+           "upd_main": {"MDS_UPD_MAIN": "1"}, "inplace": {"MDS_UPD_INPLACE": "1"}}[variant]
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    N, n2 = 1500, 300
+    A, ine = mdsgen.g3_prescribed(N, seed=7 * N, n2x2=n2)
+    b = np.random.default_rng(N + 1).standard_normal(N)
+    LD, ipiv, _ = oracle.bk_factor(A)
+    tol = oracle.default_tol(A)
+    x_or = oracle.bk_solve(LD, ipiv, b, tol)
+    ldm = N + 1 if variant == "odd_ldm" else N
+    M = torch.zeros(ldm * N, dtype=torch.float64, device="cuda")
+    host = np.zeros((N, ldm))
+    host[:, :N] = np.tril(A).T            # row j of host = column j of A (column-major M)
+    M.copy_(torch.as_tensor(host.reshape(-1)))
+    piv = torch.empty(2 * N, dtype=torch.int32, device="cuda")
+    ine_d = torch.zeros(3, dtype=torch.int64, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    fwork = torch.empty(mds.factor_workspace_size(N), dtype=torch.uint8, device="cuda")
+    swork = torch.empty(mds.solve_workspace_size(N), dtype=torch.uint8, device="cuda")
+    g_ine = mds.factor(N, M, ldm, piv, -1.0, ine_d, status, fwork, sync=True)
+    rhs = torch.as_tensor(b, dtype=torch.float64, device="cuda").contiguous()
+    x = torch.empty(N, dtype=torch.float64, device="cuda")
+    mds.solve(None, N, M, ldm, piv, rhs, None, None, None, x, None, -1.0, fwork, status, swork)
+    torch.cuda.synchronize()
+    x = x.cpu().numpy()
+    assert int(status.item()) == 0
+    assert g_ine == oracle.inertia(LD, ipiv, tol) == ine
+    As = np.tril(A) + np.tril(A, -1).T
+    assert np.abs(As @ x - b).max() / np.abs(b).max() <= 1e-10
+    assert rel_inf(x, x_or) <= 1e-8
