@@ -93,7 +93,16 @@ k_step_vectors(int64_t n, const double* __restrict__ x, const double* __restrict
   for (int j = 0; j < R.n; j++) {
     const double* v = R.p[j];
     double mx = 0.0;
-    for (int64_t i = tid; i < R.len[j]; i += nthr) mx = fmax(mx, fabs(v[i]));
+    if ((((uintptr_t)v) & 15) == 0) {
+      const int64_t h = R.len[j] / 2;
+      for (int64_t t = tid; t < h; t += nthr) {
+        const double2 q = reinterpret_cast<const double2*>(v)[t];
+        mx = fmax(mx, fmax(fabs(q.x), fabs(q.y)));
+      }
+      if (tid == 0 && (R.len[j] & 1)) mx = fmax(mx, fabs(v[R.len[j] - 1]));
+    } else {
+      for (int64_t i = tid; i < R.len[j]; i += nthr) mx = fmax(mx, fabs(v[i]));
+    }
     P.res[j] = mx;
   }
   // CTA reduction (fixed order)
@@ -135,25 +144,52 @@ k_step_vectors(int64_t n, const double* __restrict__ x, const double* __restrict
   }
   __syncthreads();
   if (!last) return;
-  // last CTA: fixed-order reduction over CTA partials (deterministic)
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const volatile double* pp = partials;
+  // last CTA: fixed-order tree reduction over the CTA partials (deterministic: the
+  // assignment of partials to threads and the combining tree depend only on the grid)
+  __threadfence();
+  {
     double q0 = 1.0, q1 = 1.0, q2 = 0.0, q3 = 0.0, q4 = 0.0;
     long long qb = LLONG_MAX;
     double qr[MAXRES];
+#pragma unroll
     for (int j = 0; j < MAXRES; j++) qr[j] = 0.0;
-    for (unsigned c = 0; c < gridDim.x; c++) {
-      const volatile double* my = pp + (size_t)c * NPART;
-      q0 = fmin(q0, my[0]); q1 = fmin(q1, my[1]); q2 = fmax(q2, my[2]); q3 += my[3]; q4 += my[4];
-      qb = min(qb, __double_as_longlong(my[5]));
-      for (int j = 0; j < MAXRES; j++) qr[j] = fmax(qr[j], my[6 + j]);
+    for (unsigned c = threadIdx.x; c < gridDim.x; c += VT) {
+      const double* my = partials + (size_t)c * NPART;
+      q0 = fmin(q0, __ldcg(my + 0)); q1 = fmin(q1, __ldcg(my + 1)); q2 = fmax(q2, __ldcg(my + 2));
+      q3 += __ldcg(my + 3); q4 += __ldcg(my + 4);
+      qb = min(qb, __double_as_longlong(__ldcg(my + 5)));
+#pragma unroll
+      for (int j = 0; j < MAXRES; j++) qr[j] = fmax(qr[j], __ldcg(my + 6 + j));
     }
-    out[0] = q0; out[1] = q1; out[2] = q2; out[3] = q3; out[4] = q4;
-    out[5] = (qb == LLONG_MAX) ? -1.0 : (double)qb;
-    for (int j = 0; j < R.n; j++) out[6 + j] = qr[j];
-    if (qb != LLONG_MAX) mds_set_status(status, MDS_ERR_NOT_INTERIOR);
-    *counter = 0u;   // leave the workspace reusable (graph replays)
+    q0 = warp_min(q0); q1 = warp_min(q1); q2 = warp_max(q2); q3 = warp_sum(q3); q4 = warp_sum(q4);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) qb = min(qb, (long long)__shfl_xor_sync(0xffffffffu, qb, o));
+#pragma unroll
+    for (int j = 0; j < MAXRES; j++) qr[j] = warp_max(qr[j]);
+    __syncthreads();
+    if (lane == 0) {
+      sh[warp][0] = q0; sh[warp][1] = q1; sh[warp][2] = q2; sh[warp][3] = q3; sh[warp][4] = q4;
+      shb[warp] = qb;
+#pragma unroll
+      for (int j = 0; j < MAXRES; j++) sh[warp][6 + j] = qr[j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double r0 = sh[0][0], r1 = sh[0][1], r2 = sh[0][2], r3 = sh[0][3], r4 = sh[0][4];
+      long long rb = shb[0];
+      double rr2[MAXRES];
+      for (int j = 0; j < MAXRES; j++) rr2[j] = sh[0][6 + j];
+      for (int w = 1; w < VT / 32; w++) {
+        r0 = fmin(r0, sh[w][0]); r1 = fmin(r1, sh[w][1]); r2 = fmax(r2, sh[w][2]);
+        r3 += sh[w][3]; r4 += sh[w][4]; rb = min(rb, shb[w]);
+        for (int j = 0; j < MAXRES; j++) rr2[j] = fmax(rr2[j], sh[w][6 + j]);
+      }
+      out[0] = r0; out[1] = r1; out[2] = r2; out[3] = r3; out[4] = r4;
+      out[5] = (rb == LLONG_MAX) ? -1.0 : (double)rb;
+      for (int j = 0; j < R.n; j++) out[6 + j] = rr2[j];
+      if (rb != LLONG_MAX) mds_set_status(status, MDS_ERR_NOT_INTERIOR);
+      *counter = 0u;   // leave the workspace reusable (graph replays)
+    }
   }
 }
 
