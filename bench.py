@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -164,9 +164,42 @@ def oracle_sample(prob, sv, ns_factor, reps=1):
                       sample=sample)
 
 
+def run_reference_c5(args):
+    import mdsgen
+    import oracle
+    N = 32768
+    ns = min(args.ref_sample, 2048)
+    A, _ = mdsgen.g3_prescribed(ns, seed=5005)   # same family, bounded size (the 8.6 GB matrix is GPU-generated)
+    projs = []
+    wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        LD, ipiv, _ = oracle.bk_factor(A)
+        tf = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        oracle.bk_solve(LD, ipiv, np.ones(ns), oracle.default_tol(A))
+        ts = time.perf_counter() - t0
+        projs.append(tf * (N / ns) ** 3 + ts * (N / ns) ** 2)
+    t_step = float(np.mean(projs))
+    val = 1.0 / t_step
+    sample = (f"oracle (plain C, 1 thread) BK factor+solve of a {ns}x{ns} G3 matrix, extrapolated x(N/{ns})^3 / "
+              f"x(N/{ns})^2 to N={N}")
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "factor_solve/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C5 " + CONFIG_DESC["C5"], "N": N},
+            "cpu_baseline": {"value": val, "unit": "factor_solve/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": "factor_solve/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": time.perf_counter() - wall0}
+    print(json.dumps(line), flush=True)
+
+
 def run_reference(args, rank, world):
     import mdsgen
     if rank != 0:
+        return
+    if args.config == "C5":
+        run_reference_c5(args)
         return
     prob = mdsgen.config_problem(args.config)
     sv = mdsgen.step_vectors_for(prob, seed=7)
@@ -197,6 +230,7 @@ CONFIG_DESC = {
     "C2": "synthetic MDS N=n_d+m=1024, n_s=100k, CSR J_s ~5 nnz/row, one Newton step",
     "C3": "ACOPF-shaped MDS N=n_d+m=8192 (n_d=4096, m_E=m_I=2048), n_s=1M, ~5 nnz/row, one Newton step",
     "C4": "SCOPF scenario N=2048, n_s=131072 (single scenario)",
+    "C5": "dense prescribed-spectrum symmetric indefinite N=n_d+m=32768 (8.6 GB), FP64 LDL^T factor+solve stress",
 }
 
 
@@ -438,6 +472,129 @@ def run_scopf(args, rank, world):
         print(json.dumps(line), flush=True)
 
 
+def run_c5(args, rank, world):
+    """C5 stress: factor + solve of the N = 32768 G3 matrix (8.6 GB) per step (replicas under torchrun).
+    M is restored from a device copy before every step, outside the timed region (CUDA events bracket
+    exactly mds_factor + mds_solve)."""
+    import torch
+    import torch.distributed as dist
+
+    import mdsgen
+    import paper_2605_13736_b200 as mds
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    N = 32768
+    A, ine = mdsgen.g3_prescribed_torch(N, seed=5005, device=dev)
+    A0 = A.T.contiguous().reshape(-1)          # column-major copy of the input
+    del A
+    M = torch.empty_like(A0)
+    piv = torch.empty(2 * N, dtype=torch.int32, device=dev)
+    ine_d = torch.zeros(3, dtype=torch.int64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    fwork = torch.empty(mds.factor_workspace_size(N), dtype=torch.uint8, device=dev)
+    swork = torch.empty(mds.solve_workspace_size(N), dtype=torch.uint8, device=dev)
+    b = torch.as_tensor(np.random.default_rng(N).standard_normal(N), dtype=torch.float64, device=dev)
+    x = torch.empty(N, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def fs():
+        mds.factor(N, M, N, piv, -1.0, ine_d, status, fwork, sync=False)
+        mds.solve(None, N, M, N, piv, b, None, None, None, x, None, -1.0, fwork, status, swork)
+
+    launches0 = mds.launch_count()
+    M.copy_(A0)
+    fs()
+    torch.cuda.synchronize()
+    launches_per_step = mds.launch_count() - launches0
+    got = tuple(int(v) for v in ine_d.cpu())
+    if int(status.item()) != 0 or got != ine:
+        raise SystemExit(f"bench C5: status={int(status.item())} inertia={got} expected={ine}")
+    for _ in range(max(args.warmup - 1, 0)):
+        M.copy_(A0)
+        fs()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(dev.index) as clk:
+        for e0, e1 in evs:
+            M.copy_(A0)
+            e0.record(stream)
+            fs()
+            e1.record(stream)
+        torch.cuda.synchronize()
+    ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+    clocks = clk.summary()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = world * args.steps / (ms_max / 1e3)
+    flops = N ** 3 / 3.0 + 2.0 * N * N
+    # profiled pass: update-kernel share and its achieved FP64 rate
+    M.copy_(A0)
+    mds.profile_begin()
+    fs()
+    prof = mds.profile_end()
+    panels = mds.factor_panels(fwork, N)
+    upd = 0
+    ends = list(panels[1:]) + [N]
+    for s0, e in zip(panels, ends):
+        n2 = N - int(e)
+        upd += n2 * (n2 + 1) * (int(e) - int(s0))
+    peak_dmma, peak_cublas = fp64_peak()
+    upd_ms, upd_n = prof["update"]
+    ach = upd / (upd_ms * 1e-3) / 1e12
+    roof = {"kernel": "k_update (DMMA trailing update)", "bound": "tensor", "achieved": ach, "peak": peak_dmma,
+            "unit": "TFLOP/s", "frac": ach / peak_dmma, "traffic": None,
+            "peak_source": "measured FP64 DMMA ceiling, profiles/fp64_peaks_r01.json", "launches": upd_n}
+    # end to end: the matrix from pinned host memory, x back
+    e2e = None
+    if not args.no_e2e:
+        hA = torch.empty(A0.shape, dtype=A0.dtype, pin_memory=True).copy_(A0.cpu())
+        hx = torch.empty(N, dtype=torch.float64, pin_memory=True)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            M.copy_(hA, non_blocking=True)
+            fs()
+            hx.copy_(x, non_blocking=True)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        e2e = {"value": args.steps / (f0.elapsed_time(f1) / 1e3) * world, "unit": "factor_solve/s",
+               "h2d_bytes_per_step": int(hA.numel() * 8), "d2h_bytes_per_step": int(N * 8)}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle
+        ns = min(args.ref_sample, 2048)
+        Ah = A0.reshape(N, N)[:ns, :ns].cpu().numpy().T.copy(order="F")
+        t0 = time.perf_counter()
+        LD, ipiv, _ = oracle.bk_factor(Ah)
+        tf = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        oracle.bk_solve(LD, ipiv, np.ones(ns), oracle.default_tol(Ah))
+        tsol = time.perf_counter() - t0
+        proj = tf * (N / ns) ** 3 + tsol * (N / ns) ** 2
+        cpu = {"value": 1.0 / proj, "unit": "factor_solve/s", "cores": 1, "kind": "oracle",
+               "sample": f"oracle (plain C, 1 thread) BK factor+solve of the leading {ns}x{ns} block, extrapolated "
+                         f"x(N/{ns})^3 / x(N/{ns})^2; measured {tf + tsol:.2f} s"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "factor_solve/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "C5 " + CONFIG_DESC["C5"], "N": N, "parallelism": "replicas" if world > 1 else "single",
+                           "l2": "inputs larger than L2 (M is 8.6 GB)", "cuda_graph": False},
+                "gpu_launches": launches_per_step * args.steps, "roofline": roof,
+                "factor_solve_fp64_tflops": flops / (ms_step * 1e-3) / 1e12,
+                "factor_solve_frac_of_peak": flops / (ms_step * 1e-3) / 1e12 / peak_dmma,
+                "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu, "inertia": list(got),
+                "kernels_ms": {c: round(v[0], 3) for c, v in prof.items() if v[1]},
+                "panels": len(panels)}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -454,6 +611,8 @@ def main():
         dist.init_process_group("nccl")
     if args.config == "C4":
         run_scopf(args, rank, world)
+    elif args.config == "C5":
+        run_c5(args, rank, world)
     else:
         run_ours(args, rank, world)
     if world > 1:

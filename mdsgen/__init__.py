@@ -238,6 +238,52 @@ def g3_prescribed(N, seed, n2x2=None, n_reflectors=8):
     return np.asfortranarray(B), (pos, 0, neg)
 
 
+def g3_prescribed_torch(N, seed, n2x2=None, n_reflectors=8, device="cuda"):
+    """G3 built with torch on `device` (the C5 size, 8.6 GB, is impractical in
+    numpy): the same random draws in the same order as g3_prescribed, the same
+    reflectors, the same final symmetrisation.  Returns (M as a torch (N, N)
+    float64 tensor, (pos, zero, neg))."""
+    import torch
+    rng = np.random.default_rng(seed)
+    if n2x2 is None:
+        n2x2 = N // 8
+    n1 = N - 2 * n2x2
+    sign = rng.choice([-1.0, 1.0], size=n1)
+    lam = sign * 10.0 ** rng.uniform(0.0, 3.0, n1)
+    pos = int((lam > 0).sum()) + n2x2
+    neg = int((lam < 0).sum()) + n2x2
+    diag = np.zeros(N)
+    off = np.zeros(N)            # off[i] = B[i, i+1] = B[i+1, i]
+    diag[:n1] = lam
+    i = n1
+    for t in range(n2x2):
+        e1, e2 = rng.uniform(-0.1, 0.1, 2)
+        diag[i], diag[i + 1] = e1, e2
+        off[i] = 1.0
+        i += 2
+    p = rng.permutation(N)
+    f64 = dict(dtype=torch.float64, device=device)
+    B = torch.zeros((N, N), **f64)
+    idx = torch.arange(N, device=device)
+    B[idx, idx] = torch.as_tensor(diag, **f64)
+    j = torch.as_tensor(np.nonzero(off)[0], device=device)
+    B[j, j + 1] = 1.0
+    B[j + 1, j] = 1.0
+    pt = torch.as_tensor(p, device=device)
+    B = B[pt][:, pt]
+    for _ in range(n_reflectors):
+        v = rng.standard_normal(N)
+        v /= np.linalg.norm(v)
+        vt = torch.as_tensor(v, **f64)
+        Bv = B @ vt
+        vBv = float(vt @ Bv)
+        B.addr_(vt, Bv, alpha=-2.0)
+        B.addr_(Bv, vt, alpha=-2.0)
+        B.addr_(vt, vt, alpha=4.0 * vBv)
+    B = 0.5 * (B + B.T)
+    return B, (pos, 0, neg)
+
+
 def g4_random_symmetric(N, seed, shrink_diag=False):
     """G4: B + B^T (inertia by eigvalsh in tests); optional shrunken diagonal to force 2x2 pivots."""
     rng = np.random.default_rng(seed)

@@ -2000,9 +2000,11 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_factor_finalize, 256, 0);
-    // a small cooperative grid (grid-stride loops): co-resident even while other
-    // streams' factorizations occupy most SMs (SCOPF batches)
-    int blocks = std::min(32, sms * std::max(1, std::min(occ, 2)));
+    // cooperative grid (grid-stride loops): the whole GPU for a lone factorization (the
+    // row-interchange pass moves O(N^2) data when pivoting is heavy), a small grid when
+    // several factorizations share the GPU (grid cap set: SCOPF batches)
+    int blocks = (g_grid_cap > 0) ? std::min(32, sms * std::max(1, std::min(occ, 2)))
+                                  : sms * std::max(1, std::min(occ, 4));
     void* args[] = {&N, &M, &ldm, &f, &piv, &inertia_dev};
     MDS_LAUNCH(PC_FINALIZE, st,
                MDS_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_factor_finalize, blocks, 256, args, 0, st)));

@@ -138,3 +138,26 @@ def test_factor_variants_pivoting(variant, monkeypatch):
     As = np.tril(A) + np.tril(A, -1).T
     assert np.abs(As @ x - b).max() / np.abs(b).max() <= 1e-10
     assert rel_inf(x, x_or) <= 1e-8
+
+
+def test_c5_factor_solve_32768():
+    # C5: N = 32768 prescribed-spectrum indefinite matrix (8.6 GB), factor + solve in the
+    # launch configuration bench.py --config C5 times; inertia against the closed form,
+    # the solve through the residual of the original system (the oracle cannot run at this size)
+    N = 32768
+    A, ine = mdsgen.g3_prescribed_torch(N, seed=5005, device="cuda")
+    M = A.T.contiguous().reshape(-1)          # column-major (A is symmetric; lower used)
+    piv = torch.empty(2 * N, dtype=torch.int32, device="cuda")
+    ine_d = torch.zeros(3, dtype=torch.int64, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    fwork = torch.empty(mds.factor_workspace_size(N), dtype=torch.uint8, device="cuda")
+    swork = torch.empty(mds.solve_workspace_size(N), dtype=torch.uint8, device="cuda")
+    g_ine = mds.factor(N, M, N, piv, -1.0, ine_d, status, fwork, sync=True)
+    b = torch.as_tensor(np.random.default_rng(N).standard_normal(N), dtype=torch.float64, device="cuda")
+    x = torch.empty(N, dtype=torch.float64, device="cuda")
+    mds.solve(None, N, M, N, piv, b, None, None, None, x, None, -1.0, fwork, status, swork)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 0
+    assert g_ine == ine
+    res = float((A @ x - b).abs().max() / b.abs().max())
+    assert res <= 1e-10, res
