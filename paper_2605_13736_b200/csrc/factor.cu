@@ -43,6 +43,9 @@ namespace cg = cooperative_groups;
 namespace {
 constexpr int NB = 64;              // panel width
 constexpr int WCOLS = NB + 1;       // W work panel columns (+1 for the 2x2 candidate)
+constexpr int XT = 512;             // threads per CTA of the multi-CTA exact panel (k_panel_exact)
+constexpr int XMAXG = 256;          // its maximum grid
+constexpr int XROWS = XT / 4;       // rows per CTA pass (a quad of threads per row)
 constexpr double ALPHA_BK = 0.64038820320220756872767623199676;  // (1+sqrt(17))/8
 
 struct FCtl {
@@ -77,6 +80,9 @@ struct FWork {
   unsigned long long* ucount;   // [3(N+2)] per-panel tile counters: [3q] rest/full update, [3q+1] next-panel
                                 //   update, [3q+2] F2 tiles of panel q (claimed by k_panel_trsm and k_update_tma<3, true>)
   unsigned* t1flag;             // [2(N/64+4)] p+1 once panel p's update of tile (row BI, column b0+c) has landed
+  unsigned* xbar;               // [N/32+8] per-panel grid-barrier counters of k_panel_exact
+  ArgMax* xpart;                // [2 banks][XMAXG] its per-CTA argmax partials (bank = barrier parity)
+  double* xaux;                 // [2] |W(imax, candidate column)| published by the owner of row imax
   const double* Wprev;          // the previous panel's W / Lb (the other parity buffers), for the
   const double* Lbprev;         //   deferred update of this panel's columns
   int fuse;           // 1: this panel's columns still lack the previous panel's update (look-ahead)
@@ -107,6 +113,9 @@ FWork carve(void* work, int64_t N, size_t* total) {
   f.pinfo = reinterpret_cast<int2*>(take(sizeof(int2) * (N + 2)));
   f.ucount = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * 3 * (N + 2)));
   f.t1flag = reinterpret_cast<unsigned*>(take(sizeof(unsigned) * 2 * (N / 64 + 4)));
+  f.xbar = reinterpret_cast<unsigned*>(take(sizeof(unsigned) * (N / 32 + 8)));
+  f.xpart = reinterpret_cast<ArgMax*>(take(sizeof(ArgMax) * 2 * XMAXG));
+  f.xaux = reinterpret_cast<double*>(take(sizeof(double) * 2));
   f.Wprev = f.W1;
   f.Lbprev = f.Lb1;
   f.fuse = 0;
@@ -137,6 +146,7 @@ __global__ void k_factor_init(int64_t N, FWork f, double zero_tol) {
   for (int64_t i = gtid; i < N; i += gth) { f.sw[i] = -1; f.bt[i] = 0; f.rowsum[i] = 0.0; }
   for (int64_t i = gtid; i < 3 * (N + 2); i += gth) f.ucount[i] = 0ull;
   for (int64_t i = gtid; i < 2 * (N / 64 + 4); i += gth) f.t1flag[i] = 0u;
+  for (int64_t i = gtid; i < N / 32 + 8; i += gth) f.xbar[i] = 0u;
   if (blockIdx.x == 0) {
     int* c = reinterpret_cast<int*>(f.ctl);
     for (int i = threadIdx.x; i < (int)(sizeof(FCtl) / sizeof(int)); i += blockDim.x) c[i] = 0;
@@ -1093,6 +1103,269 @@ __global__ void __launch_bounds__(1024) k_panel_slow(int64_t N, double* __restri
   zero_w_tail(N, k0, j, f);
 }
 
+// F4, multi-CTA: the same acceptance + exact dlasyf panel as k_panel_slow, but
+// the per-column work (two GEMVs against the panel's finished columns, the
+// column/row argmax, the interchange and the scaling) is spread over G CTAs
+// that each own a contiguous block of rows [k0, N); the BK decisions need the
+// global column max, so CTAs meet at a grid barrier after each argmax (every
+// CTA then takes the same decision from the same partials, in fixed order) and
+// once more after an interchange.  One CTA did one column in ~55 us at
+// N = 32768 (the GEMVs stream ~4-8 MB of L2 each); this takes a few us.
+// All CTAs must be co-resident: G <= the SM count, launched only after the
+// trailing update it depends on has finished (its successors are launched
+// programmatically after every CTA here has started).  Cross-CTA data is read
+// with ld.global.cg (L2), never through L1.
+// Grid barrier + argmax exchange: every CTA stores its partial (v, i) in its
+// slot of the bank of this barrier's parity, then arrives on the panel's
+// counter (release) and thread 0 spins until all G CTAs have arrived
+// (acquire); the G partials are then reduced in fixed order by every CTA.
+// (A variant where every CTA polled all G tagged records was slower: 128x
+// more pollers on L2.)  Banks alternate by barrier parity, so a CTA that runs
+// ahead never overwrites a partial another CTA has yet to read.
+__device__ __forceinline__ ArgMax x_exchange(unsigned* ctr, ArgMax* part, unsigned& nbar, ArgMax mine, ArgMax* sh) {
+  ArgMax* bank = part + XMAXG * (nbar & 1u);
+  if (threadIdx.x == 0) bank[blockIdx.x] = mine;
+  __syncthreads();   // every global write of this CTA precedes the release below
+  nbar++;
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
+    const unsigned target = nbar * gridDim.x;
+    while (ld_acquire_u32(ctr) < target) {
+    }
+  }
+  __syncthreads();
+  ArgMax a{-1.0, 0x7fffffff};
+  for (int c = threadIdx.x; c < (int)gridDim.x; c += blockDim.x)
+    a = am_better(a, ArgMax{__ldcg(&bank[c].v), __ldcg(&bank[c].i)});
+  return block_argmax(a, sh);
+}
+
+// own rows r in [rlo, rhi), r >= k:  W(r, wcol) = a_r - sum_{t<j} Lb(r, t) wv[t], with
+// a_r = A(r, kc) (column kc; for IMAX the row/column kc = imax of the lower triangle);
+// a quad of threads per row (t strided by 4, fixed-order shuffle sum).  Returns the CTA's
+// argmax of |W(r, wcol)| over r > k (column) or r != kc (IMAX).
+template <bool IMAX>
+__device__ __forceinline__ ArgMax x_gemv(const double* A, int64_t lda, const double* Lb, double* W, int64_t ldw,
+                                         int64_t rlo, int64_t rhi, int64_t k, int64_t kc, int j, int wcol,
+                                         const double* wv, double* aux) {
+  const int tid = threadIdx.x, qd = tid & 3;
+  ArgMax am{-1.0, 0x7fffffff};
+  const int64_t rfirst = rlo + ((k > rlo) ? ((k - rlo) / XROWS) * XROWS : 0);
+  for (int64_t rb = rfirst; rb < rhi; rb += XROWS) {
+    const int64_t r = rb + (tid >> 2);
+    const bool live = r < rhi && r >= k;
+    double s0 = 0.0, s1 = 0.0;
+    if (live) {
+      const double* lr = Lb + r;
+      int t = qd;
+      for (; t + 4 < j; t += 8) {
+        s0 = fma(__ldcg(lr + (int64_t)t * ldw), wv[t], s0);
+        s1 = fma(__ldcg(lr + (int64_t)(t + 4) * ldw), wv[t + 4], s1);
+      }
+      if (t < j) s0 = fma(__ldcg(lr + (int64_t)t * ldw), wv[t], s0);
+    }
+    double s = s0 + s1;
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if (live && qd == 0) {
+      const double a = IMAX ? ((r < kc) ? __ldcg(&A[kc + r * lda]) : __ldcg(&A[r + kc * lda])) : __ldcg(&A[r + kc * lda]);
+      const double v = a - s;
+      W[r + wcol * ldw] = v;
+      if (IMAX ? (r != kc) : (r > k)) am = am_better(am, ArgMax{fabs(v), (int)r});
+      if (IMAX && r == kc) *aux = fabs(v);
+    }
+  }
+  return am;
+}
+
+__global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restrict__ A, int64_t lda, FWork f,
+                                                    int32_t* piv) {
+  pdl_wait();
+  pdl_trigger();
+  FCtl* ctl = f.ctl;
+  if (ctl->abort) return;
+  const int nbp = ctl->nbp;
+  const int64_t k0 = ctl->k0;
+  const int tid = threadIdx.x;
+  const bool c0 = (blockIdx.x == 0);
+  if (nbp == 0) {
+    if (c0 && tid == 0) f.pinfo[f.pidx] = make_int2((int)k0, 0);
+    return;
+  }
+  // ---- accepted prefix (every CTA computes p; CTA 0 records it)
+  __shared__ unsigned s_fail[2], s_pos[2], s_neg[2];
+  if (tid < NB) {
+    const int jj = tid;
+    const double dj = (jj < nbp) ? ctl->d[jj] : 0.0;
+    const double cm = (jj < nbp) ? bitsd(ctl->colmax[jj]) : 0.0;
+    const bool fail = (jj >= nbp) || !(fabs(dj) >= ALPHA_BK * cm);
+    const double tol = ctl->tol;
+    const unsigned b = __ballot_sync(0xffffffffu, fail);
+    const unsigned bp = __ballot_sync(0xffffffffu, dj > tol);
+    const unsigned bn = __ballot_sync(0xffffffffu, dj < -tol);
+    if ((jj & 31) == 0) { s_fail[jj >> 5] = b; s_pos[jj >> 5] = bp; s_neg[jj >> 5] = bn; }
+  }
+  __syncthreads();
+  const int p = s_fail[0] ? (__ffs(s_fail[0]) - 1) : (s_fail[1] ? 32 + __ffs(s_fail[1]) - 1 : NB);
+  if (c0) {
+    if (tid < p) piv[k0 + tid] = (int32_t)(k0 + tid + 1);
+    if (tid == 0 && p > 0) {
+      const unsigned long long m = (p >= 64) ? ~0ull : ((1ull << p) - 1ull);
+      const unsigned long long pos = ((unsigned long long)s_pos[1] << 32 | s_pos[0]) & m;
+      const unsigned long long neg = ((unsigned long long)s_neg[1] << 32 | s_neg[0]) & m;
+      const int np = __popcll(pos), nn = __popcll(neg);
+      ctl->inertia[0] += np;
+      ctl->inertia[2] += nn;
+      ctl->inertia[1] += p - np - nn;
+    }
+  }
+  int j = p;
+  const bool last = (k0 + nbp >= N);
+  const int jlim = last ? nbp : nbp - 1;
+  double* W = f.W;
+  double* Lb = f.Lb;
+  const int64_t ldw = f.ldw;
+  if (j < jlim) {
+    __shared__ double wrow[WCOLS];
+    __shared__ ArgMax sh[33];
+    const double tol = ctl->tol;
+    const int G = (int)gridDim.x;
+    const int64_t chunk = ((N - k0 + G - 1) / G + 31) / 32 * 32;
+    const int64_t rlo = k0 + (int64_t)blockIdx.x * chunk;
+    const int64_t rhi = (rlo + chunk < N) ? rlo + chunk : N;
+    unsigned* ctr = f.xbar + f.pidx;   // this panel's barrier counter (zeroed by k_factor_init)
+    unsigned nbar = 0;                 // barriers so far
+    while (j < jlim) {
+      const int64_t k = k0 + j;
+      for (int t = tid; t < j; t += XT) wrow[t] = __ldcg(&W[k + t * ldw]);
+      __syncthreads();
+      // W(k:N, j) = A(k:N, k) - L(k:N, panel) W(k, panel)^T ; colmax / imax below k
+      ArgMax am = x_gemv<false>(A, lda, Lb, W, ldw, rlo, rhi, k, k, j, j, wrow, nullptr);
+      am = block_argmax(am, sh);
+      am = x_exchange(ctr, f.xpart, nbar, am, sh);
+      const double absakk = fabs(__ldcg(&W[k + j * ldw]));
+      const double colmax = (am.v < 0.0) ? 0.0 : am.v;
+      const int64_t imax = (am.v < 0.0) ? k : am.i;
+      int kstep = 1;
+      int64_t kp = k;
+      bool zero = false, cand = false;   // cand: the pivot column is W(:, j+1) (1x1 with kp = imax)
+      if (fmax(absakk, colmax) == 0.0) {
+        zero = true;
+      } else if (absakk >= ALPHA_BK * colmax) {
+        kp = k;
+      } else {
+        for (int t = tid; t < j; t += XT) wrow[t] = __ldcg(&W[imax + t * ldw]);
+        __syncthreads();
+        // candidate column imax, updated: W(k:N, j+1); |W(imax, j+1)| published by its owner
+        const unsigned sl = nbar & 1u;
+        ArgMax rm = x_gemv<true>(A, lda, Lb, W, ldw, rlo, rhi, k, imax, j, j + 1, wrow, f.xaux + sl);
+        rm = block_argmax(rm, sh);
+        rm = x_exchange(ctr, f.xpart, nbar, rm, sh);
+        const double rowmax = (rm.v < 0.0) ? 0.0 : rm.v;
+        const double wii = __ldcg(f.xaux + sl);
+        if (absakk >= ALPHA_BK * colmax * (colmax / rowmax)) {
+          kp = k;
+        } else if (wii >= ALPHA_BK * rowmax) {
+          kp = imax;
+          cand = true;
+        } else {
+          kp = imax;
+          kstep = 2;
+        }
+      }
+      const int64_t kk = k + kstep - 1;
+      if (kp != kk) {
+        // symmetric interchange kk <-> kp of the not-yet-factored part: owners of rows r
+        for (int64_t r = rlo + tid; r < rhi; r += XT) {
+          if (r <= kk) continue;
+          if (r < kp) A[kp + r * lda] = __ldcg(&A[r + kk * lda]);
+          else if (r > kp) A[r + kp * lda] = __ldcg(&A[r + kk * lda]);
+          // 1x1 with kp = imax: the pivot column is the candidate column (rows kk, kp: below)
+          if (cand && r != kp) W[r + j * ldw] = __ldcg(&W[r + (j + 1) * ldw]);
+        }
+        if (c0) {
+          if (tid == 0) { A[kp + kp * lda] = __ldcg(&A[kk + kk * lda]); f.sw[kk] = (int)kp; ctl->nswap += 1; }
+          // rows kk <-> kp of the panel's finished L columns and of W (column j from the candidate if cand)
+          const int nl = (int)(kk - k0), nw = (int)(kk - k0) + 1;
+          for (int c = tid; c < nl + nw; c += XT) {
+            if (c < nl) {
+              const double a = __ldcg(&Lb[kk + c * ldw]), b = __ldcg(&Lb[kp + c * ldw]);
+              Lb[kk + c * ldw] = b;
+              Lb[kp + c * ldw] = a;
+            } else {
+              const int t = c - nl;
+              const int ts = (cand && t == j) ? j + 1 : t;
+              const double a = __ldcg(&W[kk + ts * ldw]), b = __ldcg(&W[kp + ts * ldw]);
+              W[kk + t * ldw] = b;
+              W[kp + t * ldw] = a;
+            }
+          }
+        }
+        x_exchange(ctr, f.xpart, nbar, ArgMax{-1.0, 0x7fffffff}, sh);
+      }
+      if (kstep == 1) {
+        const double d = __ldcg(&W[k + j * ldw]);
+        const double r1 = zero ? 0.0 : 1.0 / d;
+        for (int64_t r = rlo + tid; r < rhi; r += XT) {
+          if (r <= k) continue;
+          const double w = __ldcg(&W[r + j * ldw]);
+          Lb[r + j * ldw] = zero ? w : w * r1;
+        }
+        if (c0 && tid == 0) {
+          Lb[k + j * ldw] = d;
+          if (d > tol) ctl->inertia[0]++;
+          else if (d < -tol) ctl->inertia[2]++;
+          else ctl->inertia[1]++;
+          piv[k] = (int32_t)(kp + 1);
+          f.bt[k] = 0;
+        }
+      } else {
+        const double w21 = __ldcg(&W[(k + 1) + j * ldw]);
+        const double w22 = __ldcg(&W[(k + 1) + (j + 1) * ldw]);
+        const double w11 = __ldcg(&W[k + j * ldw]);
+        double d21 = w21;
+        const double d11 = w22 / d21;
+        const double d22 = w11 / d21;
+        const double tt = 1.0 / (d11 * d22 - 1.0);
+        d21 = tt / d21;
+        for (int64_t r = rlo + tid; r < rhi; r += XT) {
+          if (r < k + 2) continue;
+          const double wk = __ldcg(&W[r + j * ldw]), wk1 = __ldcg(&W[r + (j + 1) * ldw]);
+          Lb[r + j * ldw] = d21 * (d11 * wk - wk1);
+          Lb[r + (j + 1) * ldw] = d21 * (d22 * wk1 - wk);
+        }
+        if (c0 && tid == 0) {
+          Lb[k + j * ldw] = w11;
+          Lb[(k + 1) + j * ldw] = w21;             // D21 (moved to the upper slot at finalize)
+          Lb[(k + 1) + (j + 1) * ldw] = w22;
+          ctl->inertia[0]++;
+          ctl->inertia[2]++;
+          piv[k] = piv[k + 1] = (int32_t)(-(kp + 1));
+          f.bt[k] = 1;
+          f.bt[k + 1] = 2;
+        }
+      }
+      __syncthreads();
+      j += kstep;
+    }
+  }
+  if (c0 && tid == 0) {
+    ctl->kb = j;
+    f.pinfo[f.pidx] = make_int2((int)k0, j);
+  }
+  // W / Lb columns [j, NB) of rows >= k0 must be exactly zero for the TMA update (grid-strided)
+  const int64_t nr = N - k0;
+  const int nc = NB - j;
+  if (nr > 0 && nc > 0) {
+    const int64_t gt = (int64_t)blockIdx.x * XT + tid, gs = (int64_t)gridDim.x * XT;
+    for (int64_t idx = gt; idx < nr * nc; idx += gs) {
+      const int64_t r = k0 + idx % nr, c = j + idx / nr;
+      f.W[r + c * ldw] = 0.0;
+      f.Lb[r + c * ldw] = 0.0;
+    }
+  }
+}
+
 // Copy the finished panel (D + L columns, rows >= the diagonal) from Lb into M.
 __global__ void __launch_bounds__(256) k_panel_store(int64_t N, double* __restrict__ A, int64_t lda, FWork f) {
   if (f.ctl->abort) return;
@@ -1896,6 +2169,17 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   };
   auto rows_of = [&](int64_t p) { return N - std::min<int64_t>(p * (NB - 1), N); };   // upper bound
   const int reserve = capped ? std::max(1, sms / 8) : 1;   // SMs left to the panel chain (F1)
+  // F4 (acceptance + exact BK columns): multi-CTA, ~256 rows per CTA, all CTAs co-resident
+  static const bool f4_one_cta = std::getenv("MDS_SLOW_1CTA") != nullptr;   // A/B: the single-CTA k_panel_slow
+  auto launch_f4 = [&](const FWork& fp, int64_t rows) -> int {
+    if (f4_one_cta) {
+      MDS_LAUNCH(PC_PANEL_SLOW, st, MDS_CUDA_TRY(launch_pdl(k_panel_slow, dim3(1), dim3(1024), 0, st, N, M, ldm, fp, piv)));
+      return MDS_OK;
+    }
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>({mds_cdiv(rows, 256), (int64_t)sms, (int64_t)XMAXG}));
+    MDS_LAUNCH(PC_PANEL_SLOW, st, MDS_CUDA_TRY(launch_pdl(k_panel_exact, dim3(g), dim3(XT), 0, st, N, M, ldm, fp, piv)));
+    return MDS_OK;
+  };
   if (lookahead) {
     // Stream roles.  Update-bound panels: U(p) runs on the main stream right after
     // F4(p) (no cross-stream hop on the critical path) and F1(p+1) on the side
@@ -1927,7 +2211,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
       } else if (p > 0) {
         MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(p - 1, 1), 0));   // U(p-1) on the side stream
       }
-      MDS_LAUNCH(PC_PANEL_SLOW, st, MDS_CUDA_TRY(launch_pdl(k_panel_slow, dim3(1), dim3(1024), 0, st, N, M, ldm, fp, piv)));
+      if (int rc = launch_f4(fp, rows)) return rc;
       MDS_CUDA_TRY(cudaEventRecord(ev(p, 0), st));
       const int64_t n2max = std::max<int64_t>(rows - 1, 0);
       const int64_t nt = mds_cdiv(n2max, UT) + 1;
@@ -1974,7 +2258,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
       const int64_t nt = mds_cdiv(n2max, UT) + 1;
       MDS_LAUNCH(PC_PANEL_DIAG, st, (k_panel_diag<<<1, 256, F1SMEM, st>>>(N, M, ldm, fp)));
       MDS_LAUNCH(PC_PANEL_TRSM, st, (k_panel_trsm<<<g64, 128, usmem, st>>>(N, M, ldm, fp)));
-      MDS_LAUNCH(PC_PANEL_SLOW, st, (k_panel_slow<<<1, 1024, 0, st>>>(N, M, ldm, fp, piv)));
+      if (int rc = launch_f4(fp, rows)) return rc;
       const CUtensorMap& mw = (p & 1) ? mapW1 : mapW;
       const CUtensorMap& ml = (p & 1) ? mapL1 : mapL0;
       MDS_LAUNCH(PC_PANEL_STORE, st, (k_panel_store<<<dim3(g256, 8), 256, 0, st>>>(N, M, ldm, fp)));

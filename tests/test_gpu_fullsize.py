@@ -103,12 +103,13 @@ def test_pivoting_heavy_multi_panel(N, n2):
 # mds_factor call.)  "odd ldm" disables the TMA path (16-byte alignment), so the
 # cp.async update kernel without look-ahead runs.
 @pytest.mark.parametrize("variant", ["tail_always", "tail_never", "no_lookahead", "no_tma", "odd_ldm", "no_pdl",
-                                     "static_sched", "upd_main", "inplace"])
+                                     "static_sched", "upd_main", "inplace", "slow_1cta"])
 def test_factor_variants_pivoting(variant, monkeypatch):
     env = {"tail_always": {"MDS_TAIL_ROWS": "100000000"}, "tail_never": {"MDS_TAIL_ROWS": "0"},
            "no_lookahead": {"MDS_NO_LOOKAHEAD": "1"}, "no_tma": {"MDS_NO_TMA": "1"}, "odd_ldm": {},
            "no_pdl": {"MDS_NO_PDL": "1"}, "static_sched": {"MDS_STATIC_SCHED": "1"},
-           "upd_main": {"MDS_UPD_MAIN": "1"}, "inplace": {"MDS_UPD_INPLACE": "1"}}[variant]
+           "upd_main": {"MDS_UPD_MAIN": "1"}, "inplace": {"MDS_UPD_INPLACE": "1"},
+           "slow_1cta": {"MDS_SLOW_1CTA": "1"}}[variant]
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     N, n2 = 1500, 300
@@ -138,6 +139,28 @@ def test_factor_variants_pivoting(variant, monkeypatch):
     As = np.tril(A) + np.tril(A, -1).T
     assert np.abs(As @ x - b).max() / np.abs(b).max() <= 1e-10
     assert rel_inf(x, x_or) <= 1e-8
+
+
+@pytest.mark.parametrize("N,n2", [(8192, 2000), (12289, 100)])
+def test_pivoting_heavy_large(N, n2):
+    # multi-CTA exact BK panels (k_panel_exact with 32-48 CTAs and grid barriers) on
+    # prescribed-spectrum matrices: inertia against the closed form, solve by the residual
+    A, ine = mdsgen.g3_prescribed_torch(N, seed=N + 11, n2x2=n2, device="cuda")
+    M = A.T.contiguous().reshape(-1)
+    piv = torch.empty(2 * N, dtype=torch.int32, device="cuda")
+    ine_d = torch.zeros(3, dtype=torch.int64, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    fwork = torch.empty(mds.factor_workspace_size(N), dtype=torch.uint8, device="cuda")
+    swork = torch.empty(mds.solve_workspace_size(N), dtype=torch.uint8, device="cuda")
+    g_ine = mds.factor(N, M, N, piv, -1.0, ine_d, status, fwork, sync=True)
+    b = torch.as_tensor(np.random.default_rng(N).standard_normal(N), dtype=torch.float64, device="cuda")
+    x = torch.empty(N, dtype=torch.float64, device="cuda")
+    mds.solve(None, N, M, N, piv, b, None, None, None, x, None, -1.0, fwork, status, swork)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 0
+    assert g_ine == ine
+    res = float((A @ x - b).abs().max() / b.abs().max())
+    assert res <= 1e-10, res
 
 
 def test_c5_factor_solve_32768():
