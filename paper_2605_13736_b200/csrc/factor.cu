@@ -1549,6 +1549,7 @@ constexpr int TSMAX = 3;                          // pipeline stages (L + W tile
 constexpr int TTHREADS = 32 * (1 + 4 * TNG);      // producer warp + consumer warps
 constexpr int TOPB = UT * NB * 8;                 // bytes per operand tile (32 KB)
 constexpr int TSTAGEB = 2 * TOPB;                 // L + W
+constexpr int TBOXB = 16 * NB * 8;                // bytes per TMA box (16 rows x 64 k, 8 KB)
 // OUTB variant: 2 stages + one 32 KB output buffer per consumer group (a stage is released as soon as
 // its k-loop is done); in-place variant: 3 stages, -P staged in the consumed stage (released after the
 // TMA reduce has read it).  Both use 192 KB.
@@ -1580,10 +1581,13 @@ __device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map
       : "memory");
 }
 // byte offset of element (row i in 0..63, k t in 0..63) inside an operand tile:
-// 8 boxes of 8 rows x 64 k (4 KB each), 64-byte swizzle (bits[4:5] ^= bits[7:8])
+// 4 boxes of 16 rows x 64 k (8 KB each), 128-byte swizzle (bits[4:6] ^= bits[7:9]).
+// (16-row boxes: the TMA engine moves 128-byte rows, 1.45x the load throughput
+// of 8-row / 64-byte boxes -- tools/tma_bw_probe.cu: 50 vs 35 B/clk/SM -- and the
+// operand loads share it with the reduce-add of the result tile.)
 __device__ __forceinline__ unsigned tma_off(int i, int t) {
-  const unsigned lin = (unsigned)(t * 64 + (i & 7) * 8);
-  return (unsigned)((i >> 3) * 4096) + (lin ^ (((lin >> 7) & 3u) << 4));
+  const unsigned lin = (unsigned)(t * 128 + (i & 15) * 8);
+  return (unsigned)((i >> 4) * TBOXB) + (lin ^ (((lin >> 7) & 7u) << 4));
 }
 
 // Tile sets: mode 0 = all lower tiles of the trailing matrix (columns >= s).
@@ -1729,9 +1733,9 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
               asm volatile("fence.proxy.async.global;\n" ::: "memory");     // X was written by the generic proxy
               mbar_expect_tx(fb, TSTAGEB);
 #pragma unroll
-              for (int b = 0; b < 8; b++) {
-                tma_load_2d(sL + b * 4096, &mapA, R0 + 8 * b, (int)s, fb);   // A21 (updated by U_next)
-                tma_load_2d(sW + b * 4096, &mapX, 8 * b, 0, fb);            // L11^{-1}
+              for (int b = 0; b < 4; b++) {
+                tma_load_2d(sL + b * TBOXB, &mapA, R0 + 16 * b, (int)s, fb);   // A21 (updated by U_next)
+                tma_load_2d(sW + b * TBOXB, &mapX, 16 * b, 0, fb);            // L11^{-1}
               }
               continue;
             }
@@ -1752,7 +1756,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
           stile[st] = (long long)((0xfffffffdull << 32) | (unsigned)R0);   // C0 = -3
           mbar_expect_tx(fb, TOPB);
 #pragma unroll
-          for (int b = 0; b < 8; b++) tma_load_2d(sL + b * 4096, &mapL, R0 + 8 * b, 0, fb);
+          for (int b = 0; b < 4; b++) tma_load_2d(sL + b * TBOXB, &mapL, R0 + 16 * b, 0, fb);
           xnext = dyn ? atom_add_u64(counter, 1ull) : xnext + gridDim.x;
           continue;
         }
@@ -1768,9 +1772,9 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
         stile[st] = (long long)(((unsigned long long)(unsigned)C0 << 32) | (unsigned)R0);   // tile origin for the consumers
         mbar_expect_tx(fb, TSTAGEB);
 #pragma unroll
-        for (int b = 0; b < 8; b++) {
-          tma_load_2d(sL + b * 4096, &mapL, R0 + 8 * b, 0, fb);
-          tma_load_2d(sW + b * 4096, &mapW, C0 + 8 * b, 0, fb);
+        for (int b = 0; b < 4; b++) {
+          tma_load_2d(sL + b * TBOXB, &mapL, R0 + 16 * b, 0, fb);
+          tma_load_2d(sW + b * TBOXB, &mapW, C0 + 16 * b, 0, fb);
         }
         xnext = dyn ? atom_add_u64(counter, 1ull) : xnext + gridDim.x;
       }
@@ -1809,17 +1813,21 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
 #pragma unroll
       for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
     const unsigned Lt = tsm + st * TSTAGEB;
-    const unsigned Lb = Lt + (unsigned)(wm >> 3) * 4096u;
-    const unsigned Wb = Lt + TOPB + (unsigned)(wn >> 3) * 4096u;
+    const unsigned Lb = Lt + (unsigned)(wm >> 4) * TBOXB;
+    const unsigned Wb = Lt + TOPB + (unsigned)(wn >> 4) * TBOXB;
     // k-loop with register double-buffered fragments (loads of step t+1 overlap the DMMAs of step t)
     double a0[4], b0v[4], a1[4], b1v[4];
+    // k-step ks, lane (g, q) reads k = t(ks, q): a permutation of 0..63 (the contraction
+    // order is free) chosen so that lanes q = 0,1 and q = 2,3 land in opposite bank
+    // halves under the 128-byte swizzle (bit 2 of t selects the half): 2 wavefronts per LDS.64
     auto frag = [&](int ks, double* av, double* bv) {
-      const unsigned t = (unsigned)(4 * ks + q);
-      const unsigned off = (t * 64u + (unsigned)g * 8u) ^ (((t >> 1) & 3u) << 4);
+      const unsigned t = 8u * (unsigned)(ks >> 1) + 4u * (unsigned)(q >> 1) + 2u * (unsigned)(ks & 1) + (unsigned)(q & 1);
+      const unsigned sw = (t & 7u) << 4;
+      const unsigned o0 = (t * 128u + (unsigned)g * 8u) ^ sw, o1 = (t * 128u + 64u + (unsigned)g * 8u) ^ sw;
 #pragma unroll
-      for (int a = 0; a < 4; a++) av[a] = lds_f64(Lb + (unsigned)a * 4096u + off);
+      for (int a = 0; a < 4; a++) av[a] = lds_f64(Lb + (unsigned)(a >> 1) * TBOXB + ((a & 1) ? o1 : o0));
 #pragma unroll
-      for (int b = 0; b < 4; b++) bv[b] = lds_f64(Wb + (unsigned)b * 4096u + off);
+      for (int b = 0; b < 4; b++) bv[b] = lds_f64(Wb + (unsigned)(b >> 1) * TBOXB + ((b & 1) ? o1 : o0));
     };
     frag(0, a0, b0v);
 #pragma unroll 1
@@ -1897,8 +1905,8 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
     asm volatile("bar.sync %0, 128;\n" ::"r"(grp + 1) : "memory");
     if (leader) {
 #pragma unroll
-      for (int b = 0; b < 8; b++)
-        if (!(sched & 4)) tma_reduce_add_2d(&mapA, (int)(R0 + 8 * b), (int)C0, Ot + b * 4096);   // (bit 2: timing experiment)
+      for (int b = 0; b < 4; b++)
+        if (!(sched & 4)) tma_reduce_add_2d(&mapA, (int)(R0 + 16 * b), (int)C0, Ot + b * TBOXB);   // (bit 2: timing experiment)
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       if (!OUTB) {
         asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");   // smem source consumed
@@ -1936,16 +1944,16 @@ PFN_encodeTiled get_encode() {
   return fn;
 }
 
-// 2-D map over a column-major (rows x cols, ld) FP64 matrix; box 8 rows x 64 cols, 64-byte swizzle
+// 2-D map over a column-major (rows x cols, ld) FP64 matrix; box 16 rows x 64 cols, 128-byte swizzle
 bool make_map(CUtensorMap* m, const double* base, int64_t rows, int64_t cols, int64_t ld) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
-  cuuint32_t box[2] = {8, 64};
+  cuuint32_t box[2] = {16, 64};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -2228,8 +2236,12 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
         if (last) break;
         if (int rc = launch_fast(p + 1)) return rc;
       } else if (!upd_main) {   // (A/B variant: U on the side stream, F1 on the main stream)
-        MDS_LAUNCH(PC_UPDATE, side,
-                   (k_update_tma<3, true><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
+        if (g_inplace)
+          MDS_LAUNCH(PC_UPDATE, side,
+                     (k_update_tma<3, false><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
+        else
+          MDS_LAUNCH(PC_UPDATE, side,
+                     (k_update_tma<3, true><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
         MDS_CUDA_TRY(cudaEventRecord(ev(p, 1), side));
         const FWork fn = fwork_for(p + 1);
         MDS_LAUNCH(PC_PANEL_DIAG, st, MDS_CUDA_TRY(launch_pdl(k_panel_diag, dim3(1), dim3(256), F1SMEM, st, N, M, ldm, fn)));
