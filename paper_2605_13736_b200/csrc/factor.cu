@@ -1638,6 +1638,9 @@ __device__ __forceinline__ double dneg(double v) {   // exact sign flip on the i
   return r;
 }
 
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(map), "r"(c0), "r"(c1) : "memory");
+}
 __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, int c0, int c1, unsigned src) {
   asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map),
                "r"(c0), "r"(c1), "r"(src)
@@ -1776,6 +1779,11 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
           tma_load_2d(sL + b * TBOXB, &mapL, R0 + 16 * b, 0, fb);
           tma_load_2d(sW + b * TBOXB, &mapW, C0 + 16 * b, 0, fb);
         }
+        // pull the C tile into L2 now, so that its reduce-add (a tile later) is an L2 hit
+        // and does not hold the TMA unit for a DRAM round trip
+        if (sched & 8)
+#pragma unroll
+          for (int b = 0; b < 4; b++) tma_prefetch_2d(&mapA, R0 + 16 * b, C0);
         xnext = dyn ? atom_add_u64(counter, 1ull) : xnext + gridDim.x;
       }
     }
@@ -2159,7 +2167,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
                    make_map(&mapL1, f.Lb1, N, NB, f.ldw) && make_map(&mapX, f.Lblk, NB, NB, NB)))
     return MDS_ERR_CUDA;
   const int g_sched = (std::getenv("MDS_STATIC_SCHED") ? 1 : 0) | (std::getenv("MDS_NO_SNAKE") ? 0 : 2) |
-                      (std::getenv("MDS_XP_NOREDUCE") ? 4 : 0);   // (bit 2: timing experiment only, wrong results)
+                      (std::getenv("MDS_XP_NOREDUCE") ? 4 : 0) | (std::getenv("MDS_NO_CPREFETCH") ? 0 : 8);   // (bit 2: timing experiment only, wrong results)
   const bool g_inplace = std::getenv("MDS_UPD_INPLACE") != nullptr;
   const bool upd_main = std::getenv("MDS_UPD_MAIN") != nullptr;   // measured slower (A/B), off by default
   // panels with at most this many remaining rows use the one-launch fast path
