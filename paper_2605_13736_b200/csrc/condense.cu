@@ -17,6 +17,8 @@
 #include <new>
 #include <vector>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 struct mds_plan {
@@ -383,17 +385,28 @@ extern "C" int mds_condense(const mds_plan* P, const double* js_val, const doubl
   }
   if (m > 0) {
     // warp-private accumulator columns: <= 4096 doubles each; warps per CTA sized to ~192 KB
-    const int64_t acc_len = std::min<int64_t>(((m + 31) / 32) * 32, 4096);
+    // (MDS_YY_ACC caps the column window: longer columns take several passes over their list,
+    //  in exchange for more resident warps; A/B knob)
+    static const int64_t acc_cap = std::getenv("MDS_YY_ACC") ? std::atoll(std::getenv("MDS_YY_ACC")) : 4096;
+    const int64_t acc_len = std::min<int64_t>(((m + 31) / 32) * 32, acc_cap);
     static bool attr_set = false;
     if (!attr_set) {
       cudaFuncSetAttribute(k_condense_yy<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * 4096 * 8);
       cudaFuncSetAttribute(k_condense_yy<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 2048 * 8);
+      cudaFuncSetAttribute(k_condense_yy<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 2048 * 8);
       (void)cudaGetLastError();
       attr_set = true;
     }
     const int64_t ntask = (m + 1) / 2;
     if (acc_len > 2048) {
       constexpr int W = 6;
+      size_t smem = sizeof(double) * acc_len * W;
+      MDS_LAUNCH(PC_CONDENSE_YY, st,
+                 MDS_CUDA_TRY(launch_pdl(k_condense_yy<W>, dim3((unsigned)mds_cdiv(ntask, W)), dim3(W * 32), smem, st,
+                     n_d, P->m_E, m, acc_len, P->rowptr, P->colidx, js_val, P->tptr, P->tkp, w_out, d_h, delta_c,
+                     r, n_s, M, ldm, rhs_c, status)));
+    } else if (acc_len == 2048 && m > 2048) {
+      constexpr int W = 12;
       size_t smem = sizeof(double) * acc_len * W;
       MDS_LAUNCH(PC_CONDENSE_YY, st,
                  MDS_CUDA_TRY(launch_pdl(k_condense_yy<W>, dim3((unsigned)mds_cdiv(ntask, W)), dim3(W * 32), smem, st,

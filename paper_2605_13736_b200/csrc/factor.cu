@@ -156,51 +156,66 @@ __global__ void k_factor_init(int64_t N, FWork f, double zero_tol) {
 }
 
 // ||M||_inf (row abs-sums via symmetry, lower storage) + non-finite scan.
-// One CTA per 32x32 lower tile; row partials atomically added to rowsum.
+// One CTA per 64x64 lower tile: each thread has its 16 loads in flight at once
+// (rows contiguous across the warp), row and column partials reduced in the CTA,
+// then 64 + 64 atomic adds into rowsum.  (HBM-bound: N^2/2 * 8 bytes.)
+constexpr int AT = 64;
 __global__ void __launch_bounds__(256) k_anorm_tiles(int64_t N, const double* __restrict__ A, int64_t lda,
                                                      double* rowsum, FCtl* ctl, int32_t* status) {
   pdl_wait();
   pdl_trigger();
-  const int64_t nt = (N + 31) / 32;
+  const int64_t nt = (N + AT - 1) / AT;
   const int64_t x = blockIdx.x;
   int64_t bi = (int64_t)((sqrt(8.0 * (double)x + 1.0) - 1.0) * 0.5);
   while (bi * (bi + 1) / 2 > x) bi--;
   while ((bi + 1) * (bi + 2) / 2 <= x) bi++;
   const int64_t bj = x - bi * (bi + 1) / 2;
   if (bi >= nt) return;
-  __shared__ double tile[32][33];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+  __shared__ double rpart[4][AT];    // row partials per column group
+  __shared__ double cpart[2][AT];    // column partials per row half (one warp each)
+  const int tx = threadIdx.x & (AT - 1), ty = threadIdx.x >> 6;   // row tx, columns ty + 4u
+  const int64_t i = bi * AT + tx;
+  double v[16];
+#pragma unroll
+  for (int u = 0; u < 16; u++) {
+    const int64_t j = bj * AT + ty + 4 * u;
+    v[u] = (i < N && j < N && i >= j) ? A[i + j * lda] : 0.0;
+  }
   bool bad = false;
-  for (int yy = ty; yy < 32; yy += 8) {
-    const int64_t i = bi * 32 + tx, j = bj * 32 + yy;
-    double v = 0.0;
-    if (i < N && j < N && i >= j) {
-      v = A[i + j * lda];
-      if (!isfinite(v)) bad = true;
-      v = fabs(v);
-    }
-    tile[yy][tx] = v;   // tile[col][row]
+  double rs = 0.0;
+#pragma unroll
+  for (int u = 0; u < 16; u++) {
+    if (!isfinite(v[u])) bad = true;
+    v[u] = fabs(v[u]);
+    rs += v[u];
   }
   if (__syncthreads_or(bad)) {
     if (threadIdx.x == 0) { mds_set_status(status, MDS_ERR_NONFINITE); ctl->abort = 1; }
     return;
   }
-  if (threadIdx.x < 32) {
-    // row sums (row i = bi*32+tx) over tile columns
-    double s = 0.0;
-    for (int c = 0; c < 32; c++) s += tile[c][threadIdx.x];
-    const int64_t i = bi * 32 + threadIdx.x;
-    if (i < N && s != 0.0) atomicAdd(&rowsum[i], s);
-  } else if (threadIdx.x < 64) {
-    // column sums excluding the diagonal (they are row j's upper part)
-    const int c = threadIdx.x - 32;
-    double s = 0.0;
-    for (int r = 0; r < 32; r++) {
-      const int64_t i = bi * 32 + r, j = bj * 32 + c;
-      if (i > j) s += tile[c][r];
-    }
-    const int64_t j = bj * 32 + c;
-    if (j < N && s != 0.0) atomicAdd(&rowsum[j], s);
+  rpart[ty][tx] = rs;
+  // column sums excluding the diagonal (they are row j's upper part): over the 32 rows of this warp
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, half = (warp & 1);
+#pragma unroll
+  for (int u = 0; u < 16; u++) {
+    const int64_t j = bj * AT + ty + 4 * u;
+    double c = (i > j) ? v[u] : 0.0;
+    c += __shfl_xor_sync(0xffffffffu, c, 16);
+    c += __shfl_xor_sync(0xffffffffu, c, 8);
+    c += __shfl_xor_sync(0xffffffffu, c, 4);
+    c += __shfl_xor_sync(0xffffffffu, c, 2);
+    c += __shfl_xor_sync(0xffffffffu, c, 1);
+    if (lane == 0) cpart[half][ty + 4 * u] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x < AT) {
+    const double s2 = (rpart[0][tx] + rpart[1][tx]) + (rpart[2][tx] + rpart[3][tx]);
+    if (i < N && s2 != 0.0) atomicAdd(&rowsum[i], s2);
+  } else if (threadIdx.x < 2 * AT) {
+    const int c = threadIdx.x - AT;
+    const int64_t j = bj * AT + c;
+    const double s2 = cpart[0][c] + cpart[1][c];
+    if (j < N && s2 != 0.0) atomicAdd(&rowsum[j], s2);
   }
 }
 
@@ -602,7 +617,7 @@ __device__ __forceinline__ void f1_body(int64_t N, double* __restrict__ A, int64
   }
   __syncthreads();
   if (tid == 0) {   // publish X / d / colmax to the F2 tiles run inside the concurrent trailing update
-    __threadfence();
+    // (st.release.gpu is cumulative over the CTA's writes ordered before it by the barrier)
     st_release_u32(&ctl->xready, (unsigned)(f.pidx + 1));
   }
   F1T(4);
@@ -2110,7 +2125,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
              MDS_CUDA_TRY(launch_pdl(k_factor_init, dim3((unsigned)std::min<int64_t>(mds_cdiv(3 * (N + 2), 256), 1184)),
                                      dim3(256), 0, st, N, f, zero_tol)));
   {
-    int64_t nt = (N + 31) / 32;
+    int64_t nt = (N + AT - 1) / AT;
     MDS_LAUNCH(PC_ANORM, st,
                MDS_CUDA_TRY(launch_pdl(k_anorm_tiles, dim3((unsigned)(nt * (nt + 1) / 2)), dim3(256), 0, st, N, M, ldm,
                                        f.rowsum, f.ctl, status)));

@@ -1,12 +1,22 @@
 #!/bin/bash
-# Round profile captures (run on the GPU box from the repo root):
-#   launch list of one eager C3 step, ncu --set full of the dominant kernels.
+# Round profile captures (run on the GPU box from the repo root; then, here,
+# `python tools/summarize_profiles.py <tag> 9` writes the profiles/ summaries):
+#   launch list of one eager C3 step (bench.py --no-graph runs 9 steps in that mode),
+#   ncu --set full of the dominant kernel and of the other hot-path kernels,
+#   ncu --set full of one multi-CTA exact BK panel on the pivot-heavy C5 matrix.
 set -x
 mkdir -p gpurun_out
+B="python bench.py --steps 1 --warmup 0 --no-graph --no-cpu --no-e2e"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 1 --warmup 0 --no-graph --ref-sample 256 > gpurun_out/launches_bench.log 2>&1
+    $B > gpurun_out/launches_bench.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:k_update_tma --launch-skip 10 --launch-count 1 \
-    -o gpurun_out/upd_full -f python bench.py --steps 1 --warmup 0 --no-graph --ref-sample 256 > /dev/null 2>&1
-ncu --set full --clock-control none -k regex:"k_condense_yy|k_panel_diag|k_trsv_fwd|k_trsv_bwd|k_panel_fast|k_panel_trsm" \
-    --launch-count 8 -o gpurun_out/misc_full -f python bench.py --steps 1 --warmup 0 --no-graph --ref-sample 256 > /dev/null 2>&1
+    -o gpurun_out/upd_full -f $B > /dev/null 2>&1
+ncu -i gpurun_out/upd_full.ncu-rep --page raw --csv > gpurun_out/upd_full_raw.csv
+ncu --set full --clock-control none \
+    -k regex:"k_condense_dense|k_condense_yy|k_panel_diag|k_panel_trsm|k_panel_exact|k_panel_fast|k_trsv_fwd|k_trsv_bwd|k_step_vectors|k_anorm_tiles" \
+    --launch-count 12 -o gpurun_out/misc_full -f $B > /dev/null 2>&1
+ncu -i gpurun_out/misc_full.ncu-rep --page raw --csv > gpurun_out/misc_full_raw.csv
+timeout 900 ncu --set full --clock-control none -k regex:k_panel_exact --launch-skip 200 --launch-count 1 \
+    -o gpurun_out/exact_full -f python bench.py --config C5 --steps 1 --warmup 0 --no-cpu --no-e2e > /dev/null 2>&1
+ncu -i gpurun_out/exact_full.ncu-rep --page raw --csv > gpurun_out/exact_full_raw.csv
 ls -la gpurun_out
