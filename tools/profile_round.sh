@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round profile captures (run on the GPU box from the repo root; then, here,
-# `python tools/summarize_profiles.py <tag> 9` writes the profiles/ summaries):
-#   launch list of one eager C3 step (bench.py --no-graph runs 9 steps in that mode),
+# `python tools/summarize_profiles.py <tag> 6` writes the profiles/ summaries):
+#   launch list of one eager C3 step (bench.py --no-graph --no-cpu --no-e2e runs 6 eager steps),
 #   ncu --set full of the dominant kernel and of the other hot-path kernels,
 #   ncu --set full of one multi-CTA exact BK panel on the pivot-heavy C5 matrix.
 set -x
