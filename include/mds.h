@@ -189,8 +189,13 @@ enum {
 };
 unsigned long long mds_launch_count(void);
 /* Tuning knob (process-wide): cap the CTA count of mds_factor's persistent
- * trailing-update kernels (0 = one per SM, the default).  Used when several
- * factorizations run concurrently on different streams (SCOPF batches). */
+ * trailing-update kernels and of the multi-CTA exact-pivot panel (0 = one per
+ * SM, the default).  Used when several factorizations run concurrently on
+ * different streams (SCOPF batches).  A cap below the SM count also selects
+ * the concurrent launch structure (no one-launch tail panels, whose waiting
+ * CTAs would hold SMs other streams need); results are bitwise identical for
+ * every cap value below the SM count, and differ from the uncapped structure
+ * only by rounding order. */
 int mds_factor_set_grid_cap(int ctas);
 int mds_profile_begin(void);
 int mds_profile_end(double *ms_by_class, int64_t *launches_by_class, int ncls);

@@ -2186,8 +2186,11 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   const bool g_inplace = std::getenv("MDS_UPD_INPLACE") != nullptr;
   const bool upd_main = std::getenv("MDS_UPD_MAIN") != nullptr;   // measured slower (A/B), off by default
   // panels with at most this many remaining rows use the one-launch fast path
-  const int64_t tail_rows = std::getenv("MDS_TAIL_ROWS") ? std::atoll(std::getenv("MDS_TAIL_ROWS")) : 4800;
   const bool capped = (g_grid_cap > 0 && g_grid_cap < sms);
+  // (not when factorizations run concurrently (grid cap set): the tail launch's F2-role CTAs
+  //  spin for X while F1 runs, which is free on an idle GPU but starves the other streams --
+  //  C4: 3278 -> 4022 scenario-steps/s without it)
+  const int64_t tail_rows = std::getenv("MDS_TAIL_ROWS") ? std::atoll(std::getenv("MDS_TAIL_ROWS")) : (capped ? 0 : 4800);
   if (capped) sms = g_grid_cap;
   const size_t usmem = 2 * NB * US * sizeof(double);
   auto fwork_for = [&](int64_t p) {

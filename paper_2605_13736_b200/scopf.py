@@ -17,6 +17,8 @@ never exchange matrix data.
 from __future__ import annotations
 
 import numpy as np
+import os
+
 import torch
 import torch.distributed as dist
 
@@ -95,7 +97,12 @@ class ScopfBatch:
         self.streams = [torch.cuda.Stream() for _ in range(max(1, min(n_streams, n)))]
         # concurrent factorizations share the SMs: cap each persistent update grid
         sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
-        set_grid_cap(max(8, sms // len(self.streams)) if len(self.streams) > 1 else 0)
+        cap = int(os.environ.get("MDS_SCOPF_CAP", "0")) or max(8, sms // len(self.streams))
+        # (a capped grid also selects the factorization's concurrent launch structure -- no
+        #  one-launch tail panels -- so a scenario's bits depend on the cap, never on the stream
+        #  count, the rank or the other scenarios)
+        self.grid_cap = cap if len(self.streams) > 1 else 0
+        set_grid_cap(self.grid_cap)
         self._ids_t = torch.tensor(self.ids, dtype=torch.float64, device=device)
         self.graph = self._capture_all()
         set_grid_cap(0)

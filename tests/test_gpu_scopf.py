@@ -31,9 +31,14 @@ def test_scopf_batch_matches_single_and_oracle():
     assert list(recs[:, 0]) == ids
     for i, s in enumerate(ids):
         p = fn(s)
-        single = mds.KKTStep(mds.DeviceProblem(p), sv=svf(p, s))
-        single.run()
-        a = single.results()
+        # alone, in the same factorization configuration (the batch's grid cap)
+        mds.set_grid_cap(batch.grid_cap)
+        try:
+            single = mds.KKTStep(mds.DeviceProblem(p), sv=svf(p, s))
+            single.run()
+            a = single.results()
+        finally:
+            mds.set_grid_cap(0)
         b = batch.steps[i].results()
         np.testing.assert_array_equal(a["dxy"], b["dxy"])
         assert a["inertia"] == b["inertia"] == p.expected_inertia
