@@ -46,6 +46,7 @@ constexpr int WCOLS = NB + 1;       // W work panel columns (+1 for the 2x2 cand
 constexpr int XT = 512;             // threads per CTA of the multi-CTA exact panel (k_panel_exact)
 constexpr int XMAXG = 256;          // its maximum grid
 constexpr int XROWS = XT / 4;       // rows per CTA pass (a quad of threads per row)
+constexpr int XLS_MAX = 200 * 1024; // k_panel_exact's shared-memory copy of its L rows (else read from L2)
 constexpr double ALPHA_BK = 0.64038820320220756872767623199676;  // (1+sqrt(17))/8
 
 struct FCtl {
@@ -1162,7 +1163,7 @@ __device__ __forceinline__ ArgMax x_exchange(unsigned* ctr, ArgMax* part, unsign
 template <bool IMAX>
 __device__ __forceinline__ ArgMax x_gemv(const double* A, int64_t lda, const double* Lb, double* W, int64_t ldw,
                                          int64_t rlo, int64_t rhi, int64_t k, int64_t kc, int j, int wcol,
-                                         const double* wv, double* aux) {
+                                         const double* wv, double* aux, const double* Ls, int lstr) {
   const int tid = threadIdx.x, qd = tid & 3;
   ArgMax am{-1.0, 0x7fffffff};
   const int64_t rfirst = rlo + ((k > rlo) ? ((k - rlo) / XROWS) * XROWS : 0);
@@ -1170,7 +1171,15 @@ __device__ __forceinline__ ArgMax x_gemv(const double* A, int64_t lda, const dou
     const int64_t r = rb + (tid >> 2);
     const bool live = r < rhi && r >= k;
     double s0 = 0.0, s1 = 0.0;
-    if (live) {
+    if (live && Ls) {   // the CTA's rows of the panel's finished columns, kept in shared memory
+      const double* lr = Ls + (r - rlo);
+      int t = qd;
+      for (; t + 4 < j; t += 8) {
+        s0 = fma(lr[t * lstr], wv[t], s0);
+        s1 = fma(lr[(t + 4) * lstr], wv[t + 4], s1);
+      }
+      if (t < j) s0 = fma(lr[t * lstr], wv[t], s0);
+    } else if (live) {
       const double* lr = Lb + r;
       int t = qd;
       for (; t + 4 < j; t += 8) {
@@ -1194,7 +1203,7 @@ __device__ __forceinline__ ArgMax x_gemv(const double* A, int64_t lda, const dou
 }
 
 __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restrict__ A, int64_t lda, FWork f,
-                                                    int32_t* piv) {
+                                                    int32_t* piv, int xchunk, int use_ls) {
   pdl_wait();
   pdl_trigger();
   FCtl* ctl = f.ctl;
@@ -1245,9 +1254,22 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
     __shared__ ArgMax sh[33];
     const double tol = ctl->tol;
     const int G = (int)gridDim.x;
-    const int64_t chunk = ((N - k0 + G - 1) / G + 31) / 32 * 32;
+    const int64_t chunk = xchunk;   // host: >= ceil((N - k0) / G), multiple of 32
+    // the CTA's rows of L (panel columns) in shared memory: Ls[t * lstr + row - rlo]
+    // (lstr = 8 mod 16: the 4 k-lanes of a quad fall in opposite bank halves pairwise)
+    extern __shared__ double xls[];
+    const int lstr = xchunk + 8;
+    const double* Ls = use_ls ? xls : nullptr;
     const int64_t rlo = k0 + (int64_t)blockIdx.x * chunk;
     const int64_t rhi = (rlo + chunk < N) ? rlo + chunk : N;
+    if (use_ls) {
+      const int64_t nr = rhi - rlo;
+      for (int64_t idx = tid; idx < nr * j; idx += XT) {
+        const int64_t rl = idx % nr, t = idx / nr;
+        xls[t * lstr + rl] = __ldcg(&Lb[(rlo + rl) + t * ldw]);
+      }
+      __syncthreads();
+    }
     unsigned* ctr = f.xbar + f.pidx;   // this panel's barrier counter (zeroed by k_factor_init)
     unsigned nbar = 0;                 // barriers so far
     while (j < jlim) {
@@ -1255,7 +1277,7 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
       for (int t = tid; t < j; t += XT) wrow[t] = __ldcg(&W[k + t * ldw]);
       __syncthreads();
       // W(k:N, j) = A(k:N, k) - L(k:N, panel) W(k, panel)^T ; colmax / imax below k
-      ArgMax am = x_gemv<false>(A, lda, Lb, W, ldw, rlo, rhi, k, k, j, j, wrow, nullptr);
+      ArgMax am = x_gemv<false>(A, lda, Lb, W, ldw, rlo, rhi, k, k, j, j, wrow, nullptr, Ls, lstr);
       am = block_argmax(am, sh);
       am = x_exchange(ctr, f.xpart, nbar, am, sh);
       const double absakk = fabs(__ldcg(&W[k + j * ldw]));
@@ -1273,7 +1295,7 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
         __syncthreads();
         // candidate column imax, updated: W(k:N, j+1); |W(imax, j+1)| published by its owner
         const unsigned sl = nbar & 1u;
-        ArgMax rm = x_gemv<true>(A, lda, Lb, W, ldw, rlo, rhi, k, imax, j, j + 1, wrow, f.xaux + sl);
+        ArgMax rm = x_gemv<true>(A, lda, Lb, W, ldw, rlo, rhi, k, imax, j, j + 1, wrow, f.xaux + sl, Ls, lstr);
         rm = block_argmax(rm, sh);
         rm = x_exchange(ctr, f.xpart, nbar, rm, sh);
         const double rowmax = (rm.v < 0.0) ? 0.0 : rm.v;
@@ -1317,6 +1339,15 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
           }
         }
         x_exchange(ctr, f.xpart, nbar, ArgMax{-1.0, 0x7fffffff}, sh);
+        if (use_ls) {   // rows kk / kp of L were swapped by CTA 0: refresh this CTA's copies
+          const int nl = j;   // finished columns (column j itself is rewritten by the scaling below)
+          for (int c = tid; c < 2 * nl; c += XT) {
+            const int64_t r = (c < nl) ? kk : kp;
+            const int t = (c < nl) ? c : c - nl;
+            if (r >= rlo && r < rhi) xls[t * lstr + (r - rlo)] = __ldcg(&Lb[r + t * ldw]);
+          }
+          // (ordered before the next GEMV by the barriers below)
+        }
       }
       if (kstep == 1) {
         const double d = __ldcg(&W[k + j * ldw]);
@@ -1324,7 +1355,9 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
         for (int64_t r = rlo + tid; r < rhi; r += XT) {
           if (r <= k) continue;
           const double w = __ldcg(&W[r + j * ldw]);
-          Lb[r + j * ldw] = zero ? w : w * r1;
+          const double l = zero ? w : w * r1;
+          Lb[r + j * ldw] = l;
+          if (use_ls) xls[j * lstr + (r - rlo)] = l;
         }
         if (c0 && tid == 0) {
           Lb[k + j * ldw] = d;
@@ -1346,8 +1379,10 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
         for (int64_t r = rlo + tid; r < rhi; r += XT) {
           if (r < k + 2) continue;
           const double wk = __ldcg(&W[r + j * ldw]), wk1 = __ldcg(&W[r + (j + 1) * ldw]);
-          Lb[r + j * ldw] = d21 * (d11 * wk - wk1);
-          Lb[r + (j + 1) * ldw] = d21 * (d22 * wk1 - wk);
+          const double l0 = d21 * (d11 * wk - wk1), l1 = d21 * (d22 * wk1 - wk);
+          Lb[r + j * ldw] = l0;
+          Lb[r + (j + 1) * ldw] = l1;
+          if (use_ls) { xls[j * lstr + (r - rlo)] = l0; xls[(j + 1) * lstr + (r - rlo)] = l1; }
         }
         if (c0 && tid == 0) {
           Lb[k + j * ldw] = w11;
@@ -2204,14 +2239,26 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   auto rows_of = [&](int64_t p) { return N - std::min<int64_t>(p * (NB - 1), N); };   // upper bound
   const int reserve = capped ? std::max(1, sms / 8) : 1;   // SMs left to the panel chain (F1)
   // F4 (acceptance + exact BK columns): multi-CTA, ~256 rows per CTA, all CTAs co-resident
-  static const bool f4_one_cta = std::getenv("MDS_SLOW_1CTA") != nullptr;   // A/B: the single-CTA k_panel_slow
+  const bool f4_one_cta = std::getenv("MDS_SLOW_1CTA") != nullptr;   // A/B: the single-CTA k_panel_slow
+  const bool f4_no_ls = std::getenv("MDS_EXACT_NO_LS") != nullptr;   // A/B: L rows read from L2
+  static bool f4_attr = false;
+  if (!f4_attr) {
+    cudaFuncSetAttribute(k_panel_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, XLS_MAX);
+    f4_attr = true;
+  }
   auto launch_f4 = [&](const FWork& fp, int64_t rows) -> int {
     if (f4_one_cta) {
       MDS_LAUNCH(PC_PANEL_SLOW, st, MDS_CUDA_TRY(launch_pdl(k_panel_slow, dim3(1), dim3(1024), 0, st, N, M, ldm, fp, piv)));
       return MDS_OK;
     }
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>({mds_cdiv(rows, 256), (int64_t)sms, (int64_t)XMAXG}));
-    MDS_LAUNCH(PC_PANEL_SLOW, st, MDS_CUDA_TRY(launch_pdl(k_panel_exact, dim3(g), dim3(XT), 0, st, N, M, ldm, fp, piv)));
+    const int chunk = (int)(mds_cdiv(mds_cdiv(std::max<int64_t>(rows, 1), g), 32) * 32);
+    const size_t lsb = (size_t)NB * (chunk + 8) * sizeof(double);
+    // (not for concurrent factorizations: a large shared-memory request per CTA would compete
+    //  with the other streams' kernels even when no column takes the exact path)
+    const int use_ls = (lsb <= (size_t)XLS_MAX && !f4_no_ls && !capped) ? 1 : 0;
+    MDS_LAUNCH(PC_PANEL_SLOW, st, MDS_CUDA_TRY(launch_pdl(k_panel_exact, dim3(g), dim3(XT), use_ls ? lsb : 0, st, N, M, ldm,
+                                                          fp, piv, chunk, use_ls)));
     return MDS_OK;
   };
   if (lookahead) {
