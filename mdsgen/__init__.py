@@ -178,6 +178,33 @@ def g2_indefinite(n_s, n_d, m_E, m_I, seed, p_neg, pattern="uniform", delta_c=1.
     return prob
 
 
+def g6_negative_curvature(n_s, n_d, m_E, m_I, seed, lam_neg=(-1.0,), jd_norm=1e-3, pattern="uniform"):
+    """G6 (inertia-correction workload): a G1 instance whose dense Hessian has
+    prescribed negative eigenvalues.  H_dd = Q diag(lambda) Q^T with lambda_i =
+    lam_neg[i] for the first len(lam_neg), U[1,10] otherwise; sigma_d = delta_w =
+    delta_c = 0; J_d scaled to ||J_d||_F = jd_norm (weak coupling).  The G1
+    y-block keeps C = J_s^T W J_s + D_h ~ O(1) positive definite, so by
+    Haynsworth the inertia of M at a regularisation delta_w is, up to an
+    O(jd_norm^2) shift of the crossover, (#{lambda+delta_w>0}, #{=0}, m+#{<0}):
+    the smallest acceptable delta_w is -min(lambda) (meta["lam"])."""
+    prob = g1_quasidefinite(n_s, n_d, m_E, m_I, seed, pattern=pattern)
+    rng = np.random.default_rng(seed + 104729)
+    Q, _ = np.linalg.qr(rng.standard_normal((n_d, n_d)))
+    lam = rng.uniform(1.0, 10.0, n_d)
+    lam[:len(lam_neg)] = np.asarray(lam_neg, dtype=np.float64)
+    prob.H_dd = np.asfortranarray((Q * lam) @ Q.T)
+    prob.sigma_d = np.zeros(n_d)
+    prob.delta_w = 0.0
+    prob.delta_c = 0.0
+    Jd = rng.standard_normal((m_E + m_I, n_d))
+    Jd *= jd_norm / np.linalg.norm(Jd)
+    prob.J_d = np.asfortranarray(Jd)
+    p = int(np.sum(lam < 0))
+    prob.expected_inertia = (n_d - p, 0, m_E + m_I + p)
+    prob.meta.update(gen="G6", lam=lam.copy())
+    return prob
+
+
 def g5_singular(n_s, n_d, m_E, m_I, seed):
     """G5: exactly singular M: equality row c0 has no J_s entries (its private
     variable removed) and a zero J_d row, delta_c = 0 -> M has an exactly zero

@@ -196,3 +196,56 @@ def newton_step(prob, tol=None):
     dxy = bk_solve(LD, ipiv, rhs, tol)
     dx_s = recover(prob, w, np.asarray(prob.r)[:prob.n_s], dxy[prob.n_d:])
     return dict(M=M, rhs_c=rhs, w=w, LD=LD, ipiv=ipiv, info=info, inertia=ine, dxy=dxy, dx_s=dx_s, tol=tol)
+
+
+# ----------------------------------------------------------------------------- inertia correction
+IC_DEFAULTS = dict(delta_w0=1e-4, delta_w_min=1e-20, delta_w_max=1e40, kappa_w_plus=8.0, kappa_w_plus_first=100.0,
+                   kappa_w_minus=1.0 / 3.0, delta_c_bar=1e-8, kappa_c=0.25)
+
+
+def factor_inertia(prob, tol=None):
+    """O1 + O3 + O4 for one regularisation (prob.delta_w, prob.delta_c): (inertia, M, LD, ipiv, tol)."""
+    M, rhs, w = condense(prob)
+    tol = default_tol(M) if tol is None else tol
+    LD, ipiv, _ = bk_factor(M)
+    return inertia(LD, ipiv, tol), dict(M=M, rhs=rhs, w=w, LD=LD, ipiv=ipiv, tol=tol)
+
+
+def inertia_correction(prob, mu, delta_w_last=0.0, params=None):
+    """Inertia correction, written out step by step (PAPER.md:161 -- regularise
+    with increasingly large multiples until the inertia of Eq.(5) is (n,0,m);
+    by PAPER.md:191 the condensed target is (n_d,0,m)), with the multiples of the
+    algorithm the paper cites for it (Wachter & Biegler 2006 Algorithm IC,
+    constants SPEC.md:354; reading R22):
+      IC-1 (0,0); IC-2 delta_c = delta_c_bar mu^kappa_c iff zero eigenvalues;
+      IC-3 delta_w = delta_w0 (delta_w_last = 0) or max(delta_w_min, kappa_w_minus delta_w_last);
+      IC-4 accept on target inertia; IC-5 delta_w *= kappa_w_plus_first (delta_w_last = 0) or
+      kappa_w_plus; IC-6 delta_w > delta_w_max -> singular.
+    Returns dict(delta_w, delta_c, delta_w_last, trials=[(dw, dc, inertia)], dxy, dx_s, inertia)."""
+    import dataclasses
+    P = dict(IC_DEFAULTS, **(params or {}))
+    target = (prob.n_d, 0, prob.m_E + prob.m_I)
+    trials = []
+
+    def attempt(dw, dc):
+        q = dataclasses.replace(prob, delta_w=float(dw), delta_c=float(dc))
+        ine, f = factor_inertia(q)
+        trials.append((float(dw), float(dc), ine))
+        return q, ine, f
+
+    q, ine, f = attempt(0.0, 0.0)
+    dw = dc = 0.0
+    if ine != target:
+        dc = P["delta_c_bar"] * mu ** P["kappa_c"] if ine[1] > 0 else 0.0
+        dw = P["delta_w0"] if delta_w_last == 0.0 else max(P["delta_w_min"], P["kappa_w_minus"] * delta_w_last)
+        while True:
+            q, ine, f = attempt(dw, dc)
+            if ine == target:
+                delta_w_last = dw
+                break
+            dw *= P["kappa_w_plus_first"] if delta_w_last == 0.0 else P["kappa_w_plus"]
+            if dw > P["delta_w_max"]:
+                raise OracleError(ERR_SINGULAR, "inertia correction: delta_w > delta_w_max")
+    dxy = bk_solve(f["LD"], f["ipiv"], f["rhs"], f["tol"])
+    dx_s = recover(q, f["w"], np.asarray(q.r)[:q.n_s], dxy[q.n_d:])
+    return dict(delta_w=dw, delta_c=dc, delta_w_last=delta_w_last, trials=trials, inertia=ine, dxy=dxy, dx_s=dx_s)

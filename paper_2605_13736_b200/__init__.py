@@ -238,3 +238,4 @@ def factor_panels(fwork, N):
 
 
 from .step import KKTStep, DeviceProblem  # noqa: E402,F401
+from .inertia import InertiaCorrection, ICParams  # noqa: E402,F401

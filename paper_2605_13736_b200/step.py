@@ -94,9 +94,17 @@ class KKTStep:
     def run(self, stream=None, sync_inertia=False, marks=None):
         """One Newton step.  `marks`: optional list of 5 CUDA events recorded on the
         stream between the four calls (wall-clock phase timing)."""
-        p = self.p
         ev = (lambda i: marks[i].record(stream) if stream is not None else marks[i].record()) if marks else \
             (lambda i: None)
+        ine = self.factor_phase(stream, sync_inertia, ev)
+        self.finish_phase(stream, ev)
+        return ine
+
+    def factor_phase(self, stream=None, sync_inertia=False, ev=None):
+        """mds_condense (with the problem's current delta_w, delta_c) + mds_factor.
+        Returns the inertia triple when sync_inertia (the only host sync), else None."""
+        p = self.p
+        ev = ev or (lambda i: None)
         self.status.zero_()
         ev(0)
         condense(p.plan, p.val, p.h_ss, p.sigma_s, p.H_dd, p.ldh, p.sigma_d, p.J_d, p.ldj, p.d_h, p.delta_w,
@@ -105,6 +113,12 @@ class KKTStep:
         ine = factor(self.N, self.M, self.ldm, self.piv, self.zero_tol, self.inertia, self.status, self.fwork,
                      sync=sync_inertia, stream=stream)
         ev(2)
+        return ine
+
+    def finish_phase(self, stream=None, ev=None):
+        """mds_solve (+ dx_s recovery) and ipm_step_vectors on the factor left by factor_phase."""
+        p = self.p
+        ev = ev or (lambda i: None)
         solve(p.plan, self.N, self.M, self.ldm, self.piv, self.rhs, p.val, self.w, p.r[:p.n_s] if p.n_s else None,
               self.dxy, self.dx_s, self.zero_tol, self.fwork, self.status, self.swork, stream)
         ev(3)
@@ -114,7 +128,6 @@ class KKTStep:
                          s["dzu"], s["tau"], s["mu"], self.vout, self.sigma, self.status, self.vwork,
                          res=(p.r,), stream=stream)
         ev(4)
-        return ine
 
     def capture(self, warmup=1):
         """CUDA-graph of run() (no host sync inside)."""

@@ -89,5 +89,16 @@ int main(int argc, char** argv) {
     sum_us += us; sum_cyc += cyc; n++;
   }
   printf("avg F1 %.1f us %.0f cycles over %d panels; err=%s\n", sum_us / n, sum_cyc / n, n, cudaGetErrorString(cudaGetLastError()));
+  // per panel (absolute us from the first F1): F1 start/end, trsm start/end, U start/end, gap U(p-1) end -> U(p) start
+  printf("csv,p,f1s,f1e,trs,tre,us,ue,gap\n");
+  double prev_ue = -1;
+  for (int p = 0; p < np; p++) {
+    if (!tr[p][0]) continue;
+    auto ab = [&](unsigned long long t) { return (t == ~0ull || t == 0) ? -1.0 : ((double)t - (double)t0) * 1e-3; };
+    const double us = ab(ut[p][0]), ue = ab(ut[p][1]);
+    printf("csv,%d,%.2f,%.2f,%.2f,%.2f,%.2f,%.2f,%.2f\n", p, ab(tr[p][0]), ab(tr[p][6]), ab(ut[p][3]), ab(ut[p][4]), us, ue,
+           (prev_ue >= 0 && us >= 0) ? us - prev_ue : -1.0);
+    prev_ue = ue;
+  }
   return 0;
 }
