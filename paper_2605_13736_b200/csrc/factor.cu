@@ -1202,8 +1202,102 @@ __device__ __forceinline__ ArgMax x_gemv(const double* A, int64_t lda, const dou
   return am;
 }
 
+// F2 tiles the concurrent trailing update did not take (it claims them only once X
+// is published and never waits for it): W21 = A21 X, L21 = W21 D^{-1}, colmax -- the
+// same arithmetic as k_panel_trsm, on warps 0-3 of a k_panel_exact CTA.  Tiles
+// [c0, ntile) are dealt to the CTAs statically (the claim counter is stable: the
+// update that claims from it has finished before this kernel starts).
+__device__ __noinline__ void x_f2_leftovers(int64_t N, const double* __restrict__ A, int64_t lda, const FWork& f,
+                                            int64_t k0, int nbp, int64_t c0, int64_t ntile, double* sm) {
+  FCtl* ctl = f.ctl;
+  const int64_t rb = k0 + nbp;
+  const int64_t rbase = (rb / UT) * UT;
+  double* As = sm;                 // [t][row]
+  double* Xs = sm + NB * US;       // [t][j]
+  __shared__ double cmax[4][32];
+  __shared__ double r1s[NB];
+  const int tid = threadIdx.x;
+  if (tid < NB) {
+    const double d = (tid < nbp) ? __ldcg(&ctl->d[tid]) : 0.0;
+    r1s[tid] = (d != 0.0) ? fast_rcp(d) : 0.0;
+  }
+  for (int idx = tid; idx < UT * NB; idx += XT) {
+    const int i = idx % UT, t = idx / UT;
+    Xs[t * US + i] = __ldcg(&f.Lblk[t * NB + i]);
+  }
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wm = ((warp & 3) >> 1) * 32, wn = (warp & 1) * 32;
+  const int g = lane >> 2, q = lane & 3;
+  double cm[4][2];
+#pragma unroll
+  for (int b = 0; b < 4; b++) cm[b][0] = cm[b][1] = 0.0;
+  for (int64_t x = c0 + blockIdx.x; x < ntile; x += gridDim.x) {
+    const int64_t R0 = rbase + x * UT;
+    __syncthreads();   // (Xs / r1s ready; As free)
+    for (int idx = tid; idx < UT * NB; idx += XT) {
+      const int i = idx % UT, t = idx / UT;
+      As[t * US + i] = (t < nbp && R0 + i < N && R0 + i >= rb) ? __ldcg(&A[(R0 + i) + (k0 + t) * lda]) : 0.0;
+    }
+    __syncthreads();
+    if (warp < 4) {
+      double acc[4][4][2];
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll 4
+      for (int t0 = 0; t0 < NB; t0 += 4) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int a = 0; a < 4; a++) av[a] = As[(t0 + q) * US + wm + 8 * a + g];
+#pragma unroll
+        for (int b = 0; b < 4; b++) bv[b] = Xs[(t0 + q) * US + wn + 8 * b + g];
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+#pragma unroll
+          for (int b = 0; b < 4; b++) dmma(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; a++) {
+        const int64_t row = R0 + wm + 8 * a + g;
+        if (row < N && row >= rb) {
+#pragma unroll
+          for (int b = 0; b < 4; b++)
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+              const int col = wn + 8 * b + 2 * q + e;
+              if (col < nbp) {
+                f.W[row + col * f.ldw] = acc[a][b][e];
+                f.Lb[row + col * f.ldw] = acc[a][b][e] * r1s[col];
+                cm[b][e] = fmax(cm[b][e], fabs(acc[a][b][e]));
+              }
+            }
+        }
+      }
+    }
+  }
+  if (warp < 4) {
+#pragma unroll
+    for (int b = 0; b < 4; b++)
+#pragma unroll
+      for (int e = 0; e < 2; e++) {
+        double v = cm[b][e];
+        v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 4));
+        v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 8));
+        v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 16));
+        if (g == 0) cmax[warp][8 * b + 2 * q + e] = v;
+      }
+  }
+  __syncthreads();
+  if (tid < NB && c0 + blockIdx.x < ntile) {
+    const int col = tid, half = col >> 5;
+    const double v = fmax(cmax[half][col & 31], cmax[half + 2][col & 31]);
+    if (col < nbp) atomicMax(&ctl->colmax[col], dbits(v));
+  }
+}
+
 __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restrict__ A, int64_t lda, FWork f,
-                                                    int32_t* piv, int xchunk, int use_ls) {
+                                                    int32_t* piv, int xchunk, int use_ls, int f2left) {
   pdl_wait();
   pdl_trigger();
   FCtl* ctl = f.ctl;
@@ -1216,12 +1310,28 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
     if (c0 && tid == 0) f.pinfo[f.pidx] = make_int2((int)k0, 0);
     return;
   }
+  extern __shared__ double xls[];
+  __shared__ ArgMax sh[33];
+  unsigned* ctr = f.xbar + f.pidx;   // this panel's barrier counter (zeroed by k_factor_init)
+  unsigned nbar = 0;                 // barriers so far
+  if (f2left) {
+    // this panel's F2 tiles the previous panel's trailing update did not take (replaces a
+    // separate k_panel_trsm launch on the critical hand-off); colmax is complete after the barrier
+    const int64_t rb = k0 + nbp;
+    const int64_t ntile = (N > rb) ? (N + UT - 1) / UT - rb / UT : 0;
+    const unsigned long long claimed = __ldcg(f.ucount + 3 * f.pidx + 2);
+    const int64_t cfirst = (claimed < (unsigned long long)ntile) ? (int64_t)claimed : ntile;
+    if (cfirst < ntile) {
+      x_f2_leftovers(N, A, lda, f, k0, nbp, cfirst, ntile, xls);
+      x_exchange(ctr, f.xpart, nbar, ArgMax{-1.0, 0x7fffffff}, sh);
+    }
+  }
   // ---- accepted prefix (every CTA computes p; CTA 0 records it)
   __shared__ unsigned s_fail[2], s_pos[2], s_neg[2];
   if (tid < NB) {
     const int jj = tid;
     const double dj = (jj < nbp) ? ctl->d[jj] : 0.0;
-    const double cm = (jj < nbp) ? bitsd(ctl->colmax[jj]) : 0.0;
+    const double cm = (jj < nbp) ? bitsd(__ldcg(&ctl->colmax[jj])) : 0.0;
     const bool fail = (jj >= nbp) || !(fabs(dj) >= ALPHA_BK * cm);
     const double tol = ctl->tol;
     const unsigned b = __ballot_sync(0xffffffffu, fail);
@@ -1251,13 +1361,11 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
   const int64_t ldw = f.ldw;
   if (j < jlim) {
     __shared__ double wrow[WCOLS];
-    __shared__ ArgMax sh[33];
     const double tol = ctl->tol;
     const int G = (int)gridDim.x;
     const int64_t chunk = xchunk;   // host: >= ceil((N - k0) / G), multiple of 32
     // the CTA's rows of L (panel columns) in shared memory: Ls[t * lstr + row - rlo]
     // (lstr = 8 mod 16: the 4 k-lanes of a quad fall in opposite bank halves pairwise)
-    extern __shared__ double xls[];
     const int lstr = xchunk + 8;
     const double* Ls = use_ls ? xls : nullptr;
     const int64_t rlo = k0 + (int64_t)blockIdx.x * chunk;
@@ -1270,8 +1378,6 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
       }
       __syncthreads();
     }
-    unsigned* ctr = f.xbar + f.pidx;   // this panel's barrier counter (zeroed by k_factor_init)
-    unsigned nbar = 0;                 // barriers so far
     while (j < jlim) {
       const int64_t k = k0 + j;
       for (int t = tid; t < j; t += XT) wrow[t] = __ldcg(&W[k + t * ldw]);
@@ -2241,12 +2347,13 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   // F4 (acceptance + exact BK columns): multi-CTA, ~256 rows per CTA, all CTAs co-resident
   const bool f4_one_cta = std::getenv("MDS_SLOW_1CTA") != nullptr;   // A/B: the single-CTA k_panel_slow
   const bool f4_no_ls = std::getenv("MDS_EXACT_NO_LS") != nullptr;   // A/B: L rows read from L2
+  const bool no_f2fold = std::getenv("MDS_F2_TRSM") != nullptr;       // A/B: leftover F2 tiles by k_panel_trsm
   static bool f4_attr = false;
   if (!f4_attr) {
     cudaFuncSetAttribute(k_panel_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, XLS_MAX);
     f4_attr = true;
   }
-  auto launch_f4 = [&](const FWork& fp, int64_t rows) -> int {
+  auto launch_f4 = [&](const FWork& fp, int64_t rows, int f2left) -> int {
     if (f4_one_cta) {
       MDS_LAUNCH(PC_PANEL_SLOW, st, MDS_CUDA_TRY(launch_pdl(k_panel_slow, dim3(1), dim3(1024), 0, st, N, M, ldm, fp, piv)));
       return MDS_OK;
@@ -2257,8 +2364,9 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     // (not for concurrent factorizations: a large shared-memory request per CTA would compete
     //  with the other streams' kernels even when no column takes the exact path)
     const int use_ls = (lsb <= (size_t)XLS_MAX && !f4_no_ls && !capped) ? 1 : 0;
-    MDS_LAUNCH(PC_PANEL_SLOW, st, MDS_CUDA_TRY(launch_pdl(k_panel_exact, dim3(g), dim3(XT), use_ls ? lsb : 0, st, N, M, ldm,
-                                                          fp, piv, chunk, use_ls)));
+    const size_t dsm = std::max<size_t>(use_ls ? lsb : 0, f2left ? usmem : 0);
+    MDS_LAUNCH(PC_PANEL_SLOW, st, MDS_CUDA_TRY(launch_pdl(k_panel_exact, dim3(g), dim3(XT), dsm, st, N, M, ldm,
+                                                          fp, piv, chunk, use_ls, f2left)));
     return MDS_OK;
   };
   if (lookahead) {
@@ -2285,14 +2393,19 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     for (;; p++) {
       const int64_t rows = rows_of(p);
       const FWork fp = fwork_for(p);
+      // F2 tiles U(p-1) did not take: a separate k_panel_trsm for the first panel (no U before it),
+      // else done inside k_panel_exact (one launch fewer on the U(p-1) -> U(p) hand-off)
+      const bool trsm_launch = !tail && (p == 0 || f4_one_cta || no_f2fold || capped);
       if (!tail) {
         if (p > 0) MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(p - 1, 1), 0));   // F1(p) (or U(p-1)) on the side stream
-        const unsigned g64 = (unsigned)std::max<int64_t>(mds_cdiv(rows, UT), 1);
-        MDS_LAUNCH(PC_PANEL_TRSM, st, (k_panel_trsm<<<g64, 128, usmem, st>>>(N, M, ldm, fp)));
+        if (trsm_launch) {
+          const unsigned g64 = (unsigned)std::max<int64_t>(mds_cdiv(rows, UT), 1);
+          MDS_LAUNCH(PC_PANEL_TRSM, st, (k_panel_trsm<<<g64, 128, usmem, st>>>(N, M, ldm, fp)));
+        }
       } else if (p > 0) {
         MDS_CUDA_TRY(cudaStreamWaitEvent(st, ev(p - 1, 1), 0));   // U(p-1) on the side stream
       }
-      if (int rc = launch_f4(fp, rows)) return rc;
+      if (int rc = launch_f4(fp, rows, (!tail && !trsm_launch) ? 1 : 0)) return rc;
       MDS_CUDA_TRY(cudaEventRecord(ev(p, 0), st));
       const int64_t n2max = std::max<int64_t>(rows - 1, 0);
       const int64_t nt = mds_cdiv(n2max, UT) + 1;
@@ -2343,7 +2456,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
       const int64_t nt = mds_cdiv(n2max, UT) + 1;
       MDS_LAUNCH(PC_PANEL_DIAG, st, (k_panel_diag<<<1, 256, F1SMEM, st>>>(N, M, ldm, fp)));
       MDS_LAUNCH(PC_PANEL_TRSM, st, (k_panel_trsm<<<g64, 128, usmem, st>>>(N, M, ldm, fp)));
-      if (int rc = launch_f4(fp, rows)) return rc;
+      if (int rc = launch_f4(fp, rows, 0)) return rc;
       const CUtensorMap& mw = (p & 1) ? mapW1 : mapW;
       const CUtensorMap& ml = (p & 1) ? mapL1 : mapL0;
       MDS_LAUNCH(PC_PANEL_STORE, st, (k_panel_store<<<dim3(g256, 8), 256, 0, st>>>(N, M, ldm, fp)));

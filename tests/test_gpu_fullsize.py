@@ -103,13 +103,14 @@ def test_pivoting_heavy_multi_panel(N, n2):
 # mds_factor call.)  "odd ldm" disables the TMA path (16-byte alignment), so the
 # cp.async update kernel without look-ahead runs.
 @pytest.mark.parametrize("variant", ["tail_always", "tail_never", "no_lookahead", "no_tma", "odd_ldm", "no_pdl",
-                                     "static_sched", "upd_main", "inplace", "slow_1cta", "exact_no_ls"])
+                                     "static_sched", "upd_main", "inplace", "slow_1cta", "exact_no_ls", "f2_trsm"])
 def test_factor_variants_pivoting(variant, monkeypatch):
     env = {"tail_always": {"MDS_TAIL_ROWS": "100000000"}, "tail_never": {"MDS_TAIL_ROWS": "0"},
            "no_lookahead": {"MDS_NO_LOOKAHEAD": "1"}, "no_tma": {"MDS_NO_TMA": "1"}, "odd_ldm": {},
            "no_pdl": {"MDS_NO_PDL": "1"}, "static_sched": {"MDS_STATIC_SCHED": "1"},
            "upd_main": {"MDS_UPD_MAIN": "1"}, "inplace": {"MDS_UPD_INPLACE": "1"},
-           "slow_1cta": {"MDS_SLOW_1CTA": "1"}, "exact_no_ls": {"MDS_EXACT_NO_LS": "1"}}[variant]
+           "slow_1cta": {"MDS_SLOW_1CTA": "1"}, "exact_no_ls": {"MDS_EXACT_NO_LS": "1"},
+           "f2_trsm": {"MDS_F2_TRSM": "1"}}[variant]
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     N, n2 = 1500, 300
