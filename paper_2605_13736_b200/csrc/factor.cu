@@ -2331,7 +2331,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   // (not when factorizations run concurrently (grid cap set): the tail launch's F2-role CTAs
   //  spin for X while F1 runs, which is free on an idle GPU but starves the other streams --
   //  C4: 3278 -> 4022 scenario-steps/s without it)
-  const int64_t tail_rows = std::getenv("MDS_TAIL_ROWS") ? std::atoll(std::getenv("MDS_TAIL_ROWS")) : (capped ? 0 : 4800);
+  const int64_t tail_rows = std::getenv("MDS_TAIL_ROWS") ? std::atoll(std::getenv("MDS_TAIL_ROWS")) : (capped ? 0 : 3500);
   if (capped) sms = g_grid_cap;
   const size_t usmem = 2 * NB * US * sizeof(double);
   auto fwork_for = [&](int64_t p) {
