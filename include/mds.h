@@ -171,6 +171,26 @@ int ipm_step_vectors(int64_t n, const double *x, const double *dx, const double 
                      void *work, size_t work_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * mds_kkt_residual — the K2 mixed sparse/dense mat-vec of PAPER.md:185 on the
+ * FULL (uncondensed) Eq.(5) matrix of PAPER.md:147-159:
+ *   K = [ Q_s     0      J_s  ]   Q_s = diag(h_ss + sigma_s + delta_w)
+ *       [ 0       Q_d    J_d^T]   Q_d = H_dd + diag(sigma_d) + delta_w I
+ *       [ J_s^T   J_d   -D_y  ]   D_y = diag(0_{m_E}, 1/d_h) + delta_c I
+ * out = b - K x (b != NULL) or K x (b == NULL), x/b/out laid out
+ * [x_s (n_s) | x_d (n_d) | y_g (m_E) | y_h (m_I)] (device, caller-owned, out
+ * must not alias x).  The same inputs as mds_condense (same layouts, H_dd lower
+ * read).  rnorm: optional device scalar, ||out||_inf.  work: >=
+ * mds_kkt_residual_workspace_size(m) bytes.  Used to check a whole Newton
+ * step (condense + factor + solve + recovery) against the original system, and
+ * as the residual of iterative refinement.  No data errors (argument errors
+ * only); deterministic (fixed-order sums). */
+size_t mds_kkt_residual_workspace_size(int64_t m);
+int mds_kkt_residual(const mds_plan *plan, const double *js_val, const double *h_ss, const double *sigma_s,
+                     const double *H_dd, int64_t ldh, const double *sigma_d, const double *J_d, int64_t ldj,
+                     const double *d_h, double delta_w, double delta_c, const double *x, const double *b,
+                     double *out, double *rnorm, void *work, size_t work_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
  * Instrumentation (not on the hot path; used by bench.py for the roofline).
  * mds_launch_count: number of kernels this library has launched since load.
  * mds_profile_begin / mds_profile_end: while enabled, every kernel launch of

@@ -249,3 +249,29 @@ def inertia_correction(prob, mu, delta_w_last=0.0, params=None):
     dxy = bk_solve(f["LD"], f["ipiv"], f["rhs"], f["tol"])
     dx_s = recover(q, f["w"], np.asarray(q.r)[:q.n_s], dxy[q.n_d:])
     return dict(delta_w=dw, delta_c=dc, delta_w_last=delta_w_last, trials=trials, inertia=ine, dxy=dxy, dx_s=dx_s)
+
+
+# ----------------------------------------------------------------------------- K2 mat-vec
+def kkt_matvec(prob, x):
+    """K x for the full (uncondensed) Eq.(5) matrix, x laid out
+    [x_s | x_d | y_g | y_h]: the block definition written out with library
+    products (scipy CSR mat-vec for J_s, numpy for the dense blocks; H_dd from its
+    lower triangle, R14):
+      (Kx)_s = (h_ss + sigma_s + delta_w) x_s + J_s y
+      (Kx)_d = (H_dd + diag(sigma_d) + delta_w I) x_d + J_d^T y
+      (Kx)_y = J_s^T x_s + J_d x_d - (diag(0_{m_E}, 1/d_h) + delta_c I) y"""
+    import scipy.sparse as sp
+    n_s, n_d, m_E, m_I = prob.n_s, prob.n_d, prob.m_E, prob.m_I
+    m = m_E + m_I
+    x = np.asarray(x, dtype=np.float64)
+    xs, xd, y = x[:n_s], x[n_s:n_s + n_d], x[n_s + n_d:]
+    Js = sp.csr_matrix((np.asarray(prob.val, dtype=np.float64), np.asarray(prob.colidx), np.asarray(prob.rowptr)),
+                       shape=(n_s, m))
+    H = np.asarray(prob.H_dd, dtype=np.float64)
+    Hs = np.tril(H) + np.tril(H, -1).T if n_d else np.zeros((0, 0))
+    Jd = np.asarray(prob.J_d, dtype=np.float64).reshape(m, n_d) if n_d and m else np.zeros((m, n_d))
+    ks = (np.asarray(prob.h_ss) + np.asarray(prob.sigma_s) + prob.delta_w) * xs + Js @ y
+    kd = Hs @ xd + (np.asarray(prob.sigma_d) + prob.delta_w) * xd + Jd.T @ y
+    dy = np.concatenate([np.zeros(m_E), 1.0 / np.asarray(prob.d_h, dtype=np.float64)]) + prob.delta_c
+    ky = Js.T @ xs + Jd @ xd - dy * y
+    return np.concatenate([ks, kd, ky])

@@ -53,7 +53,13 @@ for _f in ("mds_plan_create", "mds_plan_destroy", "mds_plan_dims", "mds_condense
            "ipm_step_vectors"):
     getattr(_lib, _f).restype = ctypes.c_int
 
-EXPORTS = ["mds_version", "mds_plan_create", "mds_plan_destroy", "mds_plan_dims", "mds_condense",
+_lib.mds_kkt_residual_workspace_size.restype = ctypes.c_size_t
+_lib.mds_kkt_residual_workspace_size.argtypes = [_I64]
+_lib.mds_kkt_residual.argtypes = [_P, _P, _P, _P, _P, _I64, _P, _P, _I64, _P, _D, _D, _P, _P, _P, _P, _P,
+                                  ctypes.c_size_t, _P]
+_lib.mds_kkt_residual.restype = ctypes.c_int
+
+EXPORTS = ["mds_kkt_residual_workspace_size", "mds_kkt_residual", "mds_version", "mds_plan_create", "mds_plan_destroy", "mds_plan_dims", "mds_condense",
            "mds_factor_workspace_size", "mds_factor", "mds_solve_workspace_size", "mds_solve",
            "ipm_step_vectors_workspace_size", "ipm_step_vectors", "mds_launch_count", "mds_profile_begin",
            "mds_profile_end", "mds_factor_panels", "mds_factor_set_grid_cap", "mds_profile_timeline"]
@@ -178,6 +184,19 @@ def solve(plan, N, LD, ldm, piv, rhs_c, js_val, w, r_xs, dxy, dx_s, zero_tol, fw
                           _ptr(fwork), _ptr(status), _ptr(work), work.numel() * work.element_size(),
                           _stream(stream))
     _check(code, "mds_solve")
+
+
+def kkt_residual(plan, js_val, h_ss, sigma_s, H_dd, ldh, sigma_d, J_d, ldj, d_h, delta_w, delta_c, x, b, out,
+                 rnorm=None, work=None, stream=None):
+    """mds_kkt_residual: out = b - K x on the full Eq.(5) matrix (K x if b is None)."""
+    if work is None:
+        work = torch.empty(int(_lib.mds_kkt_residual_workspace_size(plan.m_E + plan.m_I)), dtype=torch.uint8,
+                           device=out.device)
+    code = _lib.mds_kkt_residual(plan.handle, _f64(js_val), _f64(h_ss), _f64(sigma_s), _f64(H_dd), int(ldh),
+                                 _f64(sigma_d), _f64(J_d), int(ldj), _f64(d_h), float(delta_w), float(delta_c),
+                                 _f64(x), _f64(b), _f64(out), _f64(rnorm), _ptr(work), work.numel(), _stream(stream))
+    _check(code, "mds_kkt_residual")
+    return out
 
 
 def step_vectors(n, x, dx, lo, up, zl, zu, dzl, dzu, tau, mu, out, sigma_out, status, work, res=(), stream=None):

@@ -108,6 +108,8 @@ extern "C" int mds_plan_dims(const mds_plan* P, int64_t* out) {
 // accessor for solve.cu (same library)
 const int32_t* mds_plan_rowptr(const mds_plan* P) { return P->rowptr; }
 const int32_t* mds_plan_colidx(const mds_plan* P) { return P->colidx; }
+const int32_t* mds_plan_tptr(const mds_plan* P) { return P->tptr; }
+const int2* mds_plan_tkp(const mds_plan* P) { return P->tkp; }
 
 // ---------------------------------------------------------------------------
 // w_k = 1/q_k, q_k = h_ss + sigma_s + delta_w  (Q_{x_s}^{-1}, A2 PAPER.md:121)
