@@ -259,3 +259,39 @@ def test_graph_replay_matches_eager():
     assert rep["inertia"] == eager["inertia"]
     np.testing.assert_array_equal(rep["dxy"], eager["dxy"])
     np.testing.assert_array_equal(rep["dx_s"], eager["dx_s"])
+
+
+# ---------------------------------------------------------------- degenerate sizes
+@pytest.mark.parametrize("A,ine", [
+    (np.array([[2.5]]), (1, 0, 0)), (np.array([[-3.0]]), (0, 0, 1)),
+    (np.array([[0.0, 1.0], [1.0, 0.0]]), (1, 0, 1)),                      # one 2x2 pivot
+    (np.array([[1e-3, 2.0, 0.0], [2.0, 1e-3, 1.0], [0.0, 1.0, -4.0]]), None),
+])
+def test_tiny_dense(A, ine):
+    b = np.arange(1.0, A.shape[0] + 1.0)
+    LD, ipiv, _ = oracle.bk_factor(np.asfortranarray(np.tril(A)))
+    tol = oracle.default_tol(np.tril(A))
+    exp = oracle.inertia(LD, ipiv, tol)
+    if ine is not None:
+        assert exp == ine
+    g_ine, x, status, _ = factor_solve_dense(np.tril(A), b)
+    assert status == 0 and g_ine == exp
+    assert np.abs(A @ x - b).max() <= 1e-12 * np.abs(b).max() * max(1.0, np.abs(A).max())
+
+
+def test_singular_1x1():
+    g_ine, x, status, _ = factor_solve_dense(np.array([[0.0]]), np.array([1.0]))
+    assert g_ine == (0, 1, 0) and status == mds.SingularError.code
+
+
+@pytest.mark.parametrize("shape", [(0, 30, 10, 12), (3000, 64, 64, 0), (2500, 0, 40, 24), (777, 63, 1, 1)])
+def test_full_step_edge_shapes(shape):
+    # no sparse block, no inequalities, no dense variables, N = 65 (one full panel + 1)
+    prob = mdsgen.g1_quasidefinite(*shape, seed=3 + sum(shape))
+    st, out = run_step(prob)
+    ref = oracle.newton_step(prob)
+    assert out["status"] == 0
+    assert out["inertia"] == ref["inertia"] == prob.expected_inertia
+    check_x(ref["M"], ref["rhs_c"], out["dxy"], ref["dxy"])
+    if prob.n_s:
+        assert rel_inf(out["dx_s"], ref["dx_s"]) <= X_TOL
