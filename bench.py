@@ -498,6 +498,11 @@ def run_scopf(args, rank, world):
                            "parallelism": f"scenario-dp{world}", "cuda_graph": True},
                 "gpu_launches": per_scen * len(ids) * args.steps,
                 "factor_solve_fp64_tflops_aggregate": fl / (ms_max * 1e-3) / 1e12,
+                "roofline": {"kernel": "whole batch (factor+solve flops of all scenarios / step time)",
+                             "bound": "tensor", "achieved": fl / (ms_max * 1e-3) / 1e12 / world,
+                             "peak": fp64_peak()[0], "unit": "TFLOP/s",
+                             "frac": fl / (ms_max * 1e-3) / 1e12 / world / fp64_peak()[0], "traffic": None,
+                             "note": "per GPU; concurrent scenarios, no single dominant launch"},
                 "stop_test": st, "records_gathered": int(recs.shape[0]),
                 "all_inertia_ok": bool(st["n_bad_inertia"] == 0), "setup_s": setup_s,
                 "clocks": clk.summary(), "e2e": None, "cpu_baseline": None}
