@@ -19,4 +19,7 @@ ncu -i gpurun_out/misc_full.ncu-rep --page raw --csv > gpurun_out/misc_full_raw.
 timeout 900 ncu --set full --clock-control none -k regex:k_panel_exact --launch-skip 200 --launch-count 1 \
     -o gpurun_out/exact_full -f python bench.py --config C5 --steps 1 --warmup 0 --no-cpu --no-e2e > /dev/null 2>&1
 ncu -i gpurun_out/exact_full.ncu-rep --page raw --csv > gpurun_out/exact_full_raw.csv
+ncu --set full --clock-control none -k regex:"k_step_vectors|k_trsv_fwd|k_trsv_bwd|k_recover|k_inv_blocks|k_gather|k_dsolve" \
+    --launch-count 7 -o gpurun_out/solve_full -f $B > /dev/null 2>&1
+ncu -i gpurun_out/solve_full.ncu-rep --page raw --csv > gpurun_out/solve_full_raw.csv
 ls -la gpurun_out

@@ -74,6 +74,7 @@ def full_summary(rep, out):
 
 launch_summary()
 for rep, out in [("upd_full_raw.csv", f"ncu_k_update_tma_{tag}.csv"), ("misc_full_raw.csv", f"ncu_misc_{tag}.csv"),
-                 ("exact_full_raw.csv", f"ncu_k_panel_exact_{tag}.csv")]:
+                 ("exact_full_raw.csv", f"ncu_k_panel_exact_{tag}.csv"),
+                 ("solve_full_raw.csv", f"ncu_solve_vectors_{tag}.csv")]:
     full_summary(rep, out)
 print("\n".join(sorted(os.listdir(dst))))
