@@ -157,65 +157,66 @@ __global__ void k_factor_init(int64_t N, FWork f, double zero_tol) {
 }
 
 // ||M||_inf (row abs-sums via symmetry, lower storage) + non-finite scan.
-// One CTA per 64x64 lower tile: each thread has its 16 loads in flight at once
-// (rows contiguous across the warp), row and column partials reduced in the CTA,
-// then 64 + 64 atomic adds into rowsum.  (HBM-bound: N^2/2 * 8 bytes.)
-constexpr int AT = 64;
-__global__ void __launch_bounds__(256) k_anorm_tiles(int64_t N, const double* __restrict__ A, int64_t lda,
+// One CTA per lower block of ANR rows x ANC columns: thread t owns row r0+t and
+// has its ANC loads in flight at once; each column segment a CTA reads is
+// ANR*8 = 2 KB contiguous (DRAM-page friendly).  Row sums need no reduction
+// (one owner thread); column sums by warp shuffles + shared memory; then
+// ANR + ANC atomic adds into rowsum.  (HBM-bound: N^2/2 * 8 bytes.)
+constexpr int ANR = 256, ANC = 32;
+__global__ void __launch_bounds__(ANR) k_anorm_tiles(int64_t N, const double* __restrict__ A, int64_t lda,
                                                      double* rowsum, FCtl* ctl, int32_t* status) {
   pdl_wait();
   pdl_trigger();
-  const int64_t nt = (N + AT - 1) / AT;
+  // blocks (bi, bj): row block bi (ANR rows), column block bj (ANC columns) with bj*ANC < (bi+1)*ANR
+  const int64_t ncb = (N + ANC - 1) / ANC;
+  constexpr int RATIO = ANR / ANC;
   const int64_t x = blockIdx.x;
-  int64_t bi = (int64_t)((sqrt(8.0 * (double)x + 1.0) - 1.0) * 0.5);
-  while (bi * (bi + 1) / 2 > x) bi--;
-  while ((bi + 1) * (bi + 2) / 2 <= x) bi++;
-  const int64_t bj = x - bi * (bi + 1) / 2;
-  if (bi >= nt) return;
-  __shared__ double rpart[4][AT];    // row partials per column group
-  __shared__ double cpart[2][AT];    // column partials per row half (one warp each)
-  const int tx = threadIdx.x & (AT - 1), ty = threadIdx.x >> 6;   // row tx, columns ty + 4u
-  const int64_t i = bi * AT + tx;
-  double v[16];
+  // row block bi holds (bi+1)*RATIO column blocks (clipped to ncb): prefix sums are RATIO*bi(bi+1)/2
+  int64_t bi = (int64_t)((sqrt(8.0 * (double)x / RATIO + 1.0) - 1.0) * 0.5);
+  while (bi > 0 && RATIO * bi * (bi + 1) / 2 > x) bi--;
+  while (RATIO * (bi + 1) * (bi + 2) / 2 <= x) bi++;
+  const int64_t bj = x - RATIO * bi * (bi + 1) / 2;
+  if (bj >= ncb || bi * ANR >= N) return;
+  __shared__ double cpart[ANR / 32][ANC];
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int64_t i = bi * ANR + t;
+  double v[ANC];
 #pragma unroll
-  for (int u = 0; u < 16; u++) {
-    const int64_t j = bj * AT + ty + 4 * u;
+  for (int u = 0; u < ANC; u++) {
+    const int64_t j = bj * ANC + u;
     v[u] = (i < N && j < N && i >= j) ? A[i + j * lda] : 0.0;
   }
   bool bad = false;
   double rs = 0.0;
 #pragma unroll
-  for (int u = 0; u < 16; u++) {
+  for (int u = 0; u < ANC; u++) {
     if (!isfinite(v[u])) bad = true;
     v[u] = fabs(v[u]);
     rs += v[u];
   }
   if (__syncthreads_or(bad)) {
-    if (threadIdx.x == 0) { mds_set_status(status, MDS_ERR_NONFINITE); ctl->abort = 1; }
+    if (t == 0) { mds_set_status(status, MDS_ERR_NONFINITE); ctl->abort = 1; }
     return;
   }
-  rpart[ty][tx] = rs;
-  // column sums excluding the diagonal (they are row j's upper part): over the 32 rows of this warp
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, half = (warp & 1);
+  if (i < N && rs != 0.0) atomicAdd(&rowsum[i], rs);
+  // column sums excluding the diagonal (they are row j's upper part)
 #pragma unroll
-  for (int u = 0; u < 16; u++) {
-    const int64_t j = bj * AT + ty + 4 * u;
+  for (int u = 0; u < ANC; u++) {
+    const int64_t j = bj * ANC + u;
     double c = (i > j) ? v[u] : 0.0;
     c += __shfl_xor_sync(0xffffffffu, c, 16);
     c += __shfl_xor_sync(0xffffffffu, c, 8);
     c += __shfl_xor_sync(0xffffffffu, c, 4);
     c += __shfl_xor_sync(0xffffffffu, c, 2);
     c += __shfl_xor_sync(0xffffffffu, c, 1);
-    if (lane == 0) cpart[half][ty + 4 * u] = c;
+    if (lane == 0) cpart[warp][u] = c;
   }
   __syncthreads();
-  if (threadIdx.x < AT) {
-    const double s2 = (rpart[0][tx] + rpart[1][tx]) + (rpart[2][tx] + rpart[3][tx]);
-    if (i < N && s2 != 0.0) atomicAdd(&rowsum[i], s2);
-  } else if (threadIdx.x < 2 * AT) {
-    const int c = threadIdx.x - AT;
-    const int64_t j = bj * AT + c;
-    const double s2 = cpart[0][c] + cpart[1][c];
+  if (t < ANC) {
+    double s2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < ANR / 32; w++) s2 += cpart[w][t];
+    const int64_t j = bj * ANC + t;
     if (j < N && s2 != 0.0) atomicAdd(&rowsum[j], s2);
   }
 }
@@ -2266,9 +2267,9 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
              MDS_CUDA_TRY(launch_pdl(k_factor_init, dim3((unsigned)std::min<int64_t>(mds_cdiv(3 * (N + 2), 256), 1184)),
                                      dim3(256), 0, st, N, f, zero_tol)));
   {
-    int64_t nt = (N + AT - 1) / AT;
+    const int64_t nrb = (N + ANR - 1) / ANR, nblk = (ANR / ANC) * nrb * (nrb + 1) / 2;
     MDS_LAUNCH(PC_ANORM, st,
-               MDS_CUDA_TRY(launch_pdl(k_anorm_tiles, dim3((unsigned)(nt * (nt + 1) / 2)), dim3(256), 0, st, N, M, ldm,
+               MDS_CUDA_TRY(launch_pdl(k_anorm_tiles, dim3((unsigned)nblk), dim3(ANR), 0, st, N, M, ldm,
                                        f.rowsum, f.ctl, status)));
     MDS_LAUNCH(PC_ANORM, st, MDS_CUDA_TRY(launch_pdl(k_anorm_final, dim3(1), dim3(1024), 0, st, N, f.rowsum, f.ctl)));
   }
