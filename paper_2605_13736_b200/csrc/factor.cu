@@ -2359,7 +2359,8 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
       MDS_LAUNCH(PC_PANEL_SLOW, st, MDS_CUDA_TRY(launch_pdl(k_panel_slow, dim3(1), dim3(1024), 0, st, N, M, ldm, fp, piv)));
       return MDS_OK;
     }
-    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>({mds_cdiv(rows, 256), (int64_t)sms, (int64_t)XMAXG}));
+    static const int64_t xrows = std::getenv("MDS_EXACT_ROWS") ? std::atoll(std::getenv("MDS_EXACT_ROWS")) : 256;
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>({mds_cdiv(rows, xrows), (int64_t)sms, (int64_t)XMAXG}));
     const int chunk = (int)(mds_cdiv(mds_cdiv(std::max<int64_t>(rows, 1), g), 32) * 32);
     const size_t lsb = (size_t)NB * (chunk + 8) * sizeof(double);
     // (not for concurrent factorizations: a large shared-memory request per CTA would compete
