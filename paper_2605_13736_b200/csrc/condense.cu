@@ -131,7 +131,11 @@ __global__ void k_condense_dense(int64_t n_d, int64_t m, const double* __restric
                                  const double* __restrict__ Jd, int64_t ldj,
                                  double* __restrict__ M, int64_t ldm,
                                  const double* __restrict__ r_xd, double* __restrict__ rhs_c) {
-  pdl_wait();
+  // Launched right after k_condense_yy (programmatic dependent launch) and independent of it
+  // (inputs only; disjoint outputs), so it starts as soon as k_condense_yy has started -- whose
+  // own griddepcontrol.wait already ordered everything before mds_condense -- and runs in the
+  // SM slots the latency-bound k_condense_yy leaves free.  It waits for k_condense_yy only at
+  // its end, so its completion (what the next kernel waits for) implies the whole condensation.
   pdl_trigger();
   for (int64_t j = blockIdx.x; j < n_d; j += gridDim.x) {
     double* Mj = M + j * ldm;
@@ -145,6 +149,7 @@ __global__ void k_condense_dense(int64_t n_d, int64_t m, const double* __restric
     for (int64_t c = threadIdx.x; c < m; c += blockDim.x) Mj[n_d + c] = Jj[c];
     if (threadIdx.x == 0 && rhs_c) rhs_c[j] = r_xd[j];
   }
+  pdl_wait();
 }
 
 // M_yy column c (rows c..m-1 of the (y,y) block).  One WARP owns output
@@ -379,12 +384,6 @@ extern "C" int mds_condense(const mds_plan* P, const double* js_val, const doubl
                MDS_CUDA_TRY(launch_pdl(k_condense_w, dim3((unsigned)blocks), dim3(256), 0, st, n_s, h_ss, sigma_s, delta_w,
                                        w_out, status)));
   }
-  if (n_d > 0) {
-    int64_t blocks = std::min<int64_t>(n_d, 148 * 8);
-    MDS_LAUNCH(PC_CONDENSE_DENSE, st,
-               MDS_CUDA_TRY(launch_pdl(k_condense_dense, dim3((unsigned)blocks), dim3(256), 0, st, n_d, m, H_dd, ldh, sigma_d,
-                                       delta_w, J_d, ldj, M, ldm, r ? r + n_s : nullptr, rhs_c)));
-  }
   if (m > 0) {
     // warp-private accumulator columns: <= 4096 doubles each; warps per CTA sized to ~192 KB
     // (MDS_YY_ACC caps the column window: longer columns take several passes over their list,
@@ -422,6 +421,13 @@ extern "C" int mds_condense(const mds_plan* P, const double* js_val, const doubl
                      n_d, P->m_E, m, acc_len, P->rowptr, P->colidx, js_val, P->tptr, P->tkp, w_out, d_h, delta_c,
                      r, n_s, M, ldm, rhs_c, status)));
     }
+  }
+  // dense blocks after (and concurrently with) k_condense_yy; see k_condense_dense
+  if (n_d > 0) {
+    int64_t blocks = std::min<int64_t>(n_d, 148 * 8);
+    MDS_LAUNCH(PC_CONDENSE_DENSE, st,
+               MDS_CUDA_TRY(launch_pdl(k_condense_dense, dim3((unsigned)blocks), dim3(256), 0, st, n_d, m, H_dd, ldh, sigma_d,
+                                       delta_w, J_d, ldj, M, ldm, r ? r + n_s : nullptr, rhs_c)));
   }
   return MDS_OK;
 }
