@@ -422,6 +422,10 @@ def run_ours(args, rank, world):
                 "condense_gbs": alg["condense_bytes"] / (wall["condense"] * 1e-3) / 1e9,
                 "condense_frac_of_hbm": alg["condense_bytes"] / (wall["condense"] * 1e-3) / 1e9 / hbm,
                 "solve_gbs": alg["solve_bytes"] / (wall["solve"] * 1e-3) / 1e9,
+                # K1 barrier vectors: 8 FP64 inputs + sigma out per (x_s, x_d) component, plus the
+                # residual vector's inf-norm read (~72 B per bounded component)
+                "vectors_gbs": (72 * (prob.n_s + prob.n_d) + 8 * (prob.n_s + prob.N)) /
+                               (prof["vectors"][0] * 1e-3) / 1e9 if prof["vectors"][0] > 0 else None,
                 "hbm_peak_gbs": hbm, "hbm_peak_source": hbm_src,
                 "phase_ms_wall": wall,
                 "phase_ms_kernel_sum": {"condense": cond_ms, "factor": fac_ms, "solve": sol_ms,
