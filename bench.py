@@ -339,7 +339,7 @@ def run_ours(args, rank, world):
     prof = mds.profile_end()
     st.check_status()
     tot = sum(v[0] for v in prof.values())
-    fac_ms = sum(prof[c][0] for c in ("anorm", "panel_diag", "panel_trsm", "panel_store", "panel_slow", "update",
+    fac_ms = sum(prof[c][0] for c in ("anorm", "panel_diag", "panel_trsm", "panel_store", "panel_exact", "update",
                                       "finalize"))
     sol_ms = sum(prof[c][0] for c in ("solve_gather", "solve_fwd", "solve_d", "solve_bwd", "solve_scatter",
                                       "recover"))

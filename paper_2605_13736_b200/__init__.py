@@ -65,7 +65,7 @@ EXPORTS = ["mds_kkt_residual_workspace_size", "mds_kkt_residual", "mds_version",
            "mds_profile_end", "mds_factor_panels", "mds_factor_set_grid_cap", "mds_profile_timeline"]
 
 PROF_CLASSES = ["condense_w", "condense_dense", "condense_yy", "anorm", "panel_diag", "panel_trsm", "panel_store",
-                "panel_slow", "update", "finalize", "solve_gather", "solve_fwd", "solve_d", "solve_bwd",
+                "panel_exact", "update", "finalize", "solve_gather", "solve_fwd", "solve_d", "solve_bwd",
                 "solve_scatter", "recover", "vectors"]
 
 
