@@ -217,6 +217,18 @@ unsigned long long mds_launch_count(void);
  * every cap value below the SM count, and differ from the uncapped structure
  * only by rounding order. */
 int mds_factor_set_grid_cap(int ctas);
+/* Launch-structure variants of mds_factor / mds_solve for A/B measurement and
+ * for the variant parity tests (process-wide; the library never reads the
+ * environment).  Every variant computes the same Bunch-Kaufman factorization
+ * (same pivot rule, same inertia); results differ only by rounding order.
+ * key: "default" (reset all), "tail_rows" (panels with at most this many rows
+ * left use the one-launch tail path; < 0 = built-in choice), "exact_rows"
+ * (rows per CTA of the multi-CTA exact panel, >= 32), and the flags "no_tma",
+ * "no_lookahead", "static_sched", "no_snake", "no_cprefetch", "upd_inplace",
+ * "upd_main", "slow_1cta", "exact_no_ls", "f2_trsm", "no_pdl" (value 0/1).
+ * Returns MDS_ERR_ARG for an unknown key.  Not thread-safe against concurrent
+ * mds_factor calls (set it between calls). */
+int mds_set_variant(const char *key, long long value);
 int mds_profile_begin(void);
 int mds_profile_end(double *ms_by_class, int64_t *launches_by_class, int ncls);
 int64_t mds_factor_panels(const void *fwork, int64_t N, int32_t *starts_host, int64_t cap);

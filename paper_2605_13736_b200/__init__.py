@@ -62,7 +62,7 @@ _lib.mds_kkt_residual.restype = ctypes.c_int
 EXPORTS = ["mds_kkt_residual_workspace_size", "mds_kkt_residual", "mds_version", "mds_plan_create", "mds_plan_destroy", "mds_plan_dims", "mds_condense",
            "mds_factor_workspace_size", "mds_factor", "mds_solve_workspace_size", "mds_solve",
            "ipm_step_vectors_workspace_size", "ipm_step_vectors", "mds_launch_count", "mds_profile_begin",
-           "mds_profile_end", "mds_factor_panels", "mds_factor_set_grid_cap", "mds_profile_timeline"]
+           "mds_profile_end", "mds_factor_panels", "mds_factor_set_grid_cap", "mds_profile_timeline", "mds_set_variant"]
 
 PROF_CLASSES = ["condense_w", "condense_dense", "condense_yy", "anorm", "panel_diag", "panel_trsm", "panel_store",
                 "panel_exact", "update", "finalize", "solve_gather", "solve_fwd", "solve_d", "solve_bwd",
@@ -214,6 +214,14 @@ def set_grid_cap(ctas: int):
     """Cap the persistent update kernels' CTAs (0 = all SMs); for concurrent streams."""
     _lib.mds_factor_set_grid_cap.argtypes = [ctypes.c_int]
     _check(_lib.mds_factor_set_grid_cap(int(ctas)), "mds_factor_set_grid_cap")
+
+
+def set_variant(key: str, value: int = 1):
+    """mds_set_variant: select a launch-structure variant (A/B measurement and variant
+    parity tests; "default" resets all).  Results differ only by rounding order."""
+    _lib.mds_set_variant.argtypes = [ctypes.c_char_p, ctypes.c_longlong]
+    _lib.mds_set_variant.restype = ctypes.c_int
+    _check(_lib.mds_set_variant(key.encode(), int(value)), "mds_set_variant")
 
 
 def launch_count() -> int:

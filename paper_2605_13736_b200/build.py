@@ -8,7 +8,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmds_b200.so")
 SOURCES = ["condense.cu", "factor.cu", "solve.cu", "vectors.cu", "residual.cu", "prof.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = [*(["-DMDS_YY_NOMATCH"] if os.environ.get("MDS_YY_NOMATCH") else []), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-warn-spills"]
 
 

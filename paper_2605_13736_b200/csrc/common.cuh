@@ -67,9 +67,26 @@ static inline int64_t mds_cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // successors can never block this grid's own CTAs).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+// ---------------------------------------------------------------------------
+// Launch-structure variants (mds_set_variant, include/mds.h): process-wide,
+// explicit API only -- no environment variable is ever read.  Every variant is
+// the same Bunch-Kaufman factorization (parity-tested); they differ in launch
+// structure and therefore only in rounding order.
+struct MdsVariant {
+  long long tail_rows = -1;     // <0: default (3500, or 0 when the grid cap is set)
+  long long exact_rows = 256;   // rows per CTA of k_panel_exact
+  int no_tma = 0, no_lookahead = 0, static_sched = 0, no_snake = 0, no_cprefetch = 0;
+  int upd_inplace = 0, upd_main = 0, slow_1cta = 0, exact_no_ls = 0, f2_trsm = 0, no_pdl = 0;
+};
+extern MdsVariant g_mds_var;
+
+// true exactly once per (current device, key): guards per-device one-time setup
+// such as cudaFuncSetAttribute (thread-safe; attributes are per device)
+bool mds_once_per_device(const void* key);
+
 template <typename... KArgs, typename... Args>
 static inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t st, Args... args) {
-  static const bool off = std::getenv("MDS_NO_PDL") != nullptr;
+  const bool off = g_mds_var.no_pdl != 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = g;
   cfg.blockDim = b;
@@ -80,6 +97,29 @@ static inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = off ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
+// Cooperative + programmatic-dependent launch: for kernels whose CTAs meet at
+// a software grid barrier (k_panel_exact).  The cooperative attribute makes
+// the runtime guarantee that every CTA of the grid is resident at once (so
+// the barrier cannot deadlock even when other streams' kernels share the GPU);
+// the grid must not exceed the co-resident capacity (checked by the runtime).
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_coop_pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t st,
+                                          Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_mds_var.no_pdl ? 1 : 2;
   return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 

@@ -2071,7 +2071,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
     if (leader) {
 #pragma unroll
       for (int b = 0; b < 4; b++)
-        if (!(sched & 4)) tma_reduce_add_2d(&mapA, (int)(R0 + 16 * b), (int)C0, Ot + b * TBOXB);   // (bit 2: timing experiment)
+        tma_reduce_add_2d(&mapA, (int)(R0 + 16 * b), (int)C0, Ot + b * TBOXB);
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       if (!OUTB) {
         asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");   // smem source consumed
@@ -2095,17 +2095,16 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 PFN_encodeTiled get_encode() {
-  static PFN_encodeTiled fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  static const PFN_encodeTiled fn = []() -> PFN_encodeTiled {   // thread-safe one-time lookup
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
+    PFN_encodeTiled r = nullptr;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_encodeTiled>(p);
+      r = reinterpret_cast<PFN_encodeTiled>(p);
     (void)cudaGetLastError();
-  }
+    return r;
+  }();
   return fn;
 }
 
@@ -2138,7 +2137,13 @@ __global__ void k_factor_finalize(int64_t N, double* __restrict__ A, int64_t lda
     inertia_out->zero = ctl->inertia[1];
     inertia_out->neg = ctl->inertia[2];
   }
-  if (ctl->abort) return;
+  if (ctl->abort) {
+    // nothing was factored (non-finite input): leave a valid identity permutation with
+    // 1x1 blocks so that a solve issued without looking at the status (a captured
+    // graph) reads only in-range indices; its result is NaN and the status says why
+    for (int64_t i = gtid; i < N; i += gth) piv[N + i] = (int)i;
+    return;
+  }
   for (int64_t i = gtid; i < N; i += gth) { f.rho[i] = (int)i; f.rhoinv[i] = (int)i; }
   const int npan = ctl->npanel;
   const int nswap = ctl->nswap;
@@ -2273,8 +2278,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
                                        f.rowsum, f.ctl, status)));
     MDS_LAUNCH(PC_ANORM, st, MDS_CUDA_TRY(launch_pdl(k_anorm_final, dim3(1), dim3(1024), 0, st, N, f.rowsum, f.ctl)));
   }
-  static bool attr = false;
-  if (!attr) {
+  if (mds_once_per_device((const void*)k_update_tma<0, true>)) {
     cudaFuncSetAttribute(k_update_tma<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
     cudaFuncSetAttribute(k_update_tma<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
     cudaFuncSetAttribute(k_update_tma<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
@@ -2285,13 +2289,12 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     cudaFuncSetAttribute(k_panel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB * US * (int)sizeof(double));
     cudaFuncSetAttribute(k_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * USTAGE * (int)sizeof(double));
     cudaFuncSetAttribute(k_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * USTAGE * (int)sizeof(double));
-    attr = true;
   }
   // 16-byte cp.async path needs a 16-byte aligned M, even ldm and a 16-byte aligned W
   const bool v16 = ((reinterpret_cast<uintptr_t>(M) & 15) == 0) && (ldm % 2 == 0) &&
                    ((reinterpret_cast<uintptr_t>(f.W) & 15) == 0);
   CUtensorMap mapA, mapW;
-  const bool use_tma = v16 && std::getenv("MDS_NO_TMA") == nullptr && make_map(&mapA, M, N, N, ldm) &&
+  const bool use_tma = v16 && !g_mds_var.no_tma && make_map(&mapA, M, N, N, ldm) &&
                        make_map(&mapW, f.W, N, NB, f.ldw);
   int sms = 148;
   {
@@ -2308,7 +2311,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   // p+1's F2 tiles before any further update tile, and k_panel_trsm (after
   // U(p)) does whatever is left.  F4 (which may interchange anywhere) runs
   // after U(p).  U(p) also copies panel p's D + L from Lb into M (S tiles).
-  const bool lookahead = use_tma && std::getenv("MDS_NO_LOOKAHEAD") == nullptr;
+  const bool lookahead = use_tma && !g_mds_var.no_lookahead;
   constexpr int EVP = 2;   // events per panel: F4 done, U done
   cudaStream_t side = nullptr;
   std::vector<cudaEvent_t>* evs = nullptr;
@@ -2323,16 +2326,15 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   if (use_tma && !(make_map(&mapW1, f.W1, N, NB, f.ldw) && make_map(&mapL0, f.Lb, N, NB, f.ldw) &&
                    make_map(&mapL1, f.Lb1, N, NB, f.ldw) && make_map(&mapX, f.Lblk, NB, NB, NB)))
     return MDS_ERR_CUDA;
-  const int g_sched = (std::getenv("MDS_STATIC_SCHED") ? 1 : 0) | (std::getenv("MDS_NO_SNAKE") ? 0 : 2) |
-                      (std::getenv("MDS_XP_NOREDUCE") ? 4 : 0) | (std::getenv("MDS_NO_CPREFETCH") ? 0 : 8);   // (bit 2: timing experiment only, wrong results)
-  const bool g_inplace = std::getenv("MDS_UPD_INPLACE") != nullptr;
-  const bool upd_main = std::getenv("MDS_UPD_MAIN") != nullptr;   // measured slower (A/B), off by default
+  const int g_sched = (g_mds_var.static_sched ? 1 : 0) | (g_mds_var.no_snake ? 0 : 2) | (g_mds_var.no_cprefetch ? 0 : 8);
+  const bool g_inplace = g_mds_var.upd_inplace != 0;
+  const bool upd_main = g_mds_var.upd_main != 0;   // measured slower (A/B), off by default
   // panels with at most this many remaining rows use the one-launch fast path
   const bool capped = (g_grid_cap > 0 && g_grid_cap < sms);
   // (not when factorizations run concurrently (grid cap set): the tail launch's F2-role CTAs
   //  spin for X while F1 runs, which is free on an idle GPU but starves the other streams --
   //  C4: 3278 -> 4022 scenario-steps/s without it)
-  const int64_t tail_rows = std::getenv("MDS_TAIL_ROWS") ? std::atoll(std::getenv("MDS_TAIL_ROWS")) : (capped ? 0 : 3500);
+  const int64_t tail_rows = g_mds_var.tail_rows >= 0 ? (int64_t)g_mds_var.tail_rows : (capped ? 0 : 3500);
   if (capped) sms = g_grid_cap;
   const size_t usmem = 2 * NB * US * sizeof(double);
   auto fwork_for = [&](int64_t p) {
@@ -2346,20 +2348,17 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   auto rows_of = [&](int64_t p) { return N - std::min<int64_t>(p * (NB - 1), N); };   // upper bound
   const int reserve = capped ? std::max(1, sms / 8) : 1;   // SMs left to the panel chain (F1)
   // F4 (acceptance + exact BK columns): multi-CTA, ~256 rows per CTA, all CTAs co-resident
-  const bool f4_one_cta = std::getenv("MDS_SLOW_1CTA") != nullptr;   // A/B: the single-CTA k_panel_slow
-  const bool f4_no_ls = std::getenv("MDS_EXACT_NO_LS") != nullptr;   // A/B: L rows read from L2
-  const bool no_f2fold = std::getenv("MDS_F2_TRSM") != nullptr;       // A/B: leftover F2 tiles by k_panel_trsm
-  static bool f4_attr = false;
-  if (!f4_attr) {
+  const bool f4_one_cta = g_mds_var.slow_1cta != 0;   // A/B: the single-CTA k_panel_slow
+  const bool f4_no_ls = g_mds_var.exact_no_ls != 0;   // A/B: L rows read from L2
+  const bool no_f2fold = g_mds_var.f2_trsm != 0;       // A/B: leftover F2 tiles by k_panel_trsm
+  if (mds_once_per_device((const void*)k_panel_exact))
     cudaFuncSetAttribute(k_panel_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, XLS_MAX);
-    f4_attr = true;
-  }
   auto launch_f4 = [&](const FWork& fp, int64_t rows, int f2left) -> int {
     if (f4_one_cta) {
       MDS_LAUNCH(PC_PANEL_SLOW, st, MDS_CUDA_TRY(launch_pdl(k_panel_slow, dim3(1), dim3(1024), 0, st, N, M, ldm, fp, piv)));
       return MDS_OK;
     }
-    static const int64_t xrows = std::getenv("MDS_EXACT_ROWS") ? std::atoll(std::getenv("MDS_EXACT_ROWS")) : 256;
+    const int64_t xrows = std::max<long long>(32, g_mds_var.exact_rows);
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>({mds_cdiv(rows, xrows), (int64_t)sms, (int64_t)XMAXG}));
     const int chunk = (int)(mds_cdiv(mds_cdiv(std::max<int64_t>(rows, 1), g), 32) * 32);
     const size_t lsb = (size_t)NB * (chunk + 8) * sizeof(double);
@@ -2367,8 +2366,8 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     //  with the other streams' kernels even when no column takes the exact path)
     const int use_ls = (lsb <= (size_t)XLS_MAX && !f4_no_ls && !capped) ? 1 : 0;
     const size_t dsm = std::max<size_t>(use_ls ? lsb : 0, f2left ? usmem : 0);
-    MDS_LAUNCH(PC_PANEL_SLOW, st, MDS_CUDA_TRY(launch_pdl(k_panel_exact, dim3(g), dim3(XT), dsm, st, N, M, ldm,
-                                                          fp, piv, chunk, use_ls, f2left)));
+    MDS_LAUNCH(PC_PANEL_SLOW, st, MDS_CUDA_TRY(launch_coop_pdl(k_panel_exact, dim3(g), dim3(XT), dsm, st, N, M, ldm,
+                                                               fp, piv, chunk, use_ls, f2left)));
     return MDS_OK;
   };
   if (lookahead) {

@@ -4,6 +4,9 @@
 #include <algorithm>
 #include <atomic>
 #include <mutex>
+#include <set>
+#include <string>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -38,6 +41,36 @@ void mds_prof_stop(int cls, cudaStream_t st) {
 }
 
 extern "C" unsigned long long mds_launch_count(void) { return g_launches.load(); }
+
+bool mds_once_per_device(const void* key) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> seen;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return true;
+  std::lock_guard<std::mutex> lk(mu);
+  return seen.insert(std::make_pair(dev, key)).second;
+}
+
+// launch-structure variants (include/mds.h mds_set_variant); never read from the environment
+MdsVariant g_mds_var;
+
+extern "C" int mds_set_variant(const char* key, long long value) {
+  if (!key) return MDS_ERR_ARG;
+  std::string k(key);
+  MdsVariant& v = g_mds_var;
+  if (k == "default") { v = MdsVariant(); return MDS_OK; }
+  if (k == "tail_rows") { v.tail_rows = value; return MDS_OK; }
+  if (k == "exact_rows") { if (value < 32) return MDS_ERR_ARG; v.exact_rows = value; return MDS_OK; }
+  int* flag = k == "no_tma" ? &v.no_tma : k == "no_lookahead" ? &v.no_lookahead
+            : k == "static_sched" ? &v.static_sched : k == "no_snake" ? &v.no_snake
+            : k == "no_cprefetch" ? &v.no_cprefetch : k == "upd_inplace" ? &v.upd_inplace
+            : k == "upd_main" ? &v.upd_main : k == "slow_1cta" ? &v.slow_1cta
+            : k == "exact_no_ls" ? &v.exact_no_ls : k == "f2_trsm" ? &v.f2_trsm
+            : k == "no_pdl" ? &v.no_pdl : nullptr;
+  if (!flag) return MDS_ERR_ARG;
+  *flag = value ? 1 : 0;
+  return MDS_OK;
+}
 
 extern "C" int mds_profile_begin(void) {
   std::lock_guard<std::mutex> lk(g_mu);

@@ -510,12 +510,10 @@ extern "C" int mds_solve(const mds_plan* plan, int64_t N, const double* LD, int6
     const int64_t nblk = (N + TB - 1) / TB;
     const unsigned ge = (unsigned)std::min<int64_t>(mds_cdiv(N, 256), 148 * 8);
     MDS_LAUNCH(PC_SOLVE_GATHER, st, MDS_CUDA_TRY(launch_pdl(k_gather, dim3(ge), dim3(256), 0, st, N, piv, rhs_c, s.b, s.y, s.x, s.tickets)));
-    static bool attr = false;
-    if (!attr) {
+    if (mds_once_per_device((const void*)k_inv_blocks)) {
       cudaFuncSetAttribute(k_inv_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, IBSMEM);
       cudaFuncSetAttribute(k_trsv_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SWSMEM);
       cudaFuncSetAttribute(k_trsv_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SWSMEM);
-      attr = true;
     }
     MDS_LAUNCH(PC_SOLVE_FWD, st,
                MDS_CUDA_TRY(launch_pdl(k_inv_blocks, dim3((unsigned)nblk), dim3(256), IBSMEM, st, N, LD, ldm, s.binv, s.gf, s.gb)));

@@ -30,7 +30,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-from .errors import SingularError
+from .errors import SingularError, raise_for
 
 
 @dataclass
@@ -59,6 +59,12 @@ class InertiaCorrection:
         self.step.p.delta_w, self.step.p.delta_c = float(dw), float(dc)
         ine = tuple(int(v) for v in self.step.factor_phase(stream, sync_inertia=True))
         trials.append((float(dw), float(dc), ine))
+        # the stream is synchronised (inertia on the host): a data error of this trial
+        # (NONPOSITIVE q_k / d_h, NONFINITE input) is final -- no delta_w escalation
+        # can fix it, and its inertia is meaningless -- so raise it now
+        st = int(self.step.status.item())
+        if st != 0:
+            raise_for(st, f"inertia correction trial (delta_w={dw:g}, delta_c={dc:g})")
         return ine
 
     def solve(self, mu, stream=None):

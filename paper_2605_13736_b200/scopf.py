@@ -17,7 +17,6 @@ never exchange matrix data.
 from __future__ import annotations
 
 import numpy as np
-import os
 
 import torch
 import torch.distributed as dist
@@ -83,7 +82,7 @@ def gather_records(records: torch.Tensor, n_scenarios: int, group=None):
 class ScopfBatch:
     """The local share of a SCOPF scenario batch on one GPU."""
 
-    def __init__(self, base, scenario_fn, scenario_ids, sv_fn, n_streams=8, device="cuda"):
+    def __init__(self, base, scenario_fn, scenario_ids, sv_fn, n_streams=8, device="cuda", grid_cap=0):
         self.ids = list(scenario_ids)
         self.plan = Plan(base.n_s, base.n_d, base.m_E, base.m_I, base.rowptr, base.colidx)
         self.expected = (base.n_d, 0, base.m)
@@ -97,7 +96,7 @@ class ScopfBatch:
         self.streams = [torch.cuda.Stream() for _ in range(max(1, min(n_streams, n)))]
         # concurrent factorizations share the SMs: cap each persistent update grid
         sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
-        cap = int(os.environ.get("MDS_SCOPF_CAP", "0")) or max(8, sms // len(self.streams))
+        cap = int(grid_cap) or max(8, sms // len(self.streams))
         # (a capped grid also selects the factorization's concurrent launch structure -- no
         #  one-launch tail panels -- so a scenario's bits depend on the cap, never on the stream
         #  count, the rank or the other scenarios)

@@ -98,21 +98,28 @@ def test_pivoting_heavy_multi_panel(N, n2):
     assert rel_inf(x, x_or) <= 1e-8
 
 
-# The factorization has several launch-structure variants chosen by size or
-# environment; each must give the same BK answer.  (Env knobs are read on every
-# mds_factor call.)  "odd ldm" disables the TMA path (16-byte alignment), so the
-# cp.async update kernel without look-ahead runs.
+# The factorization has several launch-structure variants chosen by size or by
+# the explicit mds_set_variant API; each must give the same BK answer.  "odd ldm"
+# disables the TMA path (16-byte alignment), so the cp.async update kernel
+# without look-ahead runs.
+@pytest.fixture
+def variant_reset():
+    yield
+    mds.set_variant("default")
+
+
 @pytest.mark.parametrize("variant", ["tail_always", "tail_never", "no_lookahead", "no_tma", "odd_ldm", "no_pdl",
-                                     "static_sched", "upd_main", "inplace", "slow_1cta", "exact_no_ls", "f2_trsm"])
-def test_factor_variants_pivoting(variant, monkeypatch):
-    env = {"tail_always": {"MDS_TAIL_ROWS": "100000000"}, "tail_never": {"MDS_TAIL_ROWS": "0"},
-           "no_lookahead": {"MDS_NO_LOOKAHEAD": "1"}, "no_tma": {"MDS_NO_TMA": "1"}, "odd_ldm": {},
-           "no_pdl": {"MDS_NO_PDL": "1"}, "static_sched": {"MDS_STATIC_SCHED": "1"},
-           "upd_main": {"MDS_UPD_MAIN": "1"}, "inplace": {"MDS_UPD_INPLACE": "1"},
-           "slow_1cta": {"MDS_SLOW_1CTA": "1"}, "exact_no_ls": {"MDS_EXACT_NO_LS": "1"},
-           "f2_trsm": {"MDS_F2_TRSM": "1"}}[variant]
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+                                     "static_sched", "upd_main", "inplace", "slow_1cta", "exact_no_ls", "f2_trsm",
+                                     "exact_rows_64"])
+def test_factor_variants_pivoting(variant, variant_reset):
+    knobs = {"tail_always": {"tail_rows": 100000000}, "tail_never": {"tail_rows": 0},
+             "no_lookahead": {"no_lookahead": 1}, "no_tma": {"no_tma": 1}, "odd_ldm": {},
+             "no_pdl": {"no_pdl": 1}, "static_sched": {"static_sched": 1},
+             "upd_main": {"upd_main": 1}, "inplace": {"upd_inplace": 1},
+             "slow_1cta": {"slow_1cta": 1}, "exact_no_ls": {"exact_no_ls": 1},
+             "f2_trsm": {"f2_trsm": 1}, "exact_rows_64": {"exact_rows": 64}}[variant]
+    for k, v in knobs.items():
+        mds.set_variant(k, v)
     N, n2 = 1500, 300
     A, ine = mdsgen.g3_prescribed(N, seed=7 * N, n2x2=n2)
     b = np.random.default_rng(N + 1).standard_normal(N)

@@ -17,8 +17,8 @@ import mdsgen  # noqa: E402
 import oracle  # noqa: E402
 import paper_2605_13736_b200 as mds  # noqa: E402
 
-VARIANTS = [{}, {"MDS_TAIL_ROWS": "0"}, {"MDS_TAIL_ROWS": "100000000"}, {"MDS_EXACT_NO_LS": "1"},
-            {"MDS_F2_TRSM": "1"}, {"MDS_NO_PDL": "1"}, {"CAP": "8"}, {"CAP": "37"}]
+VARIANTS = [{}, {"tail_rows": 0}, {"tail_rows": 100000000}, {"exact_no_ls": 1},
+            {"f2_trsm": 1}, {"no_pdl": 1}, {"CAP": 8}, {"CAP": 37}]
 
 
 def run(A, b):
@@ -47,9 +47,10 @@ def main():
     t0 = time.time()
     for case in range(n):
         var = VARIANTS[case % len(VARIANTS)]
-        for k in [k for v in VARIANTS for k in v if k != "CAP"]:
-            os.environ.pop(k, None)
-        os.environ.update({k: v for k, v in var.items() if k != "CAP"})
+        mds.set_variant("default")
+        for k, v in var.items():
+            if k != "CAP":
+                mds.set_variant(k, v)
         mds.set_grid_cap(int(var.get("CAP", "0")))   # concurrent-factorization launch structure
         kind = "G3" if case % 3 else "G4"
         N = int(rng.integers(65, int(os.environ.get("STRESS_NMAX", "3500")) if kind == "G3" else 700))
