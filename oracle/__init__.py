@@ -32,7 +32,7 @@ ALPHA_BK = (1.0 + np.sqrt(17.0)) / 8.0
 def build(force: bool = False) -> str:
     """Compile oracle.c into liboracle.so (plain gcc, no FMA contraction)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c99", "-shared", "-fPIC",
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-std=c99", "-shared", "-fPIC",
                "-o", _LIB + ".tmp", _SRC, "-lm"]
         subprocess.run(cmd, check=True)
         os.replace(_LIB + ".tmp", _LIB)
@@ -62,10 +62,22 @@ def lib():
             L.or_recover.argtypes = [I64, P, P, P, P, P, P, P]
             L.or_step_vectors.restype = ctypes.c_int
             L.or_step_vectors.argtypes = [I64, P, P, P, P, P, P, P, P, D, D, P, P]
+            L.or_num_threads.restype = ctypes.c_int
+            L.or_set_threads.argtypes = [ctypes.c_int]
+            L.or_set_threads.restype = None
             L.or_norm_inf.restype = D
             L.or_norm_inf.argtypes = [I64, P]
             _lib = L
     return _lib
+
+
+def num_threads() -> int:
+    """Threads the BK factorization's column loop uses (OpenMP; bit-identical for any count)."""
+    return int(lib().or_num_threads())
+
+
+def set_threads(n: int) -> None:
+    lib().or_set_threads(int(n))
 
 
 def _p(a):

@@ -24,6 +24,29 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* Threads the factorization's column loop may use (OpenMP; 1 without it).
+ * Results are bit-identical for every thread count. */
+int or_num_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+void or_set_threads(int n)
+{
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
 
 #define OR_OK 0
 #define OR_ERR_ARG (-1)
@@ -252,6 +275,9 @@ int64_t or_bk_factor(int64_t N, double *A, int64_t lda, int32_t *ipiv)
         if (kstep == 1) {
             /* 1x1: A22 -= (1/d) a a^T ; a /= d   (dsyr + dscal) */
             double r1 = 1.0 / AT(A, lda, k, k);
+            /* columns j are independent (each keeps its own serial update
+               sequence), so the OpenMP split is bit-identical to 1 thread */
+            #pragma omp parallel for schedule(static) if (N - k > 512)
             for (int64_t j = k + 1; j < N; j++) {
                 double temp = -r1 * AT(A, lda, j, k);
                 for (int64_t i = j; i < N; i++)
@@ -267,14 +293,28 @@ int64_t or_bk_factor(int64_t N, double *A, int64_t lda, int32_t *ipiv)
                 double d22 = AT(A, lda, k, k) / d21;
                 double t = 1.0 / (d11 * d22 - 1.0);
                 d21 = t / d21;
+                /* dsytf2's loop computes (wk, wkp1) of column j from the ORIGINAL
+                   A(j,k), A(j,k+1), updates A(j:,j) with the original A(j:,k),
+                   A(j:,k+1), then stores (wk, wkp1) into A(j,k), A(j,k+1).  The
+                   three steps are done here as three passes so the column update
+                   can be split over threads: same operations, same operands,
+                   bit-identical to the serial loop. */
+                double *wk = (double *)malloc(sizeof(double) * 2 * (size_t)N);
+                double *wkp1 = wk + N;
                 for (int64_t j = k + 2; j < N; j++) {
-                    double wk = d21 * (d11 * AT(A, lda, j, k) - AT(A, lda, j, k + 1));
-                    double wkp1 = d21 * (d22 * AT(A, lda, j, k + 1) - AT(A, lda, j, k));
-                    for (int64_t i = j; i < N; i++)
-                        AT(A, lda, i, j) = AT(A, lda, i, j) - AT(A, lda, i, k) * wk - AT(A, lda, i, k + 1) * wkp1;
-                    AT(A, lda, j, k) = wk;
-                    AT(A, lda, j, k + 1) = wkp1;
+                    wk[j] = d21 * (d11 * AT(A, lda, j, k) - AT(A, lda, j, k + 1));
+                    wkp1[j] = d21 * (d22 * AT(A, lda, j, k + 1) - AT(A, lda, j, k));
                 }
+                #pragma omp parallel for schedule(static) if (N - k > 512)
+                for (int64_t j = k + 2; j < N; j++) {
+                    for (int64_t i = j; i < N; i++)
+                        AT(A, lda, i, j) = AT(A, lda, i, j) - AT(A, lda, i, k) * wk[j] - AT(A, lda, i, k + 1) * wkp1[j];
+                }
+                for (int64_t j = k + 2; j < N; j++) {
+                    AT(A, lda, j, k) = wk[j];
+                    AT(A, lda, j, k + 1) = wkp1[j];
+                }
+                free(wk);
             }
             ipiv[k] = (int32_t)(-(kp + 1));
             ipiv[k + 1] = (int32_t)(-(kp + 1));

@@ -1,11 +1,12 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py
 times (CUDA-graph replay of the whole step):
   C2 (N=1024, n_s=100k): every output against the oracle.
-  C3 (N=8192, n_s=1M): condensed M element by element against the oracle;
-    inertia against the closed form; the solve through properties that hold at
-    any size (relative residual of the condensed system against the oracle's
-    M <= 1e-10, dx_s equal to the recovery formula applied to the GPU's dy);
-    step vectors against the oracle on the GPU's direction."""
+  C3 (N=8192, n_s=1M): condensed M, rhs_c, w bit-exact against the oracle and
+    ||M||_inf within 1e-13; inertia against the closed form AND the oracle's BK
+    factorization; the solution element by element against the oracle's
+    (<= 1e-8) and through the residual of the condensed system (<= 1e-10);
+    step vectors against the oracle on the GPU's direction.
+  C4 (one full-size SCOPF scenario, N=2048, n_s=131072): every output vs the oracle."""
 import numpy as np
 import pytest
 
@@ -52,16 +53,19 @@ def test_c3_full_size_properties():
     sv = mdsgen.step_vectors_for(prob, seed=7)
     dp = mds.DeviceProblem(prob)
     st = mds.KKTStep(dp, sv=sv)
-    # condensation alone, element by element
+    # condensation alone, element by element (bit-exact)
+    anorm = torch.zeros(1, dtype=torch.float64, device="cuda")
     mds.condense(dp.plan, dp.val, dp.h_ss, dp.sigma_s, dp.H_dd, dp.ldh, dp.sigma_d, dp.J_d, dp.ldj, dp.d_h,
-                 dp.delta_w, dp.delta_c, dp.r, st.M, st.ldm, st.rhs, st.w, st.status)
+                 dp.delta_w, dp.delta_c, dp.r, st.M, st.ldm, st.rhs, st.w, st.status, anorm_out=anorm,
+                 work=st.cwork)
     torch.cuda.synchronize()
     M_or, rhs_or, w_or = oracle.condense(prob)
     Mg = st.M_host()
-    scale = np.abs(np.tril(M_or)).max()
-    assert np.abs(np.tril(Mg) - np.tril(M_or)).max() <= 1e-13 * scale
+    np.testing.assert_array_equal(np.tril(Mg), np.tril(M_or))
     np.testing.assert_array_equal(st.w[:prob.n_s].cpu().numpy(), w_or)
-    assert rel_inf(st.rhs[:prob.N].cpu().numpy(), rhs_or) <= 1e-13
+    np.testing.assert_array_equal(st.rhs[:prob.N].cpu().numpy(), rhs_or)
+    a_or = oracle.anorm_lower(M_or)
+    assert abs(float(anorm.item()) - a_or) <= 1e-13 * a_or
     del Mg
     # the whole step as bench.py runs it (graph replay)
     g = st.capture()
@@ -74,11 +78,39 @@ def test_c3_full_size_properties():
     dy = out["dxy"][prob.n_d:]
     dxs_ref = oracle.recover(prob, w_or, prob.r[:prob.n_s], dy)
     assert rel_inf(out["dx_s"], dxs_ref) <= 1e-12
+    # the oracle's own BK factorization + solve at full size (OpenMP, bit-identical to 1 thread)
+    ga, gt = mds.factor_tol(st.fwork)
+    tol_or = oracle.default_tol(M_or)
+    assert abs(gt - tol_or) <= 1e-13 * tol_or
+    LD, ipiv, _ = oracle.bk_factor(M_or)
+    assert oracle.inertia(LD, ipiv, tol_or) == out["inertia"]
+    x_or = oracle.bk_solve(LD, ipiv, rhs_or, tol_or)
+    del LD
+    assert rel_inf(out["dxy"], x_or) <= 1e-8, rel_inf(out["dxy"], x_or)
+    dxs_or = oracle.recover(prob, w_or, prob.r[:prob.n_s], x_or[prob.n_d:])
+    assert rel_inf(out["dx_s"], dxs_or) <= 1e-8
     dx = np.concatenate([out["dx_s"], out["dxy"][:prob.n_d]])
     s, v, sig = oracle.step_vectors(sv.x, dx, sv.lo, sv.up, sv.zl, sv.zu, sv.dzl, sv.dzu, sv.tau, sv.mu)
     assert out["vec"]["alpha_p"] == v["alpha_p"] and out["vec"]["alpha_d"] == v["alpha_d"]
     assert out["vec"]["compl_inf"] == v["compl_inf"]
     np.testing.assert_array_equal(out["sigma"], sig)
+
+
+def test_c4_scenario_full_size_vs_oracle():
+    # one SCOPF contingency scenario at the C4 size (N = 2048, n_s = 131072, bus-local pattern)
+    base = mdsgen.scopf_base()
+    prob = mdsgen.scopf_scenario(base, 37)
+    sv = mdsgen.step_vectors_for(prob, seed=37)
+    st, out = graph_step(prob, sv)
+    ref = oracle.newton_step(prob)
+    assert out["status"] == 0
+    assert out["inertia"] == ref["inertia"] == prob.expected_inertia
+    np.testing.assert_array_equal(out["rhs_c"], ref["rhs_c"])
+    np.testing.assert_array_equal(out["w"], ref["w"])
+    assert rel_inf(out["dxy"], ref["dxy"]) <= 1e-8
+    assert rel_inf(out["dx_s"], ref["dx_s"]) <= 1e-8
+    res = np.abs(sym_matvec_lower(ref["M"], out["dxy"]) - ref["rhs_c"]).max() / np.abs(ref["rhs_c"]).max()
+    assert res <= 1e-10
 
 
 @pytest.mark.parametrize("N,n2", [(1500, 300), (2111, 500)])

@@ -68,26 +68,56 @@ def check_x(A, b, x, x_or):
 # ---------------------------------------------------------------- condensation
 @pytest.mark.parametrize("shape,pattern,dw,dc", [
     ((400, 20, 10, 10), "uniform", 0.0, 0.0),          # C1
-    ((3000, 70, 33, 40), "local", 0.01, 1e-8),          # several warps/chunks, ragged
+    ((3000, 70, 33, 40), "local", 0.01, 1e-8),          # several tiles, ragged
     ((20000, 150, 100, 157), "uniform", 0.0, 0.3),
     ((5000, 0, 60, 70), "local", 0.0, 0.0),             # n_d = 0
     ((4000, 50, 90, 0), "uniform", 0.0, 0.0),           # m_I = 0
+    ((4000, 50, 0, 90), "uniform", 0.0, 0.0),           # m_E = 0
     ((0, 40, 10, 10), "uniform", 0.0, 0.0),             # n_s = 0
+    ((30000, 130, 200, 170), "local", 1e-3, 0.0),       # bus-local pattern, long runs per destination
 ])
 def test_condense_parity(shape, pattern, dw, dc):
+    # M, rhs_c and w are formed with the elimination's own operations in its own
+    # order (one sparse variable at a time): BIT-EXACT vs the oracle.
+    # ||M||_inf (fixed-order sums, a different order than the oracle's) <= 1e-13 relative.
     prob = mdsgen.g1_quasidefinite(*shape, seed=sum(shape), pattern=pattern, delta_w=dw, delta_c=dc)
     M_or, rhs_or, w_or = oracle.condense(prob)
     dp = mds.DeviceProblem(prob)
     st = mds.KKTStep(dp)
-    mds.condense(dp.plan, dp.val, dp.h_ss, dp.sigma_s, dp.H_dd, dp.ldh, dp.sigma_d, dp.J_d, dp.ldj, dp.d_h,
-                 dp.delta_w, dp.delta_c, dp.r, st.M, st.ldm, st.rhs, st.w, st.status)
+    anorm = torch.full((1,), -1.0, dtype=torch.float64, device="cuda")
+    for _ in range(2):   # the workspace (tile queue, norm tickets) must be reusable
+        mds.condense(dp.plan, dp.val, dp.h_ss, dp.sigma_s, dp.H_dd, dp.ldh, dp.sigma_d, dp.J_d, dp.ldj, dp.d_h,
+                     dp.delta_w, dp.delta_c, dp.r, st.M, st.ldm, st.rhs, st.w, st.status, anorm_out=anorm,
+                     work=st.cwork)
     torch.cuda.synchronize()
     M = st.M_host()
-    scale = max(np.abs(np.tril(M_or)).max(), 1.0)
-    assert np.abs(np.tril(M) - np.tril(M_or)).max() <= 1e-13 * scale
+    np.testing.assert_array_equal(np.tril(M), np.tril(M_or))
     np.testing.assert_array_equal(st.w[:prob.n_s].cpu().numpy(), w_or)
-    assert rel_inf(st.rhs[:prob.N].cpu().numpy(), rhs_or) <= 1e-13
+    np.testing.assert_array_equal(st.rhs[:prob.N].cpu().numpy(), rhs_or)
+    a_or = oracle.anorm_lower(M_or)
+    assert abs(float(anorm.item()) - a_or) <= 1e-13 * a_or
     assert int(st.status.item()) == 0
+
+
+def test_condense_anorm_deterministic_and_nonfinite():
+    prob = mdsgen.g1_quasidefinite(20000, 150, 100, 157, seed=4)
+    dp = mds.DeviceProblem(prob)
+    st = mds.KKTStep(dp)
+    vals = []
+    for _ in range(3):
+        st.factor_phase(sync_inertia=True)
+        vals.append(float(st.anorm.item()))
+    assert vals[0] == vals[1] == vals[2]
+    # a NaN in the inputs -> anorm_out NaN -> mds_factor reports NONFINITE and factors
+    # nothing; the solve issued anyway (as a captured graph would), on a FRESH step whose
+    # piv was never written, stays in bounds (identity permutation left by the abort)
+    dp.H_dd[5] = float("nan")
+    st2 = mds.KKTStep(dp, sv=mdsgen.step_vectors_for(prob, seed=1))
+    st2.piv.fill_(1 << 28)
+    st2.run()
+    torch.cuda.synchronize()
+    assert np.isnan(float(st2.anorm.item()))
+    assert int(st2.status.item()) == mds.NumericError.code
 
 
 def test_condense_nonpositive_status():
@@ -191,6 +221,63 @@ def test_identity_and_small_examples():
         np.testing.assert_allclose(sym_from_lower(A) @ x, b, rtol=0, atol=1e-15)
 
 
+# ---------------------------------------------------------------- zero-pivot tolerance (reading R4)
+def _dense_factor(A):
+    N = A.shape[0]
+    M, ldm = upload_dense(A)
+    piv = torch.empty(2 * N, dtype=torch.int32, device="cuda")
+    ine_d = torch.zeros(3, dtype=torch.int64, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    fwork = torch.empty(mds.factor_workspace_size(N), dtype=torch.uint8, device="cuda")
+    ine = mds.factor(N, M, ldm, piv, -1.0, ine_d, status, fwork, sync=True)
+    return ine, fwork, int(status.item())
+
+
+@pytest.mark.parametrize("kind", ["G1", "G3", "G4"])
+def test_factor_tol_matches_oracle(kind):
+    # the one threshold that decides "zero" in the inertia: tol = N eps ||M||_inf
+    if kind == "G1":
+        prob = mdsgen.g1_quasidefinite(20000, 150, 100, 157, seed=21)
+        A = oracle.condense(prob)[0]
+        st = mds.KKTStep(mds.DeviceProblem(prob))
+        st.factor_phase(sync_inertia=True)            # norm fused into the condensation
+        a_c, t_c = mds.factor_tol(st.fwork)
+        assert abs(t_c - oracle.default_tol(A)) <= 1e-13 * oracle.default_tol(A)
+    elif kind == "G3":
+        A, _ = mdsgen.g3_prescribed(1300, seed=5, n2x2=200)
+    else:
+        A = mdsgen.g4_random_symmetric(300, seed=9)
+    _, fwork, status = _dense_factor(A)                # stand-alone scan inside mds_factor
+    a_g, t_g = mds.factor_tol(fwork)
+    a_or, t_or = oracle.anorm_lower(A), oracle.default_tol(A)
+    assert status == 0
+    assert abs(a_g - a_or) <= 1e-13 * a_or and abs(t_g - t_or) <= 1e-13 * t_or
+
+
+@pytest.mark.parametrize("N,seed", [(300, 1), (1000, 2), (2111, 3)])
+def test_pivots_at_the_tolerance(N, seed):
+    # G3 plus decoupled 1x1 pivots placed at +-0.5, 0.9, 1.1, 2 and 3 times tol (and 0):
+    # their values never change during the elimination (their rows are exactly zero off the
+    # diagonal), so whether each counts as zero is decided by the tolerance alone.
+    # Expected inertia: closed form, and the oracle's.
+    n0 = N - 9
+    A0, ine0 = mdsgen.g3_prescribed(n0, seed=seed, n2x2=n0 // 6)
+    tol = N * np.finfo(float).eps * oracle.anorm_lower(A0)
+    small = np.array([0.5, -0.5, 0.9, -0.9, 0.0, 1.1, -1.1, 2.0, 3.0]) * tol
+    B = np.zeros((N, N))
+    B[:n0, :n0] = A0
+    B[np.arange(n0, N), np.arange(n0, N)] = small
+    p = np.random.default_rng(seed).permutation(N)
+    B = np.asfortranarray(B[np.ix_(p, p)])
+    expected = (ine0[0] + 3, 5, ine0[2] + 1)
+    LD, ipiv, _ = oracle.bk_factor(B)
+    t_or = oracle.default_tol(B)
+    assert oracle.inertia(LD, ipiv, t_or) == expected
+    ine, fwork, status = _dense_factor(B)
+    assert ine == expected
+    assert abs(mds.factor_tol(fwork)[1] - t_or) <= 1e-13 * t_or
+
+
 def test_nonfinite_input():
     A = mdsgen.g4_random_symmetric(100, 1)
     A[50, 3] = np.inf
@@ -284,7 +371,8 @@ def test_singular_1x1():
     assert g_ine == (0, 1, 0) and status == mds.SingularError.code
 
 
-@pytest.mark.parametrize("shape", [(0, 30, 10, 12), (3000, 64, 64, 0), (2500, 0, 40, 24), (777, 63, 1, 1)])
+@pytest.mark.parametrize("shape", [(0, 30, 10, 12), (3000, 64, 64, 0), (2500, 0, 40, 24), (777, 63, 1, 1),
+                                   (4000, 50, 0, 90)])
 def test_full_step_edge_shapes(shape):
     # no sparse block, no inequalities, no dense variables, N = 65 (one full panel + 1)
     prob = mdsgen.g1_quasidefinite(*shape, seed=3 + sum(shape))

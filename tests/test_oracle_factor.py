@@ -168,3 +168,28 @@ def test_anorm_and_nonfinite():
     with pytest.raises(oracle.OracleError) as e:
         oracle.anorm_lower(A)
     assert e.value.code == oracle.ERR_NONFINITE
+
+
+def test_threaded_factor_bit_identical_and_pinned():
+    # The OpenMP split of the trailing update (columns j are independent; the 2x2 step
+    # keeps dsytf2's operand order) must not change a single bit, and must still be BK:
+    # at N = 1400 (above the threading threshold) with many 2x2 pivots the inertia equals
+    # the closed form of the prescribed-spectrum generator, the product-form factors
+    # reconstruct A, and the solve meets the residual bar.
+    A, ine = mdsgen.g3_prescribed(1400, seed=77, n2x2=350)
+    nt = oracle.num_threads()
+    try:
+        oracle.set_threads(1)
+        LD1, ip1, _ = oracle.bk_factor(A)
+        oracle.set_threads(max(nt, 4))
+        LD4, ip4, _ = oracle.bk_factor(A)
+    finally:
+        oracle.set_threads(nt)
+    np.testing.assert_array_equal(LD1, LD4)
+    np.testing.assert_array_equal(ip1, ip4)
+    assert (ip1 < 0).sum() > 100                                     # the 2x2 branch ran
+    assert oracle.inertia(LD1, ip1, oracle.default_tol(A)) == ine
+    b = np.random.default_rng(5).standard_normal(1400)
+    x = oracle.bk_solve(LD1, ip1, b, oracle.default_tol(A))
+    As = sym_from_lower(A)
+    assert np.abs(As @ x - b).max() / np.abs(b).max() <= 1e-12
