@@ -88,16 +88,53 @@ int mds_plan_dims(const mds_plan *plan, int64_t *out5);
  *   M_yx  = J_d                                                     (blocks (2,1),(3,1))
  *   M_yy  = -J_s^T diag(w) J_s - diag(0_{m_E}, 1/d_h) - delta_c I   (blocks (2,2)..(3,3))
  *   rhs_c = [ r_xd ; r_y - J_s^T (w .* r_xs) ]
+ * plus, fused into the stores, the pre-factor scan of SURVEY §8(a3):
+ *   anorm_out = ||M||_inf (row abs-sums of the symmetric M from its lower
+ *   triangle, fixed summation order -> bitwise reproducible), or NaN if M
+ *   holds a NaN/Inf entry.  Feed it to mds_factor's `anorm` to skip its scan.
+ * Every entry of M and rhs_c is formed by the same floating-point operations
+ * in the same order as the plain elimination one sparse variable at a time
+ * (PAPER.md:166-168): for each output, the products (val_p w_k) val_p' are
+ * subtracted in ascending k.
  * Inputs (device): js_val[nnz] (values in the plan's CSR order); h_ss, sigma_s
  * [n_s]; H_dd [n_d x n_d, ldh, lower read]; sigma_d [n_d]; J_d [m x n_d, ldj];
  * d_h [m_I]; r [n_s + N] = (r_xs, r_xd, r_yg, r_yh) or NULL (then rhs_c is not
  * written).  Outputs (device): M [N x N, ldm, lower written], rhs_c [N] (or
- * NULL), w_out [n_s] (kept for mds_solve's recovery).
+ * NULL), w_out [n_s] (kept for mds_solve's recovery), anorm_out (one double,
+ * or NULL: no norm).  work: device workspace of at least
+ * mds_condense_workspace_size(plan, 1) bytes (per-entry products, norm
+ * partials, the tile queue; no zeroing needed).
  * Data errors: MDS_ERR_NONPOSITIVE if some q_k <= 0 or d_h <= 0. */
+size_t mds_condense_workspace_size(const mds_plan *plan, int64_t batch);
 int mds_condense(const mds_plan *plan, const double *js_val, const double *h_ss, const double *sigma_s,
                  const double *H_dd, int64_t ldh, const double *sigma_d, const double *J_d, int64_t ldj,
                  const double *d_h, double delta_w, double delta_c, const double *r,
-                 double *M, int64_t ldm, double *rhs_c, double *w_out, int32_t *status_dev, void *stream);
+                 double *M, int64_t ldm, double *rhs_c, double *w_out, double *anorm_out,
+                 int32_t *status_dev, void *work, size_t work_bytes, void *stream);
+
+/* mds_condense_batched — the same for `batch` independent systems that share
+ * the plan's sparsity pattern (SCOPF contingency scenarios, PAPER.md:70-78;
+ * north star: "independent contingency KKT systems are batched per GPU").
+ * Scenario s uses array X + s * str_X for every per-scenario array (strides in
+ * ELEMENTS; H_dd / J_d / M keep their leading dimensions inside a scenario).
+ * delta_w, delta_c: DEVICE arrays [batch] (NULL = 0).  status: device int32
+ * [batch] (scenario s writes only status[s]; one failing scenario does not
+ * affect the others).  anorm_out: device [batch] or NULL.  One launch sequence
+ * for the whole batch (tiles of all scenarios share one work queue).
+ * work >= mds_condense_workspace_size(plan, batch). */
+int mds_condense_batched(const mds_plan *plan, int64_t batch,
+                         const double *js_val, int64_t str_val,
+                         const double *h_ss, int64_t str_hss, const double *sigma_s, int64_t str_sig,
+                         const double *H_dd, int64_t ldh, int64_t str_H,
+                         const double *sigma_d, int64_t str_sd,
+                         const double *J_d, int64_t ldj, int64_t str_J,
+                         const double *d_h, int64_t str_dh,
+                         const double *delta_w, const double *delta_c,
+                         const double *r, int64_t str_r,
+                         double *M, int64_t ldm, int64_t str_M,
+                         double *rhs_c, int64_t str_rhs, double *w_out, int64_t str_w,
+                         double *anorm_out, int32_t *status,
+                         void *work, size_t work_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------
  * mds_factor — Bunch-Kaufman LDL^T of the symmetric indefinite M (PAPER.md:191:
@@ -115,7 +152,11 @@ int mds_condense(const mds_plan *plan, const double *js_val, const double *h_ss,
  * final permutation (row i of P M P^T is row piv[N+i] of M).  The pair (M,piv)
  * is consumed only by mds_solve.
  * zero_tol: pivots with |d| <= zero_tol count as zero; zero_tol < 0 selects
- * N * eps * ||M||_inf (computed on device; reading R4 in DESIGN.md).
+ * N * eps * ||M||_inf (reading R4 in DESIGN.md).
+ * anorm: device pointer to ||M||_inf as written by mds_condense's anorm_out
+ * (a NaN there means M is not finite -> MDS_ERR_NONFINITE), or NULL: then
+ * mds_factor scans M itself first (one fixed-order pass over the lower
+ * triangle, also detecting NaN/Inf).
  * inertia_dev: device mds_inertia (written).  inertia_host: if non-NULL the
  * call synchronises `stream` and copies the inertia there (3 integers cross
  * the bus, nothing else).
@@ -124,8 +165,11 @@ int mds_condense(const mds_plan *plan, const double *js_val, const double *h_ss,
  * factored). */
 size_t mds_factor_workspace_size(int64_t N);
 int mds_factor(int64_t N, double *M, int64_t ldm, int32_t *piv, double zero_tol,
-               mds_inertia *inertia_dev, mds_inertia *inertia_host, int32_t *status_dev,
+               const double *anorm, mds_inertia *inertia_dev, mds_inertia *inertia_host, int32_t *status_dev,
                void *work, size_t work_bytes, void *stream);
+/* ||M||_inf and the zero-pivot tolerance the last mds_factor on `work` used
+ * (host copies; synchronous).  For the parity tests of reading R4. */
+int mds_factor_tol(const void *work, double *anorm_host, double *tol_host);
 
 /* ---------------------------------------------------------------------------
  * mds_solve — x = P^T L^{-T} D^{-1} L^{-1} P rhs_c with mds_factor's output,

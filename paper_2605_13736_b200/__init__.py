@@ -32,10 +32,19 @@ _lib.mds_version.restype = ctypes.c_char_p
 _lib.mds_plan_create.argtypes = [_I64, _I64, _I64, _I64, _P, _P, ctypes.POINTER(ctypes.c_void_p)]
 _lib.mds_plan_destroy.argtypes = [_P]
 _lib.mds_plan_dims.argtypes = [_P, _P]
-_lib.mds_condense.argtypes = [_P, _P, _P, _P, _P, _I64, _P, _P, _I64, _P, _D, _D, _P, _P, _I64, _P, _P, _P, _P]
+_lib.mds_condense.argtypes = [_P, _P, _P, _P, _P, _I64, _P, _P, _I64, _P, _D, _D, _P, _P, _I64, _P, _P, _P, _P, _P,
+                              ctypes.c_size_t, _P]
+_lib.mds_condense_workspace_size.restype = ctypes.c_size_t
+_lib.mds_condense_workspace_size.argtypes = [_P, _I64]
+_lib.mds_condense_batched.argtypes = ([_P, _I64] + [_P, _I64] * 3 + [_P, _I64, _I64] + [_P, _I64] + [_P, _I64, _I64] +
+                                      [_P, _I64] + [_P, _P] + [_P, _I64] + [_P, _I64, _I64] + [_P, _I64] * 2 +
+                                      [_P, _P, _P, ctypes.c_size_t, _P])
+_lib.mds_condense_batched.restype = ctypes.c_int
+_lib.mds_factor_tol.argtypes = [_P, _P, _P]
+_lib.mds_factor_tol.restype = ctypes.c_int
 _lib.mds_factor_workspace_size.restype = ctypes.c_size_t
 _lib.mds_factor_workspace_size.argtypes = [_I64]
-_lib.mds_factor.argtypes = [_I64, _P, _I64, _P, _D, _P, _P, _P, _P, ctypes.c_size_t, _P]
+_lib.mds_factor.argtypes = [_I64, _P, _I64, _P, _D, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]
 _lib.mds_solve_workspace_size.restype = ctypes.c_size_t
 _lib.mds_solve_workspace_size.argtypes = [_I64]
 _lib.mds_solve.argtypes = [_P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _D, _P, _P, _P, ctypes.c_size_t, _P]
@@ -59,12 +68,12 @@ _lib.mds_kkt_residual.argtypes = [_P, _P, _P, _P, _P, _I64, _P, _P, _I64, _P, _D
                                   ctypes.c_size_t, _P]
 _lib.mds_kkt_residual.restype = ctypes.c_int
 
-EXPORTS = ["mds_kkt_residual_workspace_size", "mds_kkt_residual", "mds_version", "mds_plan_create", "mds_plan_destroy", "mds_plan_dims", "mds_condense",
+EXPORTS = ["mds_condense_workspace_size", "mds_condense_batched", "mds_factor_tol", "mds_kkt_residual_workspace_size", "mds_kkt_residual", "mds_version", "mds_plan_create", "mds_plan_destroy", "mds_plan_dims", "mds_condense",
            "mds_factor_workspace_size", "mds_factor", "mds_solve_workspace_size", "mds_solve",
            "ipm_step_vectors_workspace_size", "ipm_step_vectors", "mds_launch_count", "mds_profile_begin",
            "mds_profile_end", "mds_factor_panels", "mds_factor_set_grid_cap", "mds_profile_timeline", "mds_set_variant"]
 
-PROF_CLASSES = ["condense_w", "condense_dense", "condense_yy", "anorm", "panel_diag", "panel_trsm", "panel_store",
+PROF_CLASSES = ["condense_rows", "condense_norm", "condense_tiles", "anorm", "panel_diag", "panel_trsm", "panel_store",
                 "panel_exact", "update", "finalize", "solve_gather", "solve_fwd", "solve_d", "solve_bwd",
                 "solve_scatter", "recover", "vectors"]
 
@@ -141,13 +150,36 @@ class Plan:
             pass
 
 
+def condense_workspace_size(plan: Plan, batch: int = 1) -> int:
+    return int(_lib.mds_condense_workspace_size(plan.handle, int(batch)))
+
+
 def condense(plan: Plan, js_val, h_ss, sigma_s, H_dd, ldh, sigma_d, J_d, ldj, d_h, delta_w, delta_c, r,
-             M, ldm, rhs_c, w_out, status, stream=None):
-    """mds_condense (Eq.(5)->Eq.(6)); see include/mds.h."""
+             M, ldm, rhs_c, w_out, status, stream=None, anorm_out=None, work=None):
+    """mds_condense (Eq.(5)->Eq.(6), ||M||_inf into anorm_out); see include/mds.h.
+    `work`: a uint8 device tensor of condense_workspace_size(plan) bytes (allocated
+    here when None -- pass one in for graph capture / no allocation per call)."""
+    if work is None:
+        work = torch.empty(condense_workspace_size(plan), dtype=torch.uint8, device=M.device)
     code = _lib.mds_condense(plan.handle, _f64(js_val), _f64(h_ss), _f64(sigma_s), _f64(H_dd), int(ldh),
                              _f64(sigma_d), _f64(J_d), int(ldj), _f64(d_h), float(delta_w), float(delta_c),
-                             _f64(r), _f64(M), int(ldm), _f64(rhs_c), _f64(w_out), _ptr(status), _stream(stream))
+                             _f64(r), _f64(M), int(ldm), _f64(rhs_c), _f64(w_out), _f64(anorm_out), _ptr(status),
+                             _ptr(work), work.numel() * work.element_size(), _stream(stream))
     _check(code, "mds_condense")
+
+
+def condense_batched(plan: Plan, batch, js_val, h_ss, sigma_s, H_dd, ldh, sigma_d, J_d, ldj, d_h, delta_w, delta_c,
+                     r, M, ldm, rhs_c, w_out, anorm_out, status, work, strides, stream=None):
+    """mds_condense_batched: `strides` = dict of per-scenario element strides with keys
+    val, hss, sig, H, sd, J, dh, r, M, rhs, w (every array is base + s * stride)."""
+    st = strides
+    code = _lib.mds_condense_batched(
+        plan.handle, int(batch), _f64(js_val), int(st["val"]), _f64(h_ss), int(st["hss"]), _f64(sigma_s),
+        int(st["sig"]), _f64(H_dd), int(ldh), int(st["H"]), _f64(sigma_d), int(st["sd"]), _f64(J_d), int(ldj),
+        int(st["J"]), _f64(d_h), int(st["dh"]), _f64(delta_w), _f64(delta_c), _f64(r), int(st["r"]), _f64(M),
+        int(ldm), int(st["M"]), _f64(rhs_c), int(st["rhs"]), _f64(w_out), int(st["w"]), _f64(anorm_out),
+        _ptr(status), _ptr(work), work.numel() * work.element_size(), _stream(stream))
+    _check(code, "mds_condense_batched")
 
 
 def factor_workspace_size(N):
@@ -166,15 +198,23 @@ class Inertia(ctypes.Structure):
     _fields_ = [("pos", ctypes.c_int64), ("zero", ctypes.c_int64), ("neg", ctypes.c_int64)]
 
 
-def factor(N, M, ldm, piv, zero_tol, inertia_dev, status, work, sync=True, stream=None):
-    """mds_factor (Bunch-Kaufman LDL^T + inertia).  Returns the inertia tuple
-    when sync=True (one 24-byte D2H copy), else None."""
+def factor(N, M, ldm, piv, zero_tol, inertia_dev, status, work, sync=True, stream=None, anorm=None):
+    """mds_factor (Bunch-Kaufman LDL^T + inertia).  `anorm`: optional device scalar
+    ||M||_inf from condense (else M is scanned).  Returns the inertia tuple when
+    sync=True (one 24-byte D2H copy), else None."""
     host = Inertia() if sync else None
-    code = _lib.mds_factor(int(N), _f64(M), int(ldm), _ptr(piv), float(zero_tol), _ptr(inertia_dev),
+    code = _lib.mds_factor(int(N), _f64(M), int(ldm), _ptr(piv), float(zero_tol), _f64(anorm), _ptr(inertia_dev),
                            ctypes.byref(host) if sync else None, _ptr(status), _ptr(work),
                            work.numel() * work.element_size(), _stream(stream))
     _check(code, "mds_factor")
     return (host.pos, host.zero, host.neg) if sync else None
+
+
+def factor_tol(fwork):
+    """(||M||_inf, zero-pivot tolerance) the last mds_factor on `fwork` used (synchronous)."""
+    a, t = ctypes.c_double(), ctypes.c_double()
+    _check(_lib.mds_factor_tol(_ptr(fwork), ctypes.byref(a), ctypes.byref(t)), "mds_factor_tol")
+    return a.value, t.value
 
 
 def solve(plan, N, LD, ldm, piv, rhs_c, js_val, w, r_xs, dxy, dx_s, zero_tol, fwork, status, work, stream=None):

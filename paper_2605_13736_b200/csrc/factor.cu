@@ -36,6 +36,7 @@
 #include <mutex>
 #include <vector>
 
+#include "anorm.cuh"
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -71,7 +72,7 @@ struct FWork {
   int* bt;            // [N]  0: 1x1, 1: first of 2x2, 2: second of 2x2
   int* rho;           // [N]
   int* rhoinv;        // [N]
-  double* rowsum;     // [N]
+  char* nparts;       // ||M||_inf partials (anorm.cuh), parts_bytes(N)
   double* Lblk;       // [NB*NB]
   double* W;          // [ldw * WCOLS]  W panel of the current panel (host picks W0/W1 by panel parity)
   double* W1;         // second W buffer (look-ahead: panel p+1 is formed while p's update still reads W)
@@ -104,7 +105,7 @@ FWork carve(void* work, int64_t N, size_t* total) {
   f.bt = reinterpret_cast<int*>(take(sizeof(int) * N));
   f.rho = reinterpret_cast<int*>(take(sizeof(int) * N));
   f.rhoinv = reinterpret_cast<int*>(take(sizeof(int) * N));
-  f.rowsum = reinterpret_cast<double*>(take(sizeof(double) * N));
+  f.nparts = take(anorm::parts_bytes(N));
   f.Lblk = reinterpret_cast<double*>(take(sizeof(double) * NB * NB));
   f.ldw = align_up(std::max<int64_t>(N, 1), 8);
   f.W = reinterpret_cast<double*>(take(sizeof(double) * f.ldw * WCOLS));
@@ -139,102 +140,33 @@ __device__ __forceinline__ double bitsd(unsigned long long b) { return __longlon
 // ---------------------------------------------------------------------------
 // zero the per-call control state (one kernel instead of several memsets, so
 // the launch chain stays programmatic-dependent-launch friendly)
-__global__ void k_factor_init(int64_t N, FWork f, double zero_tol) {
+__global__ void k_factor_init(int64_t N, FWork f, double zero_tol, const double* anorm, int32_t* status) {
   pdl_wait();
   pdl_trigger();
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t gth = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = gtid; i < N; i += gth) { f.sw[i] = -1; f.bt[i] = 0; f.rowsum[i] = 0.0; }
+  for (int64_t i = gtid; i < N; i += gth) { f.sw[i] = -1; f.bt[i] = 0; }
   for (int64_t i = gtid; i < 3 * (N + 2); i += gth) f.ucount[i] = 0ull;
   for (int64_t i = gtid; i < 2 * (N / 64 + 4); i += gth) f.t1flag[i] = 0u;
   for (int64_t i = gtid; i < N / 32 + 8; i += gth) f.xbar[i] = 0u;
+  if (gtid < 4) anorm::parts_at(f.nparts, N).ctr[gtid] = 0u;
   if (blockIdx.x == 0) {
     int* c = reinterpret_cast<int*>(f.ctl);
     for (int i = threadIdx.x; i < (int)(sizeof(FCtl) / sizeof(int)); i += blockDim.x) c[i] = 0;
     __syncthreads();
-    if (threadIdx.x == 0) f.ctl->tol = zero_tol;
-  }
-}
-
-// ||M||_inf (row abs-sums via symmetry, lower storage) + non-finite scan.
-// One CTA per lower block of ANR rows x ANC columns: thread t owns row r0+t and
-// has its ANC loads in flight at once; each column segment a CTA reads is
-// ANR*8 = 2 KB contiguous (DRAM-page friendly).  Row sums need no reduction
-// (one owner thread); column sums by warp shuffles + shared memory; then
-// ANR + ANC atomic adds into rowsum.  (HBM-bound: N^2/2 * 8 bytes.)
-constexpr int ANR = 256, ANC = 32;
-__global__ void __launch_bounds__(ANR) k_anorm_tiles(int64_t N, const double* __restrict__ A, int64_t lda,
-                                                     double* rowsum, FCtl* ctl, int32_t* status) {
-  pdl_wait();
-  pdl_trigger();
-  // blocks (bi, bj): row block bi (ANR rows), column block bj (ANC columns) with bj*ANC < (bi+1)*ANR
-  const int64_t ncb = (N + ANC - 1) / ANC;
-  constexpr int RATIO = ANR / ANC;
-  const int64_t x = blockIdx.x;
-  // row block bi holds (bi+1)*RATIO column blocks (clipped to ncb): prefix sums are RATIO*bi(bi+1)/2
-  int64_t bi = (int64_t)((sqrt(8.0 * (double)x / RATIO + 1.0) - 1.0) * 0.5);
-  while (bi > 0 && RATIO * bi * (bi + 1) / 2 > x) bi--;
-  while (RATIO * (bi + 1) * (bi + 2) / 2 <= x) bi++;
-  const int64_t bj = x - RATIO * bi * (bi + 1) / 2;
-  if (bj >= ncb || bi * ANR >= N) return;
-  __shared__ double cpart[ANR / 32][ANC];
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int64_t i = bi * ANR + t;
-  double v[ANC];
-#pragma unroll
-  for (int u = 0; u < ANC; u++) {
-    const int64_t j = bj * ANC + u;
-    v[u] = (i < N && j < N && i >= j) ? A[i + j * lda] : 0.0;
-  }
-  bool bad = false;
-  double rs = 0.0;
-#pragma unroll
-  for (int u = 0; u < ANC; u++) {
-    if (!isfinite(v[u])) bad = true;
-    v[u] = fabs(v[u]);
-    rs += v[u];
-  }
-  if (__syncthreads_or(bad)) {
-    if (t == 0) { mds_set_status(status, MDS_ERR_NONFINITE); ctl->abort = 1; }
-    return;
-  }
-  if (i < N && rs != 0.0) atomicAdd(&rowsum[i], rs);
-  // column sums excluding the diagonal (they are row j's upper part)
-#pragma unroll
-  for (int u = 0; u < ANC; u++) {
-    const int64_t j = bj * ANC + u;
-    double c = (i > j) ? v[u] : 0.0;
-    c += __shfl_xor_sync(0xffffffffu, c, 16);
-    c += __shfl_xor_sync(0xffffffffu, c, 8);
-    c += __shfl_xor_sync(0xffffffffu, c, 4);
-    c += __shfl_xor_sync(0xffffffffu, c, 2);
-    c += __shfl_xor_sync(0xffffffffu, c, 1);
-    if (lane == 0) cpart[warp][u] = c;
-  }
-  __syncthreads();
-  if (t < ANC) {
-    double s2 = 0.0;
-#pragma unroll
-    for (int w = 0; w < ANR / 32; w++) s2 += cpart[w][t];
-    const int64_t j = bj * ANC + t;
-    if (j < N && s2 != 0.0) atomicAdd(&rowsum[j], s2);
-  }
-}
-
-__global__ void __launch_bounds__(1024) k_anorm_final(int64_t N, const double* rowsum, FCtl* ctl) {
-  pdl_wait();
-  pdl_trigger();
-  double m = 0.0;
-  for (int64_t i = threadIdx.x; i < N; i += blockDim.x) m = fmax(m, rowsum[i]);
-  m = warp_max(m);
-  __shared__ double sh[32];
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double a = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) a = fmax(a, sh[w]);
-    ctl->anorm = a;
-    if (ctl->tol < 0.0) ctl->tol = (double)N * 2.220446049250313e-16 * a;
+    if (threadIdx.x == 0) {
+      f.ctl->tol = zero_tol;
+      if (anorm) {   // ||M||_inf provided by the condensation (a3 fused into a2)
+        const double a = *anorm;
+        f.ctl->anorm = a;
+        if (!isfinite(a)) {   // NaN marks a non-finite M (anorm.cuh)
+          f.ctl->abort = 1;
+          mds_set_status(status, MDS_ERR_NONFINITE);
+        } else if (zero_tol < 0.0) {
+          f.ctl->tol = (double)N * 2.220446049250313e-16 * a;
+        }
+      }
+    }
   }
 }
 
@@ -2216,6 +2148,16 @@ double* mds_factor_tol_ptr(const void* fwork) {
   return fwork ? &reinterpret_cast<FCtl*>(const_cast<void*>(fwork))->tol : nullptr;
 }
 
+// ||M||_inf and the zero-pivot tolerance the last mds_factor on `fwork` used (synchronous)
+extern "C" int mds_factor_tol(const void* fwork, double* anorm_host, double* tol_host) {
+  if (!fwork) return MDS_ERR_ARG;
+  FCtl c;
+  if (cudaMemcpy(&c, fwork, sizeof(FCtl), cudaMemcpyDeviceToHost) != cudaSuccess) return MDS_ERR_CUDA;
+  if (anorm_host) *anorm_host = c.anorm;
+  if (tol_host) *tol_host = c.tol;
+  return MDS_OK;
+}
+
 // Side stream + reusable events for the look-ahead split, one set per CALLER
 // stream (so concurrent factorizations on different streams never share
 // events; a call on stream s always orders its side work through s).
@@ -2254,7 +2196,7 @@ extern "C" size_t mds_factor_workspace_size(int64_t N) {
 }
 
 extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, double zero_tol,
-                          mds_inertia* inertia_dev, mds_inertia* inertia_host, int32_t* status,
+                          const double* anorm, mds_inertia* inertia_dev, mds_inertia* inertia_host, int32_t* status,
                           void* work, size_t work_bytes, void* stream) {
   if (N < 0 || (N > 0 && (!M || !piv)) || ldm < std::max<int64_t>(N, 1)) return MDS_ERR_ARG;
   if (N >= (1 << 29)) return MDS_ERR_ARG;
@@ -2267,16 +2209,24 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   size_t need = mds_factor_workspace_size(N);
   if (!work || work_bytes < need) return MDS_ERR_WORKSPACE;
   FWork f = carve(work, N, nullptr);
-  // zero control + arrays (sw = -1)
+  // zero control + arrays (sw = -1); take ||M||_inf from the caller, or scan M for it
   MDS_LAUNCH(PC_ANORM, st,
              MDS_CUDA_TRY(launch_pdl(k_factor_init, dim3((unsigned)std::min<int64_t>(mds_cdiv(3 * (N + 2), 256), 1184)),
-                                     dim3(256), 0, st, N, f, zero_tol)));
-  {
-    const int64_t nrb = (N + ANR - 1) / ANR, nblk = (ANR / ANC) * nrb * (nrb + 1) / 2;
+                                     dim3(256), 0, st, N, f, zero_tol, anorm, status)));
+  if (!anorm) {
+    const int64_t nt = anorm::ntiles(N);
     MDS_LAUNCH(PC_ANORM, st,
-               MDS_CUDA_TRY(launch_pdl(k_anorm_tiles, dim3((unsigned)nblk), dim3(ANR), 0, st, N, M, ldm,
-                                       f.rowsum, f.ctl, status)));
-    MDS_LAUNCH(PC_ANORM, st, MDS_CUDA_TRY(launch_pdl(k_anorm_final, dim3(1), dim3(1024), 0, st, N, f.rowsum, f.ctl)));
+               MDS_CUDA_TRY(launch_pdl(anorm::k_anorm_scan, dim3((unsigned)nt), dim3(256), 0, st, N, (const double*)M, ldm,
+                                       anorm::parts_at(f.nparts, N))));
+    anorm::NormOut o = {};
+    o.anorm = &f.ctl->anorm;
+    o.tol0 = &f.ctl->tol;
+    o.abort0 = &f.ctl->abort;
+    o.status = status;
+    o.zero_tol = zero_tol;
+    MDS_LAUNCH(PC_ANORM, st,
+               MDS_CUDA_TRY(launch_pdl(anorm::k_anorm_rows, dim3((unsigned)mds_cdiv(N, 256), 1), dim3(256), 0, st, N,
+                                       f.nparts, (size_t)0, o)));
   }
   if (mds_once_per_device((const void*)k_update_tma<0, true>)) {
     cudaFuncSetAttribute(k_update_tma<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);

@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from . import (Plan, condense, factor, solve, step_vectors, factor_workspace_size, solve_workspace_size,
-               step_vectors_workspace_size, raise_for)
+               step_vectors_workspace_size, condense_workspace_size, raise_for)
 
 
 def _dev(a, dtype=torch.float64, device="cuda"):
@@ -67,6 +67,8 @@ class KKTStep:
         self.inertia = torch.zeros(3, dtype=torch.int64, device=device)
         self.status = torch.zeros(1, dtype=torch.int32, device=device)
         self.fwork = torch.empty(factor_workspace_size(N), dtype=torch.uint8, device=device)
+        self.cwork = torch.empty(condense_workspace_size(dprob.plan), dtype=torch.uint8, device=device)
+        self.anorm = torch.zeros(1, dtype=torch.float64, device=device)   # ||M||_inf (a3, fused into a2)
         self.swork = torch.empty(solve_workspace_size(N), dtype=torch.uint8, device=device)
         # direction laid out [dx_s | dx_d | dy_g | dy_h] so (dx_s, dx_d) is contiguous
         self.dirn = torch.empty(n_s + N + 1, **f64)
@@ -108,10 +110,11 @@ class KKTStep:
         self.status.zero_()
         ev(0)
         condense(p.plan, p.val, p.h_ss, p.sigma_s, p.H_dd, p.ldh, p.sigma_d, p.J_d, p.ldj, p.d_h, p.delta_w,
-                 p.delta_c, p.r, self.M, self.ldm, self.rhs, self.w, self.status, stream)
+                 p.delta_c, p.r, self.M, self.ldm, self.rhs, self.w, self.status, stream, anorm_out=self.anorm,
+                 work=self.cwork)
         ev(1)
         ine = factor(self.N, self.M, self.ldm, self.piv, self.zero_tol, self.inertia, self.status, self.fwork,
-                     sync=sync_inertia, stream=stream)
+                     sync=sync_inertia, stream=stream, anorm=self.anorm)
         ev(2)
         return ine
 
