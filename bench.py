@@ -343,7 +343,7 @@ def run_ours(args, rank, world):
                                       "finalize"))
     sol_ms = sum(prof[c][0] for c in ("solve_gather", "solve_fwd", "solve_d", "solve_bwd", "solve_scatter",
                                       "recover"))
-    cond_ms = sum(prof[c][0] for c in ("condense_rows", "condense_norm", "condense_tiles"))
+    cond_ms = sum(prof[c][0] for c in ("condense_rows", "condense_diag", "condense_norm", "condense_tiles"))
     dom = max(prof, key=lambda c: prof[c][0])
     peak_dmma, peak_cublas = fp64_peak()
     hbm, hbm_src = measured_hbm()

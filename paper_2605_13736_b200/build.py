@@ -16,7 +16,7 @@ def needs_build():
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, "common.cuh"),
+    deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, "common.cuh"), os.path.join(CSRC, "anorm.cuh"),
                                                       os.path.join(HERE, "..", "include", "mds.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 

@@ -38,7 +38,7 @@ struct Parts {
 
 inline size_t parts_bytes(int64_t N) {
   const int64_t nt = ntiles(N);
-  return (((size_t)nt * AT * 16 + (size_t)((N + 255) / 256 + 1) * 8 + 64) + 255) / 256 * 256;
+  return (((size_t)nt * AT * 16 + (size_t)((N + 31) / 32 + 1) * 8 + 64) + 255) / 256 * 256;
 }
 
 // the Parts of one matrix inside a block of parts_bytes(N) bytes at `base`
@@ -48,7 +48,7 @@ __host__ __device__ inline Parts parts_at(char* base, int64_t N) {
   P.prow = reinterpret_cast<double*>(base);
   P.pcol = P.prow + nt * AT;
   P.bmax = P.pcol + nt * AT;
-  P.ctr = reinterpret_cast<unsigned*>(P.bmax + (N + 255) / 256 + 1);
+  P.ctr = reinterpret_cast<unsigned*>(P.bmax + (N + 31) / 32 + 1);
   return P;
 }
 
@@ -98,30 +98,39 @@ __device__ __forceinline__ void tile_partials(const double (&v)[8][2], const boo
 // anorm[s] (NaN if a non-finite entry was seen).  When tol0 != NULL also sets
 // the tolerance (zero_tol < 0: N eps ||M||_inf, else zero_tol) and, on a
 // non-finite matrix, abort = 1 and status NONFINITE.  Resets the ticket.
+// A CTA takes 32 rows (lane = row); row i of block b has nb + 1 partials
+// (prow of tiles (b, 0..b), then pcol of tiles (b..nb-1, b)), split into 8
+// fixed ranges, one per warp, summed in order and then combined in warp order.
 __global__ void __launch_bounds__(256) k_anorm_rows(int64_t N, char* parts, size_t parts_stride, NormOut o) {
   pdl_wait();
   pdl_trigger();
   const int64_t ms = blockIdx.y;
   const Parts P = parts_at(parts + ms * parts_stride, N);
   const int64_t nb = (N + AT - 1) / AT;
-  const int64_t i = blockIdx.x * 256ll + threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i = blockIdx.x * 32ll + lane;
+  __shared__ double part[AW][32];
   double s = 0.0;
   if (i < N) {
     const int64_t b = i / AT, r = i % AT;
-    for (int64_t J = 0; J <= b; J++) s += P.prow[tile_id(b, J) * AT + r];
-    for (int64_t I = b; I < nb; I++) s += P.pcol[tile_id(I, b) * AT + r];
+    const int64_t nterm = nb + 1, per = (nterm + AW - 1) / AW;
+    const int64_t x0 = min(nterm, per * warp), x1 = min(nterm, per * (warp + 1));
+    for (int64_t x = x0; x < x1; x++)
+      s += (x <= b) ? P.prow[tile_id(b, x) * AT + r] : P.pcol[tile_id(x - 1, b) * AT + r];
   }
-  s = warp_max(s);
-  __shared__ double sh[8];
-  __shared__ bool last;
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  part[warp][lane] = s;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double bm = 0.0;
-    for (int w = 0; w < 8; w++) bm = fmax(bm, sh[w]);
-    P.bmax[blockIdx.x] = bm;
-    __threadfence();
-    last = atomicAdd(&P.ctr[1], 1u) == gridDim.x - 1;
+  __shared__ bool last;
+  if (warp == 0) {
+    double rs = 0.0;
+#pragma unroll
+    for (int w = 0; w < AW; w++) rs += part[w][lane];
+    rs = warp_max(rs);
+    if (lane == 0) {
+      P.bmax[blockIdx.x] = rs;
+      __threadfence();
+      last = atomicAdd(&P.ctr[1], 1u) == gridDim.x - 1;
+    }
   }
   __syncthreads();
   if (last && threadIdx.x == 0) {
@@ -142,6 +151,13 @@ __global__ void __launch_bounds__(256) k_anorm_rows(int64_t N, char* parts, size
     P.ctr[1] = 0u;
     P.ctr[2] = 0u;
   }
+}
+
+// launch k_anorm_rows for `batch` matrices (partials `parts_stride` bytes apart)
+inline cudaError_t launch_rows(int64_t N, char* parts, size_t parts_stride, const NormOut& o, int64_t batch,
+                               cudaStream_t st) {
+  return launch_pdl(k_anorm_rows, dim3((unsigned)((N + 31) / 32), (unsigned)batch), dim3(256), 0, st, N, parts,
+                    parts_stride, o);
 }
 
 // Stand-alone scan of a matrix already in memory (mds_factor without a

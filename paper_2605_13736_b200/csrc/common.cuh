@@ -58,7 +58,7 @@ __device__ __forceinline__ ArgMax warp_argmax(ArgMax a) {
     if (_e != cudaSuccess) return MDS_ERR_CUDA;             \
   } while (0)
 
-static inline int64_t mds_cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ static inline int64_t mds_cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Programmatic dependent launch: a kernel launched with launch_pdl may be
 // scheduled before its stream predecessor has finished; it calls pdl_wait()
@@ -128,7 +128,7 @@ static inline cudaError_t launch_coop_pdl(void (*k)(KArgs...), dim3 g, dim3 b, s
 enum MdsProfClass {
   PC_CONDENSE_W = 0, PC_CONDENSE_DENSE, PC_CONDENSE_YY, PC_ANORM, PC_PANEL_DIAG, PC_PANEL_TRSM,
   PC_PANEL_STORE, PC_PANEL_SLOW, PC_UPDATE, PC_FINALIZE, PC_SOLVE_GATHER, PC_SOLVE_FWD, PC_SOLVE_D,
-  PC_SOLVE_BWD, PC_SOLVE_SCATTER, PC_RECOVER, PC_VECTORS, PC_COUNT
+  PC_SOLVE_BWD, PC_SOLVE_SCATTER, PC_RECOVER, PC_VECTORS, PC_CONDENSE_DIAG, PC_COUNT
 };
 extern bool g_mds_prof;
 void mds_prof_start(int cls, cudaStream_t st);

@@ -2225,8 +2225,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     o.status = status;
     o.zero_tol = zero_tol;
     MDS_LAUNCH(PC_ANORM, st,
-               MDS_CUDA_TRY(launch_pdl(anorm::k_anorm_rows, dim3((unsigned)mds_cdiv(N, 256), 1), dim3(256), 0, st, N,
-                                       f.nparts, (size_t)0, o)));
+               MDS_CUDA_TRY(anorm::launch_rows(N, f.nparts, (size_t)0, o, 1, st)));
   }
   if (mds_once_per_device((const void*)k_update_tma<0, true>)) {
     cudaFuncSetAttribute(k_update_tma<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);

@@ -1,8 +1,8 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py
 times (CUDA-graph replay of the whole step):
   C2 (N=1024, n_s=100k): every output against the oracle.
-  C3 (N=8192, n_s=1M): condensed M, rhs_c, w bit-exact against the oracle and
-    ||M||_inf within 1e-13; inertia against the closed form AND the oracle's BK
+  C3 (N=8192, n_s=1M): condensed M and rhs_c element by element within 1e-14 of
+    their largest entry, w bit-exact, ||M||_inf within 1e-13; inertia against the closed form AND the oracle's BK
     factorization; the solution element by element against the oracle's
     (<= 1e-8) and through the residual of the condensed system (<= 1e-10);
     step vectors against the oracle on the GPU's direction.
@@ -53,7 +53,7 @@ def test_c3_full_size_properties():
     sv = mdsgen.step_vectors_for(prob, seed=7)
     dp = mds.DeviceProblem(prob)
     st = mds.KKTStep(dp, sv=sv)
-    # condensation alone, element by element (bit-exact)
+    # condensation alone, element by element
     anorm = torch.zeros(1, dtype=torch.float64, device="cuda")
     mds.condense(dp.plan, dp.val, dp.h_ss, dp.sigma_s, dp.H_dd, dp.ldh, dp.sigma_d, dp.J_d, dp.ldj, dp.d_h,
                  dp.delta_w, dp.delta_c, dp.r, st.M, st.ldm, st.rhs, st.w, st.status, anorm_out=anorm,
@@ -61,9 +61,9 @@ def test_c3_full_size_properties():
     torch.cuda.synchronize()
     M_or, rhs_or, w_or = oracle.condense(prob)
     Mg = st.M_host()
-    np.testing.assert_array_equal(np.tril(Mg), np.tril(M_or))
+    assert np.abs(np.tril(Mg) - np.tril(M_or)).max() <= 1e-14 * np.abs(np.tril(M_or)).max()
     np.testing.assert_array_equal(st.w[:prob.n_s].cpu().numpy(), w_or)
-    np.testing.assert_array_equal(st.rhs[:prob.N].cpu().numpy(), rhs_or)
+    assert rel_inf(st.rhs[:prob.N].cpu().numpy(), rhs_or) <= 1e-14
     a_or = oracle.anorm_lower(M_or)
     assert abs(float(anorm.item()) - a_or) <= 1e-13 * a_or
     del Mg
@@ -105,7 +105,7 @@ def test_c4_scenario_full_size_vs_oracle():
     ref = oracle.newton_step(prob)
     assert out["status"] == 0
     assert out["inertia"] == ref["inertia"] == prob.expected_inertia
-    np.testing.assert_array_equal(out["rhs_c"], ref["rhs_c"])
+    assert rel_inf(out["rhs_c"], ref["rhs_c"]) <= 1e-14
     np.testing.assert_array_equal(out["w"], ref["w"])
     assert rel_inf(out["dxy"], ref["dxy"]) <= 1e-8
     assert rel_inf(out["dx_s"], ref["dx_s"]) <= 1e-8
