@@ -47,7 +47,6 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=3072, help="oracle factor sample size (leading block)")
     ap.add_argument("--scenarios", type=int, default=256, help="C4: total SCOPF scenarios (strong scaling)")
-    ap.add_argument("--streams", type=int, default=32, help="C4: concurrent CUDA streams per GPU (8: 82.7 ms, 32: 78.6 ms per step measured)")
     return ap.parse_args()
 
 
@@ -438,7 +437,7 @@ def run_ours(args, rank, world):
 
 def run_scopf(args, rank, world):
     """C4: SCOPF scenario batch, scenarios round-robin over ranks; per Newton step
-    every local scenario's KKT step on concurrent streams + ONE small NCCL
+    the rank's whole local batch as ONE graph of batched launches + ONE small NCCL
     all-reduce pair for the global stopping test (read on the host)."""
     import torch
     import torch.distributed as dist
@@ -454,18 +453,20 @@ def run_scopf(args, rank, world):
     svf = lambda p_, s_: mdsgen.step_vectors_for(p_, seed=100 + s_)
     ids = scopf.partition(args.scenarios, world, rank)
     t0 = time.time()
-    l0 = mds.launch_count()
-    batch = scopf.ScopfBatch(base, fn, ids, svf, n_streams=args.streams)
+    batch = scopf.ScopfBatch(base, fn, ids, svf)
     setup_s = time.time() - t0
     for _ in range(args.warmup):
         batch.newton_step()
         batch.stop_test()
     torch.cuda.synchronize()
-    # launches per Newton step = per-scenario step launches x local scenarios
+    # library launches per Newton step (the graph replays exactly this sequence)
     l1 = mds.launch_count()
-    batch.steps[0].run()
+    batch.bt.run()
     torch.cuda.synchronize()
-    per_scen = mds.launch_count() - l1
+    per_step = mds.launch_count() - l1
+    mds.profile_begin()
+    batch.bt.run()
+    prof = mds.profile_end()
     if world > 1:
         dist.barrier()
     stream = torch.cuda.current_stream()
@@ -491,22 +492,35 @@ def run_scopf(args, rank, world):
     value = args.scenarios * args.steps / (ms_max / 1e3)
     if rank == 0:
         N = base.N
+        nloc = len(ids)
         fl = args.scenarios * args.steps * (N ** 3 / 3.0 + 2.0 * N * N)
+        upd_ms, upd_n = prof["update"]
+        # trailing-update flops of the local batch per step: sum over panels of n2 (n2+1) kb, kb = 64
+        upd_fl = 0.0
+        k = 0
+        while k < N:
+            kb = min(64, N - k)
+            n2 = N - k - kb
+            upd_fl += n2 * (n2 + 1) * kb
+            k += kb
+        upd_fl *= nloc
         line = {"metric": METRIC, "value": value, "unit": "scenario_newton_iters/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
                 "config": {"workload": "C4 " + f"SCOPF {args.scenarios} contingency scenarios, N=2048 each "
-                           "(n_d=1024, m_E=m_I=512, n_s=131072, shared pattern), round-robin over ranks",
-                           "N": N, "scenarios": args.scenarios, "streams_per_gpu": args.streams,
-                           "parallelism": f"scenario-dp{world}", "cuda_graph": True},
-                "gpu_launches": per_scen * len(ids) * args.steps,
+                           "(n_d=1024, m_E=m_I=512, n_s=131072, shared pattern), round-robin over ranks, "
+                           "batched C-ABI (one graph of batched launches per rank)",
+                           "N": N, "scenarios": args.scenarios, "parallelism": f"scenario-dp{world}",
+                           "cuda_graph": True, "l2": "inputs larger than L2 (8.6 GB of M per 256 scenarios)"},
+                "gpu_launches": per_step * args.steps,
                 "factor_solve_fp64_tflops_aggregate": fl / (ms_max * 1e-3) / 1e12,
-                "roofline": {"kernel": "whole batch (factor+solve flops of all scenarios / step time)",
-                             "bound": "tensor", "achieved": fl / (ms_max * 1e-3) / 1e12 / world,
-                             "peak": fp64_peak()[0], "unit": "TFLOP/s",
-                             "frac": fl / (ms_max * 1e-3) / 1e12 / world / fp64_peak()[0], "traffic": None,
-                             "note": "per GPU; concurrent scenarios, no single dominant launch"},
+                "roofline": {"kernel": "k_update_tma<5> (batched DMMA trailing update)", "bound": "tensor",
+                             "achieved": upd_fl / (upd_ms * 1e-3) / 1e12, "peak": fp64_peak()[0],
+                             "unit": "TFLOP/s", "frac": upd_fl / (upd_ms * 1e-3) / 1e12 / fp64_peak()[0],
+                             "traffic": None, "launches": upd_n, "avg_launch_us": upd_ms / max(upd_n, 1) * 1e3},
+                "factor_solve_frac_of_peak": fl / (ms_max * 1e-3) / 1e12 / world / fp64_peak()[0],
+                "kernels": {c: {"ms": round(v[0], 4), "launches": v[1]} for c, v in prof.items() if v[1]},
                 "stop_test": st, "records_gathered": int(recs.shape[0]),
                 "all_inertia_ok": bool(st["n_bad_inertia"] == 0), "setup_s": setup_s,
                 "clocks": clk.summary(), "e2e": None, "cpu_baseline": None}

@@ -92,10 +92,12 @@ int mds_plan_dims(const mds_plan *plan, int64_t *out5);
  *   anorm_out = ||M||_inf (row abs-sums of the symmetric M from its lower
  *   triangle, fixed summation order -> bitwise reproducible), or NaN if M
  *   holds a NaN/Inf entry.  Feed it to mds_factor's `anorm` to skip its scan.
- * Every entry of M and rhs_c is formed by the same floating-point operations
- * in the same order as the plain elimination one sparse variable at a time
- * (PAPER.md:166-168): for each output, the products (val_p w_k) val_p' are
- * subtracted in ascending k.
+ * w is formed with the elimination's own operations (IEEE division).  The
+ * products (val_p w_k) val_p' of each entry of M_yy (and the rhs terms) are
+ * summed in one FIXED order (diagonal: a per-column warp tree; off-diagonal:
+ * segmented shuffle trees over the plan's destination-sorted pair list), so the
+ * result is bitwise reproducible; it differs from the elimination one sparse
+ * variable at a time only by summation rounding.
  * Inputs (device): js_val[nnz] (values in the plan's CSR order); h_ss, sigma_s
  * [n_s]; H_dd [n_d x n_d, ldh, lower read]; sigma_d [n_d]; J_d [m x n_d, ldj];
  * d_h [m_I]; r [n_s + N] = (r_xs, r_xd, r_yg, r_yh) or NULL (then rhs_c is not
@@ -167,6 +169,21 @@ size_t mds_factor_workspace_size(int64_t N);
 int mds_factor(int64_t N, double *M, int64_t ldm, int32_t *piv, double zero_tol,
                const double *anorm, mds_inertia *inertia_dev, mds_inertia *inertia_host, int32_t *status_dev,
                void *work, size_t work_bytes, void *stream);
+/* mds_factor_batched — `batch` independent N x N factorizations (SCOPF scenario
+ * batches; SURVEY §8(b) _batched) in ONE launch sequence: each
+ * panel step is one launch for all scenarios (grid.y = scenario), and the DMMA
+ * trailing update is one persistent launch whose tile queue spans every
+ * scenario.  Scenario s: M + s * str_M (elements; 16-byte aligned M, even ldm
+ * and str_M required: the update is TMA-fed), piv + s * str_piv (>= 2N),
+ * inertia_dev[s], status[s] (device arrays [batch]); anorm: device [batch]
+ * (mds_condense_batched's anorm_out) or NULL (each M is scanned).  One
+ * non-finite scenario aborts only itself (status[s] = NONFINITE, identity
+ * permutation).  Same factor format and pivot rule as mds_factor.  Never
+ * synchronises.  work >= mds_factor_batched_workspace_size(N, batch). */
+size_t mds_factor_batched_workspace_size(int64_t N, int64_t batch);
+int mds_factor_batched(int64_t batch, int64_t N, double *M, int64_t ldm, int64_t str_M, int32_t *piv,
+                       int64_t str_piv, double zero_tol, const double *anorm, mds_inertia *inertia_dev,
+                       int32_t *status, void *work, size_t work_bytes, void *stream);
 /* ||M||_inf and the zero-pivot tolerance the last mds_factor on `work` used
  * (host copies; synchronous).  For the parity tests of reading R4. */
 int mds_factor_tol(const void *work, double *anorm_host, double *tol_host);
@@ -188,6 +205,20 @@ int mds_solve(const mds_plan *plan, int64_t N, const double *LD, int64_t ldm, co
               double *dxy, double *dx_s, double zero_tol, const void *fwork,
               int32_t *status_dev, void *work, size_t work_bytes, void *stream);
 
+/* mds_solve_batched — `batch` solves + recoveries with mds_factor_batched's
+ * output in one launch sequence (grid.y = scenario).  Scenario s: LD + s * str_LD,
+ * piv + s * str_piv, rhs_c + s * str_rhs, js_val + s * str_val, w + s * str_w,
+ * r_xs + s * str_r, dxy + s * str_dxy, dx_s + s * str_dxs (elements), status[s];
+ * fwork = the mds_factor_batched workspace (zero_tol < 0 reads scenario s's
+ * tolerance from it).  work >= mds_solve_batched_workspace_size(N, batch). */
+size_t mds_solve_batched_workspace_size(int64_t N, int64_t batch);
+int mds_solve_batched(const mds_plan *plan, int64_t batch, int64_t N, const double *LD, int64_t ldm, int64_t str_LD,
+                      const int32_t *piv, int64_t str_piv, const double *rhs_c, int64_t str_rhs,
+                      const double *js_val, int64_t str_val, const double *w, int64_t str_w,
+                      const double *r_xs, int64_t str_r, double *dxy, int64_t str_dxy, double *dx_s, int64_t str_dxs,
+                      double zero_tol, const void *fwork, int32_t *status_dev, void *work, size_t work_bytes,
+                      void *stream);
+
 /* ---------------------------------------------------------------------------
  * ipm_step_vectors — barrier vector kernels (K1), one fused pass:
  * fraction-to-boundary ("the point that is feasible with respect
@@ -208,6 +239,20 @@ int mds_solve(const mds_plan *plan, int64_t N, const double *LD, int64_t ldm, co
  * bytes, ZEROED once before first use (the kernel leaves it zeroed).
  * Data errors: MDS_ERR_NOT_INTERIOR. */
 size_t ipm_step_vectors_workspace_size(int64_t n);
+/* ipm_step_vectors_batched — the same for `batch` scenarios in one launch: the 8
+ * input vectors and sigma_out of scenario s at + s * str_vec (elements, >= n),
+ * out + s * str_out (>= 6 + n_res), status[s]; tau / mu from the device arrays
+ * tau_arr / mu_arr [batch] when non-NULL, else the scalars; residual j of
+ * scenario s at res[j] + s * res_str[j] (res, res_len, res_str: HOST arrays).
+ * work >= ipm_step_vectors_batched_workspace_size(n, batch) (no zeroing needed). */
+size_t ipm_step_vectors_batched_workspace_size(int64_t n, int64_t batch);
+int ipm_step_vectors_batched(int64_t batch, int64_t n, int64_t str_vec, const double *x, const double *dx,
+                             const double *lo, const double *up, const double *zl, const double *zu,
+                             const double *dzl, const double *dzu, double tau, double mu,
+                             const double *tau_arr, const double *mu_arr, int32_t n_res,
+                             const double *const *res, const int64_t *res_len, const int64_t *res_str,
+                             double *out, int64_t str_out, double *sigma_out, int32_t *status_dev,
+                             void *work, size_t work_bytes, void *stream);
 int ipm_step_vectors(int64_t n, const double *x, const double *dx, const double *lo, const double *up,
                      const double *zl, const double *zu, const double *dzl, const double *dzu,
                      double tau, double mu, int32_t n_res, const double *const *res, const int64_t *res_len,

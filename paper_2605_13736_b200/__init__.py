@@ -62,6 +62,20 @@ for _f in ("mds_plan_create", "mds_plan_destroy", "mds_plan_dims", "mds_condense
            "ipm_step_vectors"):
     getattr(_lib, _f).restype = ctypes.c_int
 
+_lib.mds_factor_batched_workspace_size.restype = ctypes.c_size_t
+_lib.mds_factor_batched_workspace_size.argtypes = [_I64, _I64]
+_lib.mds_factor_batched.argtypes = [_I64, _I64, _P, _I64, _I64, _P, _I64, _D, _P, _P, _P, _P, ctypes.c_size_t, _P]
+_lib.mds_factor_batched.restype = ctypes.c_int
+_lib.mds_solve_batched_workspace_size.restype = ctypes.c_size_t
+_lib.mds_solve_batched_workspace_size.argtypes = [_I64, _I64]
+_lib.mds_solve_batched.argtypes = ([_P, _I64, _I64, _P, _I64, _I64] + [_P, _I64] * 7 + [_D, _P, _P, _P, ctypes.c_size_t, _P])
+_lib.mds_solve_batched.restype = ctypes.c_int
+_lib.ipm_step_vectors_batched_workspace_size.restype = ctypes.c_size_t
+_lib.ipm_step_vectors_batched_workspace_size.argtypes = [_I64, _I64]
+_lib.ipm_step_vectors_batched.argtypes = ([_I64, _I64, _I64] + [_P] * 8 + [_D, _D, _P, _P, ctypes.c_int32, _P, _P, _P,
+                                          _P, _I64, _P, _P, _P, ctypes.c_size_t, _P])
+_lib.ipm_step_vectors_batched.restype = ctypes.c_int
+
 _lib.mds_kkt_residual_workspace_size.restype = ctypes.c_size_t
 _lib.mds_kkt_residual_workspace_size.argtypes = [_I64]
 _lib.mds_kkt_residual.argtypes = [_P, _P, _P, _P, _P, _I64, _P, _P, _I64, _P, _D, _D, _P, _P, _P, _P, _P,
@@ -71,7 +85,9 @@ _lib.mds_kkt_residual.restype = ctypes.c_int
 EXPORTS = ["mds_condense_workspace_size", "mds_condense_batched", "mds_factor_tol", "mds_kkt_residual_workspace_size", "mds_kkt_residual", "mds_version", "mds_plan_create", "mds_plan_destroy", "mds_plan_dims", "mds_condense",
            "mds_factor_workspace_size", "mds_factor", "mds_solve_workspace_size", "mds_solve",
            "ipm_step_vectors_workspace_size", "ipm_step_vectors", "mds_launch_count", "mds_profile_begin",
-           "mds_profile_end", "mds_factor_panels", "mds_factor_set_grid_cap", "mds_profile_timeline", "mds_set_variant"]
+           "mds_profile_end", "mds_factor_panels", "mds_factor_set_grid_cap", "mds_profile_timeline", "mds_set_variant",
+           "mds_factor_batched_workspace_size", "mds_factor_batched", "mds_solve_batched_workspace_size",
+           "mds_solve_batched", "ipm_step_vectors_batched_workspace_size", "ipm_step_vectors_batched"]
 
 PROF_CLASSES = ["condense_rows", "condense_norm", "condense_tiles", "anorm", "panel_diag", "panel_trsm", "panel_store",
                 "panel_exact", "update", "finalize", "solve_gather", "solve_fwd", "solve_d", "solve_bwd",
@@ -82,9 +98,24 @@ def version() -> str:
     return _lib.mds_version().decode()
 
 
+class DevPtr:
+    """A raw device address inside a live CUDA tensor (a strided per-scenario view
+    of a [B, W] tensor passed by its base address; the stride is a separate
+    argument of the batched calls).  Keeps the tensor alive."""
+
+    def __init__(self, t: torch.Tensor, offset_elems: int = 0):
+        if not t.is_cuda:
+            raise DimensionError("tensor must live on a CUDA device (no CPU fallback)")
+        self.t = t
+        self.ptr = t.data_ptr() + int(offset_elems) * t.element_size()
+        self.dtype = t.dtype
+
+
 def _ptr(t):
     if t is None:
         return None
+    if isinstance(t, DevPtr):
+        return t.ptr
     if not isinstance(t, torch.Tensor):
         raise TypeError("expected a torch tensor")
     if not t.is_cuda:
@@ -95,6 +126,10 @@ def _ptr(t):
 
 
 def _f64(t, n=None):
+    if isinstance(t, DevPtr):
+        if t.dtype != torch.float64:
+            raise DimensionError("FP64 tensor required")
+        return t.ptr
     if t is not None and t.dtype != torch.float64:
         raise DimensionError("FP64 tensor required")
     if t is not None and n is not None and t.numel() < n:
@@ -210,6 +245,54 @@ def factor(N, M, ldm, piv, zero_tol, inertia_dev, status, work, sync=True, strea
     return (host.pos, host.zero, host.neg) if sync else None
 
 
+def factor_batched_workspace_size(N, batch):
+    return int(_lib.mds_factor_batched_workspace_size(int(N), int(batch)))
+
+
+def solve_batched_workspace_size(N, batch):
+    return int(_lib.mds_solve_batched_workspace_size(int(N), int(batch)))
+
+
+def step_vectors_batched_workspace_size(n, batch):
+    return int(_lib.ipm_step_vectors_batched_workspace_size(int(n), int(batch)))
+
+
+def factor_batched(batch, N, M, ldm, str_M, piv, str_piv, zero_tol, inertia_dev, status, work, anorm=None,
+                   stream=None):
+    """mds_factor_batched: `batch` factorizations in one launch sequence (never syncs).
+    inertia_dev: int64 [batch, 3]; status: int32 [batch]; anorm: FP64 [batch] or None."""
+    code = _lib.mds_factor_batched(int(batch), int(N), _f64(M), int(ldm), int(str_M), _ptr(piv), int(str_piv),
+                                   float(zero_tol), _f64(anorm), _ptr(inertia_dev), _ptr(status), _ptr(work),
+                                   work.numel() * work.element_size(), _stream(stream))
+    _check(code, "mds_factor_batched")
+
+
+def solve_batched(plan, batch, N, LD, ldm, str_LD, piv, str_piv, rhs_c, str_rhs, js_val, str_val, w, str_w, r_xs,
+                  str_r, dxy, str_dxy, dx_s, str_dxs, zero_tol, fwork, status, work, stream=None):
+    """mds_solve_batched (strides in elements; see include/mds.h)."""
+    code = _lib.mds_solve_batched(plan.handle if plan is not None else None, int(batch), int(N), _f64(LD), int(ldm),
+                                  int(str_LD), _ptr(piv), int(str_piv), _f64(rhs_c), int(str_rhs), _f64(js_val),
+                                  int(str_val), _f64(w), int(str_w), _f64(r_xs), int(str_r), _f64(dxy), int(str_dxy),
+                                  _f64(dx_s), int(str_dxs), float(zero_tol), _ptr(fwork), _ptr(status), _ptr(work),
+                                  work.numel() * work.element_size(), _stream(stream))
+    _check(code, "mds_solve_batched")
+
+
+def step_vectors_batched(batch, n, str_vec, x, dx, lo, up, zl, zu, dzl, dzu, tau, mu, out, str_out, sigma_out,
+                         status, work, tau_arr=None, mu_arr=None, res=(), res_str=(), stream=None):
+    """ipm_step_vectors_batched (per-scenario vectors at + s * str_vec)."""
+    nres = len(res)
+    arr_p = (ctypes.c_void_p * max(nres, 1))(*[_f64(t) for t in res]) if nres else None
+    arr_l = (ctypes.c_int64 * max(nres, 1))(*[int(L) for L, _ in res_str]) if nres else None
+    arr_s = (ctypes.c_int64 * max(nres, 1))(*[int(S) for _, S in res_str]) if nres else None
+    code = _lib.ipm_step_vectors_batched(int(batch), int(n), int(str_vec), _f64(x), _f64(dx), _f64(lo), _f64(up),
+                                         _f64(zl), _f64(zu), _f64(dzl), _f64(dzu), float(tau), float(mu),
+                                         _f64(tau_arr), _f64(mu_arr), nres, arr_p, arr_l, arr_s, _f64(out),
+                                         int(str_out), _f64(sigma_out), _ptr(status), _ptr(work),
+                                         work.numel() * work.element_size(), _stream(stream))
+    _check(code, "ipm_step_vectors_batched")
+
+
 def factor_tol(fwork):
     """(||M||_inf, zero-pivot tolerance) the last mds_factor on `fwork` used (synchronous)."""
     a, t = ctypes.c_double(), ctypes.c_double()
@@ -305,4 +388,5 @@ def factor_panels(fwork, N):
 
 
 from .step import KKTStep, DeviceProblem  # noqa: E402,F401
+from .batch import BatchedKKTStep  # noqa: E402,F401
 from .inertia import InertiaCorrection, ICParams  # noqa: E402,F401

@@ -162,9 +162,13 @@ inline cudaError_t launch_rows(int64_t N, char* parts, size_t parts_stride, cons
 
 // Stand-alone scan of a matrix already in memory (mds_factor without a
 // condensation-provided norm): one CTA per lower tile, read once.
-__global__ void __launch_bounds__(256) k_anorm_scan(int64_t N, const double* __restrict__ A, int64_t lda, Parts P) {
+// Batched: matrix s = blockIdx.y at A + s * a_stride, partials at parts + s * parts_stride.
+__global__ void __launch_bounds__(256) k_anorm_scan(int64_t N, const double* __restrict__ A, int64_t lda,
+                                                    int64_t a_stride, char* parts, size_t parts_stride) {
   pdl_wait();
   pdl_trigger();
+  A += blockIdx.y * a_stride;
+  const Parts P = parts_at(parts + blockIdx.y * parts_stride, N);
   __shared__ double red[AW][AT];
   const int64_t t = blockIdx.x;
   int64_t I = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);

@@ -90,7 +90,24 @@ struct FWork {
   int fuse;           // 1: this panel's columns still lack the previous panel's update (look-ahead)
   int pidx;           // panel index of this launch (host loop counter)
   int64_t ldw;
+  // batched factorization (mds_factor_batched): scenario s = blockIdx.y (z for k_panel_store)
+  // owns the workspace at + s * bws bytes, M at + s * bms elements, piv at + s * bps
+  size_t bws;
+  int64_t bms, bps;
 };
+
+template <typename T>
+__device__ __forceinline__ void shp(T*& p, size_t o) { p = reinterpret_cast<T*>(reinterpret_cast<uintptr_t>(p) + o); }
+// this scenario's view of a batched factorization (no-op for s = 0 / single system):
+// workspace pointers of f, and the caller's M (and piv) pointers
+__device__ __forceinline__ void bsel_ws(FWork& f, int64_t s) {
+  if (s == 0) return;
+  const size_t o = (size_t)s * f.bws;
+  shp(f.ctl, o); shp(f.panel_start, o); shp(f.sw, o); shp(f.bt, o); shp(f.rho, o); shp(f.rhoinv, o);
+  shp(f.nparts, o); shp(f.Lblk, o); shp(f.W, o); shp(f.W1, o); shp(f.Lb, o); shp(f.Lb1, o); shp(f.pinfo, o);
+  shp(f.ucount, o); shp(f.t1flag, o); shp(f.xbar, o); shp(f.xpart, o); shp(f.xaux, o); shp(f.Wprev, o);
+  shp(f.Lbprev, o);
+}
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -122,6 +139,9 @@ FWork carve(void* work, int64_t N, size_t* total) {
   f.Lbprev = f.Lb1;
   f.fuse = 0;
   f.pidx = 0;
+  f.bws = 0;
+  f.bms = 0;
+  f.bps = 0;
   if (total) *total = off;
   return f;
 }
@@ -141,6 +161,11 @@ __device__ __forceinline__ double bitsd(unsigned long long b) { return __longlon
 // zero the per-call control state (one kernel instead of several memsets, so
 // the launch chain stays programmatic-dependent-launch friendly)
 __global__ void k_factor_init(int64_t N, FWork f, double zero_tol, const double* anorm, int32_t* status) {
+  {   // batched: scenario blockIdx.y
+    bsel_ws(f, blockIdx.y);
+    if (status) status += blockIdx.y;
+    if (anorm) anorm += blockIdx.y;
+  }
   pdl_wait();
   pdl_trigger();
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -559,6 +584,8 @@ __device__ __forceinline__ void f1_body(int64_t N, double* __restrict__ A, int64
 }
 
 __global__ void __launch_bounds__(256) k_panel_diag(int64_t N, double* __restrict__ A, int64_t lda, FWork f) {
+  bsel_ws(f, blockIdx.y);
+  A += blockIdx.y * f.bms;
   pdl_wait();
   FCtl* ctl = f.ctl;
   if (ctl->abort) return;
@@ -749,6 +776,8 @@ __global__ void __launch_bounds__(256, 1) k_panel_fast(int64_t N, double* __rest
 // draws from once this panel's X is published: whatever it has not taken is
 // done here.
 __global__ void __launch_bounds__(128) k_panel_trsm(int64_t N, const double* __restrict__ A, int64_t lda, FWork f) {
+  bsel_ws(f, blockIdx.y);
+  A += blockIdx.y * f.bms;
   pdl_trigger();   // let k_panel_slow launch and wait (griddepcontrol.wait) behind us
   FCtl* ctl = f.ctl;
   if (ctl->abort) return;
@@ -889,6 +918,9 @@ __device__ __forceinline__ void zero_w_tail(int64_t N, int64_t k0, int kb, const
 
 __global__ void __launch_bounds__(1024) k_panel_slow(int64_t N, double* __restrict__ A, int64_t lda, FWork f,
                                                      int32_t* piv) {
+  bsel_ws(f, blockIdx.y);
+  A += blockIdx.y * f.bms;
+  piv += blockIdx.y * f.bps;
   pdl_wait();
   pdl_trigger();
   FCtl* ctl = f.ctl;
@@ -1231,6 +1263,9 @@ __device__ __noinline__ void x_f2_leftovers(int64_t N, const double* __restrict_
 
 __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restrict__ A, int64_t lda, FWork f,
                                                     int32_t* piv, int xchunk, int use_ls, int f2left) {
+  bsel_ws(f, blockIdx.y);
+  A += blockIdx.y * f.bms;
+  piv += blockIdx.y * f.bps;
   pdl_wait();
   pdl_trigger();
   FCtl* ctl = f.ctl;
@@ -1457,6 +1492,8 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
 
 // Copy the finished panel (D + L columns, rows >= the diagonal) from Lb into M.
 __global__ void __launch_bounds__(256) k_panel_store(int64_t N, double* __restrict__ A, int64_t lda, FWork f) {
+  bsel_ws(f, blockIdx.z);
+  A += blockIdx.z * f.bms;
   if (f.ctl->abort) return;
   const int2 pi = f.pinfo[f.pidx];
   const int64_t k0 = pi.x;
@@ -1642,7 +1679,7 @@ constexpr int TBOXB = 16 * NB * 8;                // bytes per TMA box (16 rows 
 // OUTB variant: 2 stages + one 32 KB output buffer per consumer group (a stage is released as soon as
 // its k-loop is done); in-place variant: 3 stages, -P staged in the consumed stage (released after the
 // TMA reduce has read it).  Both use 192 KB.
-constexpr int TSMEM = TSMAX * TSTAGEB + 1024 + 16 * TSMAX + 8 * TSMAX;   // + alignment + barriers + tile slots
+constexpr int TSMEM = TSMAX * TSTAGEB + 1024 + 16 * TSMAX + 16 * TSMAX;   // + alignment + barriers + 2 tile slots
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
@@ -1735,6 +1772,22 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, int c0
                "r"(c0), "r"(c1), "r"(src)
                : "memory");
 }
+// 3-D forms (batched factorization: the third coordinate is the scenario)
+__device__ __forceinline__ void tma_load_3d(unsigned dst, const CUtensorMap* map, int c0, int c1, int c2, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(map), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, int c0, int c1, int c2, unsigned src) {
+  asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(map),
+               "r"(c0), "r"(c1), "r"(c2), "r"(src)
+               : "memory");
+}
 __device__ __forceinline__ void sts_f64(unsigned addr, double v) {
   asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(addr), "d"(v) : "memory");
 }
@@ -1750,33 +1803,43 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
                                                              const __grid_constant__ CUtensorMap mapA,
                                                              const __grid_constant__ CUtensorMap mapW,
                                                              const __grid_constant__ CUtensorMap mapL,
-                                                             const __grid_constant__ CUtensorMap mapX, int sched) {
-  const bool snake = (sched & 2) != 0;
+                                                             const __grid_constant__ CUtensorMap mapX, int sched,
+                                                             int64_t bt_tiles, int64_t bt_n) {
+  // mode 5 = mode 0 for a batch of bt_n scenarios (3-D tensor maps, third coordinate = scenario):
+  // the claim counter runs over bt_n * bt_tiles slots, slot x = scenario x / bt_tiles, tile
+  // x % bt_tiles of that scenario's own lower trailing tile set (slots past it are skipped)
+  // mode 6 = the F2 tiles of panel pidx itself (W21 = A21 X, L21, colmax) for every scenario of a
+  // batch: slot x = scenario x / bt_tiles, 64-row tile x % bt_tiles below that scenario's block
+  constexpr bool BT = (mode == 5 || mode == 6);
+  const bool snake = (sched & 2) != 0 && !BT;
   FCtl* ctl = f.ctl;
-  if (ctl->abort) return;
-  const int2 pi = f.pinfo[f.pidx];
+  if (!BT && ctl->abort) return;
+  const int2 pi = BT ? make_int2(0, 1) : f.pinfo[f.pidx];
   const int64_t k0 = pi.x;
   const int kb = pi.y;
-  const int64_t s = k0 + kb;
-  if (kb <= 0 || (mode == 0 && N - s <= 0)) return;   // (look-ahead modes still copy the last panel)
+  const int64_t s = BT ? 0 : k0 + kb;
+  if (!BT && (kb <= 0 || (mode == 0 && N - s <= 0))) return;   // (look-ahead modes still copy the last panel)
   const int64_t b0 = s / UT;
   const int64_t nt = (N - s > 0) ? (N + UT - 1) / UT - b0 : 0;
   const int64_t ntiles = (nt > 0) ? upd_ntiles(nt, mode) : 0;
   const int64_t nbn = (N - s) < NB ? (N - s) : NB;
+  const int64_t nbn0 = nbn;
   // mode 3 also runs the NEXT panel's F2 tiles (W21 = A21 X, rows >= s + nbn)
   // as soon as that panel's F1 has published X: claimed before any update
   // tile, never waited for (the leftovers are k_panel_trsm's).
   // (tiles on the absolute 64-row grid: TMA box starts stay 16-byte aligned; rows < s + nbn are masked)
   const int64_t f2r0 = s + nbn;
+  const int64_t f2r00 = f2r0;
   const int64_t f2base = (f2r0 / UT) * UT;
   const int64_t nf2 = (mode == 3 && N > f2r0) ? (N + UT - 1) / UT - f2r0 / UT : 0;
   constexpr bool LA = (mode == 3 || mode == 4);   // look-ahead modes (also copy the panel: S tiles)
-  if ((int64_t)blockIdx.x >= ntiles + nf2 + (LA ? (N + UT - 1) / UT - k0 / UT : 0)) return;
-  unsigned long long* counter = f.ucount + 3 * f.pidx;
+  if (!BT && (int64_t)blockIdx.x >= ntiles + nf2 + (LA ? (N + UT - 1) / UT - k0 / UT : 0)) return;
+  // (mode 6 claims from the panel's F2 slot: the same panel's update launch uses slot 3q)
+  unsigned long long* counter = f.ucount + 3 * f.pidx + (mode == 6 ? 2 : 0);
   const int64_t nT1 = (LA && nt > 0) ? upd_nt1(nt, mode) : 0;
   // mode 3 also copies this panel's D + L from Lb into M (64-row "S" tiles, queued after T1)
   const int64_t nS = LA ? (N + UT - 1) / UT - k0 / UT : 0;
-  const int64_t nall = ntiles + nS;
+  const int64_t nall = BT ? bt_n * bt_tiles : ntiles + nS;
   unsigned long long* f2counter = f.ucount + 3 * (f.pidx + 1) + 2;
   extern __shared__ unsigned char tsm_raw[];
   // all shared addresses as 32-bit shared-window offsets (keeps LDS, not generic LD)
@@ -1784,6 +1847,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
   constexpr int TS = OUTB ? 2 : 3;
   const unsigned full0 = tsm + TSMAX * TSTAGEB, empty0 = full0 + 8 * TSMAX;
   volatile long long* stile = reinterpret_cast<volatile long long*>(tsm_raw + (empty0 + 8 * TSMAX - smem_u32(tsm_raw)));
+  volatile long long* stile2 = stile + TSMAX;   // BT: (scenario << 32 | its trailing start s)
   const unsigned outb0 = tsm + 2 * TSTAGEB;   // OUTB: group g stages -P at outb0 + g * TOPB
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -1833,6 +1897,63 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
             }
             f2open = false;
           }
+        }
+        if constexpr (BT) {
+          // claim until a slot that holds a real tile of a live scenario, or the end
+          bool got = false;
+          while (xnext < (unsigned long long)nall) {
+            const unsigned long long xc = xnext;
+            xnext = atom_add_u64(counter, 1ull);
+            const int64_t sc = (int64_t)(xc / (unsigned long long)bt_tiles);
+            const int64_t lt = (int64_t)(xc % (unsigned long long)bt_tiles);
+            const size_t bo = (size_t)sc * f.bws;
+            const FCtl* cs = reinterpret_cast<const FCtl*>(reinterpret_cast<const char*>(f.ctl) + bo);
+            if (cs->abort) continue;
+            if constexpr (mode == 6) {
+              const int nbps = cs->nbp;
+              const int64_t k0s = cs->k0, rb = k0s + nbps;
+              if (nbps == 0 || rb >= N) continue;
+              if (lt >= (N + UT - 1) / UT - rb / UT) continue;
+              const int R0 = (int)((rb / UT + lt) * UT);
+              stile[st] = (long long)((0xfffffffeull << 32) | (unsigned)R0);   // C0 = -2: F2 tile
+              stile2[st] = (long long)(((unsigned long long)sc << 32) | (unsigned long long)rb);
+              mbar_expect_tx(fb, TSTAGEB);
+#pragma unroll
+              for (int b = 0; b < 4; b++) {
+                tma_load_3d(sL + b * TBOXB, &mapA, R0 + 16 * b, (int)k0s, (int)sc, fb);   // A21
+                tma_load_3d(sW + b * TBOXB, &mapX, 16 * b, 0, (int)sc, fb);             // X = L11^{-T}
+              }
+              got = true;
+              break;
+            }
+            const int2 ps = reinterpret_cast<const int2*>(reinterpret_cast<const char*>(f.pinfo) + bo)[f.pidx];
+            const int64_t ss = (int64_t)ps.x + ps.y;
+            if (ps.y <= 0 || N - ss <= 0) continue;
+            const int64_t sb0 = ss / UT, snt = (N + UT - 1) / UT - sb0;
+            if (lt >= snt * (snt + 1) / 2) continue;
+            int64_t bi, bj;
+            tri_tile(lt, bi, bj);
+            const int R0 = (int)((sb0 + bi) * UT), C0 = (int)((sb0 + bj) * UT);
+            stile[st] = (long long)(((unsigned long long)(unsigned)C0 << 32) | (unsigned)R0);
+            stile2[st] = (long long)(((unsigned long long)sc << 32) | (unsigned long long)ss);
+            mbar_expect_tx(fb, TSTAGEB);
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+              tma_load_3d(sL + b * TBOXB, &mapL, R0 + 16 * b, 0, (int)sc, fb);
+              tma_load_3d(sW + b * TBOXB, &mapW, C0 + 16 * b, 0, (int)sc, fb);
+            }
+            if (sched & 8)
+#pragma unroll
+              for (int b = 0; b < 4; b++) tma_prefetch_3d(&mapA, R0 + 16 * b, C0, (int)sc);
+            got = true;
+            break;
+          }
+          if (!got) {
+            stile[st] = -1;
+            mbar_arrive(fb);
+            ends++;
+          }
+          continue;
         }
         const unsigned long long xc = xnext;
         if (xc >= (unsigned long long)nall) {
@@ -1889,6 +2010,9 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
     const long long x = stile[st];
     if (x == -1) break;
     const int64_t R0 = (int64_t)(unsigned)(x & 0xffffffffll), C0 = (int64_t)(x >> 32);
+    const long long x2 = BT ? stile2[st] : 0;
+    const int bsc = (int)(x2 >> 32);                               // BT: scenario
+    const int64_t sT = BT ? (int64_t)(x2 & 0xffffffffll) : s;     // its trailing start
     if (LA && C0 == -3) {
       // S tile: panel rows R0..R0+63 of D + L (columns < kb, on/below the diagonal) into M
       const unsigned Lt = tsm + st * TSTAGEB;
@@ -1942,25 +2066,31 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
     }
     // the whole group has finished reading L/W of this stage
     asm volatile("bar.sync %0, 128;\n" ::"r"(grp + 1) : "memory");
-    if (mode == 3 && C0 == -2) {
-      // F2 tile of the next panel: W21 = acc, L21 = acc D^{-1}, colmax (the stage is free already)
+    if ((mode == 3 || mode == 6) && C0 == -2) {
+      // F2 tile of the next panel (mode 6: of this panel, scenario bsc): W21 = acc,
+      // L21 = acc D^{-1}, colmax (the stage is free already)
       if (leader) { mbar_arrive(empty0 + 8 * st); UTRACE_ADD(f.pidx, 2); }
-      double* W2 = const_cast<double*>(f.Wprev);
-      double* L2 = const_cast<double*>(f.Lbprev);
+      // (scenario bsc's control block and panel buffers by explicit byte offsets)
+      const size_t bo = (mode == 6) ? (size_t)bsc * f.bws : 0;
+      FCtl* cf = reinterpret_cast<FCtl*>(reinterpret_cast<char*>(f.ctl) + bo);
+      const int nbf = (mode == 6) ? cf->nbp : (int)nbn0;
+      const int64_t f2rf = (mode == 6) ? sT : f2r00;
+      double* W2 = (mode == 6) ? reinterpret_cast<double*>(reinterpret_cast<char*>(f.W) + bo) : const_cast<double*>(f.Wprev);
+      double* L2 = (mode == 6) ? reinterpret_cast<double*>(reinterpret_cast<char*>(f.Lb) + bo) : const_cast<double*>(f.Lbprev);
       double cm[4][2];
 #pragma unroll
       for (int b = 0; b < 4; b++)
 #pragma unroll
         for (int e = 0; e < 2; e++) {
           const int c = wn + 8 * b + 2 * q + e;
-          const double d = (c < nbn) ? __ldcg(&ctl->d[c]) : 0.0;
+          const double d = (c < nbf) ? __ldcg(&cf->d[c]) : 0.0;
           const double rd = fast_rcp(d);
           const double r1 = (d != 0.0) ? rd : 0.0;
           cm[b][e] = 0.0;
 #pragma unroll
           for (int a = 0; a < 4; a++) {
             const int64_t row = R0 + wm + 8 * a + g;
-            if (row < N && row >= f2r0 && c < nbn) {
+            if (row < N && row >= f2rf && c < nbf) {
               W2[row + c * f.ldw] = acc[a][b][e];
               L2[row + c * f.ldw] = acc[a][b][e] * r1;
               cm[b][e] = fmax(cm[b][e], fabs(acc[a][b][e]));
@@ -1970,7 +2100,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
           v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 4));
           v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 8));
           v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 16));
-          if (g == 0 && c < nbn) atomicMax(&ctl->colmax[c], dbits(v));
+          if (g == 0 && c < nbf) atomicMax(&cf->colmax[c], dbits(v));
         }
       continue;
     }
@@ -1994,7 +2124,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
         for (int e = 0; e < 2; e++) {
           const int cl = wn + 8 * b + 2 * q + e;
           const int64_t col = C0 + cl;
-          const bool upd = upd_mask(row, col, N, s, nbn, mode) && col >= s;
+          const bool upd = upd_mask(row, col, N, sT, nbn, BT ? 0 : mode) && col >= sT;
           sts_f64(Ot + tma_off(wm + 8 * a + g, cl), upd ? dneg(acc[a][b][e]) : 0.0);
         }
     }
@@ -2002,8 +2132,10 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
     asm volatile("bar.sync %0, 128;\n" ::"r"(grp + 1) : "memory");
     if (leader) {
 #pragma unroll
-      for (int b = 0; b < 4; b++)
-        tma_reduce_add_2d(&mapA, (int)(R0 + 16 * b), (int)C0, Ot + b * TBOXB);
+      for (int b = 0; b < 4; b++) {
+        if constexpr (BT) tma_reduce_add_3d(&mapA, (int)(R0 + 16 * b), (int)C0, bsc, Ot + b * TBOXB);
+        else tma_reduce_add_2d(&mapA, (int)(R0 + 16 * b), (int)C0, Ot + b * TBOXB);
+      }
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       if (!OUTB) {
         asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");   // smem source consumed
@@ -2058,12 +2190,18 @@ bool make_map(CUtensorMap* m, const double* base, int64_t rows, int64_t cols, in
 // Finalize: inertia out; convert panel-end-order L to the explicit permutation
 // form by applying every later panel's interchanges to earlier panels' rows
 // (only if any interchange happened); final permutation + 2x2 flags into piv[N..2N).
-__global__ void k_factor_finalize(int64_t N, double* __restrict__ A, int64_t lda, FWork f, int32_t* piv,
-                                  mds_inertia* inertia_out) {
-  cg::grid_group grid = cg::this_grid();
+// BLOCK = false: one cooperative grid for one system (grid.sync between phases);
+// BLOCK = true: batched, one CTA per scenario (blockIdx.x), __syncthreads between phases.
+template <bool BLOCK>
+__device__ __forceinline__ void finalize_body(int64_t N, double* __restrict__ A, int64_t lda, FWork f, int32_t* piv,
+                                              mds_inertia* inertia_out) {
+  auto gsync = [] {
+    if constexpr (BLOCK) __syncthreads();
+    else cg::this_grid().sync();
+  };
   FCtl* ctl = f.ctl;
-  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t gth = (int64_t)gridDim.x * blockDim.x;
+  const int64_t gtid = BLOCK ? (int64_t)threadIdx.x : blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gth = BLOCK ? (int64_t)blockDim.x : (int64_t)gridDim.x * blockDim.x;
   if (gtid == 0 && inertia_out) {
     inertia_out->pos = ctl->inertia[0];
     inertia_out->zero = ctl->inertia[1];
@@ -2079,7 +2217,7 @@ __global__ void k_factor_finalize(int64_t N, double* __restrict__ A, int64_t lda
   for (int64_t i = gtid; i < N; i += gth) { f.rho[i] = (int)i; f.rhoinv[i] = (int)i; }
   const int npan = ctl->npanel;
   const int nswap = ctl->nswap;
-  grid.sync();
+  gsync();
   if (nswap > 0) {
     for (int q = npan - 1; q >= 0; q--) {
       const int64_t c0 = f.panel_start[q];
@@ -2090,7 +2228,7 @@ __global__ void k_factor_finalize(int64_t N, double* __restrict__ A, int64_t lda
           const int64_t i = c1 + idx % nr, c = c0 + idx / nr;
           f.W[i + (c - c0) * f.ldw] = A[(int64_t)f.rho[i] + c * lda];
         }
-        grid.sync();
+        gsync();
         for (int64_t idx = gtid; idx < nr * nc; idx += gth) {
           const int64_t i = c1 + idx % nr, c = c0 + idx / nr;
           A[i + c * lda] = f.W[i + (c - c0) * f.ldw];
@@ -2107,7 +2245,7 @@ __global__ void k_factor_finalize(int64_t N, double* __restrict__ A, int64_t lda
           }
         }
       }
-      grid.sync();
+      gsync();
     }
   }
   for (int64_t i = gtid; i < N; i += gth) {
@@ -2117,6 +2255,18 @@ __global__ void k_factor_finalize(int64_t N, double* __restrict__ A, int64_t lda
       A[(i + 1) + i * lda] = 0.0;
     }
   }
+}
+
+__global__ void k_factor_finalize(int64_t N, double* __restrict__ A, int64_t lda, FWork f, int32_t* piv,
+                                  mds_inertia* inertia_out) {
+  finalize_body<false>(N, A, lda, f, piv, inertia_out);
+}
+__global__ void __launch_bounds__(512) k_factor_finalize_b(int64_t N, double* __restrict__ A, int64_t lda, FWork f,
+                                                            int32_t* piv, mds_inertia* inertia_out) {
+  bsel_ws(f, blockIdx.x);
+  A += blockIdx.x * f.bms;
+  piv += blockIdx.x * f.bps;
+  finalize_body<true>(N, A, lda, f, piv, inertia_out ? inertia_out + blockIdx.x : nullptr);
 }
 }  // namespace
 
@@ -2217,7 +2367,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     const int64_t nt = anorm::ntiles(N);
     MDS_LAUNCH(PC_ANORM, st,
                MDS_CUDA_TRY(launch_pdl(anorm::k_anorm_scan, dim3((unsigned)nt), dim3(256), 0, st, N, (const double*)M, ldm,
-                                       anorm::parts_at(f.nparts, N))));
+                                       (int64_t)0, f.nparts, (size_t)0)));
     anorm::NormOut o = {};
     o.anorm = &f.ctl->anorm;
     o.tol0 = &f.ctl->tol;
@@ -2367,17 +2517,17 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
       MDS_CUDA_TRY(cudaStreamWaitEvent(side, ev(p, 0), 0));
       if (next_tail) {
         MDS_LAUNCH(PC_UPDATE, side,
-                   (k_update_tma<4, true><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
+                   (k_update_tma<4, true><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched, 0ll, 0ll)));
         MDS_CUDA_TRY(cudaEventRecord(ev(p, 1), side));
         if (last) break;
         if (int rc = launch_fast(p + 1)) return rc;
       } else if (!upd_main) {   // (A/B variant: U on the side stream, F1 on the main stream)
         if (g_inplace)
           MDS_LAUNCH(PC_UPDATE, side,
-                     (k_update_tma<3, false><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
+                     (k_update_tma<3, false><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched, 0ll, 0ll)));
         else
           MDS_LAUNCH(PC_UPDATE, side,
-                     (k_update_tma<3, true><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
+                     (k_update_tma<3, true><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched, 0ll, 0ll)));
         MDS_CUDA_TRY(cudaEventRecord(ev(p, 1), side));
         const FWork fn = fwork_for(p + 1);
         MDS_LAUNCH(PC_PANEL_DIAG, st, MDS_CUDA_TRY(launch_pdl(k_panel_diag, dim3(1), dim3(256), F1SMEM, st, N, M, ldm, fn)));
@@ -2387,10 +2537,10 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
         MDS_CUDA_TRY(cudaEventRecord(ev(p, 1), side));
         if (g_inplace)
           MDS_LAUNCH(PC_UPDATE, st,
-                     (k_update_tma<3, false><<<gr, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
+                     (k_update_tma<3, false><<<gr, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched, 0ll, 0ll)));
         else
           MDS_LAUNCH(PC_UPDATE, st,
-                     (k_update_tma<3, true><<<gr, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
+                     (k_update_tma<3, true><<<gr, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched, 0ll, 0ll)));
       }
       tail = next_tail;
     }
@@ -2414,10 +2564,10 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
         const unsigned ugrid = (unsigned)std::min<int64_t>(nt * (nt + 1) / 2, sms);
         if (use_tma && g_inplace)
           MDS_LAUNCH(PC_UPDATE, st,
-                     (k_update_tma<0, false><<<ugrid, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
+                     (k_update_tma<0, false><<<ugrid, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched, 0ll, 0ll)));
         else if (use_tma)
           MDS_LAUNCH(PC_UPDATE, st,
-                     (k_update_tma<0, true><<<ugrid, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched)));
+                     (k_update_tma<0, true><<<ugrid, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched, 0ll, 0ll)));
         else if (v16)
           MDS_LAUNCH(PC_UPDATE, st,
                      (k_update<true><<<ugrid, 128, 2 * USTAGE * sizeof(double), st>>>(N, M, ldm, fp)));
@@ -2446,5 +2596,142 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     MDS_CUDA_TRY(cudaMemcpyAsync(inertia_host, inertia_dev, sizeof(mds_inertia), cudaMemcpyDeviceToHost, st));
     MDS_CUDA_TRY(cudaStreamSynchronize(st));
   }
+  return MDS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Batched factorization (SCOPF scenario batches, SURVEY §8(b) "_batched"): the
+// same Bunch-Kaufman panels for `batch` independent N x N systems, one launch
+// per step for ALL scenarios (grid.y = scenario), in the non-look-ahead order
+// F1 -> F2 -> F4 -> store -> update.  The batch supplies the parallelism:
+// F1 / F4 run one CTA per scenario, F2 / store one grid row per scenario, and
+// the DMMA trailing update is ONE persistent launch whose tile queue spans every
+// scenario's lower trailing tiles (3-D TMA maps, third coordinate = scenario).
+namespace {
+// 3-D map over `batch` column-major (rows x cols, ld) FP64 matrices `bstride` bytes apart
+bool make_map3(CUtensorMap* m, const double* base, int64_t rows, int64_t cols, int64_t ld, int64_t batch,
+               size_t bstride) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)rows, (cuuint64_t)cols, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 8, (cuuint64_t)bstride};
+  cuuint32_t box[3] = {16, 64, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+size_t factor_ws_stride(int64_t N) { return align_up(mds_factor_workspace_size(N), 256); }
+}  // namespace
+
+// per-scenario factor workspace stride (read by solve.cu for the batched tolerance)
+size_t mds_factor_ws_stride_bytes(int64_t N) { return factor_ws_stride(std::max<int64_t>(N, 1)); }
+
+extern "C" size_t mds_factor_batched_workspace_size(int64_t N, int64_t batch) {
+  if (batch < 1) return 0;
+  return (size_t)batch * factor_ws_stride(std::max<int64_t>(N, 1));
+}
+
+extern "C" int mds_factor_batched(int64_t batch, int64_t N, double* M, int64_t ldm, int64_t str_M, int32_t* piv,
+                                  int64_t str_piv, double zero_tol, const double* anorm, mds_inertia* inertia_dev,
+                                  int32_t* status, void* work, size_t work_bytes, void* stream) {
+  if (batch < 0 || N < 0 || N >= (1 << 29)) return MDS_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (batch == 0) return MDS_OK;
+  if (!inertia_dev || !status) return MDS_ERR_ARG;
+  if (N == 0) {
+    MDS_CUDA_TRY(cudaMemsetAsync(inertia_dev, 0, sizeof(mds_inertia) * batch, st));
+    return MDS_OK;
+  }
+  if (!M || !piv || ldm < N || str_M < ldm * N || str_piv < 2 * N) return MDS_ERR_ARG;
+  // the batched update is TMA-only: 16-byte aligned matrices, even ldm and stride
+  if ((reinterpret_cast<uintptr_t>(M) & 15) || (ldm & 1) || (str_M & 1)) return MDS_ERR_ARG;
+  const size_t ws = factor_ws_stride(N);
+  if (!work || work_bytes < (size_t)batch * ws) return MDS_ERR_WORKSPACE;
+  FWork f = carve(work, N, nullptr);
+  f.bws = ws;
+  f.bms = str_M;
+  f.bps = str_piv;
+  const unsigned nb = (unsigned)batch;
+  MDS_LAUNCH(PC_ANORM, st,
+             MDS_CUDA_TRY(launch_pdl(k_factor_init, dim3((unsigned)std::min<int64_t>(mds_cdiv(3 * (N + 2), 256), 64), nb),
+                                     dim3(256), 0, st, N, f, zero_tol, anorm, status)));
+  if (!anorm) {
+    MDS_LAUNCH(PC_ANORM, st,
+               MDS_CUDA_TRY(launch_pdl(anorm::k_anorm_scan, dim3((unsigned)anorm::ntiles(N), nb), dim3(256), 0, st, N,
+                                       (const double*)M, ldm, str_M, f.nparts, ws)));
+    anorm::NormOut o = {};
+    o.tol0 = &f.ctl->tol;
+    o.abort0 = &f.ctl->abort;
+    o.ctl_stride = ws;
+    o.status = status;
+    o.status_stride = 1;
+    o.zero_tol = zero_tol;
+    MDS_LAUNCH(PC_ANORM, st, MDS_CUDA_TRY(anorm::launch_rows(N, f.nparts, ws, o, batch, st)));
+  }
+  if (mds_once_per_device((const void*)k_update_tma<5, true>)) {
+    cudaFuncSetAttribute(k_update_tma<5, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
+    cudaFuncSetAttribute(k_update_tma<6, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM);
+    cudaFuncSetAttribute(k_panel_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, F1SMEM);
+    cudaFuncSetAttribute(k_panel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB * US * (int)sizeof(double));
+  }
+  CUtensorMap mapA, mapW0, mapW1, mapL0, mapL1, mapX;
+  if (!(make_map3(&mapA, M, N, N, ldm, batch, (size_t)str_M * 8) && make_map3(&mapX, f.Lblk, NB, NB, NB, batch, ws) &&
+        make_map3(&mapW0, f.W, N, NB, f.ldw, batch, ws) && make_map3(&mapW1, f.W1, N, NB, f.ldw, batch, ws) &&
+        make_map3(&mapL0, f.Lb, N, NB, f.ldw, batch, ws) && make_map3(&mapL1, f.Lb1, N, NB, f.ldw, batch, ws)))
+    return MDS_ERR_CUDA;
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int sched = (g_mds_var.no_cprefetch ? 0 : 8);
+  const size_t usmem = 2 * NB * US * sizeof(double);
+  const int64_t npmax = (N + (NB - 2)) / (NB - 1) + 1;
+  for (int64_t p = 0; p < npmax; p++) {
+    const int64_t rows = N - std::min<int64_t>(p * (NB - 1), N);   // upper bound on the rows left
+    if (rows <= 0) break;
+    FWork fp = f;
+    fp.pidx = (int)p;
+    fp.fuse = 0;
+    if (p & 1) { fp.W = f.W1; fp.Lb = f.Lb1; fp.Wprev = f.W; fp.Lbprev = f.Lb; }
+    else { fp.Wprev = f.W1; fp.Lbprev = f.Lb1; }
+    const unsigned g64 = (unsigned)std::max<int64_t>(mds_cdiv(rows, UT), 1);
+    const unsigned g256 = (unsigned)std::max<int64_t>(mds_cdiv(rows, 256), 1);
+    MDS_LAUNCH(PC_PANEL_DIAG, st, (k_panel_diag<<<dim3(1, nb), 256, F1SMEM, st>>>(N, M, ldm, fp)));
+    if (g_mds_var.f2_trsm) {   // A/B: F2 by k_panel_trsm (one grid row per scenario)
+      MDS_LAUNCH(PC_PANEL_TRSM, st, (k_panel_trsm<<<dim3(g64, nb), 128, usmem, st>>>(N, M, ldm, fp)));
+    } else {   // F2 of every scenario as one TMA-fed DMMA launch (slots: 64-row tiles below the block)
+      const int64_t rbmin = std::min<int64_t>(N, p * (NB - 1) + NB);
+      const int64_t nt2 = (N + UT - 1) / UT - rbmin / UT;
+      if (N > rbmin && nt2 > 0) {
+        const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt2 * batch, sms));
+        const CUtensorMap& mw = (p & 1) ? mapW1 : mapW0;
+        MDS_LAUNCH(PC_PANEL_TRSM, st,
+                   (k_update_tma<6, true><<<gr, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, mw, mapX, sched, nt2,
+                                                                       batch)));
+      }
+    }
+    // F4 on one CTA per scenario (rows in one chunk, L rows read through L2; no grid barrier partners)
+    const int chunk = (int)(mds_cdiv(rows, 32) * 32);
+    MDS_LAUNCH(PC_PANEL_SLOW, st,
+               MDS_CUDA_TRY(launch_pdl(k_panel_exact, dim3(1, nb), dim3(XT), 0, st, N, M, ldm, fp, piv, chunk, 0, 0)));
+    MDS_LAUNCH(PC_PANEL_STORE, st, (k_panel_store<<<dim3(g256, 8, nb), 256, 0, st>>>(N, M, ldm, fp)));
+    // trailing update of every scenario: slots per scenario = the tile count for the smallest
+    // possible trailing start (every panel before p+1 finished at least NB-1 columns)
+    const int64_t smin = std::min<int64_t>(N, (p + 1) * (NB - 1));
+    const int64_t nt = (N + UT - 1) / UT - smin / UT;
+    if (N - smin > 0 && nt > 0) {
+      const int64_t tb = nt * (nt + 1) / 2;
+      const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tb * batch, sms));
+      const CUtensorMap& mw = (p & 1) ? mapW1 : mapW0;
+      const CUtensorMap& ml = (p & 1) ? mapL1 : mapL0;
+      MDS_LAUNCH(PC_UPDATE, st,
+                 (k_update_tma<5, true><<<gr, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapA, sched, tb, batch)));
+    }
+  }
+  MDS_LAUNCH(PC_FINALIZE, st, (k_factor_finalize_b<<<nb, 512, 0, st>>>(N, M, ldm, f, piv, inertia_dev)));
   return MDS_OK;
 }

@@ -20,6 +20,7 @@
 const int32_t* mds_plan_rowptr(const mds_plan* P);
 const int32_t* mds_plan_colidx(const mds_plan* P);
 double* mds_factor_tol_ptr(const void* fwork);
+size_t mds_factor_ws_stride_bytes(int64_t N);
 
 namespace {
 constexpr int TB = 64;        // row block
@@ -36,6 +37,18 @@ struct SWork {
   int* tickets;   // [2]
 };
 constexpr unsigned long long SENT = ~0ull;   // "not yet published" (a NaN payload never stored)
+
+// Batched solves (mds_solve_batched): scenario s = blockIdx.y reads / writes every
+// array at base + s * stride (elements; workspace pointers by bytes).  All zero
+// for a single system.
+struct BStr {
+  int64_t ld, piv, rhs, dxy, val, w, rxs, dxs;
+  size_t ws, fws;   // solve / factor workspace bytes per scenario
+};
+template <typename T>
+__device__ __forceinline__ T* bsh(T* p, size_t bytes) {
+  return reinterpret_cast<T*>(reinterpret_cast<uintptr_t>(p) + bytes * blockIdx.y);
+}
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 SWork carve(void* work, int64_t N, size_t* total) {
@@ -118,9 +131,11 @@ __device__ __forceinline__ void publish(double* p, double v) {
 }
 
 __global__ void k_gather(int64_t N, const int32_t* __restrict__ piv, const double* __restrict__ b,
-                         double* __restrict__ bp, double* y, double* x, int* tickets) {
+                         double* __restrict__ bp, double* y, double* x, int* tickets, BStr z) {
   pdl_wait();
   pdl_trigger();
+  piv += blockIdx.y * z.piv; b += blockIdx.y * z.rhs;
+  bp = bsh(bp, z.ws); y = bsh(y, z.ws); x = bsh(x, z.ws); tickets = bsh(tickets, z.ws);
   if (blockIdx.x == 0 && threadIdx.x < 4) tickets[threadIdx.x] = 0;
   const double sent = __longlong_as_double((long long)SENT);   // "not yet published"
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
@@ -137,9 +152,11 @@ constexpr int TBP = TB + 1;
 constexpr int IBSMEM = (2 * TB * TBP + 4 * 16 * 17) * 8;   // L block, Binv, 16x16 temporaries
 __global__ void __launch_bounds__(256) k_inv_blocks(int64_t N, const double* __restrict__ L, int64_t lda,
                                                     double* __restrict__ binv, double* __restrict__ gf,
-                                                    double* __restrict__ gb) {
+                                                    double* __restrict__ gb, BStr z) {
   pdl_wait();
   pdl_trigger();
+  L += blockIdx.y * z.ld;
+  binv = bsh(binv, z.ws); gf = bsh(gf, z.ws); gb = bsh(gb, z.ws);
   extern __shared__ double ism[];
   double* Ls = ism;                      // Ls[k*TBP + r] = L[r][k]  (diagonal block, later the off-diagonal ones)
   double* Bs = ism + TB * TBP;           // Bs[c*TBP + r] = Binv[r][c]
@@ -249,9 +266,11 @@ constexpr int SWSMEM = 2 * TB * TB * 8;   // Binv_i and G_i in shared memory
 __global__ void __launch_bounds__(ST) k_trsv_fwd(int64_t N, const double* __restrict__ L, int64_t lda,
                                                  const double* __restrict__ b, double* y,
                                                  const double* __restrict__ binv, const double* __restrict__ gf,
-                                                 int* ticket) {
+                                                 int* ticket, BStr z) {
   pdl_wait();
   pdl_trigger();
+  L += blockIdx.y * z.ld;
+  b = bsh(b, z.ws); y = bsh(y, z.ws); binv = bsh(binv, z.ws); gf = bsh(gf, z.ws); ticket = bsh(ticket, z.ws);
   extern __shared__ double fsm[];
   double* Bs = fsm;             // Binv_i, column-major
   double* Gs = fsm + TB * TB;   // Gf_i, column-major
@@ -334,9 +353,12 @@ __global__ void __launch_bounds__(ST) k_trsv_fwd(int64_t N, const double* __rest
 
 // D solve: 1x1 and 2x2 blocks (LAPACK dsytrs scaled 2x2 formula); 2x2 off-diagonal at (k, k+1) (upper slot)
 __global__ void k_dsolve(int64_t N, const double* __restrict__ LD, int64_t lda, const int32_t* __restrict__ piv,
-                         double* y, const double* tolp, double tolv, int32_t* status) {
+                         double* y, const double* tolp, double tolv, int32_t* status, BStr z) {
   pdl_wait();
   pdl_trigger();
+  LD += blockIdx.y * z.ld; piv += blockIdx.y * z.piv; y = bsh(y, z.ws);
+  if (tolp) tolp = bsh(tolp, z.fws);
+  if (status) status += blockIdx.y * (z.ws ? 1 : 0);
   const double tol = tolp ? *tolp : tolv;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N; k += (int64_t)gridDim.x * blockDim.x) {
     const int bt = (piv[N + k] >> 29) & 3;
@@ -364,9 +386,11 @@ __global__ void k_dsolve(int64_t N, const double* __restrict__ LD, int64_t lda, 
 __global__ void __launch_bounds__(ST) k_trsv_bwd(int64_t N, const double* __restrict__ L, int64_t lda,
                                                  const double* __restrict__ z, double* x,
                                                  const double* __restrict__ binv, const double* __restrict__ gb,
-                                                 int* ticket) {
+                                                 int* ticket, BStr zs) {
   pdl_wait();
   pdl_trigger();
+  L += blockIdx.y * zs.ld;
+  z = bsh(z, zs.ws); x = bsh(x, zs.ws); binv = bsh(binv, zs.ws); gb = bsh(gb, zs.ws); ticket = bsh(ticket, zs.ws);
   extern __shared__ double fsm[];
   double* Bs = fsm;             // Binv_i, column-major
   double* Gs = fsm + TB * TB;   // Gb_i, column-major: Gs[c + k*TB] = Gb[c][k]
@@ -470,9 +494,10 @@ __global__ void __launch_bounds__(ST) k_trsv_bwd(int64_t N, const double* __rest
 }
 
 __global__ void k_scatter(int64_t N, const int32_t* __restrict__ piv, const double* __restrict__ y,
-                          double* __restrict__ x) {
+                          double* __restrict__ x, BStr z) {
   pdl_wait();
   pdl_trigger();
+  piv += blockIdx.y * z.piv; y = bsh(y, z.ws); x += blockIdx.y * z.dxy;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
     x[piv[N + i] & PERM_MASK] = y[i];
 }
@@ -481,9 +506,11 @@ __global__ void k_scatter(int64_t N, const int32_t* __restrict__ piv, const doub
 __global__ void k_recover(int64_t n_s, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
                           const double* __restrict__ val, const double* __restrict__ w,
                           const double* __restrict__ r_xs, const double* __restrict__ dy,
-                          double* __restrict__ dx_s) {
+                          double* __restrict__ dx_s, BStr z) {
   pdl_wait();
   pdl_trigger();
+  val += blockIdx.y * z.val; w += blockIdx.y * z.w; r_xs += blockIdx.y * z.rxs; dy += blockIdx.y * z.dxy;
+  dx_s += blockIdx.y * z.dxs;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n_s; k += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int p = rowptr[k]; p < rowptr[k + 1]; p++) s += val[p] * dy[colidx[p]];
@@ -498,33 +525,31 @@ extern "C" size_t mds_solve_workspace_size(int64_t N) {
   return t;
 }
 
-extern "C" int mds_solve(const mds_plan* plan, int64_t N, const double* LD, int64_t ldm, const int32_t* piv,
-                         const double* rhs_c, const double* js_val, const double* w, const double* r_xs,
-                         double* dxy, double* dx_s, double zero_tol, const void* fwork, int32_t* status,
-                         void* work, size_t work_bytes, void* stream) {
-  if (N < 0 || (N > 0 && (!LD || !piv || !rhs_c || !dxy)) || ldm < std::max<int64_t>(N, 1)) return MDS_ERR_ARG;
-  cudaStream_t st = (cudaStream_t)stream;
-  if (!work || work_bytes < mds_solve_workspace_size(N)) return MDS_ERR_WORKSPACE;
+static int solve_launch(const mds_plan* plan, int64_t batch, int64_t N, const double* LD, int64_t ldm,
+                        const int32_t* piv, const double* rhs_c, const double* js_val, const double* w,
+                        const double* r_xs, double* dxy, double* dx_s, double zero_tol, const void* fwork,
+                        int32_t* status, void* work, const BStr& z, cudaStream_t st) {
+  const unsigned nb = (unsigned)batch;
   if (N > 0) {
     SWork s = carve(work, N, nullptr);
     const int64_t nblk = (N + TB - 1) / TB;
-    const unsigned ge = (unsigned)std::min<int64_t>(mds_cdiv(N, 256), 148 * 8);
-    MDS_LAUNCH(PC_SOLVE_GATHER, st, MDS_CUDA_TRY(launch_pdl(k_gather, dim3(ge), dim3(256), 0, st, N, piv, rhs_c, s.b, s.y, s.x, s.tickets)));
+    const unsigned ge = (unsigned)std::min<int64_t>(mds_cdiv(N, 256), batch > 1 ? 16 : 148 * 8);
+    MDS_LAUNCH(PC_SOLVE_GATHER, st, MDS_CUDA_TRY(launch_pdl(k_gather, dim3(ge, nb), dim3(256), 0, st, N, piv, rhs_c, s.b, s.y, s.x, s.tickets, z)));
     if (mds_once_per_device((const void*)k_inv_blocks)) {
       cudaFuncSetAttribute(k_inv_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, IBSMEM);
       cudaFuncSetAttribute(k_trsv_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SWSMEM);
       cudaFuncSetAttribute(k_trsv_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SWSMEM);
     }
     MDS_LAUNCH(PC_SOLVE_FWD, st,
-               MDS_CUDA_TRY(launch_pdl(k_inv_blocks, dim3((unsigned)nblk), dim3(256), IBSMEM, st, N, LD, ldm, s.binv, s.gf, s.gb)));
+               MDS_CUDA_TRY(launch_pdl(k_inv_blocks, dim3((unsigned)nblk, nb), dim3(256), IBSMEM, st, N, LD, ldm, s.binv, s.gf, s.gb, z)));
     MDS_LAUNCH(PC_SOLVE_FWD, st,
-               MDS_CUDA_TRY(launch_pdl(k_trsv_fwd, dim3((unsigned)nblk), dim3(ST), SWSMEM, st, N, LD, ldm, s.b, s.y, s.binv, s.gf, s.tickets)));
+               MDS_CUDA_TRY(launch_pdl(k_trsv_fwd, dim3((unsigned)nblk, nb), dim3(ST), SWSMEM, st, N, LD, ldm, s.b, s.y, s.binv, s.gf, s.tickets, z)));
     const double* tolp = (zero_tol < 0.0 && fwork) ? mds_factor_tol_ptr(fwork) : nullptr;
     MDS_LAUNCH(PC_SOLVE_D, st,
-               MDS_CUDA_TRY(launch_pdl(k_dsolve, dim3(ge), dim3(256), 0, st, N, LD, ldm, piv, s.y, tolp, zero_tol < 0.0 ? 0.0 : zero_tol, status)));
+               MDS_CUDA_TRY(launch_pdl(k_dsolve, dim3(ge, nb), dim3(256), 0, st, N, LD, ldm, piv, s.y, tolp, zero_tol < 0.0 ? 0.0 : zero_tol, status, z)));
     MDS_LAUNCH(PC_SOLVE_BWD, st,
-               MDS_CUDA_TRY(launch_pdl(k_trsv_bwd, dim3((unsigned)nblk), dim3(ST), SWSMEM, st, N, LD, ldm, s.y, s.x, s.binv, s.gb, s.tickets + 1)));
-    MDS_LAUNCH(PC_SOLVE_SCATTER, st, MDS_CUDA_TRY(launch_pdl(k_scatter, dim3(ge), dim3(256), 0, st, N, piv, s.x, dxy)));
+               MDS_CUDA_TRY(launch_pdl(k_trsv_bwd, dim3((unsigned)nblk, nb), dim3(ST), SWSMEM, st, N, LD, ldm, s.y, s.x, s.binv, s.gb, s.tickets + 1, z)));
+    MDS_LAUNCH(PC_SOLVE_SCATTER, st, MDS_CUDA_TRY(launch_pdl(k_scatter, dim3(ge, nb), dim3(256), 0, st, N, piv, s.x, dxy, z)));
   }
   if (plan && dx_s) {
     int64_t dims[5];
@@ -533,11 +558,50 @@ extern "C" int mds_solve(const mds_plan* plan, int64_t N, const double* LD, int6
     if (dims[1] + dims[2] + dims[3] != N) return MDS_ERR_ARG;
     if (n_s > 0) {
       if (!w || !r_xs || (dims[4] > 0 && !js_val)) return MDS_ERR_ARG;
-      const unsigned g = (unsigned)std::min<int64_t>(mds_cdiv(n_s, 256), 148 * 16);
+      const unsigned g = (unsigned)std::min<int64_t>(mds_cdiv(n_s, 256), batch > 1 ? 64 : 148 * 16);
       MDS_LAUNCH(PC_RECOVER, st,
-                 MDS_CUDA_TRY(launch_pdl(k_recover, dim3(g), dim3(256), 0, st, n_s, mds_plan_rowptr(plan),
-                                         mds_plan_colidx(plan), js_val, w, r_xs, dxy + n_d, dx_s)));
+                 MDS_CUDA_TRY(launch_pdl(k_recover, dim3(g, nb), dim3(256), 0, st, n_s, mds_plan_rowptr(plan),
+                                         mds_plan_colidx(plan), js_val, w, r_xs, dxy + n_d, dx_s, z)));
     }
   }
   return MDS_OK;
+}
+
+extern "C" int mds_solve(const mds_plan* plan, int64_t N, const double* LD, int64_t ldm, const int32_t* piv,
+                         const double* rhs_c, const double* js_val, const double* w, const double* r_xs,
+                         double* dxy, double* dx_s, double zero_tol, const void* fwork, int32_t* status,
+                         void* work, size_t work_bytes, void* stream) {
+  if (N < 0 || (N > 0 && (!LD || !piv || !rhs_c || !dxy)) || ldm < std::max<int64_t>(N, 1)) return MDS_ERR_ARG;
+  if (!work || work_bytes < mds_solve_workspace_size(N)) return MDS_ERR_WORKSPACE;
+  const BStr z = {};
+  return solve_launch(plan, 1, N, LD, ldm, piv, rhs_c, js_val, w, r_xs, dxy, dx_s, zero_tol, fwork, status, work, z,
+                      (cudaStream_t)stream);
+}
+
+static size_t solve_ws_stride(int64_t N) { return align_up(mds_solve_workspace_size(N), 256); }
+
+extern "C" size_t mds_solve_batched_workspace_size(int64_t N, int64_t batch) {
+  return batch < 1 ? 0 : (size_t)batch * solve_ws_stride(N);
+}
+
+extern "C" int mds_solve_batched(const mds_plan* plan, int64_t batch, int64_t N, const double* LD, int64_t ldm,
+                                 int64_t str_LD, const int32_t* piv, int64_t str_piv, const double* rhs_c,
+                                 int64_t str_rhs, const double* js_val, int64_t str_val, const double* w, int64_t str_w,
+                                 const double* r_xs, int64_t str_r, double* dxy, int64_t str_dxy, double* dx_s,
+                                 int64_t str_dxs, double zero_tol, const void* fwork, int32_t* status, void* work,
+                                 size_t work_bytes, void* stream) {
+  if (batch < 0 || N < 0) return MDS_ERR_ARG;
+  if (batch == 0) return MDS_OK;
+  if (!status) return MDS_ERR_ARG;
+  if (N > 0 && (!LD || !piv || !rhs_c || !dxy || ldm < N || str_LD < ldm * N || str_piv < 2 * N ||
+                str_rhs < N || str_dxy < N))
+    return MDS_ERR_ARG;
+  if (!work || work_bytes < mds_solve_batched_workspace_size(N, batch)) return MDS_ERR_WORKSPACE;
+  BStr z;
+  z.ld = str_LD; z.piv = str_piv; z.rhs = str_rhs; z.dxy = str_dxy; z.val = str_val; z.w = str_w; z.rxs = str_r;
+  z.dxs = str_dxs;
+  z.ws = solve_ws_stride(N);
+  z.fws = mds_factor_ws_stride_bytes(N);
+  return solve_launch(plan, batch, N, LD, ldm, piv, rhs_c, js_val, w, r_xs, dxy, dx_s, zero_tol, fwork, status, work,
+                      z, (cudaStream_t)stream);
 }

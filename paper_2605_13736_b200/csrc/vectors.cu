@@ -16,7 +16,16 @@ constexpr int NPART = 6 + MAXRES;   // partial slots per CTA
 struct ResPtrs {
   const double* p[MAXRES];
   int64_t len[MAXRES];
+  int64_t str[MAXRES];   // batched: per-scenario element stride of residual j
   int n;
+};
+// batched (ipm_step_vectors_batched): scenario s = blockIdx.y reads the 8 vectors and
+// writes sigma at + s * vec, out at + s * out, status + s, its own partials / counter
+struct VStr {
+  int64_t vec, out;
+  const double* tau_arr;   // [batch] or NULL (scalar tau)
+  const double* mu_arr;    // [batch] or NULL (scalar mu)
+  int batched;
 };
 
 struct Part {
@@ -60,9 +69,21 @@ k_step_vectors(int64_t n, const double* __restrict__ x, const double* __restrict
                const double* __restrict__ zl, const double* __restrict__ zu,
                const double* __restrict__ dzl, const double* __restrict__ dzu,
                double tau, double mu, ResPtrs R, double* __restrict__ out, double* __restrict__ sigma,
-               int32_t* status, double* __restrict__ partials, unsigned int* counter) {
+               int32_t* status, double* __restrict__ partials, unsigned int* counter, VStr z) {
   pdl_wait();
   pdl_trigger();
+  if (z.batched) {
+    const int64_t s = blockIdx.y, o = s * z.vec;
+    x += o; dx += o; lo += o; up += o; zl += o; zu += o; dzl += o; dzu += o;
+    if (sigma) sigma += o;
+    out += s * z.out;
+    if (status) status += s;
+    partials += s * (int64_t)gridDim.x * NPART;
+    counter += s;
+    if (z.tau_arr) tau = z.tau_arr[s];
+    if (z.mu_arr) mu = z.mu_arr[s];
+    for (int j = 0; j < R.n; j++) R.p[j] += s * R.str[j];
+  }
   Part P;
   P.ap = 1.0; P.ad = 1.0; P.cinf = 0.0; P.csum = 0.0; P.nc = 0.0; P.bad = LLONG_MAX;
 #pragma unroll
@@ -214,7 +235,7 @@ extern "C" int ipm_step_vectors(int64_t n, const double* x, const double* dx, co
   if (!work || work_bytes < ipm_step_vectors_workspace_size(n)) return MDS_ERR_WORKSPACE;
   ResPtrs R;
   R.n = n_res;
-  for (int j = 0; j < MAXRES; j++) { R.p[j] = nullptr; R.len[j] = 0; }
+  for (int j = 0; j < MAXRES; j++) { R.p[j] = nullptr; R.len[j] = 0; R.str[j] = 0; }
   for (int j = 0; j < n_res; j++) {
     if (res_len[j] < 0 || (res_len[j] > 0 && !res[j])) return MDS_ERR_ARG;
     R.p[j] = res[j]; R.len[j] = res_len[j];
@@ -223,8 +244,53 @@ extern "C" int ipm_step_vectors(int64_t n, const double* x, const double* dx, co
   double* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(work) + 256);
   int grid = vec_grid(n);
   cudaStream_t st = (cudaStream_t)stream;
+  const VStr z = {};
   MDS_LAUNCH(PC_VECTORS, st,
              MDS_CUDA_TRY(launch_pdl(k_step_vectors, dim3(grid), dim3(VT), 0, st, n, x, dx, lo, up, zl, zu, dzl, dzu, tau,
-                                     mu, R, out, sigma_out, status, partials, counter)));
+                                     mu, R, out, sigma_out, status, partials, counter, z)));
+  return MDS_OK;
+}
+
+static int vec_grid_b(int64_t n) { return std::min(vec_grid(n), 64); }
+
+extern "C" size_t ipm_step_vectors_batched_workspace_size(int64_t n, int64_t batch) {
+  if (batch < 1) return 0;
+  return ((256 + 4 * (size_t)batch + 255) / 256) * 256 + sizeof(double) * NPART * (size_t)vec_grid_b(n) * batch;
+}
+
+// `batch` scenarios, each with n components at + s * str_vec (x, dx, lo, up, zl, zu, dzl,
+// dzu, sigma_out), results at out + s * str_out, status[s]; tau / mu per scenario
+// (tau_arr / mu_arr, device) or the scalars; residual j of scenario s at res[j] + s * res_str[j].
+extern "C" int ipm_step_vectors_batched(int64_t batch, int64_t n, int64_t str_vec, const double* x, const double* dx,
+                                        const double* lo, const double* up, const double* zl, const double* zu,
+                                        const double* dzl, const double* dzu, double tau, double mu,
+                                        const double* tau_arr, const double* mu_arr, int32_t n_res,
+                                        const double* const* res, const int64_t* res_len, const int64_t* res_str,
+                                        double* out, int64_t str_out, double* sigma_out, int32_t* status,
+                                        void* work, size_t work_bytes, void* stream) {
+  if (batch < 0 || n < 0 || n_res < 0 || n_res > MAXRES) return MDS_ERR_ARG;
+  if (batch == 0) return MDS_OK;
+  if (!out || !status || str_out < 6 + n_res || (n > 0 && str_vec < n)) return MDS_ERR_ARG;
+  if (n > 0 && (!x || !dx || !lo || !up || !zl || !zu || !dzl || !dzu)) return MDS_ERR_ARG;
+  if (n_res > 0 && (!res || !res_len || !res_str)) return MDS_ERR_ARG;
+  if (!work || work_bytes < ipm_step_vectors_batched_workspace_size(n, batch)) return MDS_ERR_WORKSPACE;
+  ResPtrs R;
+  R.n = n_res;
+  for (int j = 0; j < MAXRES; j++) { R.p[j] = nullptr; R.len[j] = 0; R.str[j] = 0; }
+  for (int j = 0; j < n_res; j++) {
+    if (res_len[j] < 0 || (res_len[j] > 0 && !res[j])) return MDS_ERR_ARG;
+    R.p[j] = res[j]; R.len[j] = res_len[j]; R.str[j] = res_str[j];
+  }
+  unsigned int* counter = reinterpret_cast<unsigned int*>(work);
+  double* partials = reinterpret_cast<double*>(reinterpret_cast<char*>(work) + ((256 + 4 * (size_t)batch + 255) / 256) * 256);
+  const int grid = vec_grid_b(n);
+  cudaStream_t st = (cudaStream_t)stream;
+  // counters start at 0 (each scenario's last CTA resets its own); zero them once per call
+  MDS_CUDA_TRY(cudaMemsetAsync(counter, 0, 4 * (size_t)batch, st));
+  VStr z;
+  z.vec = str_vec; z.out = str_out; z.tau_arr = tau_arr; z.mu_arr = mu_arr; z.batched = 1;
+  MDS_LAUNCH(PC_VECTORS, st,
+             MDS_CUDA_TRY(launch_pdl(k_step_vectors, dim3(grid, (unsigned)batch), dim3(VT), 0, st, n, x, dx, lo, up, zl,
+                                     zu, dzl, dzu, tau, mu, R, out, sigma_out, status, partials, counter, z)));
   return MDS_OK;
 }

@@ -4,10 +4,11 @@ box, and NCCL over NVLink is used only to gather per-scenario results and the
 global stopping test").
 
 One process per GPU.  Rank r owns the scenarios s with s % P == r (round-robin,
-so scenarios that converge at different iteration counts stay balanced).  Each
-scenario is one `KKTStep` (all share the pattern plan); the local scenarios run
-concurrently on a pool of CUDA streams, each replaying its own CUDA graph.  Per
-Newton step there is exactly ONE collective: an all-reduce of an 8-double stats
+so scenarios that converge at different iteration counts stay balanced).  The
+local scenarios form ONE `BatchedKKTStep` (all share the pattern plan): a
+Newton step for all of them is one CUDA graph of batched launches
+(mds_condense_batched / mds_factor_batched / mds_solve_batched /
+ipm_step_vectors_batched).  Per Newton step there is exactly ONE collective: an all-reduce of an 8-double stats
 vector (MAX of KKT residual / complementarity / inertia failures, MIN of step
 lengths, SUM of active scenarios).  At the end, `gather_records` all-gathers
 the per-scenario result records (scenario id, inertia, alpha_p, alpha_d,
@@ -21,8 +22,8 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import Plan, set_grid_cap
-from .step import DeviceProblem, KKTStep
+from . import Plan
+from .batch import BatchedKKTStep
 
 REC = 8   # record: [scenario, pos, zero, neg, alpha_p, alpha_d, res_inf, compl_inf]
 
@@ -82,72 +83,54 @@ def gather_records(records: torch.Tensor, n_scenarios: int, group=None):
 class ScopfBatch:
     """The local share of a SCOPF scenario batch on one GPU."""
 
-    def __init__(self, base, scenario_fn, scenario_ids, sv_fn, n_streams=8, device="cuda", grid_cap=0):
+    def __init__(self, base, scenario_fn, scenario_ids, sv_fn, device="cuda"):
         self.ids = list(scenario_ids)
         self.plan = Plan(base.n_s, base.n_d, base.m_E, base.m_I, base.rowptr, base.colidx)
         self.expected = (base.n_d, 0, base.m)
         n = len(self.ids)
         self.records = torch.zeros((n, REC), dtype=torch.float64, device=device)
-        self.steps = []
-        for i, s in enumerate(self.ids):
-            prob = scenario_fn(s)
-            st = KKTStep(DeviceProblem(prob, plan=self.plan), sv=sv_fn(prob, s))
-            self.steps.append(st)
-        self.streams = [torch.cuda.Stream() for _ in range(max(1, min(n_streams, n)))]
-        # concurrent factorizations share the SMs: cap each persistent update grid
-        sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
-        cap = int(grid_cap) or max(8, sms // len(self.streams))
-        # (a capped grid also selects the factorization's concurrent launch structure -- no
-        #  one-launch tail panels -- so a scenario's bits depend on the cap, never on the stream
-        #  count, the rank or the other scenarios)
-        self.grid_cap = cap if len(self.streams) > 1 else 0
-        set_grid_cap(self.grid_cap)
+        self.bt = None
+        if n:
+            def factory(i):
+                p = scenario_fn(self.ids[i])
+                return p, sv_fn(p, self.ids[i])
+            self.bt = BatchedKKTStep((n, factory), plan=self.plan, device=device)
         self._ids_t = torch.tensor(self.ids, dtype=torch.float64, device=device)
-        self.graph = self._capture_all()
-        set_grid_cap(0)
+        self.graph = self._capture() if n else None
 
-    def _run_all(self):
-        cur = torch.cuda.current_stream()
-        for s in self.streams:
-            s.wait_stream(cur)
-        for i, st in enumerate(self.steps):
-            s = self.streams[i % len(self.streams)]
-            with torch.cuda.stream(s):
-                st.run(stream=s)
-        for s in self.streams:
-            cur.wait_stream(s)
+    def _run(self, stream=None):
+        self.bt.run(stream=stream)
         self._fill_records()
 
-    def _capture_all(self):
-        """ONE CUDA graph for the whole local batch: the capture forks onto the
-        stream pool (one branch per stream) and joins back, so a Newton step is a
-        single graph launch."""
+    def _capture(self):
+        """ONE CUDA graph for the whole local batch (a Newton step is one graph launch)."""
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
-            self._run_all()                       # warm-up (workspaces, look-ahead contexts)
+            self._run(stream=side)                 # warm-up (workspaces, attributes)
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self._run_all()
+            self._run(stream=torch.cuda.current_stream())
         return g
 
     def newton_step(self):
         """One Newton step's KKT work for every local scenario (one graph launch)."""
-        self.graph.replay()
+        if self.graph is not None:
+            self.graph.replay()
+
+    def results(self, i):
+        return self.bt.results(i)
 
     def _fill_records(self):
-        r = self.records
-        if not self.steps:
-            return
+        r, bt = self.records, self.bt
         r[:, 0] = self._ids_t
-        r[:, 1:4] = torch.stack([st.inertia for st in self.steps]).to(torch.float64)
-        v = torch.stack([st.vout for st in self.steps])
-        r[:, 4] = v[:, 0]
-        r[:, 5] = v[:, 1]
-        r[:, 6] = v[:, 6]
-        r[:, 7] = v[:, 2]
+        r[:, 1:4] = bt.inertia.to(torch.float64)
+        r[:, 4] = bt.vout[:, 0]
+        r[:, 5] = bt.vout[:, 1]
+        r[:, 6] = bt.vout[:, 6]
+        r[:, 7] = bt.vout[:, 2]
 
     def stop_test(self, group=None):
         mx, sm = stats_vector(self.records, self.expected)

@@ -21,7 +21,7 @@ def test_scopf_batch_matches_single_and_oracle():
     fn = lambda s: mdsgen.scopf_scenario(base, s, seed=5)
     svf = lambda p, s: mdsgen.step_vectors_for(p, seed=100 + s)
     ids = scopf.partition(9, 2, 1)          # this "rank" owns 1, 3, 5, 7
-    batch = scopf.ScopfBatch(base, fn, ids, svf, n_streams=3)
+    batch = scopf.ScopfBatch(base, fn, ids, svf)
     for _ in range(2):
         batch.newton_step()
     torch.cuda.synchronize()
@@ -31,16 +31,14 @@ def test_scopf_batch_matches_single_and_oracle():
     assert list(recs[:, 0]) == ids
     for i, s in enumerate(ids):
         p = fn(s)
-        # alone, in the same factorization configuration (the batch's grid cap)
-        mds.set_grid_cap(batch.grid_cap)
-        try:
-            single = mds.KKTStep(mds.DeviceProblem(p), sv=svf(p, s))
-            single.run()
-            a = single.results()
-        finally:
-            mds.set_grid_cap(0)
-        b = batch.steps[i].results()
+        # the same scenario alone (a batch of one): bitwise the same (no cross-scenario arithmetic,
+        # so P = 1, 2, 4, 8 ranks give identical per-scenario records)
+        one = mds.BatchedKKTStep([p], plan=batch.plan, svs=[svf(p, s)])
+        one.run()
+        a = one.results(0)
+        b = batch.results(i)
         np.testing.assert_array_equal(a["dxy"], b["dxy"])
         assert a["inertia"] == b["inertia"] == p.expected_inertia
+        assert recs[i, 4] == b["vec"]["alpha_p"] and recs[i, 5] == b["vec"]["alpha_d"]
         ref = oracle.newton_step(p)
         assert np.abs(b["dxy"] - ref["dxy"]).max() <= 1e-8 * np.abs(ref["dxy"]).max()
