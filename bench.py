@@ -7,13 +7,19 @@ recovery, barrier vector kernels) on synthetic OPF-shaped MDS inputs.
 
 N=1 workload: BASELINE.json configs[2] "C3" (ACOPF-shaped, n_d+m = 8192,
 n_s = 1M) — the config the north star's FP64 target (N >= 8192) is quoted on.
-Multi-GPU (torchrun): C3 is one KKT system per Newton step and does not shard
-(BK needs a global pivot search per column), so ranks run independent
-replicas; value = steps of all ranks / max-rank time.
+Multi-GPU: `--gpus N` re-launches itself as N ranks (torch.distributed.run,
+NCCL) unless already under a launcher.  C3 is one KKT system per Newton step
+and does not shard (BK needs a global pivot search per column), so ranks run
+independent replicas; value = steps of all ranks /
+max-rank time.  The same line carries a "scopf" block: the sharded workload of
+the north star, C4's 256 SCOPF scenarios strong-scaled over the N ranks
+(round-robin, one batched graph per rank, NCCL only for the per-step stopping
+test), value = scenario Newton steps/s of the whole job.
 
---impl reference: the CPU oracle (oracle/, plain C, single thread) on a
-bounded sample of the same workload, extrapolated to the full step (see
-cpu_baseline.sample in the JSON line).
+--impl reference: the CPU oracle (oracle/, plain C, OpenMP over all host
+cores, bit-identical to one thread) on the same workload: the full step when
+it fits a 45 s budget, else a leading-block sample extrapolated and flagged
+"projected": true (see cpu_baseline.sample).
 """
 import argparse
 import json
@@ -47,6 +53,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=3072, help="oracle factor sample size (leading block)")
     ap.add_argument("--scenarios", type=int, default=256, help="C4: total SCOPF scenarios (strong scaling)")
+    ap.add_argument("--no-scopf", action="store_true", help="C3: skip the C4 scenario-batch block")
     return ap.parse_args()
 
 
@@ -147,38 +154,80 @@ def algorithmic(prob, panels):
                 solve_flops=solve_flops, solve_bytes=solve_bytes)
 
 
-# ----------------------------------------------------------------------------- CPU oracle sample
-def oracle_sample(prob, sv, ns_factor, reps=1):
-    """Time the oracle on a bounded sample of one step; returns (projected s/step, detail)."""
+# ----------------------------------------------------------------------------- CPU oracle
+FULL_STEP_BUDGET_S = 45.0   # run the full oracle step when its projection fits this budget
+
+
+def oracle_full_step(prob, sv):
+    """The oracle's whole Newton step, unextrapolated: condensation, BK factor of the
+    full N x N M (OpenMP over independent trailing-update columns: bit-identical to one
+    thread), inertia, solve, recovery, step vectors.  Returns (seconds, detail)."""
     import oracle
     t0 = time.perf_counter()
     M, rhs, w = oracle.condense(prob)
-    t_cond = time.perf_counter() - t0
-    N = M.shape[0]
+    t1 = time.perf_counter()
+    LD, ipiv, _ = oracle.bk_factor(M)
+    t2 = time.perf_counter()
+    tol = oracle.default_tol(M)
+    ine = oracle.inertia(LD, ipiv, tol)
+    x = oracle.bk_solve(LD, ipiv, rhs, tol)
+    del LD
+    dxs = oracle.recover(prob, w, prob.r[:prob.n_s], x[prob.n_d:])
+    dx = np.concatenate([dxs, x[:prob.n_d]])
+    oracle.step_vectors(sv.x, dx, sv.lo, sv.up, sv.zl, sv.zu, sv.dzl, sv.dzu, sv.tau, sv.mu)
+    oracle.norm_inf(prob.r)
+    t3 = time.perf_counter()
+    return t3 - t0, dict(t_condense=t1 - t0, t_factor=t2 - t1, t_rest=t3 - t2, inertia=ine)
+
+
+def oracle_sample(prob, sv, ns_factor, reps=1):
+    """The oracle on one step of this workload, on all host cores.  If the full step's
+    projection (from a timed leading-block factorization) fits FULL_STEP_BUDGET_S, the
+    full step is executed (projected = False); otherwise the leading ns x ns block is
+    factored and the factor / solve times are extrapolated (projected = True).
+    Returns (seconds per step, detail)."""
+    import oracle
+    nth = oracle.num_threads()
+    cpu_model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            cpu_model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "")
+    except OSError:
+        pass
+    N = prob.N
     ns = min(ns_factor, N)
+    t0 = time.perf_counter()
+    M, rhs, w = oracle.condense(prob)
+    t_cond = time.perf_counter() - t0
     A = np.asfortranarray(M[:ns, :ns])
     t0 = time.perf_counter()
     LD, ipiv, _ = oracle.bk_factor(A)
     t_fac = time.perf_counter() - t0
     t0 = time.perf_counter()
     tol = oracle.default_tol(A)
-    x = oracle.bk_solve(LD, ipiv, rhs[:ns], tol)
+    oracle.bk_solve(LD, ipiv, rhs[:ns], tol)
     t_sol = time.perf_counter() - t0
-    dy = np.zeros(prob.m)
+    del M, LD
     t0 = time.perf_counter()
-    dxs = oracle.recover(prob, w, prob.r[:prob.n_s], dy)
+    dxs = oracle.recover(prob, w, prob.r[:prob.n_s], np.zeros(prob.m))
     dx = np.concatenate([dxs, np.zeros(prob.n_d)])
     oracle.step_vectors(sv.x, dx, sv.lo, sv.up, sv.zl, sv.zu, sv.dzl, sv.dzu, sv.tau, sv.mu)
     oracle.norm_inf(prob.r)
     t_vec = time.perf_counter() - t0
-    scale3 = (N / ns) ** 3
-    scale2 = (N / ns) ** 2
-    proj = t_cond + t_fac * scale3 + t_sol * scale2 + t_vec
-    sample = (f"oracle (plain C, 1 thread) on the full {N}x{N} condensation + recovery + step vectors, and BK "
-              f"factor+solve of the leading {ns}x{ns} block of M, extrapolated x(N/{ns})^3 (factor) and x(N/{ns})^2 "
-              f"(solve); measured {t_cond + t_fac + t_sol + t_vec:.2f} s of CPU work")
-    return proj, dict(t_condense=t_cond, t_factor_sample=t_fac, t_solve_sample=t_sol, t_vec=t_vec, ns=ns,
-                      sample=sample)
+    proj = t_cond + t_fac * (N / ns) ** 3 + t_sol * (N / ns) ** 2 + t_vec
+    base = dict(cores=nth, cpu_model=cpu_model, host_cpus=os.cpu_count())
+    if ns == N or proj <= FULL_STEP_BUDGET_S:
+        t, det = (t_cond + t_fac + t_sol + t_vec, {}) if ns == N else oracle_full_step(prob, sv)
+        sample = (f"oracle (plain C, OpenMP {nth} threads on {cpu_model or 'host CPU'}) executing the FULL step: "
+                  f"condensation of all {prob.n_s} sparse variables, BK factor + solve of the full {N}x{N} M, "
+                  f"recovery, step vectors ({t:.1f} s measured, not projected)")
+        return t, dict(base, projected=False, sample=sample, **det)
+    sample = (f"oracle (plain C, OpenMP {nth} threads on {cpu_model or 'host CPU'}): full condensation + recovery + "
+              f"step vectors, BK factor+solve of the leading {ns}x{ns} block of M extrapolated x(N/{ns})^3 (factor) "
+              f"and x(N/{ns})^2 (solve) -- PROJECTED (full step projected at {proj:.0f} s > "
+              f"{FULL_STEP_BUDGET_S:.0f} s budget); measured {t_cond + t_fac + t_sol + t_vec:.2f} s of CPU work")
+    return proj, dict(base, projected=True, sample=sample, t_condense=t_cond, t_factor_sample=t_fac,
+                      t_solve_sample=t_sol, t_vec=t_vec, ns=ns)
 
 
 def run_reference_c5(args):
@@ -199,13 +248,16 @@ def run_reference_c5(args):
         projs.append(tf * (N / ns) ** 3 + ts * (N / ns) ** 2)
     t_step = float(np.mean(projs))
     val = 1.0 / t_step
-    sample = (f"oracle (plain C, 1 thread) BK factor+solve of a {ns}x{ns} G3 matrix, extrapolated x(N/{ns})^3 / "
-              f"x(N/{ns})^2 to N={N}")
+    nth = oracle.num_threads()
+    sample = (f"oracle (plain C, OpenMP {nth} threads) BK factor+solve of a {ns}x{ns} G3 matrix, extrapolated "
+              f"x(N/{ns})^3 / x(N/{ns})^2 to N={N} -- PROJECTED")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "factor_solve/s", "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "C5 " + CONFIG_DESC["C5"], "N": N},
-            "cpu_baseline": {"value": val, "unit": "factor_solve/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "projected": True,
+            "cpu_baseline": {"value": val, "unit": "factor_solve/s", "cores": nth, "kind": "oracle", "sample": sample,
+                             "projected": True},
             "e2e": {"value": val, "unit": "factor_solve/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": time.perf_counter() - wall0}
     print(json.dumps(line), flush=True)
@@ -220,23 +272,33 @@ def run_reference(args, rank, world):
         return
     prob = mdsgen.config_problem(args.config)
     sv = mdsgen.step_vectors_for(prob, seed=7)
-    for _ in range(args.warmup):
-        oracle_sample(prob, sv, min(args.ref_sample, 512))
-    projs = []
+    # one probe decides full vs projected; warm-up = the probe (page-in, thread pool)
+    t_probe, det = oracle_sample(prob, sv, args.ref_sample)
+    steps = args.steps
+    ts = []
     wall0 = time.perf_counter()
-    det = None
-    for _ in range(args.steps):
-        p, det = oracle_sample(prob, sv, args.ref_sample)
-        projs.append(p)
+    if det["projected"]:
+        for _ in range(steps):
+            t, det = oracle_sample(prob, sv, args.ref_sample)
+            ts.append(t)
+    else:
+        # full steps, bounded to ~3 minutes of CPU work in total (the count executed is reported)
+        steps = max(1, min(args.steps, int(180.0 / max(t_probe, 1e-3))))
+        for _ in range(steps):
+            t, _d = oracle_full_step(prob, sv) if prob.N > args.ref_sample else oracle_sample(prob, sv, args.ref_sample)
+            ts.append(t)
     wall = time.perf_counter() - wall0
-    t_step = float(np.mean(projs))
+    t_step = float(np.mean(ts))
     val = 1.0 / t_step
-    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": 1, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config} " + CONFIG_DESC[args.config], "N": prob.N, "n_s": prob.n_s,
                        "nnz": prob.nnz},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": det["sample"]},
+            "projected": bool(det["projected"]), "steps_requested": args.steps,
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": det["cores"], "kind": "oracle",
+                             "sample": det["sample"], "projected": bool(det["projected"]),
+                             "cpu_model": det["cpu_model"]},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": wall}
     print(json.dumps(line), flush=True)
@@ -397,8 +459,9 @@ def run_ours(args, rank, world):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        proj, det = oracle_sample(prob, sv, args.ref_sample)
-        cpu = {"value": 1.0 / proj, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": det["sample"]}
+        t_or, det = oracle_sample(prob, sv, args.ref_sample)
+        cpu = {"value": 1.0 / t_or, "unit": UNIT, "cores": det["cores"], "kind": "oracle", "sample": det["sample"],
+               "projected": bool(det["projected"]), "cpu_model": det["cpu_model"]}
 
     if rank == 0:
         fs_ms = fac_ms + sol_ms
@@ -432,10 +495,11 @@ def run_ours(args, rank, world):
                 "kernels": kern, "panels": int(len(panels)),
                 "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
                 "inertia": list(out0["inertia"])}
-        print(json.dumps(line), flush=True)
+        return line
+    return None
 
 
-def run_scopf(args, rank, world):
+def run_scopf(args, rank, world, emit=True):
     """C4: SCOPF scenario batch, scenarios round-robin over ranks; per Newton step
     the rank's whole local batch as ONE graph of batched launches + ONE small NCCL
     all-reduce pair for the global stopping test (read on the host)."""
@@ -524,7 +588,10 @@ def run_scopf(args, rank, world):
                 "stop_test": st, "records_gathered": int(recs.shape[0]),
                 "all_inertia_ok": bool(st["n_bad_inertia"] == 0), "setup_s": setup_s,
                 "clocks": clk.summary(), "e2e": None, "cpu_baseline": None}
-        print(json.dumps(line), flush=True)
+        if emit:
+            print(json.dumps(line), flush=True)
+        return line
+    return None
 
 
 def run_c5(args, rank, world):
@@ -632,9 +699,11 @@ def run_c5(args, rank, world):
         oracle.bk_solve(LD, ipiv, np.ones(ns), oracle.default_tol(Ah))
         tsol = time.perf_counter() - t0
         proj = tf * (N / ns) ** 3 + tsol * (N / ns) ** 2
-        cpu = {"value": 1.0 / proj, "unit": "factor_solve/s", "cores": 1, "kind": "oracle",
-               "sample": f"oracle (plain C, 1 thread) BK factor+solve of the leading {ns}x{ns} block, extrapolated "
-                         f"x(N/{ns})^3 / x(N/{ns})^2; measured {tf + tsol:.2f} s"}
+        cpu = {"value": 1.0 / proj, "unit": "factor_solve/s", "cores": oracle.num_threads(), "kind": "oracle",
+               "projected": True,
+               "sample": f"oracle (plain C, OpenMP {oracle.num_threads()} threads) BK factor+solve of the leading "
+                         f"{ns}x{ns} block, extrapolated x(N/{ns})^3 / x(N/{ns})^2 -- PROJECTED; measured "
+                         f"{tf + tsol:.2f} s"}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "factor_solve/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -650,12 +719,29 @@ def run_c5(args, rank, world):
         print(json.dumps(line), flush=True)
 
 
+def spawn(args):
+    """`python bench.py --gpus N` outside a launcher: re-run this script as N ranks
+    (torch.distributed.run, one process per GPU, rendezvous on 127.0.0.1, NCCL)."""
+    import socket
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "WARN")
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    if world != args.gpus and "WORLD_SIZE" in os.environ:
-        pass
+    if "WORLD_SIZE" in os.environ and world != args.gpus and rank == 0:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -669,7 +755,22 @@ def main():
     elif args.config == "C5":
         run_c5(args, rank, world)
     else:
-        run_ours(args, rank, world)
+        line = run_ours(args, rank, world)
+        if args.config == "C3" and not args.no_scopf:
+            # the sharded workload of the north star, measured in the same run: C4's scenario batch
+            # strong-scaled over the same ranks (scenarios round-robin, NCCL only for the stopping test)
+            import torch
+            torch.cuda.empty_cache()
+            sc = run_scopf(args, rank, world, emit=False)
+            if rank == 0 and line is not None and sc is not None:
+                line["scopf"] = {k: sc[k] for k in ("value", "unit", "n_gpus", "ms_per_step", "scaling",
+                                                    "gpu_launches", "factor_solve_fp64_tflops_aggregate",
+                                                    "factor_solve_frac_of_peak", "all_inertia_ok", "roofline",
+                                                    "clocks")}
+                line["scopf"]["workload"] = sc["config"]["workload"]
+                line["scopf"]["collectives_per_step"] = "1 MAX + 1 SUM all_reduce of 5 + 2 doubles (NCCL)"
+        if rank == 0 and line is not None:
+            print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -57,6 +57,15 @@ def main():
         ine, status = dense_case(A)
         ok = status == 0 and sum(ine) == N
         print(case, "inertia", ine, "status", status)
+    elif case == "batched":
+        base = mdsgen.scopf_base(seed=7, n_s=3000, n_d=60, m_E=30, m_I=40)
+        probs = [mdsgen.scopf_scenario(base, s, seed=7) for s in range(3)]
+        svs = [mdsgen.step_vectors_for(p, seed=100 + s) for s, p in enumerate(probs)]
+        bt = mds.BatchedKKTStep(probs, svs=svs)
+        bt.run()
+        outs = [bt.results(i) for i in range(3)]
+        ok = all(o["inertia"] == tuple(p.expected_inertia) and o["status"] == 0 for o, p in zip(outs, probs))
+        print(case, [o["inertia"] for o in outs], [o["status"] for o in outs])
     else:
         raise SystemExit(f"unknown case {case}")
     sys.exit(0 if ok else 1)
