@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--ref-sample", type=int, default=3072, help="oracle factor sample size (leading block)")
     ap.add_argument("--scenarios", type=int, default=256, help="C4: total SCOPF scenarios (strong scaling)")
     ap.add_argument("--no-scopf", action="store_true", help="C3: skip the C4 scenario-batch block")
+    ap.add_argument("--no-ipm", action="store_true", help="C3: skip the IPM-trajectory block")
     return ap.parse_args()
 
 
@@ -594,6 +595,48 @@ def run_scopf(args, rank, world, emit=True):
     return None
 
 
+def run_ipm(args, rank, world):
+    """NEXT-2: a whole interior-point trajectory on the C3-shaped convex QP (n_s = 1M,
+    N = 8192; mdsgen.qp_config), every Newton iteration through the hot path + the IPM
+    vector kernels (paper_2605_13736_b200.ipm, R23), to e_0 <= 1e-8.  One
+    untimed trajectory first (page-in, attributes), then a timed one from the same start."""
+    import torch
+
+    import mdsgen
+    from paper_2605_13736_b200.ipm import IPMSolver
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    t0 = time.time()
+    qp = mdsgen.qp_config(args.config)
+    setup_s = time.time() - t0
+    IPMSolver(qp).solve()
+    sol = IPMSolver(qp)
+    e0_, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        torch.cuda.synchronize()
+        e0_.record()
+        res = sol.solve()
+        e1_.record()
+        torch.cuda.synchronize()
+    ms = e0_.elapsed_time(e1_)
+    h = res["history"]
+    its = max(res["iterations"], 1)
+    return {"workload": f"{args.config}-shaped convex QP (n_s={qp.base.n_s}, n_d={qp.base.n_d}, m_E={qp.base.m_E}, "
+                        f"m_I={qp.base.m_I}, N={qp.base.N}), filter line-search IPM to e_0 <= 1e-8",
+            "status": res["status"], "iterations": res["iterations"], "e0": res["e0"], "final_mu": res["mu"],
+            "trajectory_ms": ms, "newton_iters_per_s": its / (ms / 1e3),
+            "newton_step_ms_mean": float(np.mean(res["newton_ms"])) if res["newton_ms"] else None,
+            "line_search_trials": int(sum(r["trials"] for r in h)),
+            "iterations_with_delta_w": int(sum(r["delta_w"] > 0 for r in h)),
+            "exact_bk_columns_total": int(sum(r["exact_cols"] for r in h)),
+            "exact_bk_columns_max": int(max((r["exact_cols"] for r in h), default=0)),
+            "interchanges_total": int(sum(r["swaps"] for r in h)),
+            "inertia_ok_every_iteration": bool(all(r["inertia"] == (qp.base.n_d, 0, qp.base.m) for r in h)),
+            "host_syncs_per_iteration": "inertia (24 B), error norms, line-search scalars, factor counters",
+            "setup_s": setup_s, "clocks": clk.summary()}
+
+
 def run_c5(args, rank, world):
     """C5 stress: factor + solve of the N = 32768 G3 matrix (8.6 GB) per step (replicas under torchrun).
     M is restored from a device copy before every step, outside the timed region (CUDA events bracket
@@ -769,6 +812,10 @@ def main():
                                                     "clocks")}
                 line["scopf"]["workload"] = sc["config"]["workload"]
                 line["scopf"]["collectives_per_step"] = "1 MAX + 1 SUM all_reduce of 5 + 2 doubles (NCCL)"
+        if args.config == "C3" and not args.no_ipm and rank == 0 and line is not None:
+            import torch
+            torch.cuda.empty_cache()
+            line["ipm"] = run_ipm(args, rank, world)
         if rank == 0 and line is not None:
             print(json.dumps(line), flush=True)
     if world > 1:

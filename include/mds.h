@@ -187,6 +187,10 @@ int mds_factor_batched(int64_t batch, int64_t N, double *M, int64_t ldm, int64_t
 /* ||M||_inf and the zero-pivot tolerance the last mds_factor on `work` used
  * (host copies; synchronous).  For the parity tests of reading R4. */
 int mds_factor_tol(const void *work, double *anorm_host, double *tol_host);
+/* Counters of the last mds_factor on `work` (host copies; synchronous): out4 =
+ * {panels, symmetric interchanges, columns decided by the exact BK steps (not
+ * the speculative accepted prefix), 1 if aborted on non-finite input}. */
+int mds_factor_stats(const void *work, int64_t *out4);
 
 /* ---------------------------------------------------------------------------
  * mds_solve — x = P^T L^{-T} D^{-1} L^{-1} P rhs_c with mds_factor's output,
@@ -278,6 +282,45 @@ int mds_kkt_residual(const mds_plan *plan, const double *js_val, const double *h
                      const double *H_dd, int64_t ldh, const double *sigma_d, const double *J_d, int64_t ldj,
                      const double *d_h, double delta_w, double delta_c, const double *x, const double *b,
                      double *out, double *rnorm, void *work, size_t work_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Interior-point loop vector kernels (K1 "axpy" + the filter line search's
+ * reductions) for the convex-QP IPM of DESIGN.md R23.
+ * One iterate: P = [x_s | x_d | s] (n + m_I; n = n_s + n_d), lo / up over P
+ * (slack bounds h_l / h_u in the tail; |b| >= 1e20 infinite), bound duals zl / zu
+ * over P (slack duals in the tail), y [m].  Kxy = (H x + J^T y, J x) is
+ * mds_kkt_residual's K x with sigma = delta = 0 and d_h = +inf.  All device
+ * pointers, caller-owned, stream-ordered, deterministic (fixed-order sums).
+ *
+ * ipm_rhs: sigma [n+m_I] = zl/(P-lo) + zu/(up-P) (finite terms; tail = D_h),
+ *   r [n+m] = Eq.(5) right-hand side (r_x = -(Kxy_x + c - mu/(x-lo) + mu/(up-x)),
+ *   r_yE = -(J_E x - g_E), r_yI = -(J_I x - s) + q/D_h), q [m_I] = y_h + mu/(s-h_l)
+ *   - mu/(h_u-s), res_d [n+m_I] = stationarity (x: Kxy_x + c - zl + zu; s: -y_h
+ *   - v_l + v_u), res_p [m] = (J_E x - g_E, J_I x - s).
+ * ipm_directions: from the solve's (dx, dy) [n+m]: dP = (dx, ds), ds = (dy_h + q)/D_h,
+ *   dzl = mu/gl - zl - (zl/gl) dP, dzu = mu/gu - zu + (zu/gu) dP, dx0[0..n) = dx.
+ * ipm_reduce: mode 0 out[0..4) = ||res_d||_inf, ||res_p||_inf, max gap*z, max |gap*z - mu|;
+ *   mode 1 out[0..6) = f, (H x + c).dx, dx.H dx, barrier part of grad(phi).dP,
+ *   ||res_p||_1, sum log gaps (Kd = K0 (dx, 0)); mode 2 (trial alpha) out[0..2) =
+ *   ||res_p + alpha (J dx - (0, ds))||_1, sum log gaps(P + alpha dP).
+ *   work >= ipm_workspace_size(n, m_I) bytes, zeroed once before first use.
+ * ipm_apply: P += alpha dP, y += alpha dy, z += alpha_d dz, then the dual safeguard
+ *   z in [mu/(kappa_sigma gap), kappa_sigma mu/gap]; xy [n+m] = (x, y). */
+size_t ipm_workspace_size(int64_t n, int64_t m_I);
+int ipm_rhs(int64_t n, int64_t m_E, int64_t m_I, const double *Kxy, const double *c, const double *g_E,
+            const double *P, const double *lo, const double *up, const double *zl, const double *zu,
+            const double *y, double mu, double *sigma, double *r, double *q, double *res_d, double *res_p,
+            void *stream);
+int ipm_directions(int64_t n, int64_t m_E, int64_t m_I, const double *dxy, const double *q, const double *sigma,
+                   const double *P, const double *lo, const double *up, const double *zl, const double *zu,
+                   double mu, double *dP, double *dzl, double *dzu, double *dx0, void *stream);
+int ipm_reduce(int mode, int64_t n, int64_t m_E, int64_t m_I, const double *P, const double *dP, const double *lo,
+               const double *up, const double *zl, const double *zu, const double *y, const double *c,
+               const double *Kxy, const double *Kd, const double *res_d, const double *res_p, double mu,
+               double alpha, double *out, void *work, size_t work_bytes, void *stream);
+int ipm_apply(int64_t n, int64_t m_E, int64_t m_I, double *P, double *zl, double *zu, double *y, double *xy,
+              const double *dP, const double *dzl, const double *dzu, const double *dy, const double *lo,
+              const double *up, double alpha, double alpha_d, double mu, double kappa_sigma, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Instrumentation (not on the hot path; used by bench.py for the roofline).

@@ -392,3 +392,65 @@ def scopf_scenario(base: MDSProblem, s: int, seed: int = 4000):
                       rng.uniform(0.0, 1.0, n_s), rng.uniform(0.5, 2.0, n_s), H, rng.uniform(0.1, 1.0, n_d),
                       J_d, rng.uniform(1.0, 10.0, base.m_I), 0.0, 0.0, rng.standard_normal(n_s + n_d + m),
                       expected_inertia=(n_d, 0, m), meta=dict(gen="SCOPF", seed=seed, scenario=s))
+
+
+# ----------------------------------------------------------------------------- convex QP (C3 IPM workload)
+@dataclass
+class QPProblem:
+    """Convex QP in MDS form (SURVEY.md §8(d) "C3 full IPM workload"):
+        min  1/2 x_d^T H_dd x_d + 1/2 sum h_ss x_s^2 + c^T x
+        s.t. J_E x = g_E,   h_l <= J_I x <= h_u,   lo <= x <= up
+    with J = [J_s^T  J_d] (J_s CSR n_s x m, rows = sparse variables, reading R1),
+    built around a strictly interior x_star.  Infinite bounds are +-1e20 (R10).
+    `base` carries the pattern and the Hessian / Jacobian values (an MDSProblem
+    whose sigma_s, sigma_d, d_h, r are unused placeholders)."""
+    base: MDSProblem
+    c: np.ndarray          # f64[n]
+    g_E: np.ndarray        # f64[m_E]
+    h_l: np.ndarray        # f64[m_I]
+    h_u: np.ndarray        # f64[m_I]
+    lo: np.ndarray         # f64[n]
+    up: np.ndarray         # f64[n]
+    x_star: np.ndarray     # f64[n] strictly interior, feasible
+
+    @property
+    def n(self):
+        return self.base.n_s + self.base.n_d
+
+
+def _jac_times(prob: MDSProblem, x):
+    """(J x)_c = sum_k J_s[k, c] x_s[k] + (J_d x_d)_c  -- input construction only."""
+    n_s = prob.n_s
+    rows = np.repeat(np.arange(n_s), np.diff(prob.rowptr))
+    out = np.bincount(prob.colidx, weights=prob.val * x[:n_s][rows], minlength=prob.m)
+    if prob.n_d and prob.m:
+        out = out + np.asarray(prob.J_d) @ x[n_s:]
+    return out
+
+
+def qp_problem(n_s, n_d, m_E, m_I, seed, pattern="uniform", box_frac=0.5, c_scale=1.0):
+    """Seeded convex QP with the G1 structure (private sparse variable per constraint,
+    H_dd = G G^T/n_d + I, h_ss ~ U[0.1, 1] so every sparse variable has curvature)."""
+    base = g1_quasidefinite(n_s, n_d, m_E, m_I, seed, pattern=pattern)
+    rng = np.random.default_rng([seed, 77])
+    n = n_s + n_d
+    base.h_ss = rng.uniform(0.1, 1.0, n_s)
+    x_star = rng.uniform(-5.0, 5.0, n)
+    boxed = rng.random(n) < box_frac
+    lo = np.where(boxed, -10.0, -INF)
+    up = np.where(boxed, 10.0, INF)
+    c = rng.standard_normal(n) * c_scale
+    Jx = _jac_times(base, x_star)
+    g_E = Jx[:m_E].copy()
+    h_l = Jx[m_E:] - rng.uniform(0.5, 2.0, m_I)
+    h_u = Jx[m_E:] + rng.uniform(0.5, 2.0, m_I)
+    base.meta = dict(base.meta, gen="QP", seed=seed)
+    return QPProblem(base, c, g_E, h_l, h_u, lo, up, x_star)
+
+
+def qp_config(cfg: str, seed: Optional[int] = None, pattern="uniform"):
+    """The QP of BASELINE.json config C1..C3 shapes (seed = 1000*cfg + 500)."""
+    shp = CONFIGS[cfg]
+    if seed is None:
+        seed = 1000 * int(cfg[1:]) + 500
+    return qp_problem(shp["n_s"], shp["n_d"], shp["m_E"], shp["m_I"], seed, pattern=pattern)

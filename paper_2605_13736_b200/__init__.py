@@ -76,6 +76,15 @@ _lib.ipm_step_vectors_batched.argtypes = ([_I64, _I64, _I64] + [_P] * 8 + [_D, _
                                           _P, _I64, _P, _P, _P, ctypes.c_size_t, _P])
 _lib.ipm_step_vectors_batched.restype = ctypes.c_int
 
+_lib.ipm_workspace_size.restype = ctypes.c_size_t
+_lib.ipm_workspace_size.argtypes = [_I64, _I64]
+_lib.ipm_rhs.argtypes = [_I64, _I64, _I64] + [_P] * 9 + [_D] + [_P] * 5 + [_P]
+_lib.ipm_directions.argtypes = [_I64, _I64, _I64] + [_P] * 8 + [_D] + [_P] * 4 + [_P]
+_lib.ipm_reduce.argtypes = [ctypes.c_int, _I64, _I64, _I64] + [_P] * 12 + [_D, _D, _P, _P, ctypes.c_size_t, _P]
+_lib.ipm_apply.argtypes = [_I64, _I64, _I64] + [_P] * 11 + [_D, _D, _D, _D, _P]
+for _f in ("ipm_rhs", "ipm_directions", "ipm_reduce", "ipm_apply"):
+    getattr(_lib, _f).restype = ctypes.c_int
+
 _lib.mds_kkt_residual_workspace_size.restype = ctypes.c_size_t
 _lib.mds_kkt_residual_workspace_size.argtypes = [_I64]
 _lib.mds_kkt_residual.argtypes = [_P, _P, _P, _P, _P, _I64, _P, _P, _I64, _P, _D, _D, _P, _P, _P, _P, _P,
@@ -87,7 +96,8 @@ EXPORTS = ["mds_condense_workspace_size", "mds_condense_batched", "mds_factor_to
            "ipm_step_vectors_workspace_size", "ipm_step_vectors", "mds_launch_count", "mds_profile_begin",
            "mds_profile_end", "mds_factor_panels", "mds_factor_set_grid_cap", "mds_profile_timeline", "mds_set_variant",
            "mds_factor_batched_workspace_size", "mds_factor_batched", "mds_solve_batched_workspace_size",
-           "mds_solve_batched", "ipm_step_vectors_batched_workspace_size", "ipm_step_vectors_batched"]
+           "mds_solve_batched", "ipm_step_vectors_batched_workspace_size", "ipm_step_vectors_batched",
+           "ipm_workspace_size", "ipm_rhs", "ipm_directions", "ipm_reduce", "ipm_apply", "mds_factor_stats"]
 
 PROF_CLASSES = ["condense_rows", "condense_norm", "condense_tiles", "anorm", "panel_diag", "panel_trsm", "panel_store",
                 "panel_exact", "update", "finalize", "solve_gather", "solve_fwd", "solve_d", "solve_bwd",
@@ -293,6 +303,16 @@ def step_vectors_batched(batch, n, str_vec, x, dx, lo, up, zl, zu, dzl, dzu, tau
     _check(code, "ipm_step_vectors_batched")
 
 
+def factor_stats(fwork):
+    """(panels, interchanges, exact-path columns, aborted) of the last mds_factor on `fwork` (synchronous)."""
+    import numpy as np
+    out = np.zeros(4, dtype=np.int64)
+    _lib.mds_factor_stats.argtypes = [_P, _P]
+    _lib.mds_factor_stats.restype = ctypes.c_int
+    _check(_lib.mds_factor_stats(_ptr(fwork), out.ctypes.data), "mds_factor_stats")
+    return tuple(int(v) for v in out)
+
+
 def factor_tol(fwork):
     """(||M||_inf, zero-pivot tolerance) the last mds_factor on `fwork` used (synchronous)."""
     a, t = ctypes.c_double(), ctypes.c_double()
@@ -331,6 +351,37 @@ def step_vectors(n, x, dx, lo, up, zl, zu, dzl, dzu, tau, mu, out, sigma_out, st
                                  _f64(dzu), float(tau), float(mu), nres, arr_p, arr_l, _f64(out), _f64(sigma_out),
                                  _ptr(status), _ptr(work), work.numel() * work.element_size(), _stream(stream))
     _check(code, "ipm_step_vectors")
+
+
+def ipm_workspace_size(n, m_I):
+    return int(_lib.ipm_workspace_size(int(n), int(m_I)))
+
+
+def ipm_rhs(n, m_E, m_I, Kxy, c, g_E, P, lo, up, zl, zu, y, mu, sigma, r, q, res_d, res_p, stream=None):
+    _check(_lib.ipm_rhs(int(n), int(m_E), int(m_I), _f64(Kxy), _f64(c), _f64(g_E), _f64(P), _f64(lo), _f64(up),
+                        _f64(zl), _f64(zu), _f64(y), float(mu), _f64(sigma), _f64(r), _f64(q), _f64(res_d),
+                        _f64(res_p), _stream(stream)), "ipm_rhs")
+
+
+def ipm_directions(n, m_E, m_I, dxy, q, sigma, P, lo, up, zl, zu, mu, dP, dzl, dzu, dx0, stream=None):
+    _check(_lib.ipm_directions(int(n), int(m_E), int(m_I), _f64(dxy), _f64(q), _f64(sigma), _f64(P), _f64(lo),
+                               _f64(up), _f64(zl), _f64(zu), float(mu), _f64(dP), _f64(dzl), _f64(dzu), _f64(dx0),
+                               _stream(stream)), "ipm_directions")
+
+
+def ipm_reduce(mode, n, m_E, m_I, out, work, P, lo, up, dP=None, zl=None, zu=None, y=None, c=None, Kxy=None,
+               Kd=None, res_d=None, res_p=None, mu=0.0, alpha=0.0, stream=None):
+    _check(_lib.ipm_reduce(int(mode), int(n), int(m_E), int(m_I), _f64(P), _f64(dP), _f64(lo), _f64(up), _f64(zl),
+                           _f64(zu), _f64(y), _f64(c), _f64(Kxy), _f64(Kd), _f64(res_d), _f64(res_p), float(mu),
+                           float(alpha), _f64(out), _ptr(work), work.numel() * work.element_size(), _stream(stream)),
+           "ipm_reduce")
+
+
+def ipm_apply(n, m_E, m_I, P, zl, zu, y, xy, dP, dzl, dzu, dy, lo, up, alpha, alpha_d, mu, kappa_sigma,
+              stream=None):
+    _check(_lib.ipm_apply(int(n), int(m_E), int(m_I), _f64(P), _f64(zl), _f64(zu), _f64(y), _f64(xy), _f64(dP),
+                          _f64(dzl), _f64(dzu), _f64(dy), _f64(lo), _f64(up), float(alpha), float(alpha_d),
+                          float(mu), float(kappa_sigma), _stream(stream)), "ipm_apply")
 
 
 def set_grid_cap(ctas: int):

@@ -58,7 +58,7 @@ struct FCtl {
   int nswap;       // interchanges performed (kp != kk)
   int abort;       // non-finite input: nothing is factored
   unsigned xready; // q+1 once panel q's F1 has published X, d and the in-block colmax
-  int pad;
+  int nexact;     // columns decided by the exact (dlasyf) BK steps rather than the accepted prefix
   double anorm, tol;
   long long inertia[3];
   unsigned long long colmax[NB];   // bit patterns of non-negative doubles (atomicMax-able)
@@ -1079,6 +1079,7 @@ __global__ void __launch_bounds__(1024) k_panel_slow(int64_t N, double* __restri
   }
   if (tid == 0) {
     ctl->kb = j;
+    ctl->nexact += j - p;
     f.pinfo[f.pidx] = make_int2((int)k0, j);
   }
   zero_w_tail(N, k0, j, f);
@@ -1475,6 +1476,7 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
   }
   if (c0 && tid == 0) {
     ctl->kb = j;
+    ctl->nexact += j - p;
     f.pinfo[f.pidx] = make_int2((int)k0, j);
   }
   // W / Lb columns [j, NB) of rows >= k0 must be exactly zero for the TMA update (grid-strided)
@@ -2296,6 +2298,15 @@ extern "C" int mds_factor_set_grid_cap(int ctas) {
 // read by solve.cu
 double* mds_factor_tol_ptr(const void* fwork) {
   return fwork ? &reinterpret_cast<FCtl*>(const_cast<void*>(fwork))->tol : nullptr;
+}
+
+// panels, interchanges and exact-path columns of the last mds_factor on `fwork` (synchronous)
+extern "C" int mds_factor_stats(const void* fwork, int64_t* out4) {
+  if (!fwork || !out4) return MDS_ERR_ARG;
+  FCtl c;
+  if (cudaMemcpy(&c, fwork, sizeof(FCtl), cudaMemcpyDeviceToHost) != cudaSuccess) return MDS_ERR_CUDA;
+  out4[0] = c.npanel; out4[1] = c.nswap; out4[2] = c.nexact; out4[3] = c.abort;
+  return MDS_OK;
 }
 
 // ||M||_inf and the zero-pivot tolerance the last mds_factor on `fwork` used (synchronous)

@@ -96,3 +96,20 @@ def rel_inf(a, b):
     a, b = np.asarray(a), np.asarray(b)
     den = max(np.abs(b).max(), 1e-300) if b.size else 1.0
     return np.abs(a - b).max() / den if a.size else 0.0
+
+
+def dense_qp_parts(qp):
+    """(H, J) of a mdsgen.QPProblem assembled densely from its blocks (test-only)."""
+    b = qp.base
+    Js = dense_js(b)                                          # n_s x m
+    n_s, n_d, m = b.n_s, b.n_d, b.m
+    H = np.zeros((n_s + n_d, n_s + n_d))
+    H[:n_s, :n_s] = np.diag(b.h_ss)
+    if n_d:
+        Hd = np.asarray(b.H_dd)
+        H[n_s:, n_s:] = np.tril(Hd) + np.tril(Hd, -1).T
+    J = np.zeros((m, n_s + n_d))
+    J[:, :n_s] = Js.T
+    if n_d and m:
+        J[:, n_s:] = np.asarray(b.J_d)
+    return H, J
