@@ -16,8 +16,9 @@ def needs_build():
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, "common.cuh"), os.path.join(CSRC, "anorm.cuh"),
-                                                      os.path.join(HERE, "..", "include", "mds.h")]
+    import glob
+    deps = ([os.path.join(CSRC, s) for s in SOURCES] + glob.glob(os.path.join(CSRC, "*.cuh")) +
+            [os.path.join(HERE, "..", "include", "mds.h"), os.path.abspath(__file__)])
     return any(os.path.getmtime(d) > t for d in deps)
 
 

@@ -94,6 +94,11 @@ struct FWork {
   // owns the workspace at + s * bws bytes, M at + s * bms elements, piv at + s * bps
   size_t bws;
   int64_t bms, bps;
+  // emulated-FP64 update (ozaki.cuh): int8 slices [8][N][64] of the panel's L and W, row exponents
+  int8_t* ozL;
+  int8_t* ozW;
+  int* ozeL;
+  int* ozeW;
 };
 
 template <typename T>
@@ -106,7 +111,7 @@ __device__ __forceinline__ void bsel_ws(FWork& f, int64_t s) {
   shp(f.ctl, o); shp(f.panel_start, o); shp(f.sw, o); shp(f.bt, o); shp(f.rho, o); shp(f.rhoinv, o);
   shp(f.nparts, o); shp(f.Lblk, o); shp(f.W, o); shp(f.W1, o); shp(f.Lb, o); shp(f.Lb1, o); shp(f.pinfo, o);
   shp(f.ucount, o); shp(f.t1flag, o); shp(f.xbar, o); shp(f.xpart, o); shp(f.xaux, o); shp(f.Wprev, o);
-  shp(f.Lbprev, o);
+  shp(f.Lbprev, o); shp(f.ozL, o); shp(f.ozW, o); shp(f.ozeL, o); shp(f.ozeW, o);
 }
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -135,6 +140,10 @@ FWork carve(void* work, int64_t N, size_t* total) {
   f.xbar = reinterpret_cast<unsigned*>(take(sizeof(unsigned) * (N / 32 + 8)));
   f.xpart = reinterpret_cast<ArgMax*>(take(sizeof(ArgMax) * 2 * XMAXG));
   f.xaux = reinterpret_cast<double*>(take(sizeof(double) * 2));
+  f.ozL = reinterpret_cast<int8_t*>(take((size_t)8 * N * 64));
+  f.ozW = reinterpret_cast<int8_t*>(take((size_t)8 * N * 64));
+  f.ozeL = reinterpret_cast<int*>(take(sizeof(int) * N));
+  f.ozeW = reinterpret_cast<int*>(take(sizeof(int) * N));
   f.Wprev = f.W1;
   f.Lbprev = f.Lb1;
   f.fuse = 0;
@@ -2188,6 +2197,9 @@ bool make_map(CUtensorMap* m, const double* base, int64_t rows, int64_t cols, in
   return r == CUDA_SUCCESS;
 }
 
+}  // namespace
+#include "ozaki.cuh"
+namespace {
 // ---------------------------------------------------------------------------
 // Finalize: inertia out; convert panel-end-order L to the explicit permutation
 // form by applying every later panel's interchanges to earlier panels' rows
@@ -2436,6 +2448,16 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   if (use_tma && !(make_map(&mapW1, f.W1, N, NB, f.ldw) && make_map(&mapL0, f.Lb, N, NB, f.ldw) &&
                    make_map(&mapL1, f.Lb1, N, NB, f.ldw) && make_map(&mapX, f.Lblk, NB, NB, NB)))
     return MDS_ERR_CUDA;
+  CUtensorMap mapOL, mapOW, mapOC;
+  if (use_tma && g_mds_var.ozaki) {
+    if (!(make_map_oz(&mapOL, f.ozL, N, 1, 0, OZ_TM) && make_map_oz(&mapOW, f.ozW, N, 1, 0, OZ_TN) &&
+          make_map_ozc(&mapOC, M, N, ldm, 1, (size_t)ldm * N * 8)))
+      return MDS_ERR_CUDA;
+    if (mds_once_per_device((const void*)k_update_oz<false>)) {
+      cudaFuncSetAttribute(k_update_oz<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM2);
+      cudaFuncSetAttribute(k_update_oz<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM2);
+    }
+  }
   const int g_sched = (g_mds_var.static_sched ? 1 : 0) | (g_mds_var.no_snake ? 0 : 2) | (g_mds_var.no_cprefetch ? 0 : 8);
   const bool g_inplace = g_mds_var.upd_inplace != 0;
   const bool upd_main = g_mds_var.upd_main != 0;   // measured slower (A/B), off by default
@@ -2571,7 +2593,16 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
       const CUtensorMap& mw = (p & 1) ? mapW1 : mapW;
       const CUtensorMap& ml = (p & 1) ? mapL1 : mapL0;
       MDS_LAUNCH(PC_PANEL_STORE, st, (k_panel_store<<<dim3(g256, 8), 256, 0, st>>>(N, M, ldm, fp)));
-      if (n2max > 0) {
+      if (n2max > 0 && use_tma && g_mds_var.ozaki) {
+        const int64_t smin = std::min<int64_t>(N, (p + 1) * (NB - 1));
+        const int64_t r_lo = (smin / OZ_TM) * OZ_TM;
+        MDS_LAUNCH(PC_UPDATE, st, MDS_CUDA_TRY(launch_pdl(k_oz_split, dim3((unsigned)mds_cdiv(N - r_lo, 64), 2, 1),
+                                                          dim3(256), 0, st, N, fp, r_lo)));
+        const int64_t tbo = oz_tiles(N, smin);
+        const unsigned go = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tbo, (int64_t)sms));
+        MDS_LAUNCH(PC_UPDATE, st, (k_update_oz<false><<<go, OZ_THREADS2, OZ_SMEM2, st>>>(N, fp, mapOL, mapOW, mapOC,
+                                                                                         tbo, 1)));
+      } else if (n2max > 0) {
         const unsigned ugrid = (unsigned)std::min<int64_t>(nt * (nt + 1) / 2, sms);
         if (use_tma && g_inplace)
           MDS_LAUNCH(PC_UPDATE, st,
@@ -2687,6 +2718,16 @@ extern "C" int mds_factor_batched(int64_t batch, int64_t N, double* M, int64_t l
     cudaFuncSetAttribute(k_panel_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, F1SMEM);
     cudaFuncSetAttribute(k_panel_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB * US * (int)sizeof(double));
   }
+  CUtensorMap mapOL, mapOW, mapOC;
+  if (g_mds_var.ozaki) {
+    if (!(make_map_oz(&mapOL, f.ozL, N, batch, ws, OZ_TM) && make_map_oz(&mapOW, f.ozW, N, batch, ws, OZ_TN) &&
+          make_map_ozc(&mapOC, M, N, ldm, batch, (size_t)str_M * 8)))
+      return MDS_ERR_CUDA;
+    if (mds_once_per_device((const void*)k_update_oz<true>)) {
+      cudaFuncSetAttribute(k_update_oz<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM2);
+      cudaFuncSetAttribute(k_update_oz<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM2);
+    }
+  }
   CUtensorMap mapA, mapW0, mapW1, mapL0, mapL1, mapX;
   if (!(make_map3(&mapA, M, N, N, ldm, batch, (size_t)str_M * 8) && make_map3(&mapX, f.Lblk, NB, NB, NB, batch, ws) &&
         make_map3(&mapW0, f.W, N, NB, f.ldw, batch, ws) && make_map3(&mapW1, f.W1, N, NB, f.ldw, batch, ws) &&
@@ -2739,8 +2780,18 @@ extern "C" int mds_factor_batched(int64_t batch, int64_t N, double* M, int64_t l
       const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tb * batch, sms));
       const CUtensorMap& mw = (p & 1) ? mapW1 : mapW0;
       const CUtensorMap& ml = (p & 1) ? mapL1 : mapL0;
-      MDS_LAUNCH(PC_UPDATE, st,
-                 (k_update_tma<5, true><<<gr, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapA, sched, tb, batch)));
+      if (g_mds_var.ozaki) {
+        const int64_t r_lo = (smin / OZ_TM) * OZ_TM;
+        MDS_LAUNCH(PC_UPDATE, st, MDS_CUDA_TRY(launch_pdl(k_oz_split, dim3((unsigned)mds_cdiv(N - r_lo, 64), 2, nb),
+                                                          dim3(256), 0, st, N, fp, r_lo)));
+        const int64_t tbo = oz_tiles(N, smin);
+        const unsigned go = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tbo * batch, (int64_t)sms));
+        MDS_LAUNCH(PC_UPDATE, st, (k_update_oz<true><<<go, OZ_THREADS2, OZ_SMEM2, st>>>(N, fp, mapOL, mapOW, mapOC, tbo,
+                                                                                        batch)));
+      } else {
+        MDS_LAUNCH(PC_UPDATE, st,
+                   (k_update_tma<5, true><<<gr, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapA, sched, tb, batch)));
+      }
     }
   }
   MDS_LAUNCH(PC_FINALIZE, st, (k_factor_finalize_b<<<nb, 512, 0, st>>>(N, M, ldm, f, piv, inertia_dev)));

@@ -66,7 +66,7 @@ extern "C" int mds_set_variant(const char* key, long long value) {
             : k == "no_cprefetch" ? &v.no_cprefetch : k == "upd_inplace" ? &v.upd_inplace
             : k == "upd_main" ? &v.upd_main : k == "slow_1cta" ? &v.slow_1cta
             : k == "exact_no_ls" ? &v.exact_no_ls : k == "f2_trsm" ? &v.f2_trsm
-            : k == "no_pdl" ? &v.no_pdl : nullptr;
+            : k == "no_pdl" ? &v.no_pdl : k == "ozaki" ? &v.ozaki : nullptr;
   if (!flag) return MDS_ERR_ARG;
   *flag = value ? 1 : 0;
   return MDS_OK;

@@ -136,3 +136,21 @@ def test_batched_c4_full_size_vs_oracle():
     g.replay()
     for i in range(len(ids)):
         check_vs_oracle(bt, i, probs[i], svs[i])
+
+
+@pytest.fixture
+def ozaki_variant():
+    mds.set_variant("default")
+    mds.set_variant("ozaki", 1)
+    yield
+    mds.set_variant("default")
+
+
+@pytest.mark.parametrize("N,n2,B", [(700, 150, 3), (1100, 250, 2)])
+def test_factor_batched_pivoting_ozaki(N, n2, B, ozaki_variant):
+    # the emulated-FP64 (INT8 tensor-core, Ozaki splitting) trailing update, same parity bars
+    test_factor_batched_pivoting(N, n2, B)
+
+
+def test_batched_step_vs_oracle_ozaki(ozaki_variant):
+    test_batched_step_vs_oracle((6000, 100, 40, 60), 4)

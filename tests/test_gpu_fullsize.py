@@ -224,3 +224,11 @@ def test_c5_factor_solve_32768():
     assert g_ine == ine
     res = float((A @ x - b).abs().max() / b.abs().max())
     assert res <= 1e-10, res
+
+
+@pytest.mark.parametrize("N,n2", [(1500, 300), (2111, 500)])
+def test_pivoting_heavy_ozaki_single(N, n2, variant_reset):
+    # single-system factorization with the emulated-FP64 update (non-look-ahead launch structure)
+    mds.set_variant("no_lookahead", 1)
+    mds.set_variant("ozaki", 1)
+    test_pivoting_heavy_multi_panel(N, n2)
