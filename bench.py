@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--scenarios", type=int, default=256, help="C4: total SCOPF scenarios (strong scaling)")
     ap.add_argument("--no-scopf", action="store_true", help="C3: skip the C4 scenario-batch block")
     ap.add_argument("--no-ipm", action="store_true", help="C3: skip the IPM-trajectory block")
+    ap.add_argument("--ipm-sweep", default="2000,8000,10000", help="nlpMDS_ex4 sizes k for the IPM block")
     return ap.parse_args()
 
 
@@ -634,7 +635,45 @@ def run_ipm(args, rank, world):
             "interchanges_total": int(sum(r["swaps"] for r in h)),
             "inertia_ok_every_iteration": bool(all(r["inertia"] == (qp.base.n_d, 0, qp.base.m) for r in h)),
             "host_syncs_per_iteration": "inertia (24 B), error norms, line-search scalars, factor counters",
-            "setup_s": setup_s, "clocks": clk.summary()}
+            "setup_s": setup_s, "clocks": clk.summary(),
+            "paper_sweep": ipm_paper_sweep(args)}
+
+
+def ipm_paper_sweep(args):
+    """The paper's own workload: the nlpMDS_ex4 mini-app problem (PAPER.md:536;
+    mdsgen.synthetic_problem, compressed size N = 2k+3) solved to e_0 <= 1e-8 by the device
+    IPM at k = 2000 / 8000 / 10000 (N = 4003 / 16003 / 20003: the paper's "matrix size
+    16,000" and "20,000").  Per-iteration times are context against the paper's V100
+    numbers (MAGMA 4.49 s per iteration at 16,000), not a target."""
+    import torch
+
+    import mdsgen
+    from paper_2605_13736_b200.ipm import IPMSolver
+
+    out = []
+    for k in [int(v) for v in args.ipm_sweep.split(",") if v]:
+        qp = mdsgen.synthetic_problem(k)
+        sol = IPMSolver(qp)
+        torch.cuda.synchronize()
+        e0_, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0_.record()
+        res = sol.solve()
+        e1_.record()
+        torch.cuda.synchronize()
+        ms = e0_.elapsed_time(e1_)
+        its = max(res["iterations"], 1)
+        x = sol.solution()["x"]
+        out.append({"k": k, "N": qp.base.N, "status": res["status"], "iterations": res["iterations"],
+                    "e0": res["e0"], "ms_per_iteration": ms / its,
+                    "newton_step_ms_mean": float(np.mean(res["newton_ms"])) if res["newton_ms"] else None,
+                    "newton_step_fp64_frac_of_peak": ((qp.base.N ** 3 / 3.0) / (float(np.mean(res["newton_ms"])) * 1e-3)
+                                                      / 1e12 / fp64_peak()[0]) if res["newton_ms"] else None,
+                    "max_abs_x_minus_closed_form": float(np.abs(x - 0.5).max()),
+                    "paper_context": ("V100 MAGMA 4.49 s / iteration at matrix size 16,000 (P:541)" if k == 8000 else
+                                      ("V100 peak 4.2 TF/s at 20,000 (P:634)" if k == 10000 else None))})
+        del sol
+        torch.cuda.empty_cache()
+    return out
 
 
 def run_c5(args, rank, world):

@@ -454,3 +454,52 @@ def qp_config(cfg: str, seed: Optional[int] = None, pattern="uniform"):
     if seed is None:
         seed = 1000 * int(cfg[1:]) + 500
     return qp_problem(shp["n_s"], shp["n_d"], shp["m_E"], shp["m_I"], seed, pattern=pattern)
+
+
+def synthetic_problem(k: int):
+    """The paper's mini-app problem nlpMDS_ex4 ("a convex optimization
+    problem with m = n_s + 3 constraints ... n_d = n_s = k ... compressed matrix of
+    size (2k+3) x (2k+3)"), with the model of SPEC.md:288-297:
+      f = 1/2 sum (x_s,i - 1)^2 + 1/2 x_d^T (I + e e^T / k) x_d - e^T x_d
+      (1/k) sum x_s + (1/k) sum x_d = 1,   x_s,1 - x_d,1 = 0                  (m_E = 2)
+      x_s,i + (1/k) sum_j x_d,j <= 2  (i = 1..k),  0.5 <= (1/k) sum_j x_d,j <= 3  (m_I = k + 1)
+      -10 <= x_s, x_d <= 10
+    as a QPProblem in MDS form (J_s rows = sparse variables, reading R1; the constant
+    k/2 of f dropped).  x_star is the interior start x_s = 0.5, x_d = 1 (slacks
+    strictly inside their bounds; the equalities are not satisfied there)."""
+    if k < 1:
+        raise ValueError("k >= 1")
+    n_s = n_d = k
+    m_E, m_I = 2, k + 1
+    m = m_E + m_I
+    rows, cols, vals = [], [], []
+    for i in range(k):
+        ent = [(0, 1.0 / k)]
+        if i == 0:
+            ent.append((1, 1.0))
+        ent.append((2 + i, 1.0))
+        for c, v in ent:
+            rows.append(i)
+            cols.append(c)
+            vals.append(v)
+    rowptr = np.zeros(n_s + 1, dtype=np.int64)
+    np.add.at(rowptr, np.asarray(rows) + 1, 1)
+    rowptr = np.cumsum(rowptr).astype(np.int32)
+    colidx = np.asarray(cols, dtype=np.int32)
+    val = np.asarray(vals, dtype=np.float64)
+    H = np.asfortranarray(np.eye(n_d) + np.full((n_d, n_d), 1.0 / k))
+    J_d = np.zeros((m, n_d), order="F")
+    J_d[0, :] = 1.0 / k
+    J_d[1, 0] = -1.0
+    J_d[2:, :] = 1.0 / k
+    base = MDSProblem(n_s, n_d, m_E, m_I, rowptr, colidx, val, np.ones(n_s), np.zeros(n_s), H, np.zeros(n_d),
+                      J_d, np.ones(m_I), 0.0, 0.0, np.zeros(n_s + n_d + m),
+                      meta=dict(gen="nlpMDS_ex4", k=k))
+    c = np.concatenate([-np.ones(n_s), -np.ones(n_d)])
+    g_E = np.array([1.0, 0.0])
+    h_l = np.concatenate([np.full(k, -INF), [0.5]])
+    h_u = np.concatenate([np.full(k, 2.0), [3.0]])
+    lo = np.full(n_s + n_d, -10.0)
+    up = np.full(n_s + n_d, 10.0)
+    start = np.concatenate([np.full(n_s, 0.5), np.full(n_d, 1.0)])
+    return QPProblem(base, c, g_E, h_l, h_u, lo, up, start)

@@ -43,3 +43,15 @@ def test_device_ipm_matches_oracle(shape, seed, pattern):
     assert np.abs(J[:m_E] @ out["x"] - qp.g_E).max(initial=0.0) <= 1e-7
     assert np.abs(J[m_E:] @ out["x"] - out["s"]).max(initial=0.0) <= 1e-7
     assert all(h["inertia"] == (qp.base.n_d, 0, qp.base.m) for h in res["history"])
+
+
+@pytest.mark.parametrize("k", [2, 10, 100, 1000])
+def test_device_ipm_nlpmds_ex4(k):
+    # the paper's mini-app problem: compressed size 2k+3, optimum x = 1/2 (closed form)
+    qp = mdsgen.synthetic_problem(k)
+    ref = oipm.solve(qp)
+    sol = IPMSolver(qp)
+    res = sol.solve()
+    assert res["status"] == ref["status"] == "Optimal"
+    assert res["iterations"] == ref["iterations"]
+    assert np.abs(sol.solution()["x"] - 0.5).max() <= 1e-7

@@ -95,3 +95,22 @@ def test_barrier_update_spec_example():
     mu = 0.1
     new = max(1e-6 / 10.0, min(o["kappa_mu"] * mu, mu ** o["theta_mu"]))   # SPEC.md:451 (tol = 1e-6)
     assert new == pytest.approx(0.02)
+
+
+def test_nlpmds_ex4_structure():
+    # PAPER.md:536 / SPEC.md:288-297: n_d = n_s = k, m = n_s + 3, compressed size 2k + 3
+    for k in (1, 10, 100):
+        q = mdsgen.synthetic_problem(k)
+        b = q.base
+        assert b.n_d == b.n_s == k and b.m == k + 3 and b.N == 2 * k + 3
+
+
+@pytest.mark.parametrize("k", [2, 10, 100])
+def test_nlpmds_ex4_closed_form_optimum(k):
+    # closed form: x_d's unconstrained minimiser solves (I + ee^T/k) x_d = e -> x_d = e/2, which meets
+    # the active bound mean(x_d) >= 1/2 with multiplier k/2 > 0; the first equality then forces
+    # mean(x_s) = 1/2 and stationarity in x_s (x_s - 1 + y0/k = 0 with y0 = k/2) gives x_s = e/2
+    q = mdsgen.synthetic_problem(k)
+    res = ipm.solve(q)
+    assert res["status"] == "Optimal"
+    assert np.abs(res["x"] - 0.5).max() <= 1e-7
