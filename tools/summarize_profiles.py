@@ -57,24 +57,45 @@ def launch_summary():
             f.write(f"{k},{cnt[k] / steps:.1f},{tot[k] / steps:.1f},{tot[k] / total:.4f}\n")
 
 
+SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3,
+         "second": 1e6}
+
+
+def norm(v, unit):
+    """ncu --page raw values carry per-metric units (bytes in byte/Kbyte/Mbyte/..., times in
+    nsecond/usecond/...): normalise bytes to bytes and times to microseconds."""
+    v = v.replace(",", "")
+    if unit in SCALE and v:
+        try:
+            return f"{float(v) * SCALE[unit]:.6g}"
+        except ValueError:
+            return v
+    return v
+
+
 def full_summary(rep, out):
     path = os.path.join(src, rep)
     if not os.path.exists(path):
         return
     rows = list(csv.reader(open(path)))
-    hdr = rows[0]
+    hdr, units = rows[0], rows[1]
     body = [r for r in rows[2:] if len(r) == len(hdr)]
+    unit_of = dict(zip(hdr, units))
+    cols = [k + (" [bytes]" if unit_of.get(k, "").endswith("byte") else (" [us]" if unit_of.get(k, "").endswith("second")
+                                                                         else "")) for k in KEYS]
     with open(os.path.join(dst, out), "w") as f:
-        f.write("kernel," + ",".join(KEYS) + "\n")
+        f.write("kernel," + ",".join(cols) + "\n")
         for r in body:
             d = dict(zip(hdr, r))
             f.write(short(d.get("Kernel Name", "?")).replace(",", ";") + "," +
-                    ",".join(d.get(k, "").replace(",", "") for k in KEYS) + "\n")
+                    ",".join(norm(d.get(k, ""), unit_of.get(k, "")) for k in KEYS) + "\n")
 
 
 launch_summary()
 for rep, out in [("upd_full_raw.csv", f"ncu_k_update_tma_{tag}.csv"), ("misc_full_raw.csv", f"ncu_misc_{tag}.csv"),
                  ("exact_full_raw.csv", f"ncu_k_panel_exact_{tag}.csv"),
-                 ("solve_full_raw.csv", f"ncu_solve_vectors_{tag}.csv")]:
+                 ("solve_full_raw.csv", f"ncu_solve_vectors_{tag}.csv"),
+                 ("cond_full_raw.csv", f"ncu_condense_{tag}.csv"), ("batched_full_raw.csv", f"ncu_batched_{tag}.csv"),
+                 ("ipm_full_raw.csv", f"ncu_ipm_{tag}.csv")]:
     full_summary(rep, out)
 print("\n".join(sorted(os.listdir(dst))))
