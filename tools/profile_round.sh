@@ -30,4 +30,7 @@ ncu -i gpurun_out/cond_full.ncu-rep --page raw --csv > gpurun_out/cond_full_raw.
 OZB=64 OZ=0 ncu --set full --clock-control none -k regex:"k_update_tma|k_condense_tiles" --launch-skip 20 --launch-count 3 \
     -o gpurun_out/batched_full -f python tools/oz_prof.py > /dev/null 2>&1
 ncu -i gpurun_out/batched_full.ncu-rep --page raw --csv > gpurun_out/batched_full_raw.csv
+# keep the merged-back payload under gpurun's 64 MiB: the raw CSVs are what summarize_profiles reads
+rm -f gpurun_out/misc_full.ncu-rep gpurun_out/exact_full.ncu-rep gpurun_out/solve_full.ncu-rep \
+      gpurun_out/cond_full.ncu-rep gpurun_out/batched_full.ncu-rep
 ls -la gpurun_out
