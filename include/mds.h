@@ -121,8 +121,11 @@ int mds_condense(const mds_plan *plan, const double *js_val, const double *h_ss,
  * ELEMENTS; H_dd / J_d / M keep their leading dimensions inside a scenario).
  * delta_w, delta_c: DEVICE arrays [batch] (NULL = 0).  status: device int32
  * [batch] (scenario s writes only status[s]; one failing scenario does not
- * affect the others).  anorm_out: device [batch] or NULL.  One launch sequence
- * for the whole batch (tiles of all scenarios share one work queue).
+ * affect the others).  anorm_out: device [batch] or NULL.  active: device int32
+ * [batch] or NULL (all): scenarios with active[s] == 0 are left untouched (their M,
+ * rhs_c, w, anorm, status keep their values) -- the inertia-correction loop
+ * re-condenses only its failing scenarios.  One launch sequence for the whole
+ * batch (tiles of all scenarios share one work queue).
  * work >= mds_condense_workspace_size(plan, batch). */
 int mds_condense_batched(const mds_plan *plan, int64_t batch,
                          const double *js_val, int64_t str_val,
@@ -135,7 +138,7 @@ int mds_condense_batched(const mds_plan *plan, int64_t batch,
                          const double *r, int64_t str_r,
                          double *M, int64_t ldm, int64_t str_M,
                          double *rhs_c, int64_t str_rhs, double *w_out, int64_t str_w,
-                         double *anorm_out, int32_t *status,
+                         double *anorm_out, int32_t *status, const int32_t *active,
                          void *work, size_t work_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------
@@ -178,12 +181,14 @@ int mds_factor(int64_t N, double *M, int64_t ldm, int32_t *piv, double zero_tol,
  * inertia_dev[s], status[s] (device arrays [batch]); anorm: device [batch]
  * (mds_condense_batched's anorm_out) or NULL (each M is scanned).  One
  * non-finite scenario aborts only itself (status[s] = NONFINITE, identity
- * permutation).  Same factor format and pivot rule as mds_factor.  Never
+ * permutation).  active: device int32 [batch] or NULL (all); scenarios with
+ * active[s] == 0 keep their factorization, piv, inertia and tolerance (requires
+ * anorm != NULL).  Same factor format and pivot rule as mds_factor.  Never
  * synchronises.  work >= mds_factor_batched_workspace_size(N, batch). */
 size_t mds_factor_batched_workspace_size(int64_t N, int64_t batch);
 int mds_factor_batched(int64_t batch, int64_t N, double *M, int64_t ldm, int64_t str_M, int32_t *piv,
                        int64_t str_piv, double zero_tol, const double *anorm, mds_inertia *inertia_dev,
-                       int32_t *status, void *work, size_t work_bytes, void *stream);
+                       int32_t *status, const int32_t *active, void *work, size_t work_bytes, void *stream);
 /* ||M||_inf and the zero-pivot tolerance the last mds_factor on `work` used
  * (host copies; synchronous).  For the parity tests of reading R4. */
 int mds_factor_tol(const void *work, double *anorm_host, double *tol_host);
@@ -282,6 +287,68 @@ int mds_kkt_residual(const mds_plan *plan, const double *js_val, const double *h
                      const double *H_dd, int64_t ldh, const double *sigma_d, const double *J_d, int64_t ldj,
                      const double *d_h, double delta_w, double delta_c, const double *x, const double *b,
                      double *out, double *rnorm, void *work, size_t work_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Inertia correction of a scenario batch on the device (
+ * PAPER.md:161, 191; the multiples of the cited Algorithm IC, R22).
+ * Per scenario a state machine advanced once per trial round by
+ * mds_ic_step_batched from the trial's inertia and status: phase 0 = the (0,0)
+ * trial was evaluated, 1 = a delta_w > 0 trial was evaluated, 2 = accepted,
+ * 3 = failed (delta_w > delta_w_max: singular; the step writes MDS_ERR_SINGULAR
+ * into status[s], so the solve and step vectors skip the scenario), 4 = data
+ * error (status[s] already set by the trial).  active[s] = 1
+ * exactly when scenario s needs another trial (delta_w[s], delta_c[s] set for
+ * it); *any_active = OR over the batch.  The batched condense / factor take
+ * `active` as their mask, so only failing scenarios are re-factored.  All
+ * arrays are device [batch]; delta_w_last persists across Newton iterations
+ * (warm start), the rest is reset by mds_ic_begin_batched (phase 0, active 1,
+ * delta 0, ntrial 1).  mu: device [batch] or NULL (then the scalar).
+ * mds_ic_graph_create captures the whole loop -- reset, first trial of every
+ * scenario, step, then a CUDA-graph conditional WHILE node whose body is
+ * (masked condense, masked factor, step) and whose condition the step kernel
+ * sets with cudaGraphSetConditional -- into one graph; mds_ic_graph_launch runs
+ * it on a stream: no host round trip per trial. */
+typedef struct {
+  double delta_w0, delta_w_min, delta_w_max, kappa_w_plus, kappa_w_plus_first, kappa_w_minus, delta_c_bar, kappa_c;
+} mds_ic_params;
+typedef struct {
+  double *delta_w, *delta_c, *delta_w_last;
+  int32_t *phase, *active, *ntrial, *any_active;
+} mds_ic_state;
+typedef struct {
+  int64_t batch;
+  const double *js_val; int64_t str_val;
+  const double *h_ss; int64_t str_hss;
+  const double *sigma_s; int64_t str_sig;
+  const double *H_dd; int64_t ldh, str_H;
+  const double *sigma_d; int64_t str_sd;
+  const double *J_d; int64_t ldj, str_J;
+  const double *d_h; int64_t str_dh;
+  const double *r; int64_t str_r;
+  double *M; int64_t ldm, str_M;
+  double *rhs_c; int64_t str_rhs;
+  double *w_out; int64_t str_w;
+  double *anorm_out;
+  int32_t *status;
+  void *work; size_t work_bytes;
+} mds_condense_batched_args;
+typedef struct {
+  int64_t batch, N;
+  int32_t *piv; int64_t str_piv;
+  double zero_tol;
+  mds_inertia *inertia_dev;
+  void *work; size_t work_bytes;
+} mds_factor_batched_args;
+typedef struct mds_ic_graph mds_ic_graph;
+int mds_ic_begin_batched(int64_t batch, const mds_ic_state *st, void *stream);
+int mds_ic_step_batched(int64_t batch, int64_t n_d, int64_t m, const mds_inertia *inertia, int32_t *status,
+                        const double *mu_arr, double mu, const mds_ic_params *params, const mds_ic_state *st,
+                        void *stream);
+int mds_ic_graph_create(const mds_plan *plan, const mds_condense_batched_args *ca, const mds_factor_batched_args *fa,
+                        int64_t n_d, int64_t m, const double *mu_arr, double mu, const mds_ic_params *params,
+                        const mds_ic_state *st, mds_ic_graph **out);
+int mds_ic_graph_launch(mds_ic_graph *graph, void *stream);
+int mds_ic_graph_destroy(mds_ic_graph *graph);
 
 /* ---------------------------------------------------------------------------
  * Interior-point loop vector kernels (K1 "axpy" + the filter line search's

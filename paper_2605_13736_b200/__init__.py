@@ -38,7 +38,7 @@ _lib.mds_condense_workspace_size.restype = ctypes.c_size_t
 _lib.mds_condense_workspace_size.argtypes = [_P, _I64]
 _lib.mds_condense_batched.argtypes = ([_P, _I64] + [_P, _I64] * 3 + [_P, _I64, _I64] + [_P, _I64] + [_P, _I64, _I64] +
                                       [_P, _I64] + [_P, _P] + [_P, _I64] + [_P, _I64, _I64] + [_P, _I64] * 2 +
-                                      [_P, _P, _P, ctypes.c_size_t, _P])
+                                      [_P, _P, _P, _P, ctypes.c_size_t, _P])
 _lib.mds_condense_batched.restype = ctypes.c_int
 _lib.mds_factor_tol.argtypes = [_P, _P, _P]
 _lib.mds_factor_tol.restype = ctypes.c_int
@@ -64,7 +64,7 @@ for _f in ("mds_plan_create", "mds_plan_destroy", "mds_plan_dims", "mds_condense
 
 _lib.mds_factor_batched_workspace_size.restype = ctypes.c_size_t
 _lib.mds_factor_batched_workspace_size.argtypes = [_I64, _I64]
-_lib.mds_factor_batched.argtypes = [_I64, _I64, _P, _I64, _I64, _P, _I64, _D, _P, _P, _P, _P, ctypes.c_size_t, _P]
+_lib.mds_factor_batched.argtypes = [_I64, _I64, _P, _I64, _I64, _P, _I64, _D, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]
 _lib.mds_factor_batched.restype = ctypes.c_int
 _lib.mds_solve_batched_workspace_size.restype = ctypes.c_size_t
 _lib.mds_solve_batched_workspace_size.argtypes = [_I64, _I64]
@@ -97,7 +97,9 @@ EXPORTS = ["mds_condense_workspace_size", "mds_condense_batched", "mds_factor_to
            "mds_profile_end", "mds_factor_panels", "mds_factor_set_grid_cap", "mds_profile_timeline", "mds_set_variant",
            "mds_factor_batched_workspace_size", "mds_factor_batched", "mds_solve_batched_workspace_size",
            "mds_solve_batched", "ipm_step_vectors_batched_workspace_size", "ipm_step_vectors_batched",
-           "ipm_workspace_size", "ipm_rhs", "ipm_directions", "ipm_reduce", "ipm_apply", "mds_factor_stats"]
+           "ipm_workspace_size", "ipm_rhs", "ipm_directions", "ipm_reduce", "ipm_apply", "mds_factor_stats",
+           "mds_ic_begin_batched", "mds_ic_step_batched", "mds_ic_graph_create", "mds_ic_graph_launch",
+           "mds_ic_graph_destroy"]
 
 PROF_CLASSES = ["condense_rows", "condense_norm", "condense_tiles", "anorm", "panel_diag", "panel_trsm", "panel_store",
                 "panel_exact", "update", "finalize", "solve_gather", "solve_fwd", "solve_d", "solve_bwd",
@@ -214,7 +216,7 @@ def condense(plan: Plan, js_val, h_ss, sigma_s, H_dd, ldh, sigma_d, J_d, ldj, d_
 
 
 def condense_batched(plan: Plan, batch, js_val, h_ss, sigma_s, H_dd, ldh, sigma_d, J_d, ldj, d_h, delta_w, delta_c,
-                     r, M, ldm, rhs_c, w_out, anorm_out, status, work, strides, stream=None):
+                     r, M, ldm, rhs_c, w_out, anorm_out, status, work, strides, stream=None, active=None):
     """mds_condense_batched: `strides` = dict of per-scenario element strides with keys
     val, hss, sig, H, sd, J, dh, r, M, rhs, w (every array is base + s * stride)."""
     st = strides
@@ -223,7 +225,7 @@ def condense_batched(plan: Plan, batch, js_val, h_ss, sigma_s, H_dd, ldh, sigma_
         int(st["sig"]), _f64(H_dd), int(ldh), int(st["H"]), _f64(sigma_d), int(st["sd"]), _f64(J_d), int(ldj),
         int(st["J"]), _f64(d_h), int(st["dh"]), _f64(delta_w), _f64(delta_c), _f64(r), int(st["r"]), _f64(M),
         int(ldm), int(st["M"]), _f64(rhs_c), int(st["rhs"]), _f64(w_out), int(st["w"]), _f64(anorm_out),
-        _ptr(status), _ptr(work), work.numel() * work.element_size(), _stream(stream))
+        _ptr(status), _ptr(active), _ptr(work), work.numel() * work.element_size(), _stream(stream))
     _check(code, "mds_condense_batched")
 
 
@@ -268,12 +270,12 @@ def step_vectors_batched_workspace_size(n, batch):
 
 
 def factor_batched(batch, N, M, ldm, str_M, piv, str_piv, zero_tol, inertia_dev, status, work, anorm=None,
-                   stream=None):
+                   stream=None, active=None):
     """mds_factor_batched: `batch` factorizations in one launch sequence (never syncs).
     inertia_dev: int64 [batch, 3]; status: int32 [batch]; anorm: FP64 [batch] or None."""
     code = _lib.mds_factor_batched(int(batch), int(N), _f64(M), int(ldm), int(str_M), _ptr(piv), int(str_piv),
-                                   float(zero_tol), _f64(anorm), _ptr(inertia_dev), _ptr(status), _ptr(work),
-                                   work.numel() * work.element_size(), _stream(stream))
+                                   float(zero_tol), _f64(anorm), _ptr(inertia_dev), _ptr(status), _ptr(active),
+                                   _ptr(work), work.numel() * work.element_size(), _stream(stream))
     _check(code, "mds_factor_batched")
 
 
@@ -382,6 +384,66 @@ def ipm_apply(n, m_E, m_I, P, zl, zu, y, xy, dP, dzl, dzu, dy, lo, up, alpha, al
     _check(_lib.ipm_apply(int(n), int(m_E), int(m_I), _f64(P), _f64(zl), _f64(zu), _f64(y), _f64(xy), _f64(dP),
                           _f64(dzl), _f64(dzu), _f64(dy), _f64(lo), _f64(up), float(alpha), float(alpha_d),
                           float(mu), float(kappa_sigma), _stream(stream)), "ipm_apply")
+
+
+class ICParamsC(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("delta_w0", "delta_w_min", "delta_w_max", "kappa_w_plus",
+                                              "kappa_w_plus_first", "kappa_w_minus", "delta_c_bar", "kappa_c")]
+
+
+class ICStateC(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("delta_w", "delta_c", "delta_w_last", "phase", "active", "ntrial",
+                                              "any_active")]
+
+
+class CondenseBatchedArgsC(ctypes.Structure):
+    _fields_ = [("batch", _I64), ("js_val", _P), ("str_val", _I64), ("h_ss", _P), ("str_hss", _I64),
+                ("sigma_s", _P), ("str_sig", _I64), ("H_dd", _P), ("ldh", _I64), ("str_H", _I64), ("sigma_d", _P),
+                ("str_sd", _I64), ("J_d", _P), ("ldj", _I64), ("str_J", _I64), ("d_h", _P), ("str_dh", _I64),
+                ("r", _P), ("str_r", _I64), ("M", _P), ("ldm", _I64), ("str_M", _I64), ("rhs_c", _P),
+                ("str_rhs", _I64), ("w_out", _P), ("str_w", _I64), ("anorm_out", _P), ("status", _P), ("work", _P),
+                ("work_bytes", ctypes.c_size_t)]
+
+
+class FactorBatchedArgsC(ctypes.Structure):
+    _fields_ = [("batch", _I64), ("N", _I64), ("piv", _P), ("str_piv", _I64), ("zero_tol", ctypes.c_double),
+                ("inertia_dev", _P), ("work", _P), ("work_bytes", ctypes.c_size_t)]
+
+
+_lib.mds_ic_begin_batched.argtypes = [_I64, _P, _P]
+_lib.mds_ic_step_batched.argtypes = [_I64, _I64, _I64, _P, _P, _P, _D, _P, _P, _P]
+_lib.mds_ic_graph_create.argtypes = [_P, _P, _P, _I64, _I64, _P, _D, _P, _P, ctypes.POINTER(ctypes.c_void_p)]
+_lib.mds_ic_graph_launch.argtypes = [_P, _P]
+_lib.mds_ic_graph_destroy.argtypes = [_P]
+for _f in ("mds_ic_begin_batched", "mds_ic_step_batched", "mds_ic_graph_create", "mds_ic_graph_launch",
+           "mds_ic_graph_destroy"):
+    getattr(_lib, _f).restype = ctypes.c_int
+
+
+def ic_begin_batched(batch, state, stream=None):
+    _check(_lib.mds_ic_begin_batched(int(batch), ctypes.byref(state), _stream(stream)), "mds_ic_begin_batched")
+
+
+def ic_step_batched(batch, n_d, m, inertia_dev, status, mu, params, state, mu_arr=None, stream=None):
+    _check(_lib.mds_ic_step_batched(int(batch), int(n_d), int(m), _ptr(inertia_dev), _ptr(status), _f64(mu_arr),
+                                    float(mu), ctypes.byref(params), ctypes.byref(state), _stream(stream)),
+           "mds_ic_step_batched")
+
+
+def ic_graph_create(plan, cargs, fargs, n_d, m, mu, params, state, mu_arr=None):
+    h = ctypes.c_void_p()
+    _check(_lib.mds_ic_graph_create(plan.handle, ctypes.byref(cargs), ctypes.byref(fargs), int(n_d), int(m),
+                                    _f64(mu_arr), float(mu), ctypes.byref(params), ctypes.byref(state),
+                                    ctypes.byref(h)), "mds_ic_graph_create")
+    return h
+
+
+def ic_graph_launch(h, stream=None):
+    _check(_lib.mds_ic_graph_launch(h, _stream(stream)), "mds_ic_graph_launch")
+
+
+def ic_graph_destroy(h):
+    _check(_lib.mds_ic_graph_destroy(h), "mds_ic_graph_destroy")
 
 
 def set_grid_cap(ctas: int):

@@ -18,7 +18,8 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from . import (Plan, DevPtr, condense_batched, factor_batched, solve_batched, step_vectors_batched,
+from . import (Plan, DevPtr, ICParamsC, ICStateC, CondenseBatchedArgsC, FactorBatchedArgsC, ic_begin_batched,
+               ic_step_batched, ic_graph_create, ic_graph_launch, ic_graph_destroy, condense_batched, factor_batched, solve_batched, step_vectors_batched,
                condense_workspace_size, factor_batched_workspace_size, solve_batched_workspace_size,
                step_vectors_batched_workspace_size)
 
@@ -138,6 +139,101 @@ class BatchedKKTStep:
             step_vectors_batched(B, self.nb, W, s["x"], dirn, s["lo"], s["up"], s["zl"],
                                  s["zu"], s["dzl"], s["dzu"], 0.0, 0.0, self.vout, VOUT, self.sigma, self.status,
                                  self.vwork, tau_arr=self.tau, mu_arr=self.mu, res=(self.r,),
+                                 res_str=((self.r.shape[1], self.r.shape[1]),), stream=stream)
+
+    # -- inertia correction on the device (NEXT-1) ---------------------------
+    def _ic_setup(self, params=None):
+        if getattr(self, "_ic", None) is not None:
+            return self._ic
+        from .inertia import ICParams
+        p = params or ICParams()
+        B, dev = self.B, self.M.device
+        st = dict(delta_w_last=torch.zeros(B, dtype=torch.float64, device=dev),
+                  phase=torch.zeros(B, dtype=torch.int32, device=dev),
+                  active=torch.ones(B, dtype=torch.int32, device=dev),
+                  ntrial=torch.zeros(B, dtype=torch.int32, device=dev),
+                  any_active=torch.zeros(1, dtype=torch.int32, device=dev))
+        cst = ICStateC(self.delta_w.data_ptr(), self.delta_c.data_ptr(), st["delta_w_last"].data_ptr(),
+                       st["phase"].data_ptr(), st["active"].data_ptr(), st["ntrial"].data_ptr(),
+                       st["any_active"].data_ptr())
+        cpar = ICParamsC(p.delta_w0, p.delta_w_min, p.delta_w_max, p.kappa_w_plus, p.kappa_w_plus_first,
+                         p.kappa_w_minus, p.delta_c_bar, p.kappa_c)
+        self._ic = dict(st, cstate=cst, cparams=cpar, graph=None, graph_mu=None)
+        return self._ic
+
+    def _strides(self):
+        return dict(val=self.val.shape[1], hss=self.h_ss.shape[1], sig=self.sigma_s.shape[1], H=self.H_dd.shape[1],
+                    sd=self.sigma_d.shape[1], J=self.J_d.shape[1], dh=self.d_h.shape[1], r=self.r.shape[1],
+                    M=self.M.shape[1], rhs=self.rhs.shape[1], w=self.w.shape[1])
+
+    def _trial(self, active, stream=None):
+        B, N = self.B, self.N
+        condense_batched(self.plan, B, self.val, self.h_ss, self.sigma_s, self.H_dd, self.ldh, self.sigma_d, self.J_d,
+                         self.ldj, self.d_h, self.delta_w, self.delta_c, self.r, self.M, self.ldm, self.rhs, self.w,
+                         self.anorm, self.status, self.cwork, self._strides(), stream=stream, active=active)
+        factor_batched(B, N, self.M, self.ldm, self.M.shape[1], self.piv, self.piv.shape[1], self.zero_tol,
+                       self.inertia, self.status, self.fwork, anorm=self.anorm, stream=stream, active=active)
+
+    def factor_ic(self, mu, mode="graph", params=None, stream=None):
+        """Condense + factor every scenario with the inertia correction of PAPER.md:161 on the
+        device: failing scenarios (inertia != (n_d, 0, m)) are regularised with the next
+        delta_w / delta_c of Algorithm IC and re-condensed / re-factored -- only they (mask) --
+        until every scenario is accepted, failed (singular) or in error.  mode "graph": the
+        whole loop is one CUDA graph with a conditional WHILE node (no host round trip);
+        "host": the same kernels with one 4-byte read of any_active per round."""
+        ic = self._ic_setup(params)
+        B = self.B
+        self.status.zero_()
+        if mode == "graph":
+            if ic["graph"] is None or ic["graph_mu"] != float(mu):
+                if ic["graph"] is not None:
+                    ic_graph_destroy(ic["graph"])
+                self._trial(None, stream)          # warm-up (attributes, maps) outside capture
+                ca = CondenseBatchedArgsC(B, self.val.data_ptr(), self.val.shape[1], self.h_ss.data_ptr(),
+                                          self.h_ss.shape[1], self.sigma_s.data_ptr(), self.sigma_s.shape[1],
+                                          self.H_dd.data_ptr(), self.ldh, self.H_dd.shape[1], self.sigma_d.data_ptr(),
+                                          self.sigma_d.shape[1], self.J_d.data_ptr(), self.ldj, self.J_d.shape[1],
+                                          self.d_h.data_ptr(), self.d_h.shape[1], self.r.data_ptr(), self.r.shape[1],
+                                          self.M.data_ptr(), self.ldm, self.M.shape[1], self.rhs.data_ptr(),
+                                          self.rhs.shape[1], self.w.data_ptr(), self.w.shape[1],
+                                          self.anorm.data_ptr(), self.status.data_ptr(), self.cwork.data_ptr(),
+                                          self.cwork.numel())
+                fa = FactorBatchedArgsC(B, self.N, self.piv.data_ptr(), self.piv.shape[1], self.zero_tol,
+                                        self.inertia.data_ptr(), self.fwork.data_ptr(), self.fwork.numel())
+                torch.cuda.synchronize()
+                ic["graph"] = ic_graph_create(self.plan, ca, fa, self.n_d, self.m, mu, ic["cparams"], ic["cstate"])
+                ic["graph_mu"] = float(mu)
+                self.status.zero_()
+            ic_graph_launch(ic["graph"], stream)
+        else:
+            ic_begin_batched(B, ic["cstate"], stream)
+            self._trial(None, stream)
+            ic_step_batched(B, self.n_d, self.m, self.inertia, self.status, mu, ic["cparams"], ic["cstate"],
+                            stream=stream)
+            while int(ic["any_active"].item()) != 0:
+                self._trial(ic["active"], stream)
+                ic_step_batched(B, self.n_d, self.m, self.inertia, self.status, mu, ic["cparams"], ic["cstate"],
+                                stream=stream)
+
+    def ic_results(self):
+        """(phase, ntrial, delta_w, delta_c) per scenario after factor_ic (synchronous)."""
+        ic = self._ic
+        return (ic["phase"].cpu().numpy(), ic["ntrial"].cpu().numpy(), self.delta_w.cpu().numpy(),
+                self.delta_c.cpu().numpy())
+
+    def finish(self, stream=None):
+        """Solve + recovery + step vectors on the factorization left by factor_ic / run."""
+        B, N, n_s = self.B, self.N, self.n_s
+        dirn, W = self.dirn, self.dirn.shape[1]
+        solve_batched(self.plan, B, N, self.M, self.ldm, self.M.shape[1], self.piv, self.piv.shape[1], self.rhs,
+                      self.rhs.shape[1], self.val, self.val.shape[1], self.w, self.w.shape[1], self.r,
+                      self.r.shape[1], DevPtr(dirn, n_s), W, DevPtr(dirn) if n_s else None, W, self.zero_tol,
+                      self.fwork, self.status, self.swork, stream=stream)
+        if self.sv is not None:
+            s = self.sv
+            step_vectors_batched(B, self.nb, W, s["x"], dirn, s["lo"], s["up"], s["zl"], s["zu"], s["dzl"],
+                                 s["dzu"], 0.0, 0.0, self.vout, VOUT, self.sigma, self.status, self.vwork,
+                                 tau_arr=self.tau, mu_arr=self.mu, res=(self.r,),
                                  res_str=((self.r.shape[1], self.r.shape[1]),), stream=stream)
 
     def capture(self, warmup=1):

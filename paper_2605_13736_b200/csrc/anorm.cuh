@@ -63,6 +63,7 @@ struct NormOut {
   int32_t* status;
   int64_t status_stride;
   double zero_tol;
+  const int32_t* active;   // [batch] or NULL: matrices with active[s] == 0 are skipped
 };
 
 // Per-thread share of a tile's partials.  Thread layout used by every owner:
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(256) k_anorm_rows(int64_t N, char* parts, size
   pdl_wait();
   pdl_trigger();
   const int64_t ms = blockIdx.y;
+  if (o.active && !o.active[ms]) return;
   const Parts P = parts_at(parts + ms * parts_stride, N);
   const int64_t nb = (N + AT - 1) / AT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

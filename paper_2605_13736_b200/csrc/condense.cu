@@ -243,6 +243,7 @@ namespace {
 // the single-system call uses batch = 1 and strides 0.
 struct CondArgs {
   int64_t n_s, n_d, m_E, m, N, nnz, ntile, nitems, batch;
+  const int32_t* active;                // [batch] or NULL: scenarios with active[s] == 0 are left untouched
   const int32_t* rowptr;
   const int32_t* tptr;
   const int2* tkp;
@@ -336,6 +337,7 @@ __global__ void __launch_bounds__(256) k_condense_rows(CondArgs a) {
   const unsigned long long pol_keep = pol_evict_last();
   for (int64_t g = gw; g < a.batch * nblk; g += nw) {
     const int64_t s = g / nblk, k0 = (g - s * nblk) * 32;
+    if (a.active && !a.active[s]) continue;
     const int64_t k = k0 + lane;
     const int nrow = (int)min((int64_t)32, a.n_s - k0);
     double wk = 0.0;
@@ -381,6 +383,7 @@ __global__ void __launch_bounds__(256) k_condense_diag(CondArgs a) {
   pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int64_t s = blockIdx.y;
+  if (a.active && !a.active[s]) return;
   const int64_t c = blockIdx.x * 8ll + (threadIdx.x >> 5);
   const double* r = a.r ? a.r + s * a.s_r : nullptr;
   double* rhs = (a.rhs && r) ? a.rhs + s * a.s_rhs : nullptr;
@@ -550,6 +553,7 @@ __global__ void __launch_bounds__(CW * 32, 4) k_condense_tiles(CondArgs a) {
     } else {
       s = g % a.batch;
       ij = a.order[g / a.batch];
+      if (a.active && !a.active[s]) continue;   // (uniform across the CTA)
     }
     const int64_t I = ij >> 16, J = ij & 0xffff;
     const int64_t tile = anorm::tile_id(I, J);
@@ -737,6 +741,7 @@ static int condense_launch(const mds_plan* P, CondArgs& a, void* work, size_t wo
   if (norm) {
     anorm::NormOut o = {};
     o.anorm = a.anorm;
+    o.active = a.active;
     MDS_LAUNCH(PC_CONDENSE_DENSE, st, MDS_CUDA_TRY(anorm::launch_rows(N, a.parts, a.parts_stride, o, a.batch, st)));
   }
   return MDS_OK;
@@ -766,7 +771,7 @@ extern "C" int mds_condense_batched(const mds_plan* P, int64_t batch,
                                     const double* r, int64_t str_r,
                                     double* M, int64_t ldm, int64_t str_M,
                                     double* rhs_c, int64_t str_rhs, double* w_out, int64_t str_w,
-                                    double* anorm_out, int32_t* status,
+                                    double* anorm_out, int32_t* status, const int32_t* active,
                                     void* work, size_t work_bytes, void* stream) {
   if (!P || batch < 0) return MDS_ERR_ARG;
   if (batch == 0) return MDS_OK;
@@ -778,6 +783,6 @@ extern "C" int mds_condense_batched(const mds_plan* P, int64_t batch,
   a.Jd = J_d; a.ldj = ldj; a.s_J = str_J; a.d_h = d_h; a.s_dh = str_dh;
   a.dw_arr = delta_w; a.dc_arr = delta_c; a.r = r; a.s_r = str_r;
   a.M = M; a.ldm = ldm; a.s_M = str_M; a.rhs = rhs_c; a.s_rhs = str_rhs; a.w = w_out; a.s_w = str_w;
-  a.anorm = anorm_out; a.status = status; a.s_st = 1;
+  a.anorm = anorm_out; a.status = status; a.s_st = 1; a.active = active;
   return condense_launch(P, a, work, work_bytes, (cudaStream_t)stream);
 }

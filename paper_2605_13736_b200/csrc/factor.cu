@@ -169,7 +169,8 @@ __device__ __forceinline__ double bitsd(unsigned long long b) { return __longlon
 // ---------------------------------------------------------------------------
 // zero the per-call control state (one kernel instead of several memsets, so
 // the launch chain stays programmatic-dependent-launch friendly)
-__global__ void k_factor_init(int64_t N, FWork f, double zero_tol, const double* anorm, int32_t* status) {
+__global__ void k_factor_init(int64_t N, FWork f, double zero_tol, const double* anorm, int32_t* status,
+                              const int32_t* active) {
   {   // batched: scenario blockIdx.y
     bsel_ws(f, blockIdx.y);
     if (status) status += blockIdx.y;
@@ -177,6 +178,12 @@ __global__ void k_factor_init(int64_t N, FWork f, double zero_tol, const double*
   }
   pdl_wait();
   pdl_trigger();
+  if (active && !active[blockIdx.y]) {
+    // scenario not re-factored this call: keep its factorization, tolerance and counters;
+    // abort = 2 makes every later kernel of this call skip it (finalize leaves its outputs alone)
+    if (blockIdx.x == 0 && threadIdx.x == 0) f.ctl->abort = 2;
+    return;
+  }
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t gth = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = gtid; i < N; i += gth) { f.sw[i] = -1; f.bt[i] = 0; }
@@ -2214,6 +2221,7 @@ __device__ __forceinline__ void finalize_body(int64_t N, double* __restrict__ A,
     else cg::this_grid().sync();
   };
   FCtl* ctl = f.ctl;
+  if (ctl->abort == 2) return;   // batched: scenario not re-factored this call (outputs kept)
   const int64_t gtid = BLOCK ? (int64_t)threadIdx.x : blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t gth = BLOCK ? (int64_t)blockDim.x : (int64_t)gridDim.x * blockDim.x;
   if (gtid == 0 && inertia_out) {
@@ -2385,7 +2393,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   // zero control + arrays (sw = -1); take ||M||_inf from the caller, or scan M for it
   MDS_LAUNCH(PC_ANORM, st,
              MDS_CUDA_TRY(launch_pdl(k_factor_init, dim3((unsigned)std::min<int64_t>(mds_cdiv(3 * (N + 2), 256), 1184)),
-                                     dim3(256), 0, st, N, f, zero_tol, anorm, status)));
+                                     dim3(256), 0, st, N, f, zero_tol, anorm, status, (const int32_t*)nullptr)));
   if (!anorm) {
     const int64_t nt = anorm::ntiles(N);
     MDS_LAUNCH(PC_ANORM, st,
@@ -2677,7 +2685,8 @@ extern "C" size_t mds_factor_batched_workspace_size(int64_t N, int64_t batch) {
 
 extern "C" int mds_factor_batched(int64_t batch, int64_t N, double* M, int64_t ldm, int64_t str_M, int32_t* piv,
                                   int64_t str_piv, double zero_tol, const double* anorm, mds_inertia* inertia_dev,
-                                  int32_t* status, void* work, size_t work_bytes, void* stream) {
+                                  int32_t* status, const int32_t* active, void* work, size_t work_bytes,
+                                  void* stream) {
   if (batch < 0 || N < 0 || N >= (1 << 29)) return MDS_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   if (batch == 0) return MDS_OK;
@@ -2687,6 +2696,7 @@ extern "C" int mds_factor_batched(int64_t batch, int64_t N, double* M, int64_t l
     return MDS_OK;
   }
   if (!M || !piv || ldm < N || str_M < ldm * N || str_piv < 2 * N) return MDS_ERR_ARG;
+  if (active && !anorm) return MDS_ERR_ARG;   // masked calls take ||M||_inf from the (masked) condensation
   // the batched update is TMA-only: 16-byte aligned matrices, even ldm and stride
   if ((reinterpret_cast<uintptr_t>(M) & 15) || (ldm & 1) || (str_M & 1)) return MDS_ERR_ARG;
   const size_t ws = factor_ws_stride(N);
@@ -2698,7 +2708,7 @@ extern "C" int mds_factor_batched(int64_t batch, int64_t N, double* M, int64_t l
   const unsigned nb = (unsigned)batch;
   MDS_LAUNCH(PC_ANORM, st,
              MDS_CUDA_TRY(launch_pdl(k_factor_init, dim3((unsigned)std::min<int64_t>(mds_cdiv(3 * (N + 2), 256), 64), nb),
-                                     dim3(256), 0, st, N, f, zero_tol, anorm, status)));
+                                     dim3(256), 0, st, N, f, zero_tol, anorm, status, active)));
   if (!anorm) {
     MDS_LAUNCH(PC_ANORM, st,
                MDS_CUDA_TRY(launch_pdl(anorm::k_anorm_scan, dim3((unsigned)anorm::ntiles(N), nb), dim3(256), 0, st, N,
