@@ -103,7 +103,7 @@ EXPORTS = ["mds_condense_workspace_size", "mds_condense_batched", "mds_factor_to
 
 PROF_CLASSES = ["condense_rows", "condense_norm", "condense_tiles", "anorm", "panel_diag", "panel_trsm", "panel_store",
                 "panel_exact", "update", "finalize", "solve_gather", "solve_fwd", "solve_d", "solve_bwd",
-                "solve_scatter", "recover", "vectors", "condense_diag"]
+                "solve_scatter", "recover", "vectors", "condense_diag", "condense_dense"]
 
 
 def version() -> str:

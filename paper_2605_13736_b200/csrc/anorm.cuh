@@ -117,8 +117,18 @@ __global__ void __launch_bounds__(256) k_anorm_rows(int64_t N, char* parts, size
     const int64_t b = i / AT, r = i % AT;
     const int64_t nterm = nb + 1, per = (nterm + AW - 1) / AW;
     const int64_t x0 = min(nterm, per * warp), x1 = min(nterm, per * (warp + 1));
-    for (int64_t x = x0; x < x1; x++)
-      s += (x <= b) ? P.prow[tile_id(b, x) * AT + r] : P.pcol[tile_id(x - 1, b) * AT + r];
+    constexpr int CH = 8;   // loads issued ahead of the (in-order) sum
+    for (int64_t x = x0; x < x1; x += CH) {
+      double t[CH];
+#pragma unroll
+      for (int q = 0; q < CH; q++) {
+        const int64_t xq = x + q;
+        t[q] = xq < x1 ? ((xq <= b) ? P.prow[tile_id(b, xq) * AT + r] : P.pcol[tile_id(xq - 1, b) * AT + r]) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < CH; q++)
+        if (x + q < x1) s += t[q];
+    }
   }
   part[warp][lane] = s;
   __syncthreads();
@@ -135,10 +145,12 @@ __global__ void __launch_bounds__(256) k_anorm_rows(int64_t N, char* parts, size
     }
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (last && warp == 0) {
     __threadfence();
-    double a = 0.0;
-    for (unsigned b = 0; b < gridDim.x; b++) a = fmax(a, *(volatile double*)&P.bmax[b]);
+    double a = 0.0;   // max is exact: any order
+    for (unsigned b = lane; b < gridDim.x; b += 32) a = fmax(a, *(volatile double*)&P.bmax[b]);
+    a = warp_max(a);
+    if (lane == 0) {
     const bool bad = *(volatile unsigned*)&P.ctr[2] != 0u || !isfinite(a);
     if (bad) a = __longlong_as_double(0x7ff8000000000000ll);   // NaN: "not finite"
     if (o.anorm) o.anorm[ms] = a;
@@ -152,6 +164,7 @@ __global__ void __launch_bounds__(256) k_anorm_rows(int64_t N, char* parts, size
     }
     P.ctr[1] = 0u;
     P.ctr[2] = 0u;
+    }
   }
 }
 

@@ -78,6 +78,9 @@ struct MdsVariant {
   int no_tma = 0, no_lookahead = 0, static_sched = 0, no_snake = 0, no_cprefetch = 0;
   int upd_inplace = 0, upd_main = 0, slow_1cta = 0, exact_no_ls = 0, f2_trsm = 0, no_pdl = 0;
   int ozaki = 0;   // trailing update in emulated FP64 on the INT8 tensor cores (ozaki.cuh)
+  int cdense_ctas = 2;   // CTAs per SM of k_condense_dense (runs beside the pair chain)
+  int cdense_serial = 0; // 1: k_condense_dense on the caller's stream (no fork)
+  int cdense_tma = 0;    // 1: the TMA-ring copy of the dense tiles (k_condense_dense_tma) instead of register staging
 };
 extern MdsVariant g_mds_var;
 
@@ -129,7 +132,7 @@ static inline cudaError_t launch_coop_pdl(void (*k)(KArgs...), dim3 g, dim3 b, s
 enum MdsProfClass {
   PC_CONDENSE_W = 0, PC_CONDENSE_DENSE, PC_CONDENSE_YY, PC_ANORM, PC_PANEL_DIAG, PC_PANEL_TRSM,
   PC_PANEL_STORE, PC_PANEL_SLOW, PC_UPDATE, PC_FINALIZE, PC_SOLVE_GATHER, PC_SOLVE_FWD, PC_SOLVE_D,
-  PC_SOLVE_BWD, PC_SOLVE_SCATTER, PC_RECOVER, PC_VECTORS, PC_CONDENSE_DIAG, PC_COUNT
+  PC_SOLVE_BWD, PC_SOLVE_SCATTER, PC_RECOVER, PC_VECTORS, PC_CONDENSE_DIAG, PC_CONDENSE_COPY, PC_COUNT
 };
 extern bool g_mds_prof;
 void mds_prof_start(int cls, cudaStream_t st);

@@ -11,15 +11,15 @@
 //   * pairs are sorted by destination -- 64x64 tile of M, column in the tile,
 //     row in the tile -- and, for one destination, by k;
 //   * one 64-bit word per pair: p | (p - p') << 32 | row << 52 | col << 58.
-// Per call (device, stream-ordered, two kernels + one for the norm):
+// Per call (device, stream-ordered; the pure dense tiles on a side stream, see
+// k_condense_dense, concurrently with this chain):
 //   k_condense_rows   one pass over the sparse variables (a1): q_k, w_k = 1/q_k,
 //                     status on q_k <= 0, and per CSR entry Q[p] = (val_p w_k,
 //                     val_p).
 //   k_condense_diag   one warp per constraint column: the diagonal pairs p = p'
 //                     of M_yy(c, c) and the rhs term (J_s^T (w . r_xs))_c.
 //   k_condense_tiles  persistent CTAs take 64x64 tiles of lower M from a queue
-//                     (heaviest first): the dense blocks are copied
-//                     (H_dd + diag(sigma_d) + delta_w I, J_d), the M_yy tiles are
+//                     (heaviest first; the tiles right of n_d): the M_yy tiles are
 //                     initialised (-delta_c, -1/d_h) and then stream their sorted
 //                     pair list: a warp reads 32 pair words (coalesced), gathers
 //                     the two Q values, forms the products, sums each run of equal
@@ -39,6 +39,8 @@
 #include <numeric>
 #include <vector>
 
+#include <cuda.h>
+
 #include "anorm.cuh"
 #include "common.cuh"
 
@@ -50,13 +52,14 @@ struct mds_plan {
   int2* tkp;         // [nnz]   (k, p | min(suffix,31) << 27)
   int32_t max_col_len;
   // condensation pair lists (see top of file)
-  int64_t npairs, ntile, nitems;
+  int64_t npairs, ntile, nitems, norder, ndense;
   uint32_t nbuf;               // part buffers (64x64) of the split tiles
   unsigned long long* pairs;   // [npairs] off-diagonal pairs, by tile, then (column, row), then k
   uint32_t* toff;              // [ntile + 1] pair range of each tile
   uint32_t* pbase;             // [ntile] first part buffer of a split tile
-  uint32_t* order;             // [ntile] (I << 16 | J), heaviest tiles first (batched calls)
+  uint32_t* order;             // [norder] (I << 16 | J), heaviest tiles first (batched calls)
   uint2* items;                // [nitems] (I << 16 | J, part << 16 | nparts), heaviest first (single system)
+  uint32_t* dorder;            // [ndense] (I << 16 | J): the pure dense tiles (64 J + 63 < n_d), column-block order
 };
 
 namespace {
@@ -64,6 +67,7 @@ constexpr int CT = anorm::AT;         // tile edge (64)
 constexpr int CW = anorm::AW;         // warps per CTA (8)
 constexpr int PAIR_SBITS = 20;        // p - p' < 2^20 (row length limit of the pair encoding)
 constexpr int64_t PART = 16384;       // pairs per work item of a split tile (single-system calls)
+constexpr int PAIR_U = 2;             // 32-pair chunks per pipeline stage of pair_range
 }  // namespace
 
 extern "C" const char* mds_version(void) { return "mds_b200 0.2 sm_100a"; }
@@ -155,16 +159,23 @@ extern "C" int mds_plan_create(int64_t n_s, int64_t n_d, int64_t m_E, int64_t m_
   // into parts (chunk-aligned ranges of its list); each part sums into its own
   // buffer and the last part to finish merges them in part order.  Items are
   // processed heaviest first.
+  // The pure dense tiles (every column < n_d: copies of H_dd / J_d, no pairs) are
+  // k_condense_dense's, in column-block order; the rest (M_yy and the block column
+  // that straddles n_d) go through the pair kernel's queue.
   std::vector<uint32_t> order;                 // tiles: (I << 16 | J)
   std::vector<uint2> items;                    // parts: (I << 16 | J, part << 16 | nparts)
+  std::vector<uint32_t> dorder;                // pure dense tiles
   std::vector<uint32_t> pbase(ntile, 0);
   uint32_t nbuf = 0;
+  const int64_t JD = n_d / CT;
+  for (int64_t J = 0; J < JD; J++)
+    for (int64_t I = J; I < nb; I++) dorder.push_back((uint32_t)((I << 16) | J));
   {
     std::vector<std::pair<int64_t, uint32_t>> cost;
     std::vector<std::pair<int64_t, uint2>> icost;
     cost.reserve(ntile);
     for (int64_t I = 0; I < nb; I++)
-      for (int64_t J = 0; J <= I; J++) {
+      for (int64_t J = JD; J <= I; J++) {
         const int64_t t = anorm::tile_id(I, J), np_ = tcount[t + 1] - tcount[t];
         const uint32_t ij = (uint32_t)((I << 16) | J);
         cost.emplace_back(-(4 * np_ + CT * CT / 8), ij);
@@ -192,6 +203,7 @@ extern "C" int mds_plan_create(int64_t n_s, int64_t n_d, int64_t m_E, int64_t m_
   if (!P) return MDS_ERR_ARG;
   P->n_s = n_s; P->n_d = n_d; P->m_E = m_E; P->m_I = m_I; P->nnz = nnz; P->max_col_len = maxlen;
   P->npairs = npairs; P->ntile = ntile; P->nitems = (int64_t)items.size(); P->nbuf = nbuf;
+  P->norder = (int64_t)order.size(); P->ndense = (int64_t)dorder.size(); P->dorder = nullptr;
   P->rowptr = nullptr; P->colidx = nullptr; P->tptr = nullptr; P->tkp = nullptr;
   P->pairs = nullptr; P->toff = nullptr; P->pbase = nullptr; P->order = nullptr; P->items = nullptr;
   auto up = [](void** dst, const void* src, size_t bytes) {
@@ -208,7 +220,8 @@ extern "C" int mds_plan_create(int64_t n_s, int64_t n_d, int64_t m_E, int64_t m_
             up((void**)&P->toff, toff.data(), sizeof(uint32_t) * (ntile + 1)) &&
             up((void**)&P->pbase, pbase.data(), sizeof(uint32_t) * ntile) &&
             up((void**)&P->order, order.data(), sizeof(uint32_t) * order.size()) &&
-            up((void**)&P->items, items.data(), sizeof(uint2) * items.size());
+            up((void**)&P->items, items.data(), sizeof(uint2) * items.size()) &&
+            up((void**)&P->dorder, dorder.data(), sizeof(uint32_t) * dorder.size());
   if (!ok) {
     mds_plan_destroy(P);
     return MDS_ERR_CUDA;
@@ -221,6 +234,7 @@ extern "C" int mds_plan_destroy(mds_plan* P) {
   if (!P) return MDS_ERR_ARG;
   cudaFree(P->rowptr); cudaFree(P->colidx); cudaFree(P->tptr); cudaFree(P->tkp);
   cudaFree(P->pairs); cudaFree(P->toff); cudaFree(P->pbase); cudaFree(P->order); cudaFree(P->items);
+  cudaFree(P->dorder);
   delete P;
   return MDS_OK;
 }
@@ -242,7 +256,7 @@ namespace {
 // Per-call arguments.  Every per-scenario array is (base, stride in elements);
 // the single-system call uses batch = 1 and strides 0.
 struct CondArgs {
-  int64_t n_s, n_d, m_E, m, N, nnz, ntile, nitems, batch;
+  int64_t n_s, n_d, m_E, m, N, nnz, ntile, nitems, norder, ndense, batch;
   const int32_t* active;                // [batch] or NULL: scenarios with active[s] == 0 are left untouched
   const int32_t* rowptr;
   const int32_t* tptr;
@@ -252,6 +266,7 @@ struct CondArgs {
   const uint32_t* pbase;
   const uint32_t* order;
   const uint2* items;
+  const uint32_t* dorder;
   int split;                            // 1: walk `items` (split tiles), 0: walk `order`
   const double* val; int64_t s_val;
   const double* h_ss; int64_t s_hss;
@@ -276,6 +291,8 @@ struct CondArgs {
   char* parts;       // [batch][parts_bytes(N)]
   size_t parts_stride;
   unsigned* queue;   // [4] tile queue counter
+  __device__ double* parts_prow(int64_t s) const { return anorm::parts_at(parts + (size_t)s * parts_stride, N).prow; }
+  __device__ double* parts_pcol(int64_t s) const { return anorm::parts_at(parts + (size_t)s * parts_stride, N).pcol; }
 };
 
 __device__ __forceinline__ anorm::Parts parts_of(const CondArgs& a, int64_t s) {
@@ -439,40 +456,58 @@ __global__ void __launch_bounds__(256) k_condense_diag(CondArgs a) {
 // range's first run, when it continues the pair before the range (ckey), is
 // summed into the returned carry instead (the caller subtracts it later, in
 // warp order).  *carried = its destination, or -1.
+template <int U>
 __device__ __forceinline__ double pair_range(const unsigned long long* __restrict__ pairs, uint32_t r0, uint32_t r1,
                                              int ckey, const double2* __restrict__ Q, double* T, int lane, unsigned long long pol_stream,
                                              unsigned long long pol_keep, int* carried) {
+  // software pipeline: the pair words of the next U chunks are loaded while the
+  // current chunks' operand gathers are in flight
   double carry = 0.0;
   *carried = -1;
-  for (uint32_t base = r0; base < r1; base += 64) {
-    double prod[2];
-    int key[2];
+  unsigned long long wd[U];
 #pragma unroll
-    for (int u = 0; u < 2; u++) {
-      const uint32_t idx = base + 32 * u + lane;
-      key[u] = 4096 + lane;   // invalid lanes: distinct keys that never match
-      prod[u] = 0.0;
-      if (idx < r1) {
-        const unsigned long long wd = ld_pair(pairs + idx, pol_stream);
-        const uint32_t p = (uint32_t)wd;
-        const uint32_t sft = (uint32_t)(wd >> 32) & ((1u << PAIR_SBITS) - 1u);
-        key[u] = (int)(wd >> 52);
-        prod[u] = __dmul_rn(ld_q(Q + p, pol_keep).x, ld_q(Q + (p - sft), pol_keep).y);
+  for (int u = 0; u < U; u++) {
+    const uint32_t idx = r0 + 32 * u + lane;
+    wd[u] = idx < r1 ? ld_pair(pairs + idx, pol_stream) : 0ull;
+  }
+  for (uint32_t base = r0; base < r1; base += 32 * U) {
+    double qa[U], qb[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      qa[u] = qb[u] = 0.0;
+      if (base + 32 * u + lane < r1) {
+        const uint32_t p = (uint32_t)wd[u];
+        const uint32_t sft = (uint32_t)(wd[u] >> 32) & ((1u << PAIR_SBITS) - 1u);
+        qa[u] = ld_d(&Q[p].x, pol_keep);
+        qb[u] = ld_d(&Q[p - sft].y, pol_keep);
       }
     }
+    int key[U];
 #pragma unroll
-    for (int u = 0; u < 2; u++) {
+    for (int u = 0; u < U; u++) key[u] = (base + 32 * u + lane < r1) ? (int)(wd[u] >> 52) : 4096 + lane;
+    const uint32_t nb = base + 32 * U;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t idx = nb + 32 * u + lane;
+      wd[u] = idx < r1 ? ld_pair(pairs + idx, pol_stream) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
       if (base + 32 * u >= r1) break;
-      double v = prod[u];
+      double v = __dmul_rn(qa[u], qb[u]);
       const int k = key[u];
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
+      // segmented inclusive scan over the runs of equal key (keys sorted): run heads
+      // from one ballot, and only as many doubling steps as the longest run needs
+      // (the same sums, in the same order, as the full 5-step scan)
+      const int pk = __shfl_up_sync(0xffffffffu, k, 1);
+      const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || pk != k);
+      const int dist = lane - (31 - __clz(heads & (0xffffffffu >> (31 - lane))));
+      const int maxd = __reduce_max_sync(0xffffffffu, (unsigned)dist);
+      for (int d = 1; d <= maxd; d <<= 1) {
         const double o = __shfl_up_sync(0xffffffffu, v, d);
-        const int ok = __shfl_up_sync(0xffffffffu, k, d);
-        if (lane >= d && ok == k) v += o;
+        if (dist >= d) v += o;
       }
-      const int nk = __shfl_down_sync(0xffffffffu, k, 1);
-      bool tail = (base + 32 * u + lane < r1) && (lane == 31 || nk != k);
+      bool tail = (base + 32 * u + lane < r1) && (lane == 31 || ((heads >> (lane + 1)) & 1u));
       if (ckey >= 0) {   // still inside the run continued from before the range
         const int k0 = __shfl_sync(0xffffffffu, k, 0);
         if (k0 == ckey) {
@@ -539,7 +574,7 @@ __global__ void __launch_bounds__(CW * 32, 4) k_condense_tiles(CondArgs a) {
   __shared__ bool s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned long long pol_keep = pol_evict_last(), pol_stream = pol_evict_first();
-  const int64_t nitem = a.split ? a.nitems : a.ntile * a.batch;
+  const int64_t nitem = a.split ? a.nitems : a.norder * a.batch;
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(&a.queue[0], 1u);
     __syncthreads();
@@ -553,23 +588,32 @@ __global__ void __launch_bounds__(CW * 32, 4) k_condense_tiles(CondArgs a) {
     } else {
       s = g % a.batch;
       ij = a.order[g / a.batch];
-      if (a.active && !a.active[s]) continue;   // (uniform across the CTA)
+      if (a.active && !a.active[s]) {   // (uniform across the CTA)
+        __syncthreads();                // s_item is rewritten at the top of the loop
+        continue;
+      }
     }
     const int64_t I = ij >> 16, J = ij & 0xffff;
     const int64_t tile = anorm::tile_id(I, J);
     const int64_t i0 = I * CT, j0 = J * CT;
-    const int64_t n_d = a.n_d, N = a.N;
+    const int64_t N = a.N;
     const double dw = a.dw_arr ? a.dw_arr[s] : a.delta_w;
     const double dc = a.dc_arr ? a.dc_arr[s] : a.delta_c;
     // ---- initial values: dense blocks of Eq.(6), or the M_yy diagonal start
     //      (-delta_c - 1/d_h - the diagonal pairs); a part of a split tile starts at 0
+    // (a tile strictly below the diagonal, inside M and right of n_d: all zeros)
+    const bool full = I > J && i0 + CT <= N;
+    if (nparts > 1 || (full && j0 >= a.n_d)) {
+      for (int e = threadIdx.x; e < CT * CT / 2; e += CW * 32) reinterpret_cast<double2*>(T)[e] = make_double2(0.0, 0.0);
+    } else {
 #pragma unroll
-    for (int u = 0; u < 8; u++) {
-      const int c = warp + 8 * u;
+      for (int u = 0; u < 8; u++) {
+        const int c = warp + 8 * u;
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int rr = lane + 32 * h;
-        T[c * CT + rr] = nparts == 1 ? init_value(a, s, i0 + rr, j0 + c, dw, dc, pol_stream) : 0.0;
+        for (int h = 0; h < 2; h++) {
+          const int rr = lane + 32 * h;
+          T[c * CT + rr] = init_value(a, s, i0 + rr, j0 + c, dw, dc, pol_stream);
+        }
       }
     }
     __syncthreads();
@@ -588,8 +632,8 @@ __global__ void __launch_bounds__(CW * 32, 4) k_condense_tiles(CondArgs a) {
       const uint32_t r1 = min(E1, E0 + 64u * min(nch, per * (uint32_t)(warp + 1)));
       const int ckey = (r0 > E0 && r0 < r1) ? (int)(ld_pair(a.pairs + r0 - 1, pol_stream) >> 52) : -1;
       int carried;
-      const double carry = pair_range(a.pairs, r0, r1, ckey, a.Q + s * a.nnz, T, lane,
-                                      pol_stream, pol_keep, &carried);
+      const double carry = pair_range<PAIR_U>(a.pairs, r0, r1, ckey, a.Q + s * a.nnz, T, lane,
+                                              pol_stream, pol_keep, &carried);
       if (lane == 0) { stcarry[warp] = carry; stckey[warp] = carried; }
       __syncthreads();
       if (threadIdx.x == 0) {   // carries in warp order (the previous warps' commits are done)
@@ -632,7 +676,7 @@ __global__ void __launch_bounds__(CW * 32, 4) k_condense_tiles(CondArgs a) {
       for (int h = 0; h < 2; h++) {
         const int rr = lane + 32 * h;
         const int64_t i = i0 + rr;
-        const bool in = i < N && j < N && i >= j;
+        const bool in = full || (i < N && j < N && i >= j);
         const double x = T[c * CT + rr];
         ax[h] = in ? fabs(x) : 0.0;
         st[h] = in && i > j;
@@ -664,6 +708,272 @@ __global__ void __launch_bounds__(CW * 32, 4) k_condense_tiles(CondArgs a) {
     __syncthreads();
   }
 }
+
+// ---------------------------------------------------------------------------
+// The pure dense tiles (all 64 columns < n_d): M_xx = H_dd + diag(sigma_d) +
+// delta_w I and M_yx = J_d, streamed straight from the inputs to M (no shared
+// tile), with the tile's norm partials.  It depends on no other condensation
+// kernel, so condense_launch runs it on a side stream CONCURRENTLY with the
+// rows -> diag -> pair-tile chain: that chain is gather-latency bound, this one
+// bandwidth bound.  Persistent CTAs stride over (tile, scenario) items.
+// Layout: warp w owns columns c = w + 8u (u = 0..7) of the tile; VEC: lane l
+// rows 2l, 2l+1 (16-byte loads/stores; needs even n_d, m, ld's, strides and
+// 16-byte aligned bases), else lane l rows l, l + 32.  All eight (sixteen)
+// loads of a tile are issued before the first use.  Norm partials in a fixed
+// order; a non-finite entry turns its partials into +Inf (k_anorm_rows then
+// reports NaN = "not finite"), so no counter is shared with the other chain.
+__device__ __forceinline__ double2 ld_d2(const double* a, unsigned long long pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_stream2(double* a, double2 v) {
+  asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ double inf_if_nan(double x) { return isnan(x) ? __longlong_as_double(0x7ff0000000000000ll) : x; }
+
+template <bool VEC, bool NORM>
+__global__ void __launch_bounds__(CW * 32) k_condense_dense(CondArgs a) {
+  __shared__ double red[CW][CT];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned long long pol = pol_evict_first();
+  const int64_t n_d = a.n_d, N = a.N;
+  const int64_t nitem = a.ndense * a.batch;
+  for (int64_t g = blockIdx.x; g < nitem; g += gridDim.x) {
+    const int64_t s = g % a.batch;
+    if (a.active && !a.active[s]) continue;                  // (uniform across the CTA)
+    const uint32_t ij = a.dorder[g / a.batch];
+    const int64_t I = ij >> 16, J = ij & 0xffff;
+    const int64_t i0 = I * CT, j0 = J * CT, tile = anorm::tile_id(I, J);
+    const double dw = a.dw_arr ? a.dw_arr[s] : a.delta_w;
+    const double* H = a.H + s * a.s_H;
+    const double* Jd = a.Jd + s * a.s_J;
+    const double* sd = a.sigma_d + s * a.s_sd;
+    double* M = a.M + s * a.s_M;
+    constexpr int R = VEC ? 1 : 2;      // row slots per lane
+    double2 v[8][R];
+    // ---- all loads first (predicated; zero outside the lower triangle / matrix)
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int64_t j = j0 + warp + 8 * u;
+#pragma unroll
+      for (int h = 0; h < R; h++) {
+        const int64_t i = VEC ? i0 + 2 * lane : i0 + lane + 32 * h;
+        v[u][h] = make_double2(0.0, 0.0);
+        if (VEC) {
+          if (i + 1 >= j && i < N) {   // at least one of rows i, i+1 is on/below the diagonal (N even)
+            const double* src = i < n_d ? H + i + j * a.ldh : Jd + (i - n_d) + j * a.ldj;
+            v[u][h] = ld_d2(src, pol);
+          }
+        } else if (i >= j && i < N) {
+          v[u][h].x = ld_d(i < n_d ? H + i + j * a.ldh : Jd + (i - n_d) + j * a.ldj, pol);
+        }
+      }
+    }
+    // ---- diagonal terms, stores, partials
+    double ra[2] = {0.0, 0.0};
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int c = warp + 8 * u;
+      const int64_t j = j0 + c;
+      double cs = 0.0;
+#pragma unroll
+      for (int h = 0; h < R; h++) {
+        if (VEC) {
+          const int64_t i = i0 + 2 * lane;
+          double2 x = v[u][h];
+          if (i == j) x.x = __dadd_rn(__dadd_rn(x.x, sd[j]), dw);
+          if (i + 1 == j) x.y = __dadd_rn(__dadd_rn(x.y, sd[j]), dw);
+          if (i < N) {
+            if (i >= j) {
+              st_stream2(M + i + j * a.ldm, x);
+            } else if (i + 1 == j) {
+              st_stream(M + i + 1 + j * a.ldm, x.y);
+              x.x = 0.0;
+            } else {
+              x = make_double2(0.0, 0.0);
+            }
+          }
+          const double a0 = fabs(x.x), a1 = fabs(x.y);
+          ra[0] += a0;
+          ra[1] += a1;
+          cs += (i > j ? a0 : 0.0) + (i + 1 > j ? a1 : 0.0);
+        } else {
+          const int64_t i = i0 + lane + 32 * h;
+          double x = v[u][h].x;
+          if (i == j) x = __dadd_rn(__dadd_rn(x, sd[j]), dw);
+          if (i >= j && i < N) st_stream(M + i + j * a.ldm, x);
+          const double ax = fabs(x);
+          ra[h] += ax;
+          cs += i > j ? ax : 0.0;
+        }
+      }
+      if (NORM) {
+        cs = warp_sum(cs);
+        if (lane == 0) a.parts_pcol(s)[tile * CT + c] = inf_if_nan(cs);
+      }
+    }
+    if (NORM) {
+      if (VEC) {
+        red[warp][2 * lane] = ra[0];
+        red[warp][2 * lane + 1] = ra[1];
+      } else {
+        red[warp][lane] = ra[0];
+        red[warp][lane + 32] = ra[1];
+      }
+      __syncthreads();
+      if (threadIdx.x < CT) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < CW; w++) sum += red[w][threadIdx.x];
+        a.parts_prow(s)[tile * CT + threadIdx.x] = inf_if_nan(sum);
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The same dense tiles through the Tensor Memory Accelerator (variant cdense_tma;
+// needs n_d a multiple of 64 and every leading dimension / stride / base 16-byte
+// aligned).  Measured slower than the register-staged kernel beside the pair
+// chain (C3: 0.369 vs 0.317 ms per condensation): its 4 x 32 KB ring keeps fewer
+// bytes in flight per SM than two register-staged CTAs, and the ring's shared
+// memory crowds out the pair kernel's CTAs.  Kept as a measured alternative:
+// one persistent CTA per SM, a ring of DS 32 KB stages.  Thread 0 keeps DS - 1
+// tile loads in flight (cp.async.bulk.tensor, 64 x 64 box from H_dd or J_d,
+// completion on the stage's mbarrier); an off-diagonal tile is stored back to M
+// unchanged by one TMA store straight from the stage (bulk group per iteration),
+// while the eight warps form its norm partials from shared memory.  The 64x64
+// diagonal tiles of M_xx (diagonal terms, lower part only) are written by the
+// warps.
+constexpr int DS = 4;                       // stages
+constexpr int DSTAGE = CT * CT * 8;         // bytes per stage (64 x 64 FP64)
+constexpr int DSMEM = DS * DSTAGE + 1024;   // + alignment slack
+
+__device__ __forceinline__ unsigned dsm_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void dmbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(bar), "r"(parity) : "memory");
+}
+
+template <bool NORM>
+__global__ void __launch_bounds__(CW * 32, 1) k_condense_dense_tma(CondArgs a, const __grid_constant__ CUtensorMap mH,
+                                                                   const __grid_constant__ CUtensorMap mJ,
+                                                                   const __grid_constant__ CUtensorMap mM) {
+  extern __shared__ unsigned char dsm_raw[];
+  double* stg = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) unsigned long long full[DS];
+  __shared__ double red[CW][CT];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_d = a.n_d, N = a.N, nitem = a.ndense * a.batch;
+  const int64_t nmine = nitem > blockIdx.x ? (nitem - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto item = [&](int64_t it, int64_t& s, int64_t& I, int64_t& J) {
+    const int64_t g = blockIdx.x + it * (int64_t)gridDim.x;
+    s = g % a.batch;
+    const uint32_t ij = a.dorder[g / a.batch];
+    I = ij >> 16;
+    J = ij & 0xffff;
+  };
+  auto issue = [&](int64_t it) {   // thread 0: load item `it` of this CTA into stage it % DS
+    if (it >= nmine) return;
+    int64_t s, I, J;
+    item(it, s, I, J);
+    const unsigned bar = dsm_u32(&full[it % DS]);
+    const unsigned dst = dsm_u32(stg + (it % DS) * (CT * CT));
+    if (a.active && !a.active[s]) {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+      return;
+    }
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(DSTAGE) : "memory");
+    const bool x = I * CT < n_d;
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+        ::"r"(dst), "l"(x ? &mH : &mJ), "r"((int)(x ? I * CT : I * CT - n_d)), "r"((int)(J * CT)), "r"((int)s), "r"(bar)
+        : "memory");
+  };
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < DS; q++)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(dsm_u32(&full[q])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    for (int q = 0; q < DS - 1; q++) issue(q);
+  }
+  __syncthreads();
+  for (int64_t it = 0; it < nmine; it++) {
+    const int st = (int)(it % DS);
+    dmbar_wait(dsm_u32(&full[st]), (unsigned)((it / DS) & 1));
+    int64_t s, I, J;
+    item(it, s, I, J);
+    const double* T = stg + st * (CT * CT);
+    const bool act = !(a.active && !a.active[s]);
+    const int64_t i0 = I * CT, j0 = J * CT, tile = anorm::tile_id(I, J);
+    if (act && I != J && threadIdx.x == 0) {
+      asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n"
+                   ::"l"(&mM), "r"((int)i0), "r"((int)j0), "r"((int)s), "r"(dsm_u32(T)) : "memory");
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    if (act) {
+      const double dw = a.dw_arr ? a.dw_arr[s] : a.delta_w;
+      const double* sd = a.sigma_d + s * a.s_sd;
+      double* M = a.M + s * a.s_M;
+      double ra[2] = {0.0, 0.0};
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int c = warp + 8 * u;
+        const int64_t j = j0 + c, i = i0 + 2 * lane;
+        double2 x = *reinterpret_cast<const double2*>(T + c * CT + 2 * lane);
+        double cs = 0.0;
+        if (I == J) {   // diagonal tile of M_xx: diagonal terms, lower part only, stored here
+          if (i == j) x.x = __dadd_rn(__dadd_rn(x.x, sd[j]), dw);
+          if (i + 1 == j) x.y = __dadd_rn(__dadd_rn(x.y, sd[j]), dw);
+          if (i >= j) {
+            st_stream2(M + i + j * a.ldm, x);
+          } else if (i + 1 == j) {
+            st_stream(M + i + 1 + j * a.ldm, x.y);
+            x.x = 0.0;
+          } else {
+            x = make_double2(0.0, 0.0);
+          }
+        } else if (i >= N) {
+          x = make_double2(0.0, 0.0);   // (zero-filled rows below the matrix)
+        }
+        const double a0 = fabs(x.x), a1 = fabs(x.y);
+        ra[0] += a0;
+        ra[1] += a1;
+        cs += (i > j ? a0 : 0.0) + (i + 1 > j ? a1 : 0.0);
+        if (NORM) {
+          cs = warp_sum(cs);
+          if (lane == 0) a.parts_pcol(s)[tile * CT + c] = inf_if_nan(cs);
+        }
+      }
+      if (NORM) {
+        red[warp][2 * lane] = ra[0];
+        red[warp][2 * lane + 1] = ra[1];
+      }
+    }
+    __syncthreads();
+    if (act && NORM && threadIdx.x < CT) {
+      double sum = 0.0;
+#pragma unroll
+      for (int w = 0; w < CW; w++) sum += red[w][threadIdx.x];
+      a.parts_prow(s)[tile * CT + threadIdx.x] = inf_if_nan(sum);
+    }
+    // refill the stage consumed in the previous iteration (its store has had one
+    // iteration to read it) with the item DS - 1 ahead of this one
+    if (threadIdx.x == 0) {
+      asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+      issue(it + DS - 1);
+    }
+    __syncthreads();   // red reused next iteration
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
 }  // namespace
 
 // workspace: [queue 256 B | Q (16 nnz per scenario) | dsum (8 m per scenario) |
@@ -689,12 +999,66 @@ extern "C" size_t mds_condense_workspace_size(const mds_plan* P, int64_t batch) 
   return cond_layout(P, batch).total;
 }
 
+// The side stream of the dense-tile kernel (one per host thread and device, so
+// concurrent callers never share the fork/join events; graph-capturable: the
+// fork is an event record + wait, the join likewise).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static SideStream* side_stream(int dev) {
+  thread_local SideStream ss[64];
+  if (dev < 0 || dev >= 64) return nullptr;
+  SideStream& x = ss[dev];
+  if (!x.s) {
+    if (cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess) {
+      x.s = nullptr;
+      return nullptr;
+    }
+  }
+  return &x;
+}
+
+typedef CUresult (*PFN_encTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encTiled cond_encoder() {
+  static const PFN_encTiled fn = []() -> PFN_encTiled {   // thread-safe one-time lookup
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    PFN_encTiled r = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      r = reinterpret_cast<PFN_encTiled>(p);
+    (void)cudaGetLastError();
+    return r;
+  }();
+  return fn;
+}
+// 3-D map over `batch` column-major (rows x cols, ld) FP64 matrices `bstride` elements
+// apart (0: one matrix); 64 x 64 x 1 box, no swizzle, zero fill out of bounds
+static bool cond_map(CUtensorMap* m, const double* base, int64_t rows, int64_t cols, int64_t ld, int64_t batch,
+                     int64_t bstride) {
+  PFN_encTiled enc = cond_encoder();
+  if (!enc || rows < 1 || cols < 1) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)rows, (cuuint64_t)cols, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 8, (cuuint64_t)(bstride > 0 ? bstride : ld * cols) * 8};
+  cuuint32_t box[3] = {CT, CT, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static int condense_launch(const mds_plan* P, CondArgs& a, void* work, size_t work_bytes, cudaStream_t st) {
   const int64_t n_s = P->n_s, n_d = P->n_d, m = P->m_E + P->m_I, N = n_d + m;
   a.n_s = n_s; a.n_d = n_d; a.m_E = P->m_E; a.m = m; a.N = N; a.nnz = P->nnz; a.ntile = P->ntile;
   a.nitems = P->nitems;
   a.rowptr = P->rowptr; a.tptr = P->tptr; a.tkp = P->tkp; a.pairs = P->pairs; a.toff = P->toff;
-  a.pbase = P->pbase; a.order = P->order; a.items = P->items;
+  a.pbase = P->pbase; a.order = P->order; a.items = P->items; a.dorder = P->dorder;
+  a.norder = P->norder; a.ndense = P->ndense;
   a.split = a.batch == 1 ? 1 : 0;
   if (N == 0) return MDS_OK;
   if (!a.M || a.ldm < N) return MDS_ERR_ARG;
@@ -716,6 +1080,45 @@ static int condense_launch(const mds_plan* P, CondArgs& a, void* work, size_t wo
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool norm = a.anorm != nullptr;
+  // ---- fork: the pure dense tiles on the side stream, concurrent with the chain below
+  SideStream* side = nullptr;
+  if (a.ndense > 0) {
+    side = side_stream(dev);
+    if (!side) return MDS_ERR_CUDA;
+    auto even = [](int64_t x) { return (x & 1) == 0; };
+    auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+    const bool vec = even(n_d) && even(m) && even(a.ldh) && even(a.ldj) && even(a.ldm) && even(a.s_H) &&
+                     even(a.s_J) && even(a.s_M) && al16(a.H) && al16(a.M) && (m == 0 || al16(a.Jd));
+    const unsigned grid = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>(a.ndense * a.batch, (int64_t)sms * g_mds_var.cdense_ctas));
+    cudaStream_t ds = st;
+    if (!g_mds_var.cdense_serial) {
+      MDS_CUDA_TRY(cudaEventRecord(side->fork, st));
+      MDS_CUDA_TRY(cudaStreamWaitEvent(side->s, side->fork, 0));
+      ds = side->s;
+    } else {
+      side = nullptr;
+    }
+    CUtensorMap mH, mJ, mM;
+    const bool tma = vec && n_d % CT == 0 && g_mds_var.cdense_tma && cond_map(&mH, a.H, n_d, n_d, a.ldh, a.batch, a.s_H) &&
+                     (m == 0 ? cond_map(&mJ, a.H, n_d, n_d, a.ldh, a.batch, a.s_H)
+                             : cond_map(&mJ, a.Jd, m, n_d, a.ldj, a.batch, a.s_J)) &&
+                     cond_map(&mM, a.M, N, N, a.ldm, a.batch, a.s_M);
+    if (tma) {
+      auto kt = norm ? k_condense_dense_tma<true> : k_condense_dense_tma<false>;
+      if (mds_once_per_device((const void*)k_condense_dense_tma<true>)) {
+        MDS_CUDA_TRY(cudaFuncSetAttribute(k_condense_dense_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DSMEM));
+        MDS_CUDA_TRY(cudaFuncSetAttribute(k_condense_dense_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DSMEM));
+      }
+      const unsigned gt = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.ndense * a.batch, (int64_t)sms));
+      MDS_LAUNCH(PC_CONDENSE_COPY, ds, (kt<<<gt, CW * 32, DSMEM, ds>>>(a, mH, mJ, mM)));
+    } else {
+      auto kd = vec ? (norm ? k_condense_dense<true, true> : k_condense_dense<true, false>)
+                    : (norm ? k_condense_dense<false, true> : k_condense_dense<false, false>);
+      MDS_LAUNCH(PC_CONDENSE_COPY, ds, (kd<<<grid, CW * 32, 0, ds>>>(a)));
+    }
+  }
   {
     const int64_t warps = std::max<int64_t>(a.batch * mds_cdiv(n_s, 32), 1);
     const int64_t blocks = std::max<int64_t>(std::max<int64_t>(mds_cdiv(warps, 8), mds_cdiv(a.ntile, 256)),
@@ -729,15 +1132,21 @@ static int condense_launch(const mds_plan* P, CondArgs& a, void* work, size_t wo
                MDS_CUDA_TRY(launch_pdl(k_condense_diag, dim3((unsigned)bx, (unsigned)a.batch), dim3(256), 0, st, a)));
   }
   int occ = 1;
-  const bool norm = a.anorm != nullptr;
   if (norm) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_condense_tiles<true>, CW * 32, 0);
   else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_condense_tiles<false>, CW * 32, 0);
-  const int64_t items = a.split ? P->nitems : P->ntile * a.batch;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)sms * std::max(occ, 1)));
-  if (norm)
-    MDS_LAUNCH(PC_CONDENSE_YY, st, MDS_CUDA_TRY(launch_pdl(k_condense_tiles<true>, dim3(grid), dim3(CW * 32), 0, st, a)));
-  else
-    MDS_LAUNCH(PC_CONDENSE_YY, st, MDS_CUDA_TRY(launch_pdl(k_condense_tiles<false>, dim3(grid), dim3(CW * 32), 0, st, a)));
+  const int64_t items = a.split ? P->nitems : P->norder * a.batch;
+  if (items > 0) {
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)sms * std::max(occ, 1)));
+    if (norm)
+      MDS_LAUNCH(PC_CONDENSE_YY, st, MDS_CUDA_TRY(launch_pdl(k_condense_tiles<true>, dim3(grid), dim3(CW * 32), 0, st, a)));
+    else
+      MDS_LAUNCH(PC_CONDENSE_YY, st, MDS_CUDA_TRY(launch_pdl(k_condense_tiles<false>, dim3(grid), dim3(CW * 32), 0, st, a)));
+  }
+  // ---- join
+  if (side) {
+    MDS_CUDA_TRY(cudaEventRecord(side->join, side->s));
+    MDS_CUDA_TRY(cudaStreamWaitEvent(st, side->join, 0));
+  }
   if (norm) {
     anorm::NormOut o = {};
     o.anorm = a.anorm;

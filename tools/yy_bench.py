@@ -1,6 +1,6 @@
 """Time mds_condense alone (CUDA events, L2 flushed between calls) for kernel
 experiments: per-kernel-class ms and algorithmic GB/s.
-usage: python tools/yy_bench.py [C3|C2|C4] [uniform|local]"""
+usage: python tools/yy_bench.py [C3|C2|C4] [uniform|local] [nnz_per_row]"""
 import os
 import sys
 
@@ -12,10 +12,18 @@ import paper_2605_13736_b200 as mds  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C3"
 pattern = sys.argv[2] if len(sys.argv) > 2 else "uniform"
+npr = int(sys.argv[3]) if len(sys.argv) > 3 else None
 if cfg == "C4":
     prob = mdsgen.scopf_scenario(mdsgen.scopf_base(), 1)
+elif npr is not None:
+    shp = mdsgen.CONFIGS[cfg]
+    prob = mdsgen.g1_quasidefinite(shp["n_s"], shp["n_d"], shp["m_E"], shp["m_I"], 3000, pattern=pattern,
+                                   nnz_per_row=npr)
 else:
     prob = mdsgen.config_problem(cfg, pattern=pattern)
+for kv in filter(None, os.environ.get("VARIANTS", "").split(",")):
+    k, v = kv.split("=")
+    mds.set_variant(k, int(v))
 dp = mds.DeviceProblem(prob)
 st = mds.KKTStep(dp)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -48,5 +56,5 @@ for _ in range(5):
     run()
 prof = mds.profile_end()
 ms = sorted(ts)[len(ts) // 2]
-print(f"{cfg} {pattern}: condense {ms:.4f} ms median ({min(ts):.4f} best), algorithmic {alg / 1e6:.1f} MB -> "
+print(os.environ.get("VARIANTS", ""), f"{cfg} {pattern} npr={npr} nnz={nnz} pairs={dp.plan.npairs if hasattr(dp.plan, 'npairs') else '?'}: condense {ms:.4f} ms median ({min(ts):.4f} best), algorithmic {alg / 1e6:.1f} MB -> "
       f"{alg / ms / 1e6:.0f} GB/s", {k: round(v[0] / max(v[1], 1), 4) for k, v in prof.items() if v[1]})
