@@ -247,7 +247,12 @@ __device__ __forceinline__ unsigned smid() { unsigned r; asm volatile("mov.u32 %
 #define UTRACE_MIN(p, k) atomicMin(&g_utrace[p][k], gtimer())
 #define UTRACE_MAX(p, k) atomicMax(&g_utrace[p][k], gtimer())
 #define UTRACE_ADD(p, k) atomicAdd(&g_utrace[p][k], 1ull)
+__device__ unsigned long long g_f4trace[4096][2];   // k_panel_exact: [0] first CTA past pdl_wait (min), [1] last exit (max)
+#define F4TRACE_MIN(p) do { if (threadIdx.x == 0 && (p) < 4096) atomicMin(&g_f4trace[p][0], gtimer()); } while (0)
+#define F4TRACE_MAX(p) do { if (threadIdx.x == 0 && (p) < 4096) atomicMax(&g_f4trace[p][1], gtimer()); } while (0)
 #else
+#define F4TRACE_MIN(p) do { } while (0)
+#define F4TRACE_MAX(p) do { } while (0)
 #define UTRACE_MIN(p, k) do { } while (0)
 #define UTRACE_MAX(p, k) do { } while (0)
 #define UTRACE_ADD(p, k) do { } while (0)
@@ -1285,6 +1290,7 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
   piv += blockIdx.y * f.bps;
   pdl_wait();
   pdl_trigger();
+  F4TRACE_MIN(f.pidx);
   FCtl* ctl = f.ctl;
   if (ctl->abort) return;
   const int nbp = ctl->nbp;
@@ -1506,6 +1512,7 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
       f.Lb[r + c * ldw] = 0.0;
     }
   }
+  F4TRACE_MAX(f.pidx);
 }
 
 // Copy the finished panel (D + L columns, rows >= the diagonal) from Lb into M.

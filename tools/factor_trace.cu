@@ -23,6 +23,7 @@ int main(int argc, char** argv) {
   int32_t* status; cudaMalloc(&status, 4);
   cudaStream_t st; cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
   const bool graph = argc > 2 && atoi(argv[2]) == 1;
+  for (int i = 3; i + 1 < argc; i += 2) mds_set_variant(argv[i], atoll(argv[i + 1]));   // variant key value ...
   static unsigned long long uinit[4096][6];
   for (int i = 0; i < 4096; i++) { uinit[i][0] = uinit[i][3] = ~0ull; for (int k : {1, 2, 4, 5}) uinit[i][k] = 0; }
   double* A0; cudaMalloc(&A0, sizeof(double) * N * ld);
@@ -32,7 +33,7 @@ int main(int argc, char** argv) {
     cudaGraph_t g;
     cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
     cudaMemcpyAsync(A, A0, sizeof(double) * N * ld, cudaMemcpyDeviceToDevice, st);
-    int rc = mds_factor(N, A, ld, piv, -1.0, ine, nullptr, status, work, wb, st);
+    int rc = mds_factor(N, A, ld, piv, -1.0, nullptr, ine, nullptr, status, work, wb, st);
     cudaStreamEndCapture(st, &g);
     cudaGraphInstantiate(&gexec, g, 0);
     if (rc) printf("capture rc %d\n", rc);
@@ -42,13 +43,16 @@ int main(int argc, char** argv) {
   for (int rep = 0; rep < 3; rep++) {
     cudaMemcpyToSymbol(g_utrace, uinit, sizeof(uinit));
     cudaMemcpyToSymbol(g_usm, usinit, sizeof(usinit));
+    static unsigned long long f4init[4096][2];
+    for (int i = 0; i < 4096; i++) { f4init[i][0] = ~0ull; f4init[i][1] = 0; }
+    cudaMemcpyToSymbol(g_f4trace, f4init, sizeof(f4init));
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     if (graph) {
       cudaEventRecord(a, st); cudaGraphLaunch(gexec, st); cudaEventRecord(b, st);
     } else {
       cudaMemcpyAsync(A, A0, sizeof(double) * N * ld, cudaMemcpyDeviceToDevice, st);
       cudaEventRecord(a, st);
-      int rc = mds_factor(N, A, ld, piv, -1.0, ine, nullptr, status, work, wb, st);
+      int rc = mds_factor(N, A, ld, piv, -1.0, nullptr, ine, nullptr, status, work, wb, st);
       cudaEventRecord(b, st);
       if (rc) printf("rc %d\n", rc);
     }
@@ -90,14 +94,16 @@ int main(int argc, char** argv) {
   }
   printf("avg F1 %.1f us %.0f cycles over %d panels; err=%s\n", sum_us / n, sum_cyc / n, n, cudaGetErrorString(cudaGetLastError()));
   // per panel (absolute us from the first F1): F1 start/end, trsm start/end, U start/end, gap U(p-1) end -> U(p) start
-  printf("csv,p,f1s,f1e,trs,tre,us,ue,gap\n");
+  static unsigned long long f4[4096][2];
+  cudaMemcpyFromSymbol(f4, g_f4trace, sizeof(f4));
+  printf("csv,p,f1s,f1e,trs,tre,us,ue,gap,f4s,f4e\n");
   double prev_ue = -1;
   for (int p = 0; p < np; p++) {
     if (!tr[p][0]) continue;
     auto ab = [&](unsigned long long t) { return (t == ~0ull || t == 0) ? -1.0 : ((double)t - (double)t0) * 1e-3; };
     const double us = ab(ut[p][0]), ue = ab(ut[p][1]);
-    printf("csv,%d,%.2f,%.2f,%.2f,%.2f,%.2f,%.2f,%.2f\n", p, ab(tr[p][0]), ab(tr[p][6]), ab(ut[p][3]), ab(ut[p][4]), us, ue,
-           (prev_ue >= 0 && us >= 0) ? us - prev_ue : -1.0);
+    printf("csv,%d,%.2f,%.2f,%.2f,%.2f,%.2f,%.2f,%.2f,%.2f,%.2f\n", p, ab(tr[p][0]), ab(tr[p][6]), ab(ut[p][3]), ab(ut[p][4]), us, ue,
+           (prev_ue >= 0 && us >= 0) ? us - prev_ue : -1.0, ab(f4[p][0]), ab(f4[p][1]));
     prev_ue = ue;
   }
   return 0;
