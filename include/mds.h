@@ -436,6 +436,47 @@ int64_t mds_factor_panels(const void *fwork, int64_t N, int32_t *starts_host, in
  * number of launches (copies at most cap). */
 int64_t mds_profile_timeline(double *out3, int64_t cap);
 
+/* ---------------------------------------------------------------------------
+ * Distributed LDL^T of ONE system across GPUs (the paper's
+ * implementation is single-GPU, larger systems future work,
+ * PAPER.md:100).  One process per GPU; the lower triangle of M is cut into
+ * 64-column panels, panel g owned by rank g mod P (1-D block-cyclic), each rank
+ * storing its panels full height (column-major, global row index, ld >= N).
+ * paper_2605_13736_b200/dist.py runs the panel loop and the collectives
+ * (torch.distributed); these calls are its device work, all stream-ordered,
+ * device pointers, argument errors returned, no data-dependent status.
+ *
+ * mds_dist_panel — on the panel's owner: the speculative (unpivoted) LDL^T of
+ *   the n x nb panel A (rows k0..N-1 of its columns, lda): L (unit lower; may
+ *   alias A with ldl == lda), W = L D (the columns at elimination), d[nb],
+ *   cmax[nb] (in-block column maxima), parts (workspace, >= ceil((n-nb)/128) x 64
+ *   doubles, nparts_cap = its rows), and the Bunch-Kaufman 1x1 acceptance test
+ *   |d_j| >= alpha max_i |W(i, j)| for every column (alpha =
+ *   (1+sqrt 17)/8): *accepted = 1 and inertia[0..2] += the counts of D (zero
+ *   band |d| <= tol), else *accepted = 0 (the caller then factors the Schur
+ *   complement from this panel on with mds_factor; inertia adds, Haynsworth).
+ * mds_dist_update — C -= L W^T on nq local panels (global first column kq[q],
+ *   width wq[q], stored at C + q*64*ldc; rows i >= kq[q]); L, W: rows k0..N-1 of
+ *   the broadcast panel (ldl); max_rows = N - min(kq).  FP64 DMMA.
+ * mds_dist_trsv64 — y := L11^-1 y (mode 0) or L11^-T y (mode 1), L11 unit lower nb x nb.
+ * mds_dist_gemv_n — acc[i] += sum_t L(i, t) y[t], rows r0 <= i < r1 (global row index).
+ * mds_dist_gemv_t — out[t] = sum_{r0 <= i < r1} L(i, t) x[i], t < nb.
+ * mds_dist_rowabs — rs[i] = this rank's share of the row abs-sum of symmetric M
+ *   (lower stored) for ||M||_inf: sum over its columns c <= i of |M(i, c)| plus,
+ *   for its column i, sum_{r > i} |M(r, i)|; fixed order.  Sum rs over ranks. */
+int mds_dist_panel(int64_t n, int nb, const double *A, int64_t lda, double *L, double *W, int64_t ldl, double *d,
+                   double *cmax, double *parts, int64_t nparts_cap, double tol, int32_t *accepted,
+                   long long *inertia, void *stream);
+int mds_dist_update(int64_t N, int64_t k0, int nb, const double *L, const double *W, int64_t ldl, double *C,
+                    int64_t ldc, const int64_t *kq, const int *wq, int nq, int64_t max_rows, void *stream);
+int mds_dist_trsv64(int nb, const double *L, int64_t ldl, double *y, int mode, void *stream);
+int mds_dist_gemv_n(int64_t r0, int64_t r1, int nb, const double *L, int64_t ldl, const double *y, double *acc,
+                    void *stream);
+int mds_dist_gemv_t(int64_t r0, int64_t r1, int nb, const double *L, int64_t ldl, const double *x, double *out,
+                    void *stream);
+int mds_dist_rowabs(int64_t N, const double *C, int64_t ldc, const int64_t *kq, const int *wq, int nq, double *rs,
+                    void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -99,7 +99,8 @@ EXPORTS = ["mds_condense_workspace_size", "mds_condense_batched", "mds_factor_to
            "mds_solve_batched", "ipm_step_vectors_batched_workspace_size", "ipm_step_vectors_batched",
            "ipm_workspace_size", "ipm_rhs", "ipm_directions", "ipm_reduce", "ipm_apply", "mds_factor_stats",
            "mds_ic_begin_batched", "mds_ic_step_batched", "mds_ic_graph_create", "mds_ic_graph_launch",
-           "mds_ic_graph_destroy"]
+           "mds_ic_graph_destroy", "mds_dist_panel", "mds_dist_update", "mds_dist_trsv64", "mds_dist_gemv_n",
+           "mds_dist_gemv_t", "mds_dist_rowabs"]
 
 PROF_CLASSES = ["condense_rows", "condense_norm", "condense_tiles", "anorm", "panel_diag", "panel_trsm", "panel_store",
                 "panel_exact", "update", "finalize", "solve_gather", "solve_fwd", "solve_d", "solve_bwd",
@@ -444,6 +445,47 @@ def ic_graph_launch(h, stream=None):
 
 def ic_graph_destroy(h):
     _check(_lib.mds_ic_graph_destroy(h), "mds_ic_graph_destroy")
+
+
+_lib.mds_dist_panel.argtypes = [_I64, ctypes.c_int, _P, _I64, _P, _P, _I64, _P, _P, _P, _I64, _D, _P, _P, _P]
+_lib.mds_dist_update.argtypes = [_I64, _I64, ctypes.c_int, _P, _P, _I64, _P, _I64, _P, _P, ctypes.c_int, _I64, _P]
+_lib.mds_dist_trsv64.argtypes = [ctypes.c_int, _P, _I64, _P, ctypes.c_int, _P]
+_lib.mds_dist_gemv_n.argtypes = [_I64, _I64, ctypes.c_int, _P, _I64, _P, _P, _P]
+_lib.mds_dist_gemv_t.argtypes = [_I64, _I64, ctypes.c_int, _P, _I64, _P, _P, _P]
+_lib.mds_dist_rowabs.argtypes = [_I64, _P, _I64, _P, _P, ctypes.c_int, _P, _P]
+for _f in ("mds_dist_panel", "mds_dist_update", "mds_dist_trsv64", "mds_dist_gemv_n", "mds_dist_gemv_t",
+           "mds_dist_rowabs"):
+    getattr(_lib, _f).restype = ctypes.c_int
+
+
+def dist_panel(n, nb, A, lda, L, W, ldl, d, cmax, parts, nparts_cap, tol, accepted, inertia, stream=None):
+    _check(_lib.mds_dist_panel(int(n), int(nb), _ptr(A), int(lda), _ptr(L), _ptr(W), int(ldl), _ptr(d), _ptr(cmax),
+                               _ptr(parts), int(nparts_cap), float(tol), _ptr(accepted), _ptr(inertia),
+                               _stream(stream)), "mds_dist_panel")
+
+
+def dist_update(N, k0, nb, L, W, ldl, C, ldc, kq, wq, nq, max_rows, stream=None):
+    _check(_lib.mds_dist_update(int(N), int(k0), int(nb), _ptr(L), _ptr(W), int(ldl), _ptr(C), int(ldc), _ptr(kq),
+                                _ptr(wq), int(nq), int(max_rows), _stream(stream)), "mds_dist_update")
+
+
+def dist_trsv64(nb, L, ldl, y, mode, stream=None):
+    _check(_lib.mds_dist_trsv64(int(nb), _ptr(L), int(ldl), _ptr(y), int(mode), _stream(stream)), "mds_dist_trsv64")
+
+
+def dist_gemv_n(r0, r1, nb, L, ldl, y, acc, stream=None):
+    _check(_lib.mds_dist_gemv_n(int(r0), int(r1), int(nb), _ptr(L), int(ldl), _ptr(y), _ptr(acc), _stream(stream)),
+           "mds_dist_gemv_n")
+
+
+def dist_gemv_t(r0, r1, nb, L, ldl, x, out, stream=None):
+    _check(_lib.mds_dist_gemv_t(int(r0), int(r1), int(nb), _ptr(L), int(ldl), _ptr(x), _ptr(out), _stream(stream)),
+           "mds_dist_gemv_t")
+
+
+def dist_rowabs(N, C, ldc, kq, wq, nq, rs, stream=None):
+    _check(_lib.mds_dist_rowabs(int(N), _ptr(C), int(ldc), _ptr(kq), _ptr(wq), int(nq), _ptr(rs), _stream(stream)),
+           "mds_dist_rowabs")
 
 
 def set_grid_cap(ctas: int):

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmds_b200.so")
-SOURCES = ["condense.cu", "factor.cu", "solve.cu", "vectors.cu", "residual.cu", "ipm.cu", "ic.cu", "prof.cu"]
+SOURCES = ["condense.cu", "factor.cu", "solve.cu", "vectors.cu", "residual.cu", "ipm.cu", "ic.cu", "dist.cu", "prof.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-warn-spills"]
