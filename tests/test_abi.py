@@ -14,7 +14,7 @@ PKG = os.path.join(ROOT, "paper_2605_13736_b200")
 def declared_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(mds_[a-z_]+|ipm_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(mds_[a-z0-9_]+|ipm_[a-z0-9_]+)\s*\(", src)))
 
 
 def lib_path():
