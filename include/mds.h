@@ -424,7 +424,11 @@ int mds_factor_set_grid_cap(int ctas);
  * left use the one-launch tail path; < 0 = built-in choice), "exact_rows"
  * (rows per CTA of the multi-CTA exact panel, >= 32), and the flags "no_tma",
  * "no_lookahead", "static_sched", "no_snake", "no_cprefetch", "upd_inplace",
- * "upd_main", "slow_1cta", "exact_no_ls", "f2_trsm", "no_pdl" (value 0/1).
+ * "upd_main", "slow_1cta", "exact_no_ls", "f2_trsm", "no_pdl", "ozaki" (value 0/1);
+ * for mds_condense[_batched]: "cdense_ctas" (1..8), "cdense_serial",
+ * "cdense_tma" (0/1) and "cond_group" (batched pair tiles: scenarios whose
+ * tiles are interleaved in the work order, 1..65536; bitwise identical results
+ * for every value -- each tile's sums do not depend on the order).
  * Returns MDS_ERR_ARG for an unknown key.  Not thread-safe against concurrent
  * mds_factor calls (set it between calls). */
 int mds_set_variant(const char *key, long long value);

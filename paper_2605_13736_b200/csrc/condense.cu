@@ -268,6 +268,7 @@ struct CondArgs {
   const uint2* items;
   const uint32_t* dorder;
   int split;                            // 1: walk `items` (split tiles), 0: walk `order`
+  int64_t group;                        // batched: scenarios per group (see k_condense_tiles)
   const double* val; int64_t s_val;
   const double* h_ss; int64_t s_hss;
   const double* sigma_s; int64_t s_sig;
@@ -559,8 +560,8 @@ __device__ __forceinline__ double init_value(const CondArgs& a, int64_t s, int64
 
 // ---------------------------------------------------------------------------
 // The tile kernel (see the top of the file).  Persistent CTAs take work items
-// from a queue: for batched calls item g -> (tile order position g / batch,
-// scenario g % batch); for a single system item g = items[g] (a tile, or one
+// from a queue: for batched calls item g -> (scenario group, tile order position,
+// scenario in the group); for a single system item g = items[g] (a tile, or one
 // part of a split tile).  T is the tile in shared memory, column-major.
 template <bool NORM>
 __global__ void __launch_bounds__(CW * 32, 4) k_condense_tiles(CondArgs a) {
@@ -586,8 +587,12 @@ __global__ void __launch_bounds__(CW * 32, 4) k_condense_tiles(CondArgs a) {
       const uint2 it = a.items[g];
       ij = it.x; part = it.y >> 16; nparts = it.y & 0xffff;
     } else {
-      s = g % a.batch;
-      ij = a.order[g / a.batch];
+      // (scenario group, tile in heaviest-first order, scenario in the group): the CTAs
+      // in flight gather the Q operands of a few scenarios only, so those stay in L2
+      const int64_t per = a.norder * a.group, grp = g / per, pos = g - grp * per;
+      const int64_t gs = min(a.group, a.batch - grp * a.group);
+      s = grp * a.group + pos % gs;
+      ij = a.order[pos / gs];
       if (a.active && !a.active[s]) {   // (uniform across the CTA)
         __syncthreads();                // s_item is rewritten at the top of the loop
         continue;
@@ -1060,6 +1065,7 @@ static int condense_launch(const mds_plan* P, CondArgs& a, void* work, size_t wo
   a.pbase = P->pbase; a.order = P->order; a.items = P->items; a.dorder = P->dorder;
   a.norder = P->norder; a.ndense = P->ndense;
   a.split = a.batch == 1 ? 1 : 0;
+  a.group = std::max<int64_t>(1, std::min<int64_t>(g_mds_var.cond_group, a.batch));
   if (N == 0) return MDS_OK;
   if (!a.M || a.ldm < N) return MDS_ERR_ARG;
   if (n_s > 0 && (!a.h_ss || !a.sigma_s || !a.w || (P->nnz > 0 && !a.val))) return MDS_ERR_ARG;

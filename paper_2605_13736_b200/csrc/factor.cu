@@ -1837,6 +1837,9 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
   // batch: slot x = scenario x / bt_tiles, 64-row tile x % bt_tiles below that scenario's block
   constexpr bool BT = (mode == 5 || mode == 6);
   const bool snake = (sched & 2) != 0 && !BT;
+  // (a no-op unless launched as a programmatic dependent: then the whole predecessor --
+  //  the exact panel that wrote pinfo / abort -- has completed and flushed past this point)
+  pdl_wait();
   FCtl* ctl = f.ctl;
   if (!BT && ctl->abort) return;
   const int2 pi = BT ? make_int2(0, 1) : f.pinfo[f.pidx];
@@ -2021,6 +2024,9 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
           for (int b = 0; b < 4; b++) tma_prefetch_2d(&mapA, R0 + 16 * b, C0);
         xnext = dyn ? atom_add_u64(counter, 1ull) : xnext + gridDim.x;
       }
+      // every tile of this CTA is claimed: the next kernel of the stream (the next
+      // panel's exact step) may be scheduled now; it still waits for this grid's end
+      pdl_trigger();
     }
     return;
   }
@@ -2583,12 +2589,14 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
         const FWork fn = fwork_for(p + 1);
         MDS_LAUNCH(PC_PANEL_DIAG, side, (k_panel_diag<<<1, 256, F1SMEM, side>>>(N, M, ldm, fn)));
         MDS_CUDA_TRY(cudaEventRecord(ev(p, 1), side));
+        // programmatic dependent of the exact panel (same stream): the CTAs are resident and
+        // past their prologue when it ends
         if (g_inplace)
-          MDS_LAUNCH(PC_UPDATE, st,
-                     (k_update_tma<3, false><<<gr, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched, 0ll, 0ll)));
+          MDS_LAUNCH(PC_UPDATE, st, MDS_CUDA_TRY(launch_pdl(k_update_tma<3, false>, dim3(gr), dim3(TTHREADS), TSMEM, st, N, M,
+                                                            ldm, fp, mapA, mw, ml, mapX, g_sched, 0ll, 0ll)));
         else
-          MDS_LAUNCH(PC_UPDATE, st,
-                     (k_update_tma<3, true><<<gr, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched, 0ll, 0ll)));
+          MDS_LAUNCH(PC_UPDATE, st, MDS_CUDA_TRY(launch_pdl(k_update_tma<3, true>, dim3(gr), dim3(TTHREADS), TSMEM, st, N, M,
+                                                            ldm, fp, mapA, mw, ml, mapX, g_sched, 0ll, 0ll)));
       }
       tail = next_tail;
     }

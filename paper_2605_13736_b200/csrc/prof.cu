@@ -61,6 +61,7 @@ extern "C" int mds_set_variant(const char* key, long long value) {
   if (k == "default") { v = MdsVariant(); return MDS_OK; }
   if (k == "tail_rows") { v.tail_rows = value; return MDS_OK; }
   if (k == "exact_rows") { if (value < 32) return MDS_ERR_ARG; v.exact_rows = value; return MDS_OK; }
+  if (k == "cond_group") { if (value < 1 || value > 65536) return MDS_ERR_ARG; v.cond_group = (int)value; return MDS_OK; }
   if (k == "cdense_ctas") { if (value < 1 || value > 8) return MDS_ERR_ARG; v.cdense_ctas = (int)value; return MDS_OK; }
   int* flag = k == "no_tma" ? &v.no_tma : k == "no_lookahead" ? &v.no_lookahead
             : k == "static_sched" ? &v.static_sched : k == "no_snake" ? &v.no_snake
