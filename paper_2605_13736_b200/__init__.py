@@ -542,6 +542,6 @@ def factor_panels(fwork, N):
     return buf[:n].copy()
 
 
-from .step import KKTStep, DeviceProblem  # noqa: E402,F401
+from .step import KKTStep, DeviceProblem, HostPipeline  # noqa: E402,F401
 from .batch import BatchedKKTStep  # noqa: E402,F401
 from .inertia import InertiaCorrection, ICParams  # noqa: E402,F401

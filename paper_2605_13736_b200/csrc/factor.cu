@@ -1813,6 +1813,11 @@ __device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, int c0
                "r"(c0), "r"(c1), "r"(c2), "r"(src)
                : "memory");
 }
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int c1, int c2, unsigned src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(c2), "r"(src)
+               : "memory");
+}
 __device__ __forceinline__ void sts_f64(unsigned addr, double v) {
   asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(addr), "d"(v) : "memory");
 }
@@ -1933,10 +1938,29 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
             const unsigned long long xc = xnext;
             xnext = atom_add_u64(counter, 1ull);
             const int64_t sc = (int64_t)(xc / (unsigned long long)bt_tiles);
-            const int64_t lt = (int64_t)(xc % (unsigned long long)bt_tiles);
+            int64_t lt = (int64_t)(xc % (unsigned long long)bt_tiles);
             const size_t bo = (size_t)sc * f.bws;
             const FCtl* cs = reinterpret_cast<const FCtl*>(reinterpret_cast<const char*>(f.ctl) + bo);
             if (cs->abort) continue;
+            if constexpr (mode == 5) {
+              // the first sched >> 8 slots of a scenario are its S tiles: 64-row blocks of the
+              // panel's D + L (Lb) copied into M (replaces a separate k_panel_store launch)
+              const int64_t nSmax = (int64_t)(sched >> 8);
+              if (lt < nSmax) {
+                const int2 ps = reinterpret_cast<const int2*>(reinterpret_cast<const char*>(f.pinfo) + bo)[f.pidx];
+                const int64_t k0s = ps.x;
+                if (ps.y <= 0 || lt >= (N + UT - 1) / UT - k0s / UT) continue;
+                const int R0 = (int)((k0s / UT + lt) * UT);
+                stile[st] = (long long)((0xfffffffdull << 32) | (unsigned)R0);   // C0 = -3: S tile
+                stile2[st] = (long long)(((unsigned long long)sc << 32) | (unsigned long long)k0s);
+                mbar_expect_tx(fb, TOPB);
+#pragma unroll
+                for (int b = 0; b < 4; b++) tma_load_3d(sL + b * TBOXB, &mapL, R0 + 16 * b, 0, (int)sc, fb);
+                got = true;
+                break;
+              }
+              lt -= nSmax;
+            }
             if constexpr (mode == 6) {
               const int nbps = cs->nbp;
               const int64_t k0s = cs->k0, rb = k0s + nbps;
@@ -2044,16 +2068,36 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
     const long long x2 = BT ? stile2[st] : 0;
     const int bsc = (int)(x2 >> 32);                               // BT: scenario
     const int64_t sT = BT ? (int64_t)(x2 & 0xffffffffll) : s;     // its trailing start
-    if (LA && C0 == -3) {
+    if ((LA || mode == 5) && C0 == -3) {
       // S tile: panel rows R0..R0+63 of D + L (columns < kb, on/below the diagonal) into M
+      double* Ac = A;
+      int64_t k0c = k0;
+      int kbc = kb;
+      if constexpr (mode == 5) {   // (batched: that scenario's matrix and panel)
+        Ac = A + (int64_t)bsc * f.bms;
+        k0c = sT;
+        kbc = reinterpret_cast<const int2*>(reinterpret_cast<const char*>(f.pinfo) + (size_t)bsc * f.bws)[f.pidx].y;
+      }
       const unsigned Lt = tsm + st * TSTAGEB;
+      if (mode == 5 && kbc == NB && R0 >= k0c + NB - 1) {
+        // a full block strictly below the diagonal block: one TMA store of the staged Lb rows
+        // (same swizzled 16 x 64 boxes as the load) into M
+        if (leader) {
+#pragma unroll
+          for (int b = 0; b < 4; b++) tma_store_3d(&mapA, (int)(R0 + 16 * b), (int)k0c, bsc, Lt + b * TBOXB);
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");   // stage read by the TMA unit
+          mbar_arrive(empty0 + 8 * st);
+        }
+        continue;
+      }
       const int tq = (int)threadIdx.x - 32 - grp * 128;   // 0..127 within the group
       const int i = tq & 63;
       const int64_t row = R0 + i;
 #pragma unroll 4
       for (int c = tq >> 6; c < NB; c += 2) {
         const double v = lds_f64(Lt + tma_off(i, c));
-        if (c < kb && row < N && row >= k0 + c) A[row + (k0 + c) * lda] = v;
+        if (c < kbc && row < N && row >= k0c + c) Ac[row + (k0c + c) * lda] = v;
       }
       asm volatile("bar.sync %0, 128;\n" ::"r"(grp + 1) : "memory");
       if (leader) mbar_arrive(empty0 + 8 * st);
@@ -2795,13 +2839,16 @@ extern "C" int mds_factor_batched(int64_t batch, int64_t N, double* M, int64_t l
     const int chunk = (int)(mds_cdiv(rows, 32) * 32);
     MDS_LAUNCH(PC_PANEL_SLOW, st,
                MDS_CUDA_TRY(launch_pdl(k_panel_exact, dim3(1, nb), dim3(XT), 0, st, N, M, ldm, fp, piv, chunk, 0, 0)));
-    MDS_LAUNCH(PC_PANEL_STORE, st, (k_panel_store<<<dim3(g256, 8, nb), 256, 0, st>>>(N, M, ldm, fp)));
     // trailing update of every scenario: slots per scenario = the tile count for the smallest
-    // possible trailing start (every panel before p+1 finished at least NB-1 columns)
+    // possible trailing start (every panel before p+1 finished at least NB-1 columns); the DMMA
+    // update also copies the panel into M (S tiles, the first nS slots of each scenario)
     const int64_t smin = std::min<int64_t>(N, (p + 1) * (NB - 1));
     const int64_t nt = (N + UT - 1) / UT - smin / UT;
+    const bool fold_store = N - smin > 0 && nt > 0 && !g_mds_var.ozaki;
+    if (!fold_store) MDS_LAUNCH(PC_PANEL_STORE, st, (k_panel_store<<<dim3(g256, 8, nb), 256, 0, st>>>(N, M, ldm, fp)));
     if (N - smin > 0 && nt > 0) {
-      const int64_t tb = nt * (nt + 1) / 2;
+      const int64_t nS = (N + UT - 1) / UT - (p * (NB - 1)) / UT;   // 64-row blocks of the panel (k0 >= p (NB-1))
+      const int64_t tb = nt * (nt + 1) / 2 + nS;
       const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tb * batch, sms));
       const CUtensorMap& mw = (p & 1) ? mapW1 : mapW0;
       const CUtensorMap& ml = (p & 1) ? mapL1 : mapL0;
@@ -2815,7 +2862,8 @@ extern "C" int mds_factor_batched(int64_t batch, int64_t N, double* M, int64_t l
                                                                                         batch)));
       } else {
         MDS_LAUNCH(PC_UPDATE, st,
-                   (k_update_tma<5, true><<<gr, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapA, sched, tb, batch)));
+                   (k_update_tma<5, true><<<gr, TTHREADS, TSMEM, st>>>(N, M, ldm, fp, mapA, mw, ml, mapA,
+                                                                       sched | (int)(nS << 8), tb, batch)));
       }
     }
   }

@@ -168,3 +168,83 @@ class KKTStep:
                               first_bad=int(v[5]), res_inf=v[6])
             out["sigma"] = self.sigma[: self.nb].cpu().numpy()
         return out
+
+
+class HostPipeline:
+    """Newton steps whose inputs live in HOST (pinned) memory, end to end: each step
+    uploads its inputs (the DeviceProblem arrays), runs the hot path, and downloads
+    its results (dx, inertia, step-vector scalars).  The copies of step i+1 and
+    step i-1 run on a copy stream while step i computes: two device input sets and
+    two `KKTStep`s (one plan) alternate, so the PCIe traffic overlaps the factorization
+    instead of adding to it.  Stream order alone carries every dependency (no host
+    synchronisation inside `run`)."""
+
+    IN = ("val", "h_ss", "sigma_s", "H_dd", "sigma_d", "J_d", "d_h", "r")
+
+    def __init__(self, prob, sv=None, device="cuda", use_graph=True):
+        d0 = DeviceProblem(prob, device)
+        self.dp = [d0, DeviceProblem(prob, device, plan=d0.plan)]
+        self.st = [KKTStep(dp, sv=sv, device=device) for dp in self.dp]
+        self.graphs = [s.capture() for s in self.st] if use_graph else None
+        self.comp = torch.cuda.Stream(device=device)
+        self.copy = torch.cuda.Stream(device=device)
+        self.up = [torch.cuda.Event() for _ in range(2)]
+        self.done = [torch.cuda.Event() for _ in range(2)]
+
+    def pinned_inputs(self):
+        """A pinned host copy of the current inputs (one set; the caller may refill it)."""
+        return [torch.empty(getattr(self.dp[0], k).shape, dtype=torch.float64, pin_memory=True).copy_(
+            getattr(self.dp[0], k).cpu()) for k in self.IN]
+
+    def outputs(self, k):
+        s = self.st[k]
+        o = [s.dxy, s.inertia]
+        if s.dx_s is not None:
+            o.append(s.dx_s)
+        if s.sv is not None:
+            o.append(s.vout)
+        return o
+
+    def pinned_outputs(self):
+        return [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in self.outputs(0)]
+
+    def bytes_per_step(self, host_in, host_out):
+        return (sum(t.numel() * t.element_size() for t in host_in),
+                sum(t.numel() * t.element_size() for t in host_out))
+
+    def _upload(self, k, host_in):
+        with torch.cuda.stream(self.copy):
+            self.copy.wait_event(self.done[k])       # slot k's previous step has consumed its inputs
+            for name, h in zip(self.IN, host_in):
+                getattr(self.dp[k], name).copy_(h, non_blocking=True)
+            self.up[k].record(self.copy)
+
+    def run(self, steps, host_in, host_out, start=None, end=None):
+        """`steps` Newton steps, each from `host_in` (pinned, `pinned_inputs()` layout) with the
+        results of each step written to `host_out` (`pinned_outputs()`).  `start` / `end`:
+        optional CUDA events recorded around the whole sequence (on the copy stream)."""
+        cur = torch.cuda.current_stream()
+        self.copy.wait_stream(cur)
+        self.comp.wait_stream(cur)
+        if start is not None:
+            start.record(self.copy)
+        self._upload(0, host_in)
+        for i in range(steps):
+            k = i & 1
+            self.comp.wait_event(self.up[k])
+            with torch.cuda.stream(self.comp):
+                if self.graphs is not None:
+                    self.graphs[k].replay()
+                else:
+                    self.st[k].run(stream=self.comp)
+                self.done[k].record(self.comp)
+            if i + 1 < steps:
+                self._upload(k ^ 1, host_in)          # step i+1's inputs while step i computes
+            with torch.cuda.stream(self.copy):
+                self.copy.wait_event(self.done[k])
+                for h, d in zip(host_out, self.outputs(k)):
+                    h.copy_(d, non_blocking=True)
+        if end is not None:
+            end.record(self.copy)
+        cur.wait_stream(self.copy)
+        cur.wait_stream(self.comp)
