@@ -278,11 +278,12 @@ int ipm_step_vectors(int64_t n, const double *x, const double *dx, const double 
  * [x_s (n_s) | x_d (n_d) | y_g (m_E) | y_h (m_I)] (device, caller-owned, out
  * must not alias x).  The same inputs as mds_condense (same layouts, H_dd lower
  * read).  rnorm: optional device scalar, ||out||_inf.  work: >=
- * mds_kkt_residual_workspace_size(m) bytes.  Used to check a whole Newton
+ * mds_kkt_residual_workspace_size(plan) bytes (per-tile partial sums: every
+ * entry of the lower H_dd and of J_d is read once).  Used to check a whole Newton
  * step (condense + factor + solve + recovery) against the original system, and
  * as the residual of iterative refinement.  No data errors (argument errors
  * only); deterministic (fixed-order sums). */
-size_t mds_kkt_residual_workspace_size(int64_t m);
+size_t mds_kkt_residual_workspace_size(const mds_plan *plan);
 int mds_kkt_residual(const mds_plan *plan, const double *js_val, const double *h_ss, const double *sigma_s,
                      const double *H_dd, int64_t ldh, const double *sigma_d, const double *J_d, int64_t ldj,
                      const double *d_h, double delta_w, double delta_c, const double *x, const double *b,

@@ -86,7 +86,7 @@ for _f in ("ipm_rhs", "ipm_directions", "ipm_reduce", "ipm_apply"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 _lib.mds_kkt_residual_workspace_size.restype = ctypes.c_size_t
-_lib.mds_kkt_residual_workspace_size.argtypes = [_I64]
+_lib.mds_kkt_residual_workspace_size.argtypes = [ctypes.c_void_p]
 _lib.mds_kkt_residual.argtypes = [_P, _P, _P, _P, _P, _I64, _P, _P, _I64, _P, _D, _D, _P, _P, _P, _P, _P,
                                   ctypes.c_size_t, _P]
 _lib.mds_kkt_residual.restype = ctypes.c_int
@@ -332,11 +332,16 @@ def solve(plan, N, LD, ldm, piv, rhs_c, js_val, w, r_xs, dxy, dx_s, zero_tol, fw
     _check(code, "mds_solve")
 
 
+def kkt_residual_workspace_size(plan):
+    """Bytes of device workspace mds_kkt_residual needs for this plan's dimensions."""
+    return int(_lib.mds_kkt_residual_workspace_size(plan.handle))
+
+
 def kkt_residual(plan, js_val, h_ss, sigma_s, H_dd, ldh, sigma_d, J_d, ldj, d_h, delta_w, delta_c, x, b, out,
                  rnorm=None, work=None, stream=None):
     """mds_kkt_residual: out = b - K x on the full Eq.(5) matrix (K x if b is None)."""
     if work is None:
-        work = torch.empty(int(_lib.mds_kkt_residual_workspace_size(plan.m_E + plan.m_I)), dtype=torch.uint8,
+        work = torch.empty(int(kkt_residual_workspace_size(plan)), dtype=torch.uint8,
                            device=out.device)
     code = _lib.mds_kkt_residual(plan.handle, _f64(js_val), _f64(h_ss), _f64(sigma_s), _f64(H_dd), int(ldh),
                                  _f64(sigma_d), _f64(J_d), int(ldj), _f64(d_h), float(delta_w), float(delta_c),

@@ -22,6 +22,7 @@ import numpy as np
 import torch
 
 from . import (factor_stats, ipm_apply, ipm_directions, ipm_reduce, ipm_rhs, ipm_workspace_size, kkt_residual,
+               kkt_residual_workspace_size,
                step_vectors, step_vectors_workspace_size, raise_for)
 from .inertia import InertiaCorrection
 from .step import DeviceProblem, KKTStep
@@ -57,7 +58,7 @@ class IPMSolver:
         self.zero_s = torch.zeros(max(b.n_s, 1), **f64)
         self.zero_d = torch.zeros(max(b.n_d, 1), **f64)
         self.inf_h = torch.full((max(m_I, 1),), float("inf"), **f64)
-        self.kwork = torch.empty(8 * max(m, 1), dtype=torch.uint8, device=device)   # mds_kkt_residual_workspace_size
+        self.kwork = torch.empty(kkt_residual_workspace_size(dp.plan), dtype=torch.uint8, device=device)
         # problem data over the P = [x | s] layout
         self.c = dev(qp.c)
         self.g_E = dev(qp.g_E) if b.m_E else torch.zeros(1, **f64)
