@@ -604,8 +604,9 @@ def run_ipm(args, rank, world):
     t0 = time.time()
     qp = mdsgen.qp_config(args.config)
     setup_s = time.time() - t0
-    IPMSolver(qp).solve()
     sol = IPMSolver(qp)
+    sol.solve()          # untimed: page-in, attributes, graph capture
+    sol.reset(qp)
     e0_, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clk:
         torch.cuda.synchronize()
@@ -647,6 +648,8 @@ def ipm_paper_sweep(args):
     for k in [int(v) for v in args.ipm_sweep.split(",") if v]:
         qp = mdsgen.synthetic_problem(k)
         sol = IPMSolver(qp)
+        sol.solve()      # untimed: page-in, graph capture
+        sol.reset(qp)
         torch.cuda.synchronize()
         e0_, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0_.record()

@@ -49,15 +49,26 @@ class InertiaCorrection:
     """Inertia-corrected Newton step on one `KKTStep`.  `delta_w_last` persists
     across calls (warm start of the next Newton iteration's correction)."""
 
-    def __init__(self, step, params: ICParams | None = None):
+    def __init__(self, step, params: ICParams | None = None, use_graph=False):
+        """use_graph: the unregularised first trial (delta_w = delta_c = 0, the usual
+        accepted one) and the solve replay CUDA graphs of the step (captured on first use,
+        on the caller's current stream); later trials are issued eagerly."""
         self.step = step
         self.params = params or ICParams()
         self.delta_w_last = 0.0
         self.target = (step.p.n_d, 0, step.p.m)
+        self.use_graph = use_graph
+        self._graphs = None
 
     def _attempt(self, dw, dc, trials, stream):
         self.step.p.delta_w, self.step.p.delta_c = float(dw), float(dc)
-        ine = tuple(int(v) for v in self.step.factor_phase(stream, sync_inertia=True))
+        if self.use_graph and stream is None and dw == 0.0 and dc == 0.0:
+            if self._graphs is None:
+                self._graphs = self.step.capture_phases()
+            self._graphs[0].replay()
+            ine = tuple(int(v) for v in self.step.inertia.cpu())
+        else:
+            ine = tuple(int(v) for v in self.step.factor_phase(stream, sync_inertia=True))
         trials.append((float(dw), float(dc), ine))
         # the stream is synchronised (inertia on the host): a data error of this trial
         # (NONPOSITIVE q_k / d_h, NONFINITE input) is final -- no delta_w escalation
@@ -87,5 +98,8 @@ class InertiaCorrection:
                 if dw > P.delta_w_max:                                         # IC-6
                     raise SingularError(f"inertia correction: delta_w > {P.delta_w_max:g} "
                                         f"(last inertia {ine}, target {self.target})")
-        self.step.finish_phase(stream)
+        if self._graphs is not None and stream is None and dw == 0.0 and dc == 0.0:
+            self._graphs[1].replay()
+        else:
+            self.step.finish_phase(stream)
         return dict(delta_w=dw, delta_c=dc, inertia=ine, trials=trials)

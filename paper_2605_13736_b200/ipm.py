@@ -34,7 +34,7 @@ OPTS = dict(tol=1e-8, mu0=0.1, max_iter=200, tau_min=0.99, kappa_mu=0.2, theta_m
 
 
 class IPMSolver:
-    def __init__(self, qp, opts=None, device="cuda"):
+    def __init__(self, qp, opts=None, device="cuda", use_graph=True):
         self.o = dict(OPTS, **(opts or {}))
         b = qp.base
         self.n_s, self.n_d, self.m_E, self.m_I = b.n_s, b.n_d, b.m_E, b.m_I
@@ -53,7 +53,7 @@ class IPMSolver:
         dp.r = self.r[:n + m]
         dp.delta_w = dp.delta_c = 0.0
         self.step = KKTStep(dp, device=device)
-        self.ic = InertiaCorrection(self.step)
+        self.ic = InertiaCorrection(self.step, use_graph=use_graph)
         # K0 = the Eq.(5) blocks with sigma = delta = 0, D_y = 0 (for (H x + J^T y, J x) products)
         self.zero_s = torch.zeros(max(b.n_s, 1), **f64)
         self.zero_d = torch.zeros(max(b.n_d, 1), **f64)
@@ -86,6 +86,12 @@ class IPMSolver:
         self.rwork = torch.zeros(ipm_workspace_size(n, m_I), dtype=torch.uint8, device=device)
         self.red = torch.zeros((3, 8), **f64)
         self._init_point(qp)
+
+    def reset(self, qp):
+        """Back to the initial point of `qp` (same problem data), keeping the device buffers
+        and the captured graphs: a second trajectory from the same start."""
+        self._init_point(qp)
+        self.ic.delta_w_last = 0.0
 
     # -- K0 product: out = (H v_x + J^T v_y, J v_x)
     def _k0(self, v, out):

@@ -145,6 +145,23 @@ class KKTStep:
             self.run(stream=torch.cuda.current_stream())
         return g
 
+    def capture_phases(self, warmup=1):
+        """CUDA graphs of factor_phase() (with the problem's current delta_w, delta_c, which
+        the graph bakes in) and of finish_phase(): the two halves of run() around the
+        inertia check."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self.run(stream=s)
+        torch.cuda.current_stream().wait_stream(s)
+        gf, gs = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gf):
+            self.factor_phase(stream=torch.cuda.current_stream())
+        with torch.cuda.graph(gs):
+            self.finish_phase(stream=torch.cuda.current_stream())
+        return gf, gs
+
     # -- host views --------------------------------------------------------
     def check_status(self):
         st = int(self.status.item())

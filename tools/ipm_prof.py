@@ -15,8 +15,9 @@ from paper_2605_13736_b200.ipm import IPMSolver  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C3"
 qp = mdsgen.qp_config(cfg)
-IPMSolver(qp).solve()
-s = IPMSolver(qp)
+s = IPMSolver(qp, use_graph=os.environ.get("GRAPH", "1") == "1")
+s.solve()
+s.reset(qp)
 torch.cuda.synchronize()
 t = time.perf_counter()
 r = s.solve()
@@ -25,7 +26,7 @@ wall = (time.perf_counter() - t) * 1e3
 its = max(r["iterations"], 1)
 print(f"{cfg}: {its} iterations, {wall:.1f} ms wall = {wall / its:.2f} ms/iter; newton mean "
       f"{sum(r['newton_ms']) / len(r['newton_ms']):.2f} ms")
-s = IPMSolver(qp)
+s.reset(qp)
 mds.profile_begin()
 r = s.solve()
 prof = mds.profile_end()
