@@ -672,6 +672,53 @@ def ipm_paper_sweep(args):
     return out
 
 
+def pivot_heavy_block(N, steps, dev):
+    """The C3-sized Newton matrix when Bunch-Kaufman has to pivot: factor + solve of the
+    N x N G3 matrix (prescribed spectrum, N/8 2x2 blocks, random orthogonal mixing:
+    the speculative panels fail and the exact BK columns run), timed like C5 (M restored
+    outside the events).  Context for the C3 line, whose quasi-definite matrix never
+    leaves the fast path."""
+    import torch
+
+    import mdsgen
+    import paper_2605_13736_b200 as mds
+
+    A, ine = mdsgen.g3_prescribed_torch(N, seed=3003, device=dev)
+    A0 = A.T.contiguous().reshape(-1)
+    del A
+    M = torch.empty_like(A0)
+    piv = torch.empty(2 * N, dtype=torch.int32, device=dev)
+    ine_d = torch.zeros(3, dtype=torch.int64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    fwork = torch.empty(mds.factor_workspace_size(N), dtype=torch.uint8, device=dev)
+    swork = torch.empty(mds.solve_workspace_size(N), dtype=torch.uint8, device=dev)
+    b = torch.as_tensor(np.random.default_rng(N).standard_normal(N), dtype=torch.float64, device=dev)
+    x = torch.empty(N, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def fs():
+        mds.factor(N, M, N, piv, -1.0, ine_d, status, fwork, sync=False)
+        mds.solve(None, N, M, N, piv, b, None, None, None, x, None, -1.0, fwork, status, swork)
+
+    M.copy_(A0)
+    fs()
+    torch.cuda.synchronize()
+    got = tuple(int(v) for v in ine_d.cpu())
+    stats = mds.factor_stats(fwork)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for e0, e1 in evs:
+        M.copy_(A0)
+        e0.record(stream)
+        fs()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / steps
+    return {"workload": f"G3 prescribed-spectrum N={N} ({N // 8} 2x2 blocks, orthogonally mixed), factor + solve",
+            "ms": ms, "factor_solve_per_s": 1e3 / ms, "fp64_frac_of_peak": (N ** 3 / 3.0) / (ms * 1e-3) / 1e12
+            / fp64_peak()[0], "inertia_ok": got == tuple(ine) and int(status.item()) == 0,
+            "panels": int(stats[0]), "interchanges": int(stats[1]), "exact_bk_columns": int(stats[2])}
+
+
 def run_c5(args, rank, world):
     """C5 stress: factor + solve of the N = 32768 G3 matrix (8.6 GB) per step (replicas under torchrun).
     M is restored from a device copy before every step, outside the timed region (CUDA events bracket
@@ -851,6 +898,10 @@ def main():
             import torch
             torch.cuda.empty_cache()
             line["ipm"] = run_ipm(args, rank, world)
+        if args.config == "C3" and not args.no_ipm and rank == 0 and line is not None:
+            import torch
+            torch.cuda.empty_cache()
+            line["pivot_heavy"] = pivot_heavy_block(8192, 3, torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
         if rank == 0 and line is not None:
             print(json.dumps(line), flush=True)
     if world > 1:
