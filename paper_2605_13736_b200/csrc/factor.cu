@@ -84,7 +84,7 @@ struct FWork {
   unsigned* t1flag;             // [2(N/64+4)] p+1 once panel p's update of tile (row BI, column b0+c) has landed
   unsigned* xbar;               // [N/32+8] per-panel grid-barrier counters of k_panel_exact
   ArgMax* xpart;                // [2 banks][XMAXG] its per-CTA argmax partials (bank = barrier parity)
-  double* xaux;                 // [2] |W(imax, candidate column)| published by the owner of row imax
+  double* xpay;                 // [2 banks][XMAXG][2] per-CTA payloads of those exchanges (W values of one owned row)
   const double* Wprev;          // the previous panel's W / Lb (the other parity buffers), for the
   const double* Lbprev;         //   deferred update of this panel's columns
   int fuse;           // 1: this panel's columns still lack the previous panel's update (look-ahead)
@@ -110,7 +110,7 @@ __device__ __forceinline__ void bsel_ws(FWork& f, int64_t s) {
   const size_t o = (size_t)s * f.bws;
   shp(f.ctl, o); shp(f.panel_start, o); shp(f.sw, o); shp(f.bt, o); shp(f.rho, o); shp(f.rhoinv, o);
   shp(f.nparts, o); shp(f.Lblk, o); shp(f.W, o); shp(f.W1, o); shp(f.Lb, o); shp(f.Lb1, o); shp(f.pinfo, o);
-  shp(f.ucount, o); shp(f.t1flag, o); shp(f.xbar, o); shp(f.xpart, o); shp(f.xaux, o); shp(f.Wprev, o);
+  shp(f.ucount, o); shp(f.t1flag, o); shp(f.xbar, o); shp(f.xpart, o); shp(f.xpay, o); shp(f.Wprev, o);
   shp(f.Lbprev, o); shp(f.ozL, o); shp(f.ozW, o); shp(f.ozeL, o); shp(f.ozeW, o);
 }
 
@@ -139,7 +139,7 @@ FWork carve(void* work, int64_t N, size_t* total) {
   f.t1flag = reinterpret_cast<unsigned*>(take(sizeof(unsigned) * 2 * (N / 64 + 4)));
   f.xbar = reinterpret_cast<unsigned*>(take(sizeof(unsigned) * (N / 32 + 8)));
   f.xpart = reinterpret_cast<ArgMax*>(take(sizeof(ArgMax) * 2 * XMAXG));
-  f.xaux = reinterpret_cast<double*>(take(sizeof(double) * 2));
+  f.xpay = reinterpret_cast<double*>(take(sizeof(double) * 2 * XMAXG * 2));
   f.ozL = reinterpret_cast<int8_t*>(take((size_t)8 * N * 64));
   f.ozW = reinterpret_cast<int8_t*>(take((size_t)8 * N * 64));
   f.ozeL = reinterpret_cast<int*>(take(sizeof(int) * N));
@@ -1125,8 +1125,14 @@ __global__ void __launch_bounds__(1024) k_panel_slow(int64_t N, double* __restri
 // (A variant where every CTA polled all G tagged records was slower: 128x
 // more pollers on L2.)  Banks alternate by barrier parity, so a CTA that runs
 // ahead never overwrites a partial another CTA has yet to read.
-__device__ __forceinline__ ArgMax x_exchange(unsigned* ctr, ArgMax* part, unsigned& nbar, ArgMax mine, ArgMax* sh) {
-  ArgMax* bank = part + XMAXG * (nbar & 1u);
+// pay / pay_owner / pay_out: the two payload doubles CTA pay_owner wrote into its slot of
+// this exchange's payload bank (before the exchange) are read with the partials (same
+// round trip) and left in pay_out (shared memory) for every thread.
+__device__ __forceinline__ ArgMax x_exchange(unsigned* ctr, ArgMax* part, unsigned& nbar, ArgMax mine, ArgMax* sh,
+                                             const double* pay = nullptr, int pay_owner = -1,
+                                             double* pay_out = nullptr) {
+  const unsigned bk = nbar & 1u;
+  ArgMax* bank = part + XMAXG * bk;
   if (threadIdx.x == 0) bank[blockIdx.x] = mine;
   __syncthreads();   // every global write of this CTA precedes the release below
   nbar++;
@@ -1138,9 +1144,15 @@ __device__ __forceinline__ ArgMax x_exchange(unsigned* ctr, ArgMax* part, unsign
   }
   __syncthreads();
   ArgMax a{-1.0, 0x7fffffff};
-  for (int c = threadIdx.x; c < (int)gridDim.x; c += blockDim.x)
+  for (int c = threadIdx.x; c < (int)gridDim.x; c += blockDim.x) {
     a = am_better(a, ArgMax{__ldcg(&bank[c].v), __ldcg(&bank[c].i)});
-  return block_argmax(a, sh);
+    if (c == pay_owner) {
+      const double* ps = pay + ((size_t)bk * XMAXG + c) * 2;
+      pay_out[0] = __ldcg(ps);
+      pay_out[1] = __ldcg(ps + 1);
+    }
+  }
+  return block_argmax(a, sh);   // (its block barriers publish pay_out)
 }
 
 // own rows r in [rlo, rhi), r >= k:  W(r, wcol) = a_r - sum_{t<j} Lb(r, t) wv[t], with
@@ -1157,6 +1169,9 @@ __device__ __forceinline__ ArgMax x_gemv(const double* A, int64_t lda, const dou
   for (int64_t rb = rfirst; rb < rhi; rb += XROWS) {
     const int64_t r = rb + (tid >> 2);
     const bool live = r < rhi && r >= k;
+    double a = 0.0;   // issued before the dot product (its latency overlaps it)
+    if (live && qd == 0)
+      a = IMAX ? ((r < kc) ? __ldcg(&A[kc + r * lda]) : __ldcg(&A[r + kc * lda])) : __ldcg(&A[r + kc * lda]);
     double s0 = 0.0, s1 = 0.0;
     if (live && Ls) {   // the CTA's rows of the panel's finished columns, kept in shared memory
       const double* lr = Ls + (r - rlo);
@@ -1179,11 +1194,13 @@ __device__ __forceinline__ ArgMax x_gemv(const double* A, int64_t lda, const dou
     s += __shfl_xor_sync(0xffffffffu, s, 1);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
     if (live && qd == 0) {
-      const double a = IMAX ? ((r < kc) ? __ldcg(&A[kc + r * lda]) : __ldcg(&A[r + kc * lda])) : __ldcg(&A[r + kc * lda]);
       const double v = a - s;
       W[r + wcol * ldw] = v;
       if (IMAX ? (r != kc) : (r > k)) am = am_better(am, ArgMax{fabs(v), (int)r});
-      if (IMAX && r == kc) *aux = fabs(v);
+      // payload of the row the decision needs, published through the exchange (no reload):
+      // W(k, j) by the owner of row k; W(imax, j+1) and W(imax, j) by the owner of row imax
+      if (!IMAX && r == k) aux[0] = v;
+      if (IMAX && r == kc) { aux[0] = v; aux[1] = __ldcg(&W[r + (wcol - 1) * ldw]); }
     }
   }
   return am;
@@ -1303,6 +1320,7 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
   }
   extern __shared__ double xls[];
   __shared__ ArgMax sh[33];
+  __shared__ double s_pay[2];
   unsigned* ctr = f.xbar + f.pidx;   // this panel's barrier counter (zeroed by k_factor_init)
   unsigned nbar = 0;                 // barriers so far
   if (f2left) {
@@ -1374,10 +1392,13 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
       for (int t = tid; t < j; t += XT) wrow[t] = __ldcg(&W[k + t * ldw]);
       __syncthreads();
       // W(k:N, j) = A(k:N, k) - L(k:N, panel) W(k, panel)^T ; colmax / imax below k
-      ArgMax am = x_gemv<false>(A, lda, Lb, W, ldw, rlo, rhi, k, k, j, j, wrow, nullptr, Ls, lstr);
+      double* myslot = f.xpay + ((size_t)(nbar & 1u) * XMAXG + blockIdx.x) * 2;
+      ArgMax am = x_gemv<false>(A, lda, Lb, W, ldw, rlo, rhi, k, k, j, j, wrow, myslot, Ls, lstr);
       am = block_argmax(am, sh);
-      am = x_exchange(ctr, f.xpart, nbar, am, sh);
-      const double absakk = fabs(__ldcg(&W[k + j * ldw]));
+      am = x_exchange(ctr, f.xpart, nbar, am, sh, f.xpay, (int)((k - k0) / chunk), s_pay);
+      const double wkk = s_pay[0];   // W(k, j), from the owner of row k
+      const double absakk = fabs(wkk);
+      double wij1 = 0.0, wij = 0.0;   // W(imax, j+1), W(imax, j) (candidate path)
       const double colmax = (am.v < 0.0) ? 0.0 : am.v;
       const int64_t imax = (am.v < 0.0) ? k : am.i;
       int kstep = 1;
@@ -1390,13 +1411,15 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
       } else {
         for (int t = tid; t < j; t += XT) wrow[t] = __ldcg(&W[imax + t * ldw]);
         __syncthreads();
-        // candidate column imax, updated: W(k:N, j+1); |W(imax, j+1)| published by its owner
-        const unsigned sl = nbar & 1u;
-        ArgMax rm = x_gemv<true>(A, lda, Lb, W, ldw, rlo, rhi, k, imax, j, j + 1, wrow, f.xaux + sl, Ls, lstr);
+        // candidate column imax, updated: W(k:N, j+1); W(imax, j+1) and W(imax, j) published by its owner
+        double* pslot = f.xpay + ((size_t)(nbar & 1u) * XMAXG + blockIdx.x) * 2;
+        ArgMax rm = x_gemv<true>(A, lda, Lb, W, ldw, rlo, rhi, k, imax, j, j + 1, wrow, pslot, Ls, lstr);
         rm = block_argmax(rm, sh);
-        rm = x_exchange(ctr, f.xpart, nbar, rm, sh);
+        rm = x_exchange(ctr, f.xpart, nbar, rm, sh, f.xpay, (int)((imax - k0) / chunk), s_pay);
         const double rowmax = (rm.v < 0.0) ? 0.0 : rm.v;
-        const double wii = __ldcg(f.xaux + sl);
+        wij1 = s_pay[0];
+        wij = s_pay[1];
+        const double wii = fabs(wij1);
         if (absakk >= ALPHA_BK * colmax * (colmax / rowmax)) {
           kp = k;
         } else if (wii >= ALPHA_BK * rowmax) {
@@ -1447,7 +1470,7 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
         }
       }
       if (kstep == 1) {
-        const double d = __ldcg(&W[k + j * ldw]);
+        const double d = cand ? wij1 : wkk;   // W(k, j) after the interchange (the candidate column's W(imax, j+1) if cand)
         const double r1 = zero ? 0.0 : 1.0 / d;
         for (int64_t r = rlo + tid; r < rhi; r += XT) {
           if (r <= k) continue;
@@ -1465,9 +1488,10 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
           f.bt[k] = 0;
         }
       } else {
-        const double w21 = __ldcg(&W[(k + 1) + j * ldw]);
-        const double w22 = __ldcg(&W[(k + 1) + (j + 1) * ldw]);
-        const double w11 = __ldcg(&W[k + j * ldw]);
+        // rows k+1 <-> kp = imax interchanged: W(k+1, j) = W(imax, j), W(k+1, j+1) = W(imax, j+1)
+        const double w21 = wij;
+        const double w22 = wij1;
+        const double w11 = wkk;
         double d21 = w21;
         const double d11 = w22 / d21;
         const double d22 = w11 / d21;
