@@ -547,6 +547,43 @@ def run_scopf(args, rank, world, emit=True):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
+    # end to end: every step uploads the local batch's inputs from pinned host memory and
+    # downloads its results (directions, inertias, step-vector scalars); copies not overlapped
+    e2e = None
+    if not args.no_e2e:
+        bt = batch.bt
+        ins = [bt.val, bt.h_ss, bt.sigma_s, bt.H_dd, bt.sigma_d, bt.J_d, bt.d_h, bt.r]
+        host = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True).copy_(x.cpu()) for x in ins]
+        outs = [bt.dirn, bt.inertia] + ([bt.vout] if bt.sv is not None else [])
+        hout = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in outs]
+        h2d = sum(x.numel() * x.element_size() for x in host)
+        d2h = sum(x.numel() * x.element_size() for x in hout)
+
+        def e2e_step():
+            for d_, h_ in zip(ins, host):
+                d_.copy_(h_, non_blocking=True)
+            batch.newton_step()
+            for h_, d_ in zip(hout, outs):
+                h_.copy_(d_, non_blocking=True)
+            return batch.stop_test()
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": args.scenarios * args.steps / (float(te.item()) / 1e3), "unit": "scenario_newton_iters/s",
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+               "note": "per step the whole batch's inputs cross PCIe (~25 MB per scenario), not overlapped"}
+        del host, hout
     recs = scopf.gather_records(batch.records, args.scenarios)
     value = args.scenarios * args.steps / (ms_max / 1e3)
     if rank == 0:
@@ -582,7 +619,7 @@ def run_scopf(args, rank, world, emit=True):
                 "kernels": {c: {"ms": round(v[0], 4), "launches": v[1]} for c, v in prof.items() if v[1]},
                 "stop_test": st, "records_gathered": int(recs.shape[0]),
                 "all_inertia_ok": bool(st["n_bad_inertia"] == 0), "setup_s": setup_s,
-                "clocks": clk.summary(), "e2e": None, "cpu_baseline": None}
+                "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": None}
         if emit:
             print(json.dumps(line), flush=True)
         return line
@@ -891,7 +928,7 @@ def main():
                 line["scopf"] = {k: sc[k] for k in ("value", "unit", "n_gpus", "ms_per_step", "scaling",
                                                     "gpu_launches", "factor_solve_fp64_tflops_aggregate",
                                                     "factor_solve_frac_of_peak", "all_inertia_ok", "roofline",
-                                                    "clocks")}
+                                                    "clocks", "e2e")}
                 line["scopf"]["workload"] = sc["config"]["workload"]
                 line["scopf"]["collectives_per_step"] = "1 MAX + 1 SUM all_reduce of 5 + 2 doubles (NCCL)"
         if args.config == "C3" and not args.no_ipm and rank == 0 and line is not None:
