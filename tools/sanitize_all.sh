@@ -14,7 +14,7 @@ run() {  # tool case timeout
   echo "rc=$rc" | tee -a "$out/summary.txt"
 }
 python tools/sanitize_case.py c1 > /dev/null 2>&1   # warm (page in torch)
-for c in c1 c2 g3_700 g4_300 batched; do run memcheck $c 900; done
-for c in c1 g3_700 batched; do run racecheck $c 1200; done
-for c in c1 g3_700 batched; do run synccheck $c 900; done
+for c in c1 c2 g3_700 g4_300 batched ipm pipeline; do run memcheck $c 900; done
+for c in c1 g3_700 batched ipm; do run racecheck $c 1200; done
+for c in c1 g3_700 batched ipm; do run synccheck $c 900; done
 run initcheck c1 600

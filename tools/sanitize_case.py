@@ -1,7 +1,7 @@
 """One small hot-path invocation for compute-sanitizer (memcheck / racecheck /
 synccheck / initcheck), run eagerly (no CUDA graph) through the C-ABI.
 
-usage: python tools/sanitize_case.py {c1|c2|g3_700|g4_300|batched}
+usage: python tools/sanitize_case.py {c1|c2|g3_700|g4_300|batched|ipm|pipeline}
 Exit 0 iff the case ran and matched the oracle's inertia (the sanitizer's own
 report decides the rest)."""
 import os
@@ -66,6 +66,23 @@ def main():
         outs = [bt.results(i) for i in range(3)]
         ok = all(o["inertia"] == tuple(p.expected_inertia) and o["status"] == 0 for o, p in zip(outs, probs))
         print(case, [o["inertia"] for o in outs], [o["status"] for o in outs])
+    elif case == "ipm":
+        # small convex QP, eager: K0 products (mds_kkt_residual tiles), the IPM vector kernels,
+        # inertia correction, the hot path per Newton iteration
+        from paper_2605_13736_b200.ipm import IPMSolver
+        qp = mdsgen.qp_problem(2000, 40, 15, 20, seed=5)
+        res = IPMSolver(qp, use_graph=False).solve()
+        ok = res["status"] == "Optimal"
+        print(case, res["status"], res["iterations"], res["e0"])
+    elif case == "pipeline":
+        prob = mdsgen.config_problem("C1")
+        sv = mdsgen.step_vectors_for(prob, seed=1)
+        pipe = mds.HostPipeline(prob, sv=sv, use_graph=False)
+        host, hout = pipe.pinned_inputs(), pipe.pinned_outputs()
+        pipe.run(3, host, hout)
+        torch.cuda.synchronize()
+        ok = tuple(int(v) for v in hout[1]) == tuple(prob.expected_inertia)
+        print(case, tuple(int(v) for v in hout[1]))
     else:
         raise SystemExit(f"unknown case {case}")
     sys.exit(0 if ok else 1)
