@@ -136,16 +136,26 @@ __global__ void __launch_bounds__(256) k_res_final(int64_t n_s, int64_t n_d, int
   if (i < n_d) {
     const int64_t bb = i / RT, e = i % RT, ns = a.nbd + 1 + a.nbm;
     const double* p = a.pd + bb * ns * RT + e;
-    double v = 0.0;
-    for (int64_t sl = 0; sl < ns; sl++) v += p[sl * RT];
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;   // four interleaved partial sums (fixed order)
+    int64_t sl = 0;
+    for (; sl + 4 <= ns; sl += 4) {
+      v0 += p[sl * RT]; v1 += p[(sl + 1) * RT]; v2 += p[(sl + 2) * RT]; v3 += p[(sl + 3) * RT];
+    }
+    for (; sl < ns; sl++) v0 += p[sl * RT];
+    double v = (v0 + v1) + (v2 + v3);
     v += (sigma_d[i] + delta_w) * x[n_s + i];
     const int64_t o = n_s + i;
     out[o] = b ? b[o] - v : v;
   } else if (i < n_d + m) {
     const int64_t c = i - n_d, cb = c / RT, e = c % RT;
     const double* p = a.py + cb * a.nbd * RT + e;
-    double v = ys[c];
-    for (int64_t sl = 0; sl < a.nbd; sl++) v += p[sl * RT];
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    int64_t sl = 0;
+    for (; sl + 4 <= a.nbd; sl += 4) {
+      v0 += p[sl * RT]; v1 += p[(sl + 1) * RT]; v2 += p[(sl + 2) * RT]; v3 += p[(sl + 3) * RT];
+    }
+    for (; sl < a.nbd; sl++) v0 += p[sl * RT];
+    double v = ys[c] + ((v0 + v1) + (v2 + v3));
     const double yc = x[n_s + n_d + c];
     const double dy = (c >= m_E ? 1.0 / d_h[c - m_E] : 0.0) + delta_c;
     v -= dy * yc;
@@ -162,19 +172,25 @@ __global__ void k_res_y(int64_t m, const int32_t* __restrict__ tptr, const int2*
   const int lane = threadIdx.x & 31;
   const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (c >= m) return;
-  double v0 = 0.0, v1 = 0.0;
+  constexpr int U = 4;   // independent entries (gathers) in flight per lane
+  double acc[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) acc[u] = 0.0;
   const int32_t e1 = tptr[c + 1];
-  int32_t e = tptr[c] + lane;
-  for (; e + 32 < e1; e += 64) {
-    const int2 k0 = tkp[e], k1 = tkp[e + 32];
-    v0 += val[(unsigned)k0.y & TKP_PMASK_R] * x[k0.x];
-    v1 += val[(unsigned)k1.y & TKP_PMASK_R] * x[k1.x];
+  for (int32_t e = tptr[c] + lane; e < e1; e += 32 * U) {
+    int2 kp[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) kp[u] = (e + 32 * u < e1) ? tkp[e + 32 * u] : make_int2(-1, 0);
+    double pv[U], xv[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      pv[u] = (kp[u].x >= 0) ? val[(unsigned)kp[u].y & TKP_PMASK_R] : 0.0;
+      xv[u] = (kp[u].x >= 0) ? x[kp[u].x] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) acc[u] = fma(pv[u], xv[u], acc[u]);
   }
-  if (e < e1) {
-    const int2 k0 = tkp[e];
-    v0 += val[(unsigned)k0.y & TKP_PMASK_R] * x[k0.x];
-  }
-  const double v = warp_sum(v0 + v1);
+  const double v = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
   if (lane == 0) ys[c] = v;
 }
 
