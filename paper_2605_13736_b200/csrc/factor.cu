@@ -248,11 +248,19 @@ __device__ __forceinline__ unsigned smid() { unsigned r; asm volatile("mov.u32 %
 #define UTRACE_MAX(p, k) atomicMax(&g_utrace[p][k], gtimer())
 #define UTRACE_ADD(p, k) atomicAdd(&g_utrace[p][k], 1ull)
 __device__ unsigned long long g_f4trace[4096][2];   // k_panel_exact: [0] first CTA past pdl_wait (min), [1] last exit (max)
+// per-phase cycles of CTA 0 of k_panel_exact, summed over all exact columns (tools/exact_trace.cu)
+__device__ unsigned long long g_xph[10];
+#define XPH_DECL unsigned long long xph_t = clock64()
+#define XPH(i) do { if (threadIdx.x == 0 && blockIdx.x == 0) { const unsigned long long t_ = clock64(); atomicAdd(&g_xph[i], t_ - xph_t); xph_t = t_; } } while (0)
+#define XPH_COUNT atomicAdd(&g_xph[9], 1ull)
 #define F4TRACE_MIN(p) do { if (threadIdx.x == 0 && (p) < 4096) atomicMin(&g_f4trace[p][0], gtimer()); } while (0)
 #define F4TRACE_MAX(p) do { if (threadIdx.x == 0 && (p) < 4096) atomicMax(&g_f4trace[p][1], gtimer()); } while (0)
 #else
 #define F4TRACE_MIN(p) do { } while (0)
 #define F4TRACE_MAX(p) do { } while (0)
+#define XPH_DECL do { } while (0)
+#define XPH(i) do { } while (0)
+#define XPH_COUNT do { } while (0)
 #define UTRACE_MIN(p, k) do { } while (0)
 #define UTRACE_MAX(p, k) do { } while (0)
 #define UTRACE_ADD(p, k) do { } while (0)
@@ -1388,14 +1396,19 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
       __syncthreads();
     }
     while (j < jlim) {
+      XPH_DECL;
       const int64_t k = k0 + j;
       for (int t = tid; t < j; t += XT) wrow[t] = __ldcg(&W[k + t * ldw]);
       __syncthreads();
+      XPH(0);
       // W(k:N, j) = A(k:N, k) - L(k:N, panel) W(k, panel)^T ; colmax / imax below k
       double* myslot = f.xpay + ((size_t)(nbar & 1u) * XMAXG + blockIdx.x) * 2;
       ArgMax am = x_gemv<false>(A, lda, Lb, W, ldw, rlo, rhi, k, k, j, j, wrow, myslot, Ls, lstr);
+      XPH(1);
       am = block_argmax(am, sh);
+      XPH(2);
       am = x_exchange(ctr, f.xpart, nbar, am, sh, f.xpay, (int)((k - k0) / chunk), s_pay);
+      XPH(3);
       const double wkk = s_pay[0];   // W(k, j), from the owner of row k
       const double absakk = fabs(wkk);
       double wij1 = 0.0, wij = 0.0;   // W(imax, j+1), W(imax, j) (candidate path)
@@ -1430,6 +1443,7 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
           kstep = 2;
         }
       }
+      XPH(4);   // (the candidate path, when taken)
       const int64_t kk = k + kstep - 1;
       if (kp != kk) {
         // symmetric interchange kk <-> kp of the not-yet-factored part: owners of rows r
@@ -1469,6 +1483,7 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
           // (ordered before the next GEMV by the barriers below)
         }
       }
+      XPH(5);   // (the interchange, when taken)
       if (kstep == 1) {
         const double d = cand ? wij1 : wkk;   // W(k, j) after the interchange (the candidate column's W(imax, j+1) if cand)
         const double r1 = zero ? 0.0 : 1.0 / d;
@@ -1516,7 +1531,10 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
           f.bt[k + 1] = 2;
         }
       }
+      XPH(6);   // scaling
       __syncthreads();
+      XPH(7);
+      if (threadIdx.x == 0 && blockIdx.x == 0) XPH_COUNT;
       j += kstep;
     }
   }
