@@ -106,20 +106,23 @@ class ClockSampler:
 
 def update_traffic():
     """DRAM bytes (read + write) of the one k_update_tma launch captured with ncu --set full
-    (profiles/ncu_k_update_tma_r01.csv, C3 panel 10: trailing order n2 = 7488) and that launch's
-    algorithmic bytes (C lower read + written once, L21 and W21 panels read once)."""
-    path = os.path.join(ROOT, "profiles", "ncu_k_update_tma_r01.csv")
-    try:
-        import csv
-        rows = list(csv.reader(open(path)))
-        d = dict(zip(rows[0], rows[1]))
-        b = (float(d["dram__bytes_read.sum"]) + float(d["dram__bytes_write.sum"])) * 1e6
-        n2 = 7488
-        alg = 2 * 8 * n2 * (n2 + 1) / 2 + 2 * 8 * n2 * 64
-        return b, {"source": "profiles/ncu_k_update_tma_r01.csv", "launch": "C3 panel 10, n2 = 7488",
-                   "dram_bytes": b, "algorithmic_bytes": alg, "ratio": b / alg}
-    except Exception:
-        return None, None
+    (profiles/ncu_k_update_tma_r02.csv, C3 panel 10: trailing order n2 = 7488; r01 as fallback)
+    and that launch's algorithmic bytes (C lower read + written once, L21 and W21 read once)."""
+    import csv
+    n2 = 7488
+    alg = 2 * 8 * n2 * (n2 + 1) / 2 + 2 * 8 * n2 * 64
+    for tag, cols, scale in (("r02", ("dram__bytes_read.sum [bytes]", "dram__bytes_write.sum [bytes]"), 1.0),
+                             ("r01", ("dram__bytes_read.sum", "dram__bytes_write.sum"), 1e6)):
+        path = os.path.join(ROOT, "profiles", f"ncu_k_update_tma_{tag}.csv")
+        try:
+            rows = list(csv.reader(open(path)))
+            d = dict(zip(rows[0], rows[1]))
+            b = (float(d[cols[0]]) + float(d[cols[1]])) * scale
+            return b, {"source": f"profiles/ncu_k_update_tma_{tag}.csv", "launch": "C3 panel 10, n2 = 7488",
+                       "dram_bytes": b, "algorithmic_bytes": alg, "ratio": b / alg}
+        except Exception:
+            continue
+    return None, None
 
 
 def fp64_peak():

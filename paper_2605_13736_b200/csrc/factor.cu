@@ -1379,7 +1379,6 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
   if (j < jlim) {
     __shared__ double wrow[WCOLS];
     const double tol = ctl->tol;
-    const int G = (int)gridDim.x;
     const int64_t chunk = xchunk;   // host: >= ceil((N - k0) / G), multiple of 32
     // the CTA's rows of L (panel columns) in shared memory: Ls[t * lstr + row - rlo]
     // (lstr = 8 mod 16: the 4 k-lanes of a quad fall in opposite bank halves pairwise)
