@@ -77,6 +77,7 @@ struct MdsVariant {
   long long exact_rows = 256;   // rows per CTA of k_panel_exact
   int no_tma = 0, no_lookahead = 0, static_sched = 0, no_snake = 0, no_cprefetch = 0;
   int upd_inplace = 0, upd_main = 0, slow_1cta = 0, exact_no_ls = 0, f2_trsm = 0, no_pdl = 0;
+  int no_cluster = 0;   // 1: the exact panel always on the global-counter grid barrier (no cluster launch)
   int ozaki = 0;   // trailing update in emulated FP64 on the INT8 tensor cores (ozaki.cuh)
   int cdense_ctas = 2;   // CTAs per SM of k_condense_dense (runs beside the pair chain)
   int cdense_serial = 0; // 1: k_condense_dense on the caller's stream (no fork)

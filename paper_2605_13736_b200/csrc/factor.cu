@@ -1163,6 +1163,37 @@ __device__ __forceinline__ ArgMax x_exchange(unsigned* ctr, ArgMax* part, unsign
   return block_argmax(a, sh);   // (its block barriers publish pay_out)
 }
 
+// The same exchange inside ONE thread-block cluster (the exact panel launched as a
+// cluster of G <= 16 CTAs): the argmax partials go to CTA 0's shared memory over DSMEM
+// and the hardware cluster barrier (release / acquire at cluster scope, global memory
+// included) replaces the global counter -- ~0.7 instead of ~1.75 us (tools/barrier_bench).
+// The payloads stay in global memory (ordered by the same barrier).
+constexpr int XCL = 16;
+struct ClBank {
+  ArgMax rec[2][XCL];
+};
+__device__ __forceinline__ ArgMax x_exchange_cl(ClBank* local, unsigned& nbar, ArgMax mine, ArgMax* sh,
+                                                const double* pay = nullptr, int pay_owner = -1,
+                                                double* pay_out = nullptr) {
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned bk = nbar & 1u;
+  ClBank* b0 = cl.map_shared_rank(local, 0);
+  if (threadIdx.x == 0) b0->rec[bk][cl.block_rank()] = mine;
+  nbar++;
+  cl.sync();
+  ArgMax a{-1.0, 0x7fffffff};
+  const int G = (int)cl.num_blocks();
+  for (int c = threadIdx.x; c < G; c += blockDim.x) {
+    a = am_better(a, b0->rec[bk][c]);
+    if (c == pay_owner) {
+      const double* ps = pay + ((size_t)bk * XMAXG + c) * 2;
+      pay_out[0] = __ldcg(ps);
+      pay_out[1] = __ldcg(ps + 1);
+    }
+  }
+  return block_argmax(a, sh);
+}
+
 // own rows r in [rlo, rhi), r >= k:  W(r, wcol) = a_r - sum_{t<j} Lb(r, t) wv[t], with
 // a_r = A(r, kc) (column kc; for IMAX the row/column kc = imax of the lower triangle);
 // a quad of threads per row (t strided by 4, fixed-order shuffle sum).  Returns the CTA's
@@ -1308,6 +1339,7 @@ __device__ __noinline__ void x_f2_leftovers(int64_t N, const double* __restrict_
   }
 }
 
+template <bool CL>
 __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restrict__ A, int64_t lda, FWork f,
                                                     int32_t* piv, int xchunk, int use_ls, int f2left) {
   bsel_ws(f, blockIdx.y);
@@ -1329,8 +1361,14 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
   extern __shared__ double xls[];
   __shared__ ArgMax sh[33];
   __shared__ double s_pay[2];
+  __shared__ ClBank clb;             // (CL: CTA 0's copy receives the partials)
   unsigned* ctr = f.xbar + f.pidx;   // this panel's barrier counter (zeroed by k_factor_init)
   unsigned nbar = 0;                 // barriers so far
+  // grid exchange: the global counter, or the cluster barrier (CL)
+  auto xch = [&](ArgMax mine, const double* pay, int owner, double* out) -> ArgMax {
+    if constexpr (CL) return x_exchange_cl(&clb, nbar, mine, sh, pay, owner, out);
+    else return x_exchange(ctr, f.xpart, nbar, mine, sh, pay, owner, out);
+  };
   if (f2left) {
     // this panel's F2 tiles the previous panel's trailing update did not take (replaces a
     // separate k_panel_trsm launch on the critical hand-off); colmax is complete after the barrier
@@ -1340,7 +1378,7 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
     const int64_t cfirst = (claimed < (unsigned long long)ntile) ? (int64_t)claimed : ntile;
     if (cfirst < ntile) {
       x_f2_leftovers(N, A, lda, f, k0, nbp, cfirst, ntile, xls);
-      x_exchange(ctr, f.xpart, nbar, ArgMax{-1.0, 0x7fffffff}, sh);
+      xch(ArgMax{-1.0, 0x7fffffff}, nullptr, -1, nullptr);
     }
   }
   // ---- accepted prefix (every CTA computes p; CTA 0 records it)
@@ -1406,7 +1444,7 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
       XPH(1);
       am = block_argmax(am, sh);
       XPH(2);
-      am = x_exchange(ctr, f.xpart, nbar, am, sh, f.xpay, (int)((k - k0) / chunk), s_pay);
+      am = xch(am, f.xpay, (int)((k - k0) / chunk), s_pay);
       XPH(3);
       const double wkk = s_pay[0];   // W(k, j), from the owner of row k
       const double absakk = fabs(wkk);
@@ -1427,7 +1465,7 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
         double* pslot = f.xpay + ((size_t)(nbar & 1u) * XMAXG + blockIdx.x) * 2;
         ArgMax rm = x_gemv<true>(A, lda, Lb, W, ldw, rlo, rhi, k, imax, j, j + 1, wrow, pslot, Ls, lstr);
         rm = block_argmax(rm, sh);
-        rm = x_exchange(ctr, f.xpart, nbar, rm, sh, f.xpay, (int)((imax - k0) / chunk), s_pay);
+        rm = xch(rm, f.xpay, (int)((imax - k0) / chunk), s_pay);
         const double rowmax = (rm.v < 0.0) ? 0.0 : rm.v;
         wij1 = s_pay[0];
         wij = s_pay[1];
@@ -1471,7 +1509,7 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
             }
           }
         }
-        x_exchange(ctr, f.xpart, nbar, ArgMax{-1.0, 0x7fffffff}, sh);
+        xch(ArgMax{-1.0, 0x7fffffff}, nullptr, -1, nullptr);
         if (use_ls) {   // rows kk / kp of L were swapped by CTA 0: refresh this CTA's copies
           const int nl = j;   // finished columns (column j itself is rewritten by the scaling below)
           for (int c = tid; c < 2 * nl; c += XT) {
@@ -1553,6 +1591,7 @@ __global__ void __launch_bounds__(XT) k_panel_exact(int64_t N, double* __restric
       f.Lb[r + c * ldw] = 0.0;
     }
   }
+  if constexpr (CL) cg::this_cluster().sync();   // CTA 0's shared bank outlives every reader
   F4TRACE_MAX(f.pidx);
 }
 
@@ -2589,22 +2628,63 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
   const bool f4_one_cta = g_mds_var.slow_1cta != 0;   // A/B: the single-CTA k_panel_slow
   const bool f4_no_ls = g_mds_var.exact_no_ls != 0;   // A/B: L rows read from L2
   const bool no_f2fold = g_mds_var.f2_trsm != 0;       // A/B: leftover F2 tiles by k_panel_trsm
-  if (mds_once_per_device((const void*)k_panel_exact))
-    cudaFuncSetAttribute(k_panel_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, XLS_MAX);
+  static thread_local int cl_ok = -1;   // (per thread; the attribute calls are idempotent)
+  if (mds_once_per_device((const void*)k_panel_exact<false>)) {
+    cudaFuncSetAttribute(k_panel_exact<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, XLS_MAX);
+    cudaFuncSetAttribute(k_panel_exact<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, XLS_MAX);
+    cudaFuncSetAttribute(k_panel_exact<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cl_ok = -1;
+  }
+  if (cl_ok < 0) {   // can a 16-CTA cluster with the full shared-memory request be resident?
+    cudaLaunchConfig_t qc = {};
+    qc.gridDim = dim3(XCL);
+    qc.blockDim = dim3(XT);
+    qc.dynamicSmemBytes = XLS_MAX;
+    cudaLaunchAttribute qa[1];
+    qa[0].id = cudaLaunchAttributeClusterDimension;
+    qa[0].val.clusterDim.x = XCL; qa[0].val.clusterDim.y = 1; qa[0].val.clusterDim.z = 1;
+    qc.attrs = qa;
+    qc.numAttrs = 1;
+    int ncl = 0;
+    cl_ok = (cudaOccupancyMaxActiveClusters(&ncl, k_panel_exact<true>, &qc) == cudaSuccess && ncl > 0) ? 1 : 0;
+    (void)cudaGetLastError();
+  }
   auto launch_f4 = [&](const FWork& fp, int64_t rows, int f2left) -> int {
     if (f4_one_cta) {
       MDS_LAUNCH(PC_PANEL_SLOW, st, MDS_CUDA_TRY(launch_pdl(k_panel_slow, dim3(1), dim3(1024), 0, st, N, M, ldm, fp, piv)));
       return MDS_OK;
     }
     const int64_t xrows = std::max<long long>(32, g_mds_var.exact_rows);
-    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>({mds_cdiv(rows, xrows), (int64_t)sms, (int64_t)XMAXG}));
+    // one thread-block cluster when its <= 16 CTAs keep their L rows in shared memory
+    // (cluster barrier instead of the global counter); not for concurrent factorizations
+    const bool cl = cl_ok == 1 && !capped && !f4_no_ls && !g_mds_var.no_cluster &&
+                    rows <= (int64_t)XCL * ((XLS_MAX / (NB * 8) - 8) / 32 * 32);
+    const unsigned g = cl ? (unsigned)std::max<int64_t>(1, std::min<int64_t>(mds_cdiv(rows, xrows), XCL))
+                          : (unsigned)std::max<int64_t>(1, std::min<int64_t>({mds_cdiv(rows, xrows), (int64_t)sms, (int64_t)XMAXG}));
     const int chunk = (int)(mds_cdiv(mds_cdiv(std::max<int64_t>(rows, 1), g), 32) * 32);
     const size_t lsb = (size_t)NB * (chunk + 8) * sizeof(double);
     // (not for concurrent factorizations: a large shared-memory request per CTA would compete
     //  with the other streams' kernels even when no column takes the exact path)
     const int use_ls = (lsb <= (size_t)XLS_MAX && !f4_no_ls && !capped) ? 1 : 0;
     const size_t dsm = std::max<size_t>(use_ls ? lsb : 0, f2left ? usmem : 0);
-    MDS_LAUNCH(PC_PANEL_SLOW, st, MDS_CUDA_TRY(launch_coop_pdl(k_panel_exact, dim3(g), dim3(XT), dsm, st, N, M, ldm,
+    if (cl && use_ls) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(g);
+      cfg.blockDim = dim3(XT);
+      cfg.dynamicSmemBytes = dsm;
+      cfg.stream = st;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = g; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = g_mds_var.no_pdl ? 1 : 2;
+      MDS_LAUNCH(PC_PANEL_SLOW, st, MDS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_panel_exact<true>, N, M, ldm, fp, piv, chunk,
+                                                                    use_ls, f2left)));
+      return MDS_OK;
+    }
+    MDS_LAUNCH(PC_PANEL_SLOW, st, MDS_CUDA_TRY(launch_coop_pdl(k_panel_exact<false>, dim3(g), dim3(XT), dsm, st, N, M, ldm,
                                                                fp, piv, chunk, use_ls, f2left)));
     return MDS_OK;
   };
@@ -2879,7 +2959,7 @@ extern "C" int mds_factor_batched(int64_t batch, int64_t N, double* M, int64_t l
     // F4 on one CTA per scenario (rows in one chunk, L rows read through L2; no grid barrier partners)
     const int chunk = (int)(mds_cdiv(rows, 32) * 32);
     MDS_LAUNCH(PC_PANEL_SLOW, st,
-               MDS_CUDA_TRY(launch_pdl(k_panel_exact, dim3(1, nb), dim3(XT), 0, st, N, M, ldm, fp, piv, chunk, 0, 0)));
+               MDS_CUDA_TRY(launch_pdl(k_panel_exact<false>, dim3(1, nb), dim3(XT), 0, st, N, M, ldm, fp, piv, chunk, 0, 0)));
     // trailing update of every scenario: slots per scenario = the tile count for the smallest
     // possible trailing start (every panel before p+1 finished at least NB-1 columns); the DMMA
     // update also copies the panel into M (S tiles, the first nS slots of each scenario)
