@@ -197,17 +197,34 @@ __global__ void __launch_bounds__(IT) k_ipm_reduce(IpmDims d, RedIn a, double* _
     last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (last) {
+    // the whole last CTA combines the per-CTA partials: thread t takes blocks t, t + IT, ...
+    // in order, then the same fixed warp / CTA tree as above (deterministic)
     __threadfence();
-    for (int k = 0; k < NV; k++) {
-      double v = __ldcg(&partials[k]);
-      for (unsigned b = 1; b < gridDim.x; b++) {
+    double v2[NV];
+#pragma unroll
+    for (int k = 0; k < NV; k++) v2[k] = 0.0;   // (the max-reduced values are absolute values)
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += IT)
+#pragma unroll
+      for (int k = 0; k < NV; k++) {
         const double w = __ldcg(&partials[(size_t)b * NOUT + k]);
-        v = IS_MAX[MODE][k] ? fmax(v, w) : v + w;
+        v2[k] = IS_MAX[MODE][k] ? fmax(v2[k], w) : v2[k] + w;
       }
-      out[k] = v;
+    __syncthreads();   // (sh is reused)
+#pragma unroll
+    for (int k = 0; k < NV; k++) {
+      const double v = wred(v2[k], IS_MAX[MODE][k]);
+      if (lane == 0) sh[warp][k] = v;
     }
-    *counter = 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < NV; k++) {
+        double v = sh[0][k];
+        for (int w = 1; w < IT / 32; w++) v = IS_MAX[MODE][k] ? fmax(v, sh[w][k]) : v + sh[w][k];
+        out[k] = v;
+      }
+      *counter = 0u;
+    }
   }
 }
 
