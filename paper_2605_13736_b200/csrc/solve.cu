@@ -156,7 +156,9 @@ __global__ void __launch_bounds__(256) k_inv_blocks(int64_t N, const double* __r
   pdl_wait();
   pdl_trigger();
   L += blockIdx.y * z.ld;
-  binv = bsh(binv, z.ws); gf = bsh(gf, z.ws); gb = bsh(gb, z.ws);
+  const bool need_g = gf != nullptr;   // (the batched per-scenario sweeps use Binv only)
+  binv = bsh(binv, z.ws);
+  if (need_g) { gf = bsh(gf, z.ws); gb = bsh(gb, z.ws); }
   extern __shared__ double ism[];
   double* Ls = ism;                      // Ls[k*TBP + r] = L[r][k]  (diagonal block, later the off-diagonal ones)
   double* Bs = ism + TB * TBP;           // Bs[c*TBP + r] = Binv[r][c]
@@ -216,6 +218,7 @@ __global__ void __launch_bounds__(256) k_inv_blocks(int64_t N, const double* __r
     const int r = idx % TB, cc = idx / TB;
     out[idx] = Bs[cc * TBP + r];
   }
+  if (!need_g) return;
   // thread (r = tid & 63, column group cg = tid >> 6) computes 16 outputs of each G
   const int r = threadIdx.x & (TB - 1), cg = threadIdx.x >> 6;
   if (i >= 1) {
@@ -349,6 +352,136 @@ __global__ void __launch_bounds__(ST) k_trsv_fwd(int64_t N, const double* __rest
     const int rr = threadIdx.x;
     if (rr < nr) publish(&y[r0 + rr], cvec[rr] - ((part[0][rr] + part[1][rr]) + (part[2][rr] + part[3][rr])));
   }
+}
+
+// Batched sweeps (mds_solve_batched): ONE CTA per scenario walks the whole chain, so
+// no CTA waits on another (the single-system sweeps above chain 64-row blocks over
+// CTAs through published values).  Right-looking over 64-column blocks of L with the
+// vector in shared memory: forward, v_b := Binv_b v_b then v_r -= L(r, b) v_b for the
+// rows below (L streamed once, coalesced down each column); backward, t = v_b -
+// L(rows below, b)^T v, v_b := Binv_b^T t, last block first.  Fixed-order sums.
+constexpr int BST = 512;
+constexpr int BSMAX = 128 * 1024;   // largest per-scenario vector kept in shared memory (N <= 16384)
+__device__ __forceinline__ double red8(double a) {
+  a += __shfl_xor_sync(0xffffffffu, a, 1);
+  a += __shfl_xor_sync(0xffffffffu, a, 2);
+  a += __shfl_xor_sync(0xffffffffu, a, 4);
+  return a;
+}
+__global__ void __launch_bounds__(BST) k_bsolve_fwd(int64_t N, const double* __restrict__ L, int64_t lda,
+                                                    const double* __restrict__ b, double* __restrict__ y,
+                                                    const double* __restrict__ binv, BStr z) {
+  pdl_wait();
+  pdl_trigger();
+  L += blockIdx.y * z.ld;
+  b = bsh(b, z.ws); y = bsh(y, z.ws); binv = bsh(binv, z.ws);
+  extern __shared__ double bv[];   // [N]
+  const int tid = threadIdx.x;
+  for (int64_t i = tid; i < N; i += BST) bv[i] = b[i];
+  __syncthreads();
+  const int64_t nblk = (N + TB - 1) / TB;
+  const int r8 = tid >> 3, part = tid & 7;
+  for (int64_t bb = 0; bb < nblk; bb++) {
+    const int64_t r0 = bb * TB;
+    const int nr = (int)((N - r0) < TB ? (N - r0) : TB);
+    // v_b := Binv_b v_b  (row r8, columns 8 part .. 8 part + 7)
+    const double* B = binv + (size_t)bb * TB * TB;
+    double acc = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int c = part * 8 + u;
+      acc = fma(B[r8 + c * TB], c < nr ? bv[r0 + c] : 0.0, acc);
+    }
+    acc = red8(acc);
+    __syncthreads();
+    if (part == 0 && r8 < nr) bv[r0 + r8] = acc;
+    __syncthreads();
+    // rows below: v_r -= sum_c L(r, r0 + c) v_b[c]
+    // (two rows per thread, 16 loads in flight; each row's sum in the same fixed order)
+    for (int64_t r = r0 + TB + tid; r < N; r += 2 * BST) {
+      const int64_t r2 = r + BST;
+      const bool two = r2 < N;
+      const double* lr = L + r + r0 * lda;
+      const double* lr2 = L + (two ? r2 : r) + r0 * lda;
+      double a[8], b8[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) a[u] = b8[u] = 0.0;
+      int c = 0;
+      for (; c + 8 <= nr; c += 8) {
+        double l[8], l2[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          l[u] = __ldcs(lr + (int64_t)(c + u) * lda);   // (streamed once)
+          l2[u] = __ldcs(lr2 + (int64_t)(c + u) * lda);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          a[u] = fma(l[u], bv[r0 + c + u], a[u]);
+          b8[u] = fma(l2[u], bv[r0 + c + u], b8[u]);
+        }
+      }
+      for (; c < nr; c++) {
+        a[0] = fma(lr[(int64_t)c * lda], bv[r0 + c], a[0]);
+        b8[0] = fma(lr2[(int64_t)c * lda], bv[r0 + c], b8[0]);
+      }
+      bv[r] -= ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+      if (two) bv[r2] -= ((b8[0] + b8[1]) + (b8[2] + b8[3])) + ((b8[4] + b8[5]) + (b8[6] + b8[7]));
+    }
+    __syncthreads();
+  }
+  for (int64_t i = tid; i < N; i += BST) y[i] = bv[i];
+}
+
+__global__ void __launch_bounds__(BST) k_bsolve_bwd(int64_t N, const double* __restrict__ L, int64_t lda,
+                                                    const double* __restrict__ y, double* __restrict__ x,
+                                                    const double* __restrict__ binv, BStr z) {
+  pdl_wait();
+  pdl_trigger();
+  L += blockIdx.y * z.ld;
+  y = bsh(y, z.ws); x = bsh(x, z.ws); binv = bsh(binv, z.ws);
+  extern __shared__ double bv[];   // [N]
+  __shared__ double tb[TB];
+  const int tid = threadIdx.x;
+  for (int64_t i = tid; i < N; i += BST) bv[i] = y[i];
+  __syncthreads();
+  const int64_t nblk = (N + TB - 1) / TB;
+  const int c8 = tid >> 3, sl = tid & 7;
+  for (int64_t bb = nblk - 1; bb >= 0; bb--) {
+    const int64_t r0 = bb * TB;
+    const int nr = (int)((N - r0) < TB ? (N - r0) : TB);
+    // t_c = v_b[c] - sum_{rows below} L(r, r0 + c) v_r  (column c8, rows strided by 8 from sl)
+    double a0 = 0.0, a1 = 0.0;
+    if (c8 < nr) {
+      const double* lc = L + (r0 + c8) * lda;
+      int64_t r = r0 + TB + sl;
+      double a2 = 0.0, a3 = 0.0;
+      for (; r + 24 < N; r += 32) {
+        const double l0 = __ldcs(lc + r), l1 = __ldcs(lc + r + 8), l2 = __ldcs(lc + r + 16), l3 = __ldcs(lc + r + 24);
+        a0 = fma(l0, bv[r], a0);
+        a1 = fma(l1, bv[r + 8], a1);
+        a2 = fma(l2, bv[r + 16], a2);
+        a3 = fma(l3, bv[r + 24], a3);
+      }
+      for (; r < N; r += 8) a0 = fma(lc[r], bv[r], a0);
+      a0 += a2;
+      a1 += a3;
+    }
+    const double dsum = red8(a0 + a1);
+    if (sl == 0) tb[c8] = (c8 < nr) ? bv[r0 + c8] - dsum : 0.0;
+    __syncthreads();
+    // v_b := Binv_b^T t  (Binv^T[r][c] = Binv[c][r])
+    const double* B = binv + (size_t)bb * TB * TB;
+    double acc = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int c = sl * 8 + u;
+      acc = fma(B[c + c8 * TB], tb[c], acc);
+    }
+    acc = red8(acc);
+    if (sl == 0 && c8 < nr) bv[r0 + c8] = acc;
+    __syncthreads();
+  }
+  for (int64_t i = tid; i < N; i += BST) x[i] = bv[i];
 }
 
 // D solve: 1x1 and 2x2 blocks (LAPACK dsytrs scaled 2x2 formula); 2x2 off-diagonal at (k, k+1) (upper slot)
@@ -528,7 +661,7 @@ extern "C" size_t mds_solve_workspace_size(int64_t N) {
 static int solve_launch(const mds_plan* plan, int64_t batch, int64_t N, const double* LD, int64_t ldm,
                         const int32_t* piv, const double* rhs_c, const double* js_val, const double* w,
                         const double* r_xs, double* dxy, double* dx_s, double zero_tol, const void* fwork,
-                        int32_t* status, void* work, const BStr& z, cudaStream_t st) {
+                        int32_t* status, void* work, const BStr& z, cudaStream_t st, bool batched_api = false) {
   const unsigned nb = (unsigned)batch;
   if (N > 0) {
     SWork s = carve(work, N, nullptr);
@@ -540,13 +673,28 @@ static int solve_launch(const mds_plan* plan, int64_t batch, int64_t N, const do
       cudaFuncSetAttribute(k_trsv_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SWSMEM);
       cudaFuncSetAttribute(k_trsv_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SWSMEM);
     }
+    // batched API: one CTA per scenario per sweep (the vector of N doubles in shared memory)
+    const bool per_scen = batched_api && (size_t)N * 8 <= (size_t)BSMAX;
     MDS_LAUNCH(PC_SOLVE_FWD, st,
-               MDS_CUDA_TRY(launch_pdl(k_inv_blocks, dim3((unsigned)nblk, nb), dim3(256), IBSMEM, st, N, LD, ldm, s.binv, s.gf, s.gb, z)));
+               MDS_CUDA_TRY(launch_pdl(k_inv_blocks, dim3((unsigned)nblk, nb), dim3(256), IBSMEM, st, N, LD, ldm, s.binv,
+                                       per_scen ? (double*)nullptr : s.gf, per_scen ? (double*)nullptr : s.gb, z)));
+    if (per_scen && mds_once_per_device((const void*)k_bsolve_fwd)) {
+      cudaFuncSetAttribute(k_bsolve_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, BSMAX);
+      cudaFuncSetAttribute(k_bsolve_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, BSMAX);
+    }
+    if (per_scen)
+      MDS_LAUNCH(PC_SOLVE_FWD, st,
+                 MDS_CUDA_TRY(launch_pdl(k_bsolve_fwd, dim3(1, nb), dim3(BST), (size_t)N * 8, st, N, LD, ldm, (const double*)s.b, s.y, (const double*)s.binv, z)));
+    else
     MDS_LAUNCH(PC_SOLVE_FWD, st,
                MDS_CUDA_TRY(launch_pdl(k_trsv_fwd, dim3((unsigned)nblk, nb), dim3(ST), SWSMEM, st, N, LD, ldm, s.b, s.y, s.binv, s.gf, s.tickets, z)));
     const double* tolp = (zero_tol < 0.0 && fwork) ? mds_factor_tol_ptr(fwork) : nullptr;
     MDS_LAUNCH(PC_SOLVE_D, st,
                MDS_CUDA_TRY(launch_pdl(k_dsolve, dim3(ge, nb), dim3(256), 0, st, N, LD, ldm, piv, s.y, tolp, zero_tol < 0.0 ? 0.0 : zero_tol, status, z)));
+    if (per_scen)
+      MDS_LAUNCH(PC_SOLVE_BWD, st,
+                 MDS_CUDA_TRY(launch_pdl(k_bsolve_bwd, dim3(1, nb), dim3(BST), (size_t)N * 8, st, N, LD, ldm, (const double*)s.y, s.x, (const double*)s.binv, z)));
+    else
     MDS_LAUNCH(PC_SOLVE_BWD, st,
                MDS_CUDA_TRY(launch_pdl(k_trsv_bwd, dim3((unsigned)nblk, nb), dim3(ST), SWSMEM, st, N, LD, ldm, s.y, s.x, s.binv, s.gb, s.tickets + 1, z)));
     MDS_LAUNCH(PC_SOLVE_SCATTER, st, MDS_CUDA_TRY(launch_pdl(k_scatter, dim3(ge, nb), dim3(256), 0, st, N, piv, s.x, dxy, z)));
@@ -603,5 +751,5 @@ extern "C" int mds_solve_batched(const mds_plan* plan, int64_t batch, int64_t N,
   z.ws = solve_ws_stride(N);
   z.fws = mds_factor_ws_stride_bytes(N);
   return solve_launch(plan, batch, N, LD, ldm, piv, rhs_c, js_val, w, r_xs, dxy, dx_s, zero_tol, fwork, status, work,
-                      z, (cudaStream_t)stream);
+                      z, (cudaStream_t)stream, true);
 }
