@@ -82,7 +82,7 @@ struct MdsVariant {
   int cdense_ctas = 2;   // CTAs per SM of k_condense_dense (runs beside the pair chain)
   int cdense_serial = 0; // 1: k_condense_dense on the caller's stream (no fork)
   int cdense_tma = 0;    // 1: the TMA-ring copy of the dense tiles (k_condense_dense_tma) instead of register staging
-  int cond_group = 4;    // batched pair tiles: scenarios per group of the (scenario group, tile, scenario) order
+  int cond_group = 8;    // batched pair tiles: scenarios per group of the (scenario group, tile, scenario) order
 };
 extern MdsVariant g_mds_var;
 

@@ -285,7 +285,9 @@ struct CondArgs {
   double* anorm;                        // [batch] or NULL
   int32_t* status; int64_t s_st;        // per-scenario status (stride 0: shared)
   // workspace
-  double2* Q;        // [batch][nnz]  (val_p w_k, val_p)
+  double2* Q;        // [batch][nnz]  (val_p w_k, val_p); batched: 4 scenarios interleaved per entry (qst)
+  int qst;           // entry stride of one scenario's Q: 1, or 4 (batched: entry p of scenario s at
+                     //   ((s / 4) nnz + p) 4 + s % 4, so the 4 scenarios of a tile group share sectors)
   double* dsum;      // [batch][m]    sum over column c of val^2 w (the diagonal pairs)
   double* pbuf;      // [nbuf][64*64] part sums of split tiles
   unsigned* ticket;  // [ntile]       parts finished per split tile
@@ -296,6 +298,10 @@ struct CondArgs {
   __device__ double* parts_pcol(int64_t s) const { return anorm::parts_at(parts + (size_t)s * parts_stride, N).pcol; }
 };
 
+// scenario s's view of Q (entry p at qbase(a, s)[p * a.qst])
+__device__ __forceinline__ double2* qbase(const CondArgs& a, int64_t s) {
+  return a.qst == 1 ? a.Q + s * a.nnz : a.Q + (size_t)(s >> 2) * a.nnz * 4 + (s & 3);
+}
 __device__ __forceinline__ anorm::Parts parts_of(const CondArgs& a, int64_t s) {
   return anorm::parts_at(a.parts + (size_t)s * a.parts_stride, a.N);
 }
@@ -353,6 +359,60 @@ __global__ void __launch_bounds__(256) k_condense_rows(CondArgs a) {
   const int64_t nblk = mds_cdiv(a.n_s, 32);
   const int64_t gw = gt >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const unsigned long long pol_keep = pol_evict_last();
+  if (a.qst == 4) {
+    // batched (interleaved Q): a warp takes 32 sparse variables of the 4 scenarios of a group;
+    // lane (entry e = lane / 4, scenario s0 + lane % 4) writes one 16-byte Q entry, so the
+    // warp's 32 stores are 512 contiguous bytes.  Same arithmetic as below.
+    const int64_t ngrp = (a.batch + 3) / 4;
+    for (int64_t g = gw; g < ngrp * nblk; g += nw) {
+      const int64_t grp = g / nblk, k0 = (g - grp * nblk) * 32, s0 = grp * 4;
+      const int64_t k = k0 + lane;
+      const int nrow = (int)min((int64_t)32, a.n_s - k0);
+      double wk[4];
+      int rp = 0;
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t s = s0 + u;
+        wk[u] = 0.0;
+        if (lane < nrow && s < a.batch && !(a.active && !a.active[s])) {
+          const double dw = a.dw_arr ? a.dw_arr[s] : a.delta_w;
+          const double q = __dadd_rn(__dadd_rn(a.h_ss[s * a.s_hss + k], a.sigma_s[s * a.s_sig + k]), dw);
+          if (!(q > 0.0)) mds_set_status(a.status + s * a.s_st, MDS_ERR_NONPOSITIVE);
+          wk[u] = 1.0 / q;
+          a.w[s * a.s_w + k] = wk[u];
+        }
+      }
+      if (lane < nrow) rp = a.rowptr[k];
+      const int p0 = __shfl_sync(0xffffffffu, rp, 0);
+      const int p1 = a.rowptr[k0 + nrow];
+      const int e = lane >> 2, su = lane & 3;
+      const int64_t s = s0 + su;
+      const bool live_s = s < a.batch && !(a.active && !a.active[s]);
+      const double* val = a.val + (live_s ? s : 0) * a.s_val;
+      double2* Qg = a.Q + (size_t)grp * a.nnz * 4 + su;
+      for (int pb = p0; pb < p1; pb += 8) {
+        const int p = pb + e;
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const int cand = lo + step;
+          const int rc = __shfl_sync(0xffffffffu, rp, cand < nrow ? cand : 0);
+          if (cand < nrow && rc <= p) lo = cand;
+        }
+        double wr = 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const double x = __shfl_sync(0xffffffffu, wk[u], lo);
+          if (su == u) wr = x;
+        }
+        if (p < p1 && live_s) {
+          const double v = val[p];
+          st_keep2(Qg + (size_t)p * 4, make_double2(__dmul_rn(v, wr), v), pol_keep);
+        }
+      }
+    }
+    return;
+  }
   for (int64_t g = gw; g < a.batch * nblk; g += nw) {
     const int64_t s = g / nblk, k0 = (g - s * nblk) * 32;
     if (a.active && !a.active[s]) continue;
@@ -371,7 +431,7 @@ __global__ void __launch_bounds__(256) k_condense_rows(CondArgs a) {
     const int p0 = __shfl_sync(0xffffffffu, rp, 0);
     const int p1 = a.rowptr[k0 + nrow];
     const double* val = a.val + s * a.s_val;
-    double2* Q = a.Q + s * a.nnz;
+    double2* Q = qbase(a, s);
     for (int p = p0 + lane; __any_sync(0xffffffffu, p < p1); p += 32) {
       // largest row r < nrow with rowptr[k0 + r] <= p (rows may be empty)
       int lo = 0;
@@ -384,7 +444,7 @@ __global__ void __launch_bounds__(256) k_condense_rows(CondArgs a) {
       const double wr = __shfl_sync(0xffffffffu, wk, lo);
       if (p < p1) {
         const double v = val[p];
-        st_keep2(Q + p, make_double2(__dmul_rn(v, wr), v), pol_keep);
+        st_keep2(Q + (size_t)p * a.qst, make_double2(__dmul_rn(v, wr), v), pol_keep);
       }
     }
   }
@@ -410,7 +470,7 @@ __global__ void __launch_bounds__(256) k_condense_diag(CondArgs a) {
       rhs[j] = r[a.n_s + j];
   }
   if (c >= a.m) return;
-  const double2* Q = a.Q + s * a.nnz;
+  const double2* Q = qbase(a, s);
   const unsigned long long pol_keep = pol_evict_last();
   const int e0 = a.tptr[c], e1 = a.tptr[c + 1];
   constexpr int U = 4;               // independent entries in flight per lane
@@ -428,7 +488,7 @@ __global__ void __launch_bounds__(256) k_condense_diag(CondArgs a) {
       q[u] = make_double2(0.0, 0.0);
       rk[u] = 0.0;
       if (kp[u].x >= 0) {
-        q[u] = ld_q(Q + (kp[u].y & ((1 << 27) - 1)), pol_keep);
+        q[u] = ld_q(Q + (size_t)(kp[u].y & ((1 << 27) - 1)) * a.qst, pol_keep);
         if (r) rk[u] = r[kp[u].x];
       }
     }
@@ -460,7 +520,7 @@ __global__ void __launch_bounds__(256) k_condense_diag(CondArgs a) {
 template <int U>
 __device__ __forceinline__ double pair_range(const unsigned long long* __restrict__ pairs, uint32_t r0, uint32_t r1,
                                              int ckey, const double2* __restrict__ Q, double* T, int lane, unsigned long long pol_stream,
-                                             unsigned long long pol_keep, int* carried) {
+                                             unsigned long long pol_keep, int* carried, int qst) {
   // software pipeline: the pair words of the next U chunks are loaded while the
   // current chunks' operand gathers are in flight
   double carry = 0.0;
@@ -479,8 +539,8 @@ __device__ __forceinline__ double pair_range(const unsigned long long* __restric
       if (base + 32 * u + lane < r1) {
         const uint32_t p = (uint32_t)wd[u];
         const uint32_t sft = (uint32_t)(wd[u] >> 32) & ((1u << PAIR_SBITS) - 1u);
-        qa[u] = ld_d(&Q[p].x, pol_keep);
-        qb[u] = ld_d(&Q[p - sft].y, pol_keep);
+        qa[u] = ld_d(&Q[(size_t)p * qst].x, pol_keep);
+        qb[u] = ld_d(&Q[(size_t)(p - sft) * qst].y, pol_keep);
       }
     }
     int key[U];
@@ -637,8 +697,8 @@ __global__ void __launch_bounds__(CW * 32, 4) k_condense_tiles(CondArgs a) {
       const uint32_t r1 = min(E1, E0 + 64u * min(nch, per * (uint32_t)(warp + 1)));
       const int ckey = (r0 > E0 && r0 < r1) ? (int)(ld_pair(a.pairs + r0 - 1, pol_stream) >> 52) : -1;
       int carried;
-      const double carry = pair_range<PAIR_U>(a.pairs, r0, r1, ckey, a.Q + s * a.nnz, T, lane,
-                                              pol_stream, pol_keep, &carried);
+      const double carry = pair_range<PAIR_U>(a.pairs, r0, r1, ckey, qbase(a, s), T, lane,
+                                              pol_stream, pol_keep, &carried, a.qst);
       if (lane == 0) { stcarry[warp] = carry; stckey[warp] = carried; }
       __syncthreads();
       if (threadIdx.x == 0) {   // carries in warp order (the previous warps' commits are done)
@@ -991,7 +1051,7 @@ static CondLayout cond_layout(const mds_plan* P, int64_t batch) {
   const int64_t m = P->m_E + P->m_I, N = std::max<int64_t>(P->n_d + m, 1);
   CondLayout L;
   L.q = 256;
-  L.dsum = L.q + al256((size_t)batch * P->nnz * 16);
+  L.dsum = L.q + al256((size_t)(batch > 1 ? (batch + 3) / 4 * 4 : 1) * P->nnz * 16);
   L.ticket = L.dsum + al256((size_t)batch * std::max<int64_t>(m, 1) * 8);
   L.pbuf = L.ticket + al256((size_t)P->ntile * 4);
   L.parts = L.pbuf + (batch == 1 ? (size_t)P->nbuf * CT * CT * 8 : 0);
@@ -1065,6 +1125,7 @@ static int condense_launch(const mds_plan* P, CondArgs& a, void* work, size_t wo
   a.pbase = P->pbase; a.order = P->order; a.items = P->items; a.dorder = P->dorder;
   a.norder = P->norder; a.ndense = P->ndense;
   a.split = a.batch == 1 ? 1 : 0;
+  a.qst = a.batch > 1 ? 4 : 1;
   a.group = std::max<int64_t>(1, std::min<int64_t>(g_mds_var.cond_group, a.batch));
   if (N == 0) return MDS_OK;
   if (!a.M || a.ldm < N) return MDS_ERR_ARG;
