@@ -299,8 +299,9 @@ struct CondArgs {
 };
 
 // scenario s's view of Q (entry p at qbase(a, s)[p * a.qst])
+constexpr int QI = 4;   // scenarios interleaved per Q entry (batched; 8 measured: tiles 4.2 -> 3.9 ms but the a1 pass 2.4 -> 2.6, step +0.4 ms)
 __device__ __forceinline__ double2* qbase(const CondArgs& a, int64_t s) {
-  return a.qst == 1 ? a.Q + s * a.nnz : a.Q + (size_t)(s >> 2) * a.nnz * 4 + (s & 3);
+  return a.qst == 1 ? a.Q + s * a.nnz : a.Q + (size_t)(s / QI) * a.nnz * QI + (s % QI);
 }
 __device__ __forceinline__ anorm::Parts parts_of(const CondArgs& a, int64_t s) {
   return anorm::parts_at(a.parts + (size_t)s * a.parts_stride, a.N);
@@ -359,19 +360,19 @@ __global__ void __launch_bounds__(256) k_condense_rows(CondArgs a) {
   const int64_t nblk = mds_cdiv(a.n_s, 32);
   const int64_t gw = gt >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const unsigned long long pol_keep = pol_evict_last();
-  if (a.qst == 4) {
+  if (a.qst == QI) {
     // batched (interleaved Q): a warp takes 32 sparse variables of the 4 scenarios of a group;
     // lane (entry e = lane / 4, scenario s0 + lane % 4) writes one 16-byte Q entry, so the
     // warp's 32 stores are 512 contiguous bytes.  Same arithmetic as below.
-    const int64_t ngrp = (a.batch + 3) / 4;
+    const int64_t ngrp = (a.batch + QI - 1) / QI;
     for (int64_t g = gw; g < ngrp * nblk; g += nw) {
-      const int64_t grp = g / nblk, k0 = (g - grp * nblk) * 32, s0 = grp * 4;
+      const int64_t grp = g / nblk, k0 = (g - grp * nblk) * 32, s0 = grp * QI;
       const int64_t k = k0 + lane;
       const int nrow = (int)min((int64_t)32, a.n_s - k0);
-      double wk[4];
+      double wk[QI];
       int rp = 0;
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
+      for (int u = 0; u < QI; u++) {
         const int64_t s = s0 + u;
         wk[u] = 0.0;
         if (lane < nrow && s < a.batch && !(a.active && !a.active[s])) {
@@ -385,12 +386,12 @@ __global__ void __launch_bounds__(256) k_condense_rows(CondArgs a) {
       if (lane < nrow) rp = a.rowptr[k];
       const int p0 = __shfl_sync(0xffffffffu, rp, 0);
       const int p1 = a.rowptr[k0 + nrow];
-      const int e = lane >> 2, su = lane & 3;
+      const int e = lane / QI, su = lane % QI;
       const int64_t s = s0 + su;
       const bool live_s = s < a.batch && !(a.active && !a.active[s]);
       const double* val = a.val + (live_s ? s : 0) * a.s_val;
-      double2* Qg = a.Q + (size_t)grp * a.nnz * 4 + su;
-      for (int pb = p0; pb < p1; pb += 8) {
+      double2* Qg = a.Q + (size_t)grp * a.nnz * QI + su;
+      for (int pb = p0; pb < p1; pb += 32 / QI) {
         const int p = pb + e;
         int lo = 0;
 #pragma unroll
@@ -401,13 +402,13 @@ __global__ void __launch_bounds__(256) k_condense_rows(CondArgs a) {
         }
         double wr = 0.0;
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
+        for (int u = 0; u < QI; u++) {
           const double x = __shfl_sync(0xffffffffu, wk[u], lo);
           if (su == u) wr = x;
         }
         if (p < p1 && live_s) {
           const double v = val[p];
-          st_keep2(Qg + (size_t)p * 4, make_double2(__dmul_rn(v, wr), v), pol_keep);
+          st_keep2(Qg + (size_t)p * QI, make_double2(__dmul_rn(v, wr), v), pol_keep);
         }
       }
     }
@@ -1051,7 +1052,7 @@ static CondLayout cond_layout(const mds_plan* P, int64_t batch) {
   const int64_t m = P->m_E + P->m_I, N = std::max<int64_t>(P->n_d + m, 1);
   CondLayout L;
   L.q = 256;
-  L.dsum = L.q + al256((size_t)(batch > 1 ? (batch + 3) / 4 * 4 : 1) * P->nnz * 16);
+  L.dsum = L.q + al256((size_t)(batch > 1 ? (batch + QI - 1) / QI * QI : 1) * P->nnz * 16);
   L.ticket = L.dsum + al256((size_t)batch * std::max<int64_t>(m, 1) * 8);
   L.pbuf = L.ticket + al256((size_t)P->ntile * 4);
   L.parts = L.pbuf + (batch == 1 ? (size_t)P->nbuf * CT * CT * 8 : 0);
@@ -1125,7 +1126,7 @@ static int condense_launch(const mds_plan* P, CondArgs& a, void* work, size_t wo
   a.pbase = P->pbase; a.order = P->order; a.items = P->items; a.dorder = P->dorder;
   a.norder = P->norder; a.ndense = P->ndense;
   a.split = a.batch == 1 ? 1 : 0;
-  a.qst = a.batch > 1 ? 4 : 1;
+  a.qst = a.batch > 1 ? QI : 1;
   a.group = std::max<int64_t>(1, std::min<int64_t>(g_mds_var.cond_group, a.batch));
   if (N == 0) return MDS_OK;
   if (!a.M || a.ldm < N) return MDS_ERR_ARG;
