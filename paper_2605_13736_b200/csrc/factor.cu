@@ -2183,6 +2183,22 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
       if (leader) mbar_arrive(empty0 + 8 * st);
       continue;
     }
+    // F2 tile: its panel's width and pivots d, loaded now so their latency hides behind the
+    // k-loop instead of stalling the epilogue's reciprocals
+    int nbf = 0;
+    double dpre[4][2];
+    if ((mode == 3 || mode == 6) && C0 == -2) {
+      const size_t bo = (mode == 6) ? (size_t)bsc * f.bws : 0;
+      const FCtl* cf = reinterpret_cast<const FCtl*>(reinterpret_cast<const char*>(f.ctl) + bo);
+      nbf = (mode == 6) ? __ldcg(&cf->nbp) : (int)nbn0;
+#pragma unroll
+      for (int b = 0; b < 4; b++)
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const int c = wn + 8 * b + 2 * q + e;
+          dpre[b][e] = (c < nbf) ? __ldcg(&cf->d[c]) : 0.0;
+        }
+    }
     double acc[4][4][2];
 #pragma unroll
     for (int a = 0; a < 4; a++)
@@ -2228,7 +2244,6 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
       // (scenario bsc's control block and panel buffers by explicit byte offsets)
       const size_t bo = (mode == 6) ? (size_t)bsc * f.bws : 0;
       FCtl* cf = reinterpret_cast<FCtl*>(reinterpret_cast<char*>(f.ctl) + bo);
-      const int nbf = (mode == 6) ? cf->nbp : (int)nbn0;
       const int64_t f2rf = (mode == 6) ? sT : f2r00;
       double* W2 = (mode == 6) ? reinterpret_cast<double*>(reinterpret_cast<char*>(f.W) + bo) : const_cast<double*>(f.Wprev);
       double* L2 = (mode == 6) ? reinterpret_cast<double*>(reinterpret_cast<char*>(f.Lb) + bo) : const_cast<double*>(f.Lbprev);
@@ -2238,7 +2253,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
 #pragma unroll
         for (int e = 0; e < 2; e++) {
           const int c = wn + 8 * b + 2 * q + e;
-          const double d = (c < nbf) ? __ldcg(&cf->d[c]) : 0.0;
+          const double d = dpre[b][e];
           const double rd = fast_rcp(d);
           const double r1 = (d != 0.0) ? rd : 0.0;
           cm[b][e] = 0.0;
