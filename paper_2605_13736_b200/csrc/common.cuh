@@ -1,5 +1,6 @@
 // common.cuh — shared device helpers of the product path (NOT shared with oracle/).
 #pragma once
+#include <climits>
 #include <cuda_runtime.h>
 #include <cstdlib>
 #include <stdint.h>
@@ -79,9 +80,10 @@ struct MdsVariant {
   int upd_inplace = 0, upd_main = 0, slow_1cta = 0, exact_no_ls = 0, f2_trsm = 0, no_pdl = 0;
   int no_cluster = 0;   // 1: the exact panel always on the global-counter grid barrier (no cluster launch)
   int ozaki = 0;   // trailing update in emulated FP64 on the INT8 tensor cores (ozaki.cuh)
-  int cdense_ctas = 2;   // CTAs per SM of k_condense_dense (runs beside the pair chain)
+  int cdense_ctas = 0;   // CTAs per SM of k_condense_dense (runs beside the pair chain); 0: one CTA per tile
   int cdense_serial = 0; // 1: k_condense_dense on the caller's stream (no fork)
   int cdense_tma = 0;    // 1: the TMA-ring copy of the dense tiles (k_condense_dense_tma) instead of register staging
+  int cond_prio = 1;     // 1: the pair chain at the highest launch priority, the dense tiles at the lowest
   int cond_group = 8;    // batched pair tiles: scenarios per group of the (scenario group, tile, scenario) order
 };
 extern MdsVariant g_mds_var;
@@ -103,6 +105,33 @@ static inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = off ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
+// launch_pdl with an explicit scheduling priority (cudaLaunchAttributePriority; kept
+// in captured graphs as the kernel node's priority).  prio = INT_MIN: none.
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl_prio(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t st, int prio,
+                                          Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (!g_mds_var.no_pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    na++;
+  }
+  if (prio != INT_MIN) {
+    at[na].id = cudaLaunchAttributePriority;
+    at[na].val.priority = prio;
+    na++;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 

@@ -1149,6 +1149,8 @@ static int condense_launch(const mds_plan* P, CondArgs& a, void* work, size_t wo
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const bool norm = a.anorm != nullptr;
+  int prio_lo = INT_MIN, prio_hi = INT_MIN;   // (variant cond_prio)
+  if (g_mds_var.cond_prio) cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   // ---- fork: the pure dense tiles on the side stream, concurrent with the chain below
   SideStream* side = nullptr;
   if (a.ndense > 0) {
@@ -1159,7 +1161,8 @@ static int condense_launch(const mds_plan* P, CondArgs& a, void* work, size_t wo
     const bool vec = even(n_d) && even(m) && even(a.ldh) && even(a.ldj) && even(a.ldm) && even(a.s_H) &&
                      even(a.s_J) && even(a.s_M) && al16(a.H) && al16(a.M) && (m == 0 || al16(a.Jd));
     const unsigned grid = (unsigned)std::max<int64_t>(
-        1, std::min<int64_t>(a.ndense * a.batch, (int64_t)sms * g_mds_var.cdense_ctas));
+        1, g_mds_var.cdense_ctas == 0 ? a.ndense * a.batch   // (0: one CTA per tile, not persistent)
+                                      : std::min<int64_t>(a.ndense * a.batch, (int64_t)sms * g_mds_var.cdense_ctas));
     cudaStream_t ds = st;
     if (!g_mds_var.cdense_serial) {
       MDS_CUDA_TRY(cudaEventRecord(side->fork, st));
@@ -1184,20 +1187,23 @@ static int condense_launch(const mds_plan* P, CondArgs& a, void* work, size_t wo
     } else {
       auto kd = vec ? (norm ? k_condense_dense<true, true> : k_condense_dense<true, false>)
                     : (norm ? k_condense_dense<false, true> : k_condense_dense<false, false>);
-      MDS_LAUNCH(PC_CONDENSE_COPY, ds, (kd<<<grid, CW * 32, 0, ds>>>(a)));
+      if (prio_lo != INT_MIN)
+        MDS_LAUNCH(PC_CONDENSE_COPY, ds, MDS_CUDA_TRY(launch_pdl_prio(kd, dim3(grid), dim3(CW * 32), 0, ds, prio_lo, a)));
+      else
+        MDS_LAUNCH(PC_CONDENSE_COPY, ds, (kd<<<grid, CW * 32, 0, ds>>>(a)));
     }
   }
   {
     const int64_t warps = std::max<int64_t>(a.batch * mds_cdiv(n_s, 32), 1);
     const int64_t blocks = std::max<int64_t>(std::max<int64_t>(mds_cdiv(warps, 8), mds_cdiv(a.ntile, 256)),
                                              mds_cdiv(a.batch * 4, 256));
-    MDS_LAUNCH(PC_CONDENSE_W, st, MDS_CUDA_TRY(launch_pdl(k_condense_rows, dim3((unsigned)std::min<int64_t>(blocks, (int64_t)sms * 16)),
-                                                          dim3(256), 0, st, a)));
+    MDS_LAUNCH(PC_CONDENSE_W, st, MDS_CUDA_TRY(launch_pdl_prio(k_condense_rows, dim3((unsigned)std::min<int64_t>(blocks, (int64_t)sms * 16)),
+                                                               dim3(256), 0, st, prio_hi, a)));
   }
   {
     const int64_t bx = std::max<int64_t>(mds_cdiv(std::max<int64_t>(m, 1), 8), 1);
     MDS_LAUNCH(PC_CONDENSE_DIAG, st,
-               MDS_CUDA_TRY(launch_pdl(k_condense_diag, dim3((unsigned)bx, (unsigned)a.batch), dim3(256), 0, st, a)));
+               MDS_CUDA_TRY(launch_pdl_prio(k_condense_diag, dim3((unsigned)bx, (unsigned)a.batch), dim3(256), 0, st, prio_hi, a)));
   }
   int occ = 1;
   if (norm) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_condense_tiles<true>, CW * 32, 0);
@@ -1206,9 +1212,9 @@ static int condense_launch(const mds_plan* P, CondArgs& a, void* work, size_t wo
   if (items > 0) {
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)sms * std::max(occ, 1)));
     if (norm)
-      MDS_LAUNCH(PC_CONDENSE_YY, st, MDS_CUDA_TRY(launch_pdl(k_condense_tiles<true>, dim3(grid), dim3(CW * 32), 0, st, a)));
+      MDS_LAUNCH(PC_CONDENSE_YY, st, MDS_CUDA_TRY(launch_pdl_prio(k_condense_tiles<true>, dim3(grid), dim3(CW * 32), 0, st, prio_hi, a)));
     else
-      MDS_LAUNCH(PC_CONDENSE_YY, st, MDS_CUDA_TRY(launch_pdl(k_condense_tiles<false>, dim3(grid), dim3(CW * 32), 0, st, a)));
+      MDS_LAUNCH(PC_CONDENSE_YY, st, MDS_CUDA_TRY(launch_pdl_prio(k_condense_tiles<false>, dim3(grid), dim3(CW * 32), 0, st, prio_hi, a)));
   }
   // ---- join
   if (side) {

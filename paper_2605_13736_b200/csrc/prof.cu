@@ -62,14 +62,15 @@ extern "C" int mds_set_variant(const char* key, long long value) {
   if (k == "tail_rows") { v.tail_rows = value; return MDS_OK; }
   if (k == "exact_rows") { if (value < 32) return MDS_ERR_ARG; v.exact_rows = value; return MDS_OK; }
   if (k == "cond_group") { if (value < 1 || value > 65536) return MDS_ERR_ARG; v.cond_group = (int)value; return MDS_OK; }
-  if (k == "cdense_ctas") { if (value < 1 || value > 8) return MDS_ERR_ARG; v.cdense_ctas = (int)value; return MDS_OK; }
+  if (k == "cdense_ctas") { if (value < 0 || value > 8) return MDS_ERR_ARG; v.cdense_ctas = (int)value; return MDS_OK; }
   int* flag = k == "no_tma" ? &v.no_tma : k == "no_lookahead" ? &v.no_lookahead
             : k == "static_sched" ? &v.static_sched : k == "no_snake" ? &v.no_snake
             : k == "no_cprefetch" ? &v.no_cprefetch : k == "upd_inplace" ? &v.upd_inplace
             : k == "upd_main" ? &v.upd_main : k == "slow_1cta" ? &v.slow_1cta
             : k == "exact_no_ls" ? &v.exact_no_ls : k == "f2_trsm" ? &v.f2_trsm
             : k == "no_pdl" ? &v.no_pdl : k == "ozaki" ? &v.ozaki : k == "no_cluster" ? &v.no_cluster
-            : k == "cdense_serial" ? &v.cdense_serial : k == "cdense_tma" ? &v.cdense_tma : nullptr;
+            : k == "cdense_serial" ? &v.cdense_serial : k == "cdense_tma" ? &v.cdense_tma
+            : k == "cond_prio" ? &v.cond_prio : nullptr;
   if (!flag) return MDS_ERR_ARG;
   *flag = value ? 1 : 0;
   return MDS_OK;
