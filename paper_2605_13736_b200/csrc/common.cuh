@@ -78,12 +78,13 @@ struct MdsVariant {
   long long exact_rows = 256;   // rows per CTA of k_panel_exact
   int no_tma = 0, no_lookahead = 0, static_sched = 0, no_snake = 0, no_cprefetch = 0;
   int upd_inplace = 0, upd_main = 0, slow_1cta = 0, exact_no_ls = 0, f2_trsm = 0, no_pdl = 0;
-  int no_cluster = 0;   // 1: the exact panel always on the global-counter grid barrier (no cluster launch)
+  int exact_cluster = 0;   // 1: the exact panel as one thread-block cluster when it fits (see factor.cu)
   int ozaki = 0;   // trailing update in emulated FP64 on the INT8 tensor cores (ozaki.cuh)
   int cdense_ctas = 0;   // CTAs per SM of k_condense_dense (runs beside the pair chain); 0: one CTA per tile
   int cdense_serial = 0; // 1: k_condense_dense on the caller's stream (no fork)
   int cdense_tma = 0;    // 1: the TMA-ring copy of the dense tiles (k_condense_dense_tma) instead of register staging
   int cond_prio = 1;     // 1: the pair chain at the highest launch priority, the dense tiles at the lowest
+  int fac_prio = 0;      // 1: the factorization's panel kernels at the highest launch priority
   int cond_group = 8;    // batched pair tiles: scenarios per group of the (scenario group, tile, scenario) order
 };
 extern MdsVariant g_mds_var;
@@ -148,14 +149,33 @@ static inline cudaError_t launch_coop_pdl(void (*k)(KArgs...), dim3 g, dim3 b, s
   cfg.blockDim = b;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[3];
+  int na = 0;
+  at[na].id = cudaLaunchAttributeCooperative;
+  at[na].val.cooperative = 1;
+  na++;
+  if (!g_mds_var.no_pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    na++;
+  }
+  if (g_mds_var.fac_prio) {   // (the panel chain ahead of the concurrent trailing update)
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    at[na].id = cudaLaunchAttributePriority;
+    at[na].val.priority = hi;
+    na++;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = g_mds_var.no_pdl ? 1 : 2;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+// the panel chain's launches: highest priority under variant fac_prio
+static inline int chain_prio() {
+  if (!g_mds_var.fac_prio) return INT_MIN;
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  return hi;
 }
 
 // ---------------------------------------------------------------------------

@@ -2187,7 +2187,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
     // k-loop instead of stalling the epilogue's reciprocals
     int nbf = 0;
     double dpre[4][2];
-    if ((mode == 3 || mode == 6) && C0 == -2) {
+    if (mode == 6 && C0 == -2) {   // (not mode 3: the extra live registers cost the single-system update more)
       const size_t bo = (mode == 6) ? (size_t)bsc * f.bws : 0;
       const FCtl* cf = reinterpret_cast<const FCtl*>(reinterpret_cast<const char*>(f.ctl) + bo);
       nbf = (mode == 6) ? __ldcg(&cf->nbp) : (int)nbn0;
@@ -2245,6 +2245,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
       const size_t bo = (mode == 6) ? (size_t)bsc * f.bws : 0;
       FCtl* cf = reinterpret_cast<FCtl*>(reinterpret_cast<char*>(f.ctl) + bo);
       const int64_t f2rf = (mode == 6) ? sT : f2r00;
+      if (mode == 3) nbf = (int)nbn0;
       double* W2 = (mode == 6) ? reinterpret_cast<double*>(reinterpret_cast<char*>(f.W) + bo) : const_cast<double*>(f.Wprev);
       double* L2 = (mode == 6) ? reinterpret_cast<double*>(reinterpret_cast<char*>(f.Lb) + bo) : const_cast<double*>(f.Lbprev);
       double cm[4][2];
@@ -2253,7 +2254,7 @@ __global__ void __launch_bounds__(TTHREADS, 1) k_update_tma(int64_t N, double* _
 #pragma unroll
         for (int e = 0; e < 2; e++) {
           const int c = wn + 8 * b + 2 * q + e;
-          const double d = dpre[b][e];
+          const double d = (mode == 6) ? dpre[b][e] : ((c < nbf) ? __ldcg(&cf->d[c]) : 0.0);
           const double rd = fast_rcp(d);
           const double r1 = (d != 0.0) ? rd : 0.0;
           cm[b][e] = 0.0;
@@ -2672,7 +2673,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
     const int64_t xrows = std::max<long long>(32, g_mds_var.exact_rows);
     // one thread-block cluster when its <= 16 CTAs keep their L rows in shared memory
     // (cluster barrier instead of the global counter); not for concurrent factorizations
-    const bool cl = cl_ok == 1 && !capped && !f4_no_ls && !g_mds_var.no_cluster &&
+    const bool cl = cl_ok == 1 && !capped && !f4_no_ls && g_mds_var.exact_cluster &&
                     rows <= (int64_t)XCL * ((XLS_MAX / (NB * 8) - 8) / 32 * 32);
     const unsigned g = cl ? (unsigned)std::max<int64_t>(1, std::min<int64_t>(mds_cdiv(rows, xrows), XCL))
                           : (unsigned)std::max<int64_t>(1, std::min<int64_t>({mds_cdiv(rows, xrows), (int64_t)sms, (int64_t)XMAXG}));
@@ -2713,7 +2714,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
       const FWork fp = fwork_for(p);
       const unsigned g64 = (unsigned)std::max<int64_t>(mds_cdiv(rows_of(p), UT), 1);
       const unsigned gf = (unsigned)(1 + std::max<int64_t>(1, std::min<int64_t>(g64, 4 * (int64_t)sms)));
-      MDS_LAUNCH(PC_PANEL_DIAG, st, MDS_CUDA_TRY(launch_pdl(k_panel_fast, dim3(gf), dim3(256), F1SMEM, st, N, M, ldm, fp)));
+      MDS_LAUNCH(PC_PANEL_DIAG, st, MDS_CUDA_TRY(launch_pdl_prio(k_panel_fast, dim3(gf), dim3(256), F1SMEM, st, chain_prio(), N, M, ldm, fp)));
       return MDS_OK;
     };
     int64_t p = 0;
@@ -2722,7 +2723,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
       if (int rc = launch_fast(0)) return rc;
     } else {
       const FWork fp = fwork_for(0);
-      MDS_LAUNCH(PC_PANEL_DIAG, st, MDS_CUDA_TRY(launch_pdl(k_panel_diag, dim3(1), dim3(256), F1SMEM, st, N, M, ldm, fp)));
+      MDS_LAUNCH(PC_PANEL_DIAG, st, MDS_CUDA_TRY(launch_pdl_prio(k_panel_diag, dim3(1), dim3(256), F1SMEM, st, chain_prio(), N, M, ldm, fp)));
     }
     for (;; p++) {
       const int64_t rows = rows_of(p);
@@ -2764,7 +2765,7 @@ extern "C" int mds_factor(int64_t N, double* M, int64_t ldm, int32_t* piv, doubl
                      (k_update_tma<3, true><<<gr, TTHREADS, TSMEM, side>>>(N, M, ldm, fp, mapA, mw, ml, mapX, g_sched, 0ll, 0ll)));
         MDS_CUDA_TRY(cudaEventRecord(ev(p, 1), side));
         const FWork fn = fwork_for(p + 1);
-        MDS_LAUNCH(PC_PANEL_DIAG, st, MDS_CUDA_TRY(launch_pdl(k_panel_diag, dim3(1), dim3(256), F1SMEM, st, N, M, ldm, fn)));
+        MDS_LAUNCH(PC_PANEL_DIAG, st, MDS_CUDA_TRY(launch_pdl_prio(k_panel_diag, dim3(1), dim3(256), F1SMEM, st, chain_prio(), N, M, ldm, fn)));
       } else {
         const FWork fn = fwork_for(p + 1);
         MDS_LAUNCH(PC_PANEL_DIAG, side, (k_panel_diag<<<1, 256, F1SMEM, side>>>(N, M, ldm, fn)));

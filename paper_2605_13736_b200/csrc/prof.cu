@@ -68,9 +68,9 @@ extern "C" int mds_set_variant(const char* key, long long value) {
             : k == "no_cprefetch" ? &v.no_cprefetch : k == "upd_inplace" ? &v.upd_inplace
             : k == "upd_main" ? &v.upd_main : k == "slow_1cta" ? &v.slow_1cta
             : k == "exact_no_ls" ? &v.exact_no_ls : k == "f2_trsm" ? &v.f2_trsm
-            : k == "no_pdl" ? &v.no_pdl : k == "ozaki" ? &v.ozaki : k == "no_cluster" ? &v.no_cluster
+            : k == "no_pdl" ? &v.no_pdl : k == "ozaki" ? &v.ozaki : k == "exact_cluster" ? &v.exact_cluster
             : k == "cdense_serial" ? &v.cdense_serial : k == "cdense_tma" ? &v.cdense_tma
-            : k == "cond_prio" ? &v.cond_prio : nullptr;
+            : k == "cond_prio" ? &v.cond_prio : k == "fac_prio" ? &v.fac_prio : nullptr;
   if (!flag) return MDS_ERR_ARG;
   *flag = value ? 1 : 0;
   return MDS_OK;

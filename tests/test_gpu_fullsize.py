@@ -142,7 +142,7 @@ def variant_reset():
 
 @pytest.mark.parametrize("variant", ["tail_always", "tail_never", "no_lookahead", "no_tma", "odd_ldm", "no_pdl",
                                      "static_sched", "upd_main", "inplace", "slow_1cta", "exact_no_ls", "f2_trsm",
-                                     "exact_rows_64", "no_cluster"])
+                                     "exact_rows_64", "exact_cluster"])
 def test_factor_variants_pivoting(variant, variant_reset):
     knobs = {"tail_always": {"tail_rows": 100000000}, "tail_never": {"tail_rows": 0},
              "no_lookahead": {"no_lookahead": 1}, "no_tma": {"no_tma": 1}, "odd_ldm": {},
@@ -150,7 +150,7 @@ def test_factor_variants_pivoting(variant, variant_reset):
              "upd_main": {"upd_main": 1}, "inplace": {"upd_inplace": 1},
              "slow_1cta": {"slow_1cta": 1}, "exact_no_ls": {"exact_no_ls": 1},
              "f2_trsm": {"f2_trsm": 1}, "exact_rows_64": {"exact_rows": 64},
-             "no_cluster": {"no_cluster": 1}}[variant]
+             "exact_cluster": {"exact_cluster": 1}}[variant]
     for k, v in knobs.items():
         mds.set_variant(k, v)
     N, n2 = 1500, 300
