@@ -264,6 +264,26 @@ __global__ void __launch_bounds__(256) k_inv_blocks(int64_t N, const double* __r
   }
 }
 
+// Binv_i and G_i into shared memory with all of a thread's 32 loads in flight at
+// once (a load-store loop waits out one round trip per element pair)
+__device__ __forceinline__ void stage_chain_ops(double* Bs, double* Gs, const double* __restrict__ bsrc,
+                                                const double* __restrict__ gsrc, bool has_g) {
+  constexpr int PER = TB * TB / ST;
+  double tb[PER], tg[PER];
+#pragma unroll
+  for (int u = 0; u < PER; u++) {
+    const int idx = threadIdx.x + u * ST;
+    tb[u] = bsrc[idx];
+    tg[u] = has_g ? gsrc[idx] : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < PER; u++) {
+    const int idx = threadIdx.x + u * ST;
+    Bs[idx] = tb[u];
+    Gs[idx] = tg[u];
+  }
+}
+
 // forward: L y = b (unit lower; 2x2 D off-diagonals were moved out of L by the factor).
 constexpr int SWSMEM = 2 * TB * TB * 8;   // Binv_i and G_i in shared memory
 __global__ void __launch_bounds__(ST) k_trsv_fwd(int64_t N, const double* __restrict__ L, int64_t lda,
@@ -287,10 +307,7 @@ __global__ void __launch_bounds__(ST) k_trsv_fwd(int64_t N, const double* __rest
   const int64_t r0 = i * TB;
   const int nr = (int)((N - r0) < TB ? (N - r0) : TB);
   const int r = threadIdx.x & (TB - 1), cgp = threadIdx.x / TB;   // 4 column groups of 16
-  for (int idx = threadIdx.x; idx < TB * TB; idx += ST) {
-    Bs[idx] = binv[(size_t)i * TB * TB + idx];
-    Gs[idx] = (i >= 1) ? gf[(size_t)i * TB * TB + idx] : 0.0;
-  }
+  stage_chain_ops(Bs, Gs, binv + (size_t)i * TB * TB, gf + (size_t)i * TB * TB, i >= 1);
   const double bi = (threadIdx.x < TB && r < nr) ? b[r0 + r] : 0.0;   // off the chain
   double acc = 0.0;
   double lv[16], ln[16];
@@ -539,10 +556,7 @@ __global__ void __launch_bounds__(ST) k_trsv_bwd(int64_t N, const double* __rest
   const int64_t r0 = i * TB;
   const int nr = (int)((N - r0) < TB ? (N - r0) : TB);
   const int k = threadIdx.x & (TB - 1), cgp = threadIdx.x / TB;
-  for (int idx = threadIdx.x; idx < TB * TB; idx += ST) {
-    Bs[idx] = binv[(size_t)i * TB * TB + idx];
-    Gs[idx] = (i + 1 < nblk) ? gb[(size_t)i * TB * TB + idx] : 0.0;
-  }
+  stage_chain_ops(Bs, Gs, binv + (size_t)i * TB * TB, gb + (size_t)i * TB * TB, i + 1 < nblk);
   const double zi = (threadIdx.x < TB && k < nr) ? z[r0 + k] : 0.0;   // off the chain
   double acc[16];
 #pragma unroll
