@@ -77,13 +77,25 @@ class ClockSampler:
                  "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
-        time.sleep(0.3)
+        # nvidia-smi can take a second or more to start: wait for its first sample
+        # (up to 10 s) so the timed region is covered
+        t0 = time.time()
+        while self.p is not None and time.time() - t0 < 10.0:
+            if os.path.getsize(self.f.name) > 0 or self.p.poll() is not None:
+                break
+            time.sleep(0.05)
+        time.sleep(0.15)
         return self
 
     def __exit__(self, *a):
         if self.p is not None:
-            self.p.kill()
-            self.p.wait()
+            time.sleep(0.15)   # one more sample after the timed region
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+                self.p.wait()
         self.f.flush()
 
     def summary(self):

@@ -166,10 +166,21 @@ __global__ void __launch_bounds__(256) k_inv_blocks(int64_t N, const double* __r
   const int64_t i = blockIdx.x;
   const int64_t r0 = i * TB;
   const int nr = (int)((N - r0) < TB ? (N - r0) : TB);
-  for (int idx = threadIdx.x; idx < TB * TB; idx += blockDim.x) {
-    const int r = idx % TB, c = idx / TB;
-    Ls[c * TBP + r] = (r < nr && c < nr && r > c) ? L[(r0 + r) + (r0 + c) * lda] : 0.0;
-    Bs[c * TBP + r] = (r == c) ? 1.0 : 0.0;
+  // (every block load below keeps a thread's 16 loads in flight at once)
+  constexpr int PER = TB * TB / 256;
+  {
+    double t[PER];
+#pragma unroll
+    for (int u = 0; u < PER; u++) {
+      const int idx = threadIdx.x + u * 256, r = idx % TB, c = idx / TB;
+      t[u] = (r < nr && c < nr && r > c) ? L[(r0 + r) + (r0 + c) * lda] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < PER; u++) {
+      const int idx = threadIdx.x + u * 256, r = idx % TB, c = idx / TB;
+      Ls[c * TBP + r] = t[u];
+      Bs[c * TBP + r] = (r == c) ? 1.0 : 0.0;
+    }
   }
   __syncthreads();
   // blocked inversion of the unit-lower block: (1) the four 16x16 diagonal
@@ -224,9 +235,19 @@ __global__ void __launch_bounds__(256) k_inv_blocks(int64_t N, const double* __r
   if (i >= 1) {
     // Gf[r][c] = sum_k Binv[r][k] L_{i,i-1}[k][c]
     __syncthreads();
-    for (int idx = threadIdx.x; idx < TB * TB; idx += blockDim.x) {
-      const int rr = idx % TB, c = idx / TB;
-      Ls[c * TBP + rr] = (rr < nr) ? L[(r0 + rr) + (r0 - TB + c) * lda] : 0.0;
+#pragma unroll
+    for (int h = 0; h < PER; h += PER / 2) {   // two halves of 8 loads in flight (no spills)
+      double t[PER / 2];
+#pragma unroll
+      for (int u = 0; u < PER / 2; u++) {
+        const int idx = threadIdx.x + (h + u) * 256, rr = idx % TB, c = idx / TB;
+        t[u] = (rr < nr) ? L[(r0 + rr) + (r0 - TB + c) * lda] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < PER / 2; u++) {
+        const int idx = threadIdx.x + (h + u) * 256, rr = idx % TB, c = idx / TB;
+        Ls[c * TBP + rr] = t[u];
+      }
     }
     __syncthreads();
     double acc[16];
@@ -245,9 +266,19 @@ __global__ void __launch_bounds__(256) k_inv_blocks(int64_t N, const double* __r
     // Gb[c][k] = sum_m L_{i+1,i}[k][m] Binv[m][c]   (thread: c = r, k = cg*16+u)
     const int nr1 = (int)((N - r0 - TB) < TB ? (N - r0 - TB) : TB);
     __syncthreads();
-    for (int idx = threadIdx.x; idx < TB * TB; idx += blockDim.x) {
-      const int kk = idx % TB, m = idx / TB;
-      Ls[m * TBP + kk] = (kk < nr1 && m < nr) ? L[(r0 + TB + kk) + (r0 + m) * lda] : 0.0;
+#pragma unroll
+    for (int h = 0; h < PER; h += PER / 2) {
+      double t[PER / 2];
+#pragma unroll
+      for (int u = 0; u < PER / 2; u++) {
+        const int idx = threadIdx.x + (h + u) * 256, kk = idx % TB, m = idx / TB;
+        t[u] = (kk < nr1 && m < nr) ? L[(r0 + TB + kk) + (r0 + m) * lda] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < PER / 2; u++) {
+        const int idx = threadIdx.x + (h + u) * 256, kk = idx % TB, m = idx / TB;
+        Ls[m * TBP + kk] = t[u];
+      }
     }
     __syncthreads();
     double acc[16];
