@@ -150,13 +150,16 @@ __global__ void k_gather(int64_t N, const int32_t* __restrict__ piv, const doubl
 // one-step chain operators Gf_i = Binv_i L_{i,i-1}, Gb_i = (L_{i+1,i} Binv_i)^T.
 constexpr int TBP = TB + 1;
 constexpr int IBSMEM = (2 * TB * TBP + 4 * 16 * 17) * 8;   // L block, Binv, 16x16 temporaries
-__global__ void __launch_bounds__(256) k_inv_blocks(int64_t N, const double* __restrict__ L, int64_t lda,
+// G = false (batched per-scenario sweeps: Binv only) compiles without the chain-operator
+// GEMMs (one CTA per block and scenario, 2 per SM)
+template <bool G>
+__global__ void __launch_bounds__(256, G ? 1 : 2) k_inv_blocks(int64_t N, const double* __restrict__ L, int64_t lda,
                                                     double* __restrict__ binv, double* __restrict__ gf,
                                                     double* __restrict__ gb, BStr z) {
   pdl_wait();
   pdl_trigger();
   L += blockIdx.y * z.ld;
-  const bool need_g = gf != nullptr;   // (the batched per-scenario sweeps use Binv only)
+  constexpr bool need_g = G;   // (the batched per-scenario sweeps use Binv only)
   binv = bsh(binv, z.ws);
   if (need_g) { gf = bsh(gf, z.ws); gb = bsh(gb, z.ws); }
   extern __shared__ double ism[];
@@ -713,15 +716,16 @@ static int solve_launch(const mds_plan* plan, int64_t batch, int64_t N, const do
     const int64_t nblk = (N + TB - 1) / TB;
     const unsigned ge = (unsigned)std::min<int64_t>(mds_cdiv(N, 256), batch > 1 ? 16 : 148 * 8);
     MDS_LAUNCH(PC_SOLVE_GATHER, st, MDS_CUDA_TRY(launch_pdl(k_gather, dim3(ge, nb), dim3(256), 0, st, N, piv, rhs_c, s.b, s.y, s.x, s.tickets, z)));
-    if (mds_once_per_device((const void*)k_inv_blocks)) {
-      cudaFuncSetAttribute(k_inv_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, IBSMEM);
+    if (mds_once_per_device((const void*)k_inv_blocks<true>)) {
+      cudaFuncSetAttribute(k_inv_blocks<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, IBSMEM);
+      cudaFuncSetAttribute(k_inv_blocks<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, IBSMEM);
       cudaFuncSetAttribute(k_trsv_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SWSMEM);
       cudaFuncSetAttribute(k_trsv_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SWSMEM);
     }
     // batched API: one CTA per scenario per sweep (the vector of N doubles in shared memory)
     const bool per_scen = batched_api && (size_t)N * 8 <= (size_t)BSMAX;
     MDS_LAUNCH(PC_SOLVE_FWD, st,
-               MDS_CUDA_TRY(launch_pdl(k_inv_blocks, dim3((unsigned)nblk, nb), dim3(256), IBSMEM, st, N, LD, ldm, s.binv,
+               MDS_CUDA_TRY(launch_pdl(per_scen ? k_inv_blocks<false> : k_inv_blocks<true>, dim3((unsigned)nblk, nb), dim3(256), IBSMEM, st, N, LD, ldm, s.binv,
                                        per_scen ? (double*)nullptr : s.gf, per_scen ? (double*)nullptr : s.gb, z)));
     if (per_scen && mds_once_per_device((const void*)k_bsolve_fwd)) {
       cudaFuncSetAttribute(k_bsolve_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, BSMAX);
