@@ -272,6 +272,29 @@ __device__ unsigned long long g_xph[10];
 constexpr int F1S = NB + 1;                     // F1 smem column stride
 constexpr int UT = 64;                          // DMMA tile edge
 constexpr int US = UT + 4;                      // F2 smem row stride (conflict-free fragment loads)
+static_assert(UT == NB, "X staging assumes square 64x64 tiles");
+// X = L11^{-T} (row-major [t][j], NB x NB in f.Lblk) into shared memory at row
+// stride US, with up to 16 loads of a thread in flight before its stores (a
+// load-store loop waits one round trip per element)
+template <int NT, bool CG>
+__device__ __forceinline__ void stage_x(double* dst, const double* __restrict__ src, int tid) {
+  constexpr int PER = NB * NB / NT;
+  constexpr int H = PER > 16 ? 16 : PER;
+#pragma unroll
+  for (int h = 0; h < PER; h += H) {
+    double v[H];
+#pragma unroll
+    for (int u = 0; u < H; u++) {
+      const int idx = tid + (h + u) * NT;
+      v[u] = CG ? __ldcg(&src[idx]) : src[idx];
+    }
+#pragma unroll
+    for (int u = 0; u < H; u++) {
+      const int idx = tid + (h + u) * NT;
+      dst[(idx >> 6) * US + (idx & (NB - 1))] = v[u];
+    }
+  }
+}
 constexpr int PF_BUF = NB * US;                 // doubles per shared buffer (>= NB * F1S)
 constexpr int F1SMEM = (3 * PF_BUF + NB) * 8;   // 3 buffers + 1/d
 
@@ -711,10 +734,7 @@ __device__ __forceinline__ void f2_role(int64_t N, double* __restrict__ A, int64
         while (ld_acquire_u32(&ctl->xready) < (unsigned)(f.pidx + 1)) __nanosleep(32);
       }
       __syncthreads();
-      for (int idx = tid; idx < NB * NB; idx += 256) {
-        const int j = idx & (NB - 1), t = idx >> 6;
-        S2[t * US + j] = __ldcg(&f.Lblk[t * NB + j]);
-      }
+      stage_x<256, true>(S2, f.Lblk, tid);
       if (tid < NB) {
         const double d = (tid < nbp) ? __ldcg(&ctl->d[tid]) : 0.0;
         const double rd = fast_rcp(d);
@@ -836,10 +856,7 @@ __global__ void __launch_bounds__(128) k_panel_trsm(int64_t N, const double* __r
     const double d = (tid < nbp) ? ctl->d[tid] : 0.0;
     r1s[tid] = (d != 0.0) ? fast_rcp(d) : 0.0;
   }
-  for (int idx = tid; idx < UT * NB; idx += 128) {
-    const int i = idx % UT, t = idx / UT;
-    Xs[t * US + i] = f.Lblk[t * NB + i];   // X[t][j=i]
-  }
+  stage_x<128, false>(Xs, f.Lblk, tid);   // Xs[t * US + i] = X[t][j=i]
   const int warp = tid >> 5, lane = tid & 31;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int g = lane >> 2, q = lane & 3;
@@ -1264,10 +1281,7 @@ __device__ __noinline__ void x_f2_leftovers(int64_t N, const double* __restrict_
     const double d = (tid < nbp) ? __ldcg(&ctl->d[tid]) : 0.0;
     r1s[tid] = (d != 0.0) ? fast_rcp(d) : 0.0;
   }
-  for (int idx = tid; idx < UT * NB; idx += XT) {
-    const int i = idx % UT, t = idx / UT;
-    Xs[t * US + i] = __ldcg(&f.Lblk[t * NB + i]);
-  }
+  stage_x<XT, true>(Xs, f.Lblk, tid);
   const int warp = tid >> 5, lane = tid & 31;
   const int wm = ((warp & 3) >> 1) * 32, wn = (warp & 1) * 32;
   const int g = lane >> 2, q = lane & 3;
